@@ -1,0 +1,182 @@
+/*
+ * sklsq.h — C ABI of the B200-native sketch-preconditioned least-squares kernels.
+ *
+ * Drop-in boundary for the hot path of the reference package `sketchlsq` 0.1.0
+ * (arXiv 2603.16644, Algorithm 1).  The reference is pure Python/numpy, so it has
+ * no native FFI of its own; these entry points replace, one for one, the numpy /
+ * BLAS / pocketfft calls that its Python functions make (cited per function as
+ * `src/<file>:<line>` = /root/reference/pkg/src/sketchlsq/<file>:<line>).  The
+ * Python layer `paper_2603_16644_b200` binds them with ctypes.
+ *
+ * Conventions
+ *  - All matrix pointers are DEVICE pointers (cudaMalloc / torch CUDA storage).
+ *    Matrices are row-major with an explicit leading dimension (elements) unless
+ *    a function says otherwise.  No torch types appear in any signature.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Work is
+ *    stream-ordered.  Functions that return a numerical verdict (QR, Cholesky, LU,
+ *    kappa0, finiteness) synchronise `stream` before returning it.
+ *  - `ws` / `ws_bytes`: caller-owned device workspace; query the size with the
+ *    matching *_workspace() call.  No allocation happens on the hot path.
+ *  - Return: SK_OK (0), a numerical failure code (>0, 1:1 with the reference
+ *    exception classes of src/errors.py:10-55), SK_ERR_CUDA (-1) or SK_ERR_ARG (-2).
+ *    Detail (offending column / pivot value) goes to the optional sk_status*;
+ *    sk_last_error() returns a thread-local message.
+ */
+#ifndef SKLSQ_H
+#define SKLSQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *sk_stream_t;
+
+enum sk_code {
+    SK_OK = 0,
+    SK_RANK_DEFICIENT = 1,        /* errors.RankDeficient        src/errors.py:14 */
+    SK_SINGULAR_TRIANGULAR = 2,   /* errors.SingularTriangular   src/errors.py:18 */
+    SK_NUMERICALLY_SINGULAR = 3,  /* errors.NumericallySingular  src/errors.py:22 */
+    SK_NOT_POSITIVE_DEFINITE = 4, /* errors.NotPositiveDefinite  src/errors.py:26 */
+    SK_OVERFLOW = 5,              /* errors.Overflow             src/errors.py:54 */
+    SK_DIMENSION_MISMATCH = 6,    /* errors.DimensionMismatch    src/errors.py:34 */
+    SK_NO_CONVERGENCE = 7,        /* errors.NoConvergence        src/errors.py:30 */
+    SK_NOT_SYMMETRIC = 8,         /* ValueError, src/dense.py:332-335 */
+    SK_NON_FINITE = 9,            /* ValueError, src/dense.py:63-64 */
+    SK_ERR_CUDA = -1,
+    SK_ERR_ARG = -2
+};
+
+enum sk_level { SK_BINARY16 = 16, SK_BINARY32 = 32, SK_BINARY64 = 64 };
+enum sk_transform { SK_DCT2 = 0, SK_WHT = 1 };
+enum sk_dtype { SK_F16 = 2, SK_F32 = 4, SK_F64 = 8 };
+
+typedef struct sk_status {
+    int32_t code;     /* sk_code */
+    int32_t pad;
+    int64_t index;    /* column / pivot index of the failure, -1 if none */
+    double value;     /* pivot value or magnitude at the failure */
+    double aux;       /* threshold (LU) or extra detail */
+} sk_status;
+
+/* ---- library ------------------------------------------------------------ */
+int sk_version(void);
+const char *sk_last_error(void);
+int sk_sm_count(int device);
+
+/* ---- streaming passes over A (HBM-bound) --------------------------------- */
+/* _as_matrix + astype(float64) + ||A||_F^2 in one pass: src/dense.py:57-65,
+ * src/solvers.py:87-96, src/solvers.py:102.  src dtype SK_F16/F32/F64 -> dst f64.
+ * stats_host[0] = number of non-finite entries, stats_host[1] = sum of squares. */
+size_t sk_matrix_stats_workspace(int64_t rows, int64_t cols);
+int sk_cast_stats(const void *src, int src_dtype, int64_t rows, int64_t cols, int64_t ld_src,
+                  double *dst, int64_t ld_dst, double *stats_host,
+                  void *ws, size_t ws_bytes, sk_stream_t stream);
+
+/* round_to_precision(A, level).overflowed without materialising the rounding:
+ * src/precision.py:90-103, src/solvers.py:191-193.  *overflowed_host = 0/1. */
+int sk_level_overflow(const double *a, int64_t rows, int64_t cols, int64_t lda, int level,
+                      int *overflowed_host, void *ws, size_t ws_bytes, sk_stream_t stream);
+
+/* r = A x - b; out_host[0] = ||r||^2, out_host[1] = ||x||^2: src/solvers.py:99-117. */
+int sk_residual(const double *a, int64_t rows, int64_t cols, int64_t lda, const double *x,
+                const double *b, double *r, double *out_host, void *ws, size_t ws_bytes,
+                sk_stream_t stream);
+
+/* ---- FP64 tensor-pipe (DMMA) products ------------------------------------ */
+/* G (n x n, row-major, ldg) = X^T Y with X (m x n, ldx), Y (m x n, ldy).
+ * If Y == X the SYRK path runs (lower tiles + exact mirror; numpy's a.T @ a is
+ * exactly symmetric, src/dense.py:332-335 relies on it).
+ * Replaces `a.T @ a` src/precision.py:230, `a_p.T @ a_p` src/solvers.py:230,
+ * `a_p.T @ a` src/solvers.py:251, `b_matrix.T @ a` src/solvers.py:164,
+ * `a.T @ a` src/solvers.py:137.  If `accumulate` != 0, G += X^T Y. */
+size_t sk_gram_workspace(int64_t m, int64_t n);
+int sk_gram_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
+                double *g, int64_t ldg, int accumulate, void *ws, size_t ws_bytes,
+                sk_stream_t stream);
+
+/* out (n) = X^T v (X m x n row-major): `a_p.T @ b` src/solvers.py:231/251. */
+size_t sk_gemv_t_workspace(int64_t m, int64_t n);
+int sk_gemv_t_f64(const double *x, int64_t ldx, int64_t m, int64_t n, const double *v,
+                  double *out, int accumulate, void *ws, size_t ws_bytes, sk_stream_t stream);
+
+/* A_p = A R^{-1} (R n x n upper, row-major ldr): precondition_matrix
+ * src/solvers.py:205-215 via triangular_solve(R, A^T, transposed=True)
+ * src/dense.py:204-242.  Returns SK_SINGULAR_TRIANGULAR on an exactly zero
+ * diagonal (index in status).  ap may alias a. */
+int sk_trsm_right_upper_f64(const double *a, int64_t lda, int64_t m, int64_t n, const double *r,
+                            int64_t ldr, double *ap, int64_t ldap, sk_status *status,
+                            sk_stream_t stream);
+
+/* ---- sketch --------------------------------------------------------------- */
+/* Partial SRTT sketch of a row block: out (d x n, COLUMN-major, ldo >= d, f64)
+ * (+)= Omega[:, row_offset : row_offset+m_local] * round_level(A_local) where
+ * Omega = S F D is the unscaled operator of src/sketch.py:138-169 (signs of
+ * length m_pad as +-1 doubles, sampled rows int64).  The sqrt(m_pad/d) scale and
+ * the final rounding happen in sk_sketch_finalize so that partials can be summed
+ * across row shards (NCCL) first.  Overflow of the demotion is OR-ed into
+ * *overflow_flag_dev (device int).  transform SK_DCT2/SK_WHT, level 16/32/64. */
+size_t sk_sketch_workspace(int64_t m_local, int64_t n, int64_t d);
+int sk_sketch_partial(int level, int transform, const double *a, int64_t lda, int64_t m_local,
+                      int64_t row_offset, int64_t m_pad, int64_t n, const double *signs,
+                      const int64_t *rows, int64_t d, double *out, int64_t ldo, int accumulate,
+                      int *overflow_flag_dev, void *ws, size_t ws_bytes, sk_stream_t stream);
+
+/* Finish the sketch: A_s = level(level(sum) * level(sqrt(m_pad/d))) written as a
+ * COLUMN-major d x n matrix in the level dtype (f16/f32/f64), the layout the
+ * level QR works on.  Also writes the f64 promotion to out_f64 (row-major, may
+ * be NULL) for apply_sketch's return value. */
+int sk_sketch_finalize(int level, const double *sum, int64_t ldsum, int64_t d, int64_t n,
+                       int64_t m_pad, void *a_s_level, double *out_f64, sk_stream_t stream);
+
+/* ---- level-precision Householder QR (R only) ------------------------------ */
+/* qr_in_precision(A_s, level).r : src/precision.py:153-202 + householder_reduce
+ * src/dense.py:108-161.  A_s: d x n COLUMN-major in the level dtype, overwritten.
+ * binary16 follows the reference op for op (power-of-two prescale, every scalar
+ * op rounded to binary16, pairwise trees of src/precision.py:106-115).
+ * R (n x n row-major f64, upper, exact zeros below) is the exact promotion (and,
+ * for binary16, un-scaling).  Failures: SK_RANK_DEFICIENT (index = column),
+ * SK_OVERFLOW. */
+size_t sk_qr_workspace(int level, int64_t d, int64_t n);
+int sk_qr_r(int level, void *a_s, int64_t d, int64_t n, double *r, int64_t ldr,
+            sk_status *status, void *ws, size_t ws_bytes, sk_stream_t stream);
+
+/* ---- n x n FP64 kernels (replicated, latency-bound) ---------------------- */
+/* x = S^{-1} rhs by Cholesky: cholesky_solve src/dense.py:314-342 (symmetry gate
+ * 10 eps max|S| -> SK_NOT_SYMMETRIC, pivot <= 0 or non-finite ->
+ * SK_NOT_POSITIVE_DEFINITE).  S row-major n x n (symmetric).  x may alias rhs. */
+size_t sk_nxn_workspace(int64_t n);
+int sk_chol_solve_f64(const double *s, int64_t n, const double *rhs, double *x,
+                      sk_status *status, void *ws, size_t ws_bytes, sk_stream_t stream);
+
+/* x = G^{-1} rhs by LU with partial pivoting: lu_solve src/dense.py:245-286
+ * (lowest index on ties; pivot < n eps max|G| -> SK_NUMERICALLY_SINGULAR). */
+int sk_lu_solve_f64(const double *g, int64_t n, const double *rhs, double *x,
+                    sk_status *status, void *ws, size_t ws_bytes, sk_stream_t stream);
+
+/* Triangular solve R x = rhs (or R^T x = rhs): triangular_solve src/dense.py:204-242
+ * for a single right-hand side.  R row-major upper.  x may alias rhs. */
+int sk_trsv_f64(const double *r, int64_t ldr, int64_t n, int transposed, const double *rhs,
+                double *x, sk_status *status, void *ws, size_t ws_bytes, sk_stream_t stream);
+
+/* kappa0 from a Gram matrix G = A^T A (n x n row-major): the remainder of
+ * estimate_log10_condition src/precision.py:205-251 (finite check, ||G||_1,
+ * Cholesky without fallback, <=5 Hager iterations src/dense.py:451-480).
+ * *kappa0_host = NaN and *overflowed_host = 1 on any breakdown. */
+int sk_kappa0_from_gram(const double *g, int64_t n, double *kappa0_host, int *overflowed_host,
+                        void *ws, size_t ws_bytes, sk_stream_t stream);
+
+/* Singular values of an n x n (row-major) matrix by one-sided Jacobi with the
+ * reference's round-robin schedule, gate and tolerance (jacobi_singular_values
+ * src/dense.py:365-415).  sv (host, n) descending.  SK_NO_CONVERGENCE after
+ * max_sweeps. Diagnostic only. */
+size_t sk_jacobi_workspace(int64_t rows, int64_t n);
+int sk_jacobi_sv_f64(const double *a, int64_t rows, int64_t n, int64_t lda, int max_sweeps,
+                     double tol, double *sv_host, void *ws, size_t ws_bytes, sk_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKLSQ_H */

@@ -1,0 +1,137 @@
+// Shared device/host helpers for libsklsq (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cooperative_groups.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/sklsq.h"
+
+namespace sk {
+
+// ---------------------------------------------------------------- errors ---
+void set_error(const char *fmt, ...);
+int cuda_fail(cudaError_t e, const char *where);
+inline int fill_status(sk_status *st, int code, int64_t index, double value, double aux) {
+    if (st) { st->code = code; st->pad = 0; st->index = index; st->value = value; st->aux = aux; }
+    return code;
+}
+
+#define SK_CUDA(call)                                                   \
+    do {                                                                \
+        cudaError_t _e = (call);                                        \
+        if (_e != cudaSuccess) return ::sk::cuda_fail(_e, #call);      \
+    } while (0)
+
+#define SK_LAUNCH_CHECK(where)                                          \
+    do {                                                                \
+        cudaError_t _e = cudaGetLastError();                            \
+        if (_e != cudaSuccess) return ::sk::cuda_fail(_e, where);      \
+    } while (0)
+
+int sm_count();                 // of the current device (cached per device)
+int max_coop_blocks(const void *kernel, int threads, size_t smem);
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Device-side status record for kernels that detect numerical failures.
+struct DevStatus {
+    int code;
+    int pad;
+    long long index;
+    double value;
+    double aux;
+};
+
+// ------------------------------------------------------------ DMMA (FP64) --
+// mma.sync m8n8k4 f64: A 8x4 (row), B 4x8 (col), C/D 8x8.  Lowers to DMMA.8x8x4
+// on sm_100a (tcgen05 has no f64 kind).  Fragment ownership, lane = 4*g + t:
+//   a = A[g][t], b = B[t][g], c0/c1 = C[g][2t], C[g][2t+1].
+__device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// ------------------------------------------------------------- cp.async ----
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// 16-byte async copy with zero fill of the (16 - src_bytes) tail.
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async8(void *dst, const void *src, int src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ------------------------------------------------------------ reductions ---
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Level-precision scalar arithmetic.  binary16 follows numpy float16 semantics
+// (op in binary32, one round-to-nearest-even to binary16; for + - * / sqrt this
+// equals the correctly rounded binary16 op since 24 >= 2*11+2).  The explicit
+// _rn intrinsics forbid FMA contraction, which numpy never does.
+template <typename T> struct LevelOps;
+
+template <> struct LevelOps<__half> {
+    using T = __half;
+    __device__ static __forceinline__ T add(T a, T b) { return __float2half_rn(__fadd_rn(__half2float(a), __half2float(b))); }
+    __device__ static __forceinline__ T sub(T a, T b) { return __float2half_rn(__fsub_rn(__half2float(a), __half2float(b))); }
+    __device__ static __forceinline__ T mul(T a, T b) { return __float2half_rn(__fmul_rn(__half2float(a), __half2float(b))); }
+    __device__ static __forceinline__ T div(T a, T b) { return __float2half_rn(__fdiv_rn(__half2float(a), __half2float(b))); }
+    __device__ static __forceinline__ T sqrt(T a) { return __float2half_rn(__fsqrt_rn(__half2float(a))); }
+    __device__ static __forceinline__ double to_f64(T a) { return (double)__half2float(a); }
+    __device__ static __forceinline__ T from_f64(double a) { return __double2half(a); }
+    __device__ static __forceinline__ bool finite(T a) { return isfinite(__half2float(a)); }
+    __device__ static __forceinline__ T zero() { return __float2half_rn(0.f); }
+};
+template <> struct LevelOps<float> {
+    using T = float;
+    __device__ static __forceinline__ T add(T a, T b) { return __fadd_rn(a, b); }
+    __device__ static __forceinline__ T sub(T a, T b) { return __fsub_rn(a, b); }
+    __device__ static __forceinline__ T mul(T a, T b) { return __fmul_rn(a, b); }
+    __device__ static __forceinline__ T div(T a, T b) { return __fdiv_rn(a, b); }
+    __device__ static __forceinline__ T sqrt(T a) { return __fsqrt_rn(a); }
+    __device__ static __forceinline__ double to_f64(T a) { return (double)a; }
+    __device__ static __forceinline__ T from_f64(double a) { return __double2float_rn(a); }
+    __device__ static __forceinline__ bool finite(T a) { return isfinite(a); }
+    __device__ static __forceinline__ T zero() { return 0.f; }
+};
+template <> struct LevelOps<double> {
+    using T = double;
+    __device__ static __forceinline__ T add(T a, T b) { return __dadd_rn(a, b); }
+    __device__ static __forceinline__ T sub(T a, T b) { return __dsub_rn(a, b); }
+    __device__ static __forceinline__ T mul(T a, T b) { return __dmul_rn(a, b); }
+    __device__ static __forceinline__ T div(T a, T b) { return __ddiv_rn(a, b); }
+    __device__ static __forceinline__ T sqrt(T a) { return __dsqrt_rn(a); }
+    __device__ static __forceinline__ double to_f64(T a) { return a; }
+    __device__ static __forceinline__ T from_f64(double a) { return a; }
+    __device__ static __forceinline__ bool finite(T a) { return isfinite(a); }
+    __device__ static __forceinline__ T zero() { return 0.0; }
+};
+
+}  // namespace sk

@@ -1,0 +1,607 @@
+// n x n FP64 kernels: Cholesky solve, LU solve with partial pivoting, triangular
+// solves, and the kappa0 condition estimate.  These run replicated on every GPU
+// (the n x n systems are tiny next to the m x n passes) and are latency-bound, so
+// they are cooperative persistent kernels with grid barriers (factorisations) or
+// single-CTA kernels (substitution, Hager).
+//
+// Reference semantics kept exactly:
+//  - cholesky_factor src/dense.py:289-311: factor (S + S^T)/2, pivot must be > 0
+//    and finite, else NotPositiveDefinite.  cholesky_solve :314-342 gates on
+//    max|S - S^T| <= 10 eps max|S| (ValueError otherwise).
+//  - lu_solve src/dense.py:245-286: partial pivoting, largest magnitude with the
+//    LOWEST index on ties, threshold n*eps*max|G|, row swaps, multipliers
+//    l = a_ik / a_kk then a_ij -= l * u_kj as a rounded product and a rounded
+//    subtraction (np.outer then -=): the factorisation is op-for-op the reference's.
+//  - triangular_solve src/dense.py:204-242: SingularTriangular on an exactly zero
+//    diagonal; x_i = (b_i - sum) / r_ii.
+//  - estimate_log10_condition src/precision.py:205-251 and Hager
+//    src/dense.py:451-480 (x0 = 1/n, <= 5 iterations, lowest-index argmax,
+//    stop when |z_j| <= z.x).
+#include <cmath>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace sk {
+namespace nxn {
+
+constexpr int THREADS = 256;
+
+// ------------------------------------------------------------ reductions ----
+// out[0] = max|a_ij|, out[1] = max|a_ij - a_ji|, out[2] = #non-finite,
+// out[3] = max_j sum_i |a_ij| (1-norm; columns)   (row-major input)
+__global__ void sym_stats(const double *a, int n, double *out) {
+    double mx = 0, dev = 0, nf = 0;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / n), j = (int)(idx % n);
+        const double v = a[idx];
+        if (!isfinite(v)) nf += 1;
+        mx = fmax(mx, fabs(v));
+        dev = fmax(dev, fabs(v - a[(int64_t)j * n + i]));
+    }
+    mx = warp_max(mx);
+    dev = warp_max(dev);
+    nf = warp_sum(nf);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(reinterpret_cast<unsigned long long *>(out), (unsigned long long)__double_as_longlong(mx));
+        atomicMax(reinterpret_cast<unsigned long long *>(out + 1), (unsigned long long)__double_as_longlong(dev));
+        atomicAdd(out + 2, nf);
+    }
+}
+__global__ void col_abs_sums(const double *a, int n, double *colsum) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    double s = 0;
+    for (int i = 0; i < n; ++i) s += fabs(a[(int64_t)i * n + j]);
+    colsum[j] = s;
+}
+
+// row-major g -> column-major w
+__global__ void transpose_copy(const double *g, int n, double *w) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(idx / n), i = (int)(idx % n);
+        w[idx] = g[(int64_t)i * n + j];
+    }
+}
+
+// ------------------------------------------------------------- Cholesky -----
+// W (col-major n x n) = (S + S^T)/2; L (col-major) receives the factor.
+__global__ void symmetrize(const double *s, int n, double *w) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(idx / n), i = (int)(idx % n);   // w col-major: w[i + j n]
+        w[idx] = (s[(int64_t)i * n + j] + s[(int64_t)j * n + i]) / 2.0;
+    }
+}
+
+struct FactorCtl {
+    int fail_code;
+    int fail_col;
+    double fail_value;
+};
+
+// Right-looking: at step j every thread computes d = sqrt(W_jj) (uniform verdict),
+// writes L[:, j] = W[:, j] / d and updates the trailing lower triangle.  L is a
+// separate array so W's column j is never overwritten while being read.
+__global__ void __launch_bounds__(THREADS) chol_kernel(double *w, double *l, int n, FactorCtl *ctl) {
+    cg::grid_group grid = cg::this_grid();
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    for (int j = 0; j < n; ++j) {
+        const double c0 = w[(int64_t)j * n + j];
+        if (!(c0 > 0.0) || !isfinite(c0)) {
+            if (tid == 0) { ctl->fail_code = SK_NOT_POSITIVE_DEFINITE; ctl->fail_col = j; ctl->fail_value = c0; }
+            return;
+        }
+        const double d = sqrt(c0);
+        const int rem = n - j - 1;
+        // column j of L
+        for (int64_t t = tid; t <= rem; t += nthreads) {
+            const int i = j + (int)t;
+            l[(int64_t)j * n + i] = (t == 0) ? d : w[(int64_t)j * n + i] / d;
+        }
+        // trailing lower triangle: pairs (i, k), j < k <= i  -> linear index over rem*(rem+1)/2
+        const int64_t tri = (int64_t)rem * (rem + 1) / 2;
+        for (int64_t t = tid; t < tri; t += nthreads) {
+            // column-major enumeration of the lower triangle: k-th column has rem-k entries
+            // invert t -> (kk, ii) with kk from the quadratic formula
+            const double tt = (double)t;
+            const double b = 2.0 * rem + 1.0;
+            int kk = (int)((b - sqrt(b * b - 8.0 * tt)) * 0.5);
+            if (kk < 0) kk = 0;
+            while (kk > 0 && (int64_t)kk * (2 * rem - kk + 1) / 2 > t) --kk;
+            while ((int64_t)(kk + 1) * (2 * rem - kk) / 2 <= t) ++kk;
+            const int64_t start = (int64_t)kk * (2 * rem - kk + 1) / 2;
+            const int ii = kk + (int)(t - start);
+            const int k = j + 1 + kk, i = j + 1 + ii;
+            const double li = w[(int64_t)j * n + i] / d, lk = w[(int64_t)j * n + k] / d;
+            double *p = w + (int64_t)k * n + i;
+            *p = __dsub_rn(*p, __dmul_rn(li, lk));
+        }
+        grid.sync();
+    }
+}
+
+// --------------------------------------------------------------------- LU ---
+struct LuCtl {
+    int fail_code;
+    int fail_col;
+    double fail_value;
+    double thresh;
+};
+
+// candidate (value, index) per block, double-buffered by step parity
+__device__ __forceinline__ void better(double &bv, int &bi, double v, int i) {
+    if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+}
+
+__device__ void block_argmax(double v, int i, double *sv, int *si, double *outv, int *outi) {
+    // lowest index wins ties; NaN never wins (reference np.argmax would pick NaN,
+    // but a NaN pivot fails the threshold either way)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+        better(v, i, ov, oi);
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) { sv[warp] = v; si[warp] = i; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double bv = -1.0;
+        int bi = INT32_MAX;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) better(bv, bi, sv[k], si[k]);
+        *outv = bv;
+        *outi = bi;
+    }
+    __syncthreads();
+}
+
+// w: col-major n x n working copy (U in the upper part); lmul: col-major multipliers;
+// perm: int permutation.  cand: 2 x gridDim.x (value, index) pairs.
+__global__ void __launch_bounds__(THREADS)
+lu_kernel(double *w, double *lmul, int *perm, int n, double *candv, int *candi, LuCtl *ctl) {
+    __shared__ double sv[THREADS / 32];
+    __shared__ int si[THREADS / 32];
+    cg::grid_group grid = cg::this_grid();
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const double thresh = ctl->thresh;
+    // candidates for column 0
+    {
+        double bv = -1.0;
+        int bi = INT32_MAX;
+        for (int64_t i = tid; i < n; i += nthreads) better(bv, bi, fabs(w[i]), (int)i);
+        block_argmax(bv, bi, sv, si, &candv[blockIdx.x], &candi[blockIdx.x]);
+    }
+    for (int64_t i = tid; i < n; i += nthreads) perm[i] = (int)i;
+    grid.sync();
+    for (int k = 0; k < n; ++k) {
+        const int buf = k & 1;
+        // every thread reduces the block candidates in block order (deterministic)
+        double bv = -1.0;
+        int p = INT32_MAX;
+        for (int b = 0; b < (int)gridDim.x; ++b) better(bv, p, candv[buf * gridDim.x + b], candi[buf * gridDim.x + b]);
+        const double piv = bv;
+        if (piv < thresh || piv == 0.0 || !(piv == piv)) {
+            if (tid == 0) { ctl->fail_code = SK_NUMERICALLY_SINGULAR; ctl->fail_col = k; ctl->fail_value = piv; }
+            return;
+        }
+        // swap rows k and p over all columns (one thread per column: no race)
+        if (p != k) {
+            for (int64_t j = tid; j < n; j += nthreads) {
+                double *a = w + j * n;
+                const double t = a[k];
+                a[k] = a[p];
+                a[p] = t;
+                if (j < k) {   // multipliers of earlier steps move with their rows
+                    double *lm = lmul + j * n;
+                    const double u = lm[k];
+                    lm[k] = lm[p];
+                    lm[p] = u;
+                }
+            }
+            if (tid == 0) { const int t = perm[k]; perm[k] = perm[p]; perm[p] = t; }
+        }
+        grid.sync();
+        // multipliers and trailing update; candidates for column k+1 on the fly
+        const double akk = w[(int64_t)k * n + k];
+        const int rem = n - k - 1;
+        double cbv = -1.0;
+        int cbi = INT32_MAX;
+        const int64_t cnt = (int64_t)rem * (rem + 1);   // columns k..n-1 (rem+1) x rows k+1..n-1 (rem)
+        for (int64_t t = tid; t < cnt; t += nthreads) {
+            const int jj = (int)(t / rem), ii = (int)(t % rem);
+            const int i = k + 1 + ii, j = k + jj;
+            const double li = __ddiv_rn(w[(int64_t)k * n + i], akk);
+            if (j == k) {
+                lmul[(int64_t)k * n + i] = li;
+            } else {
+                double *q = w + (int64_t)j * n + i;
+                const double nv = __dsub_rn(*q, __dmul_rn(li, w[(int64_t)j * n + k]));
+                *q = nv;
+                if (j == k + 1) better(cbv, cbi, fabs(nv), i);
+            }
+        }
+        block_argmax(cbv, cbi, sv, si, &candv[(buf ^ 1) * gridDim.x + blockIdx.x], &candi[(buf ^ 1) * gridDim.x + blockIdx.x]);
+        grid.sync();
+    }
+}
+
+// ------------------------------------------------------------ substitution --
+// Single-CTA blocked triangular solve over an element accessor M(i,k) = m[i*rs + k*cs].
+// lower: x_i depends on k < i (forward); else k > i (backward).  unit: diag == 1.
+// x holds rhs on entry (in shared or global memory) and the solution on exit.
+struct TriView {
+    const double *m;
+    int64_t rs, cs;
+    __device__ __forceinline__ double operator()(int i, int k) const { return m[i * rs + k * cs]; }
+};
+
+__device__ void block_trsv(const TriView M, int n, bool lower, bool unit, double *x) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    const int nb = (n + 31) / 32;
+    for (int bb = 0; bb < nb; ++bb) {
+        const int b = lower ? bb : nb - 1 - bb;
+        const int r0 = b * 32, r1 = min(n, r0 + 32);
+        const int w = r1 - r0;
+        if (warp == 0) {
+            double v = (lane < w) ? x[r0 + lane] : 0.0;
+            for (int s = 0; s < w; ++s) {
+                const int r = lower ? s : w - 1 - s;
+                double xr = 0.0;
+                if (lane == r) { xr = unit ? v : v / M(r0 + r, r0 + r); v = xr; }
+                xr = __shfl_sync(0xffffffffu, xr, r);
+                const bool dep = lower ? (lane > r) : (lane < r);
+                if (dep && lane < w) v -= M(r0 + lane, r0 + r) * xr;
+            }
+            if (lane < w) x[r0 + lane] = v;
+        }
+        __syncthreads();
+        // update the rows not yet solved: lower -> rows >= r1, upper -> rows < r0
+        const int lo = lower ? r1 : 0, hi = lower ? n : r0;
+        if (M.rs == 1) {   // column-major: thread per row, coalesced
+            for (int i = lo + tid; i < hi; i += nt) {
+                double s = 0.0;
+                for (int k = r0; k < r1; ++k) s += M(i, k) * x[k];
+                x[i] -= s;
+            }
+        } else {           // row-major: warp per row, lanes over the block
+            for (int i = lo + warp; i < hi; i += nw) {
+                double s = (lane < w) ? M(i, r0 + lane) * x[r0 + lane] : 0.0;
+                s = warp_sum(s);
+                if (lane == 0) x[i] -= s;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(1024) trsv_kernel(TriView M, int n, bool lower, bool unit, const double *rhs,
+                                                    const int *perm, double *x) {
+    extern __shared__ double xs[];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = perm ? rhs[perm[i]] : rhs[i];
+    __syncthreads();
+    block_trsv(M, n, lower, unit, xs);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = xs[i];
+}
+
+__global__ void first_zero_diag(TriView M, int n, int *out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        if (M(i, i) == 0.0) atomicMin(out, i);
+}
+
+// Hager on G^{-1} with G = L L^T (L col-major), all in one CTA.
+// est_out = best (the estimate of ||G^{-1}||_1).
+__global__ void __launch_bounds__(1024) hager_kernel(const double *l, int n, double *est_out) {
+    extern __shared__ double hs[];
+    double *x = hs, *y = hs + n, *z = hs + 2 * n;
+    __shared__ double red[32];
+    __shared__ int redi[32];
+    __shared__ int stop;
+    const TriView Lv{l, 1, n};          // L(i,k) = l[i + k n]
+    const TriView LTv{l, n, 1};         // L^T(i,k) = L(k,i) = l[k + i n]
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    for (int i = tid; i < n; i += nt) x[i] = 1.0 / n;
+    double best = 0.0;
+    __syncthreads();
+    for (int it = 0; it < 5; ++it) {
+        // y = G^{-1} x : forward with L, backward with L^T
+        for (int i = tid; i < n; i += nt) y[i] = x[i];
+        __syncthreads();
+        block_trsv(Lv, n, true, false, y);
+        block_trsv(LTv, n, false, false, y);
+        // ||y||_1
+        double s = 0.0;
+        for (int i = tid; i < n; i += nt) s += fabs(y[i]);
+        s = warp_sum(s);
+        if (lane == 0) red[warp] = s;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int k = 0; k < nw; ++k) t += red[k];
+            best = fmax(best, t);
+            red[0] = best;
+        }
+        __syncthreads();
+        best = red[0];
+        __syncthreads();
+        // z = G^{-T} sign(y)  (G symmetric: same solve)
+        for (int i = tid; i < n; i += nt) z[i] = (y[i] >= 0.0) ? 1.0 : -1.0;
+        __syncthreads();
+        block_trsv(Lv, n, true, false, z);
+        block_trsv(LTv, n, false, false, z);
+        // j = argmax |z| (lowest index), z.x
+        double bv = -1.0, zx = 0.0;
+        int bi = INT32_MAX;
+        for (int i = tid; i < n; i += nt) {
+            better(bv, bi, fabs(z[i]), i);
+            zx += z[i] * x[i];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            better(bv, bi, ov, oi);
+        }
+        zx = warp_sum(zx);
+        __shared__ double zxs[32];
+        if (lane == 0) { red[warp] = bv; redi[warp] = bi; zxs[warp] = zx; }
+        __syncthreads();
+        if (tid == 0) {
+            double v = -1.0, t = 0.0;
+            int idx = INT32_MAX;
+            for (int k = 0; k < nw; ++k) { better(v, idx, red[k], redi[k]); t += zxs[k]; }
+            stop = (v <= t) ? 1 : 0;
+            redi[0] = idx;
+        }
+        __syncthreads();
+        if (stop) break;
+        const int j = redi[0];
+        for (int i = tid; i < n; i += nt) x[i] = (i == j) ? 1.0 : 0.0;
+        __syncthreads();
+    }
+    if (tid == 0) *est_out = best;
+}
+
+// --------------------------------------------------------------- helpers ----
+struct Ws {
+    double *w, *l, *stats, *vec, *candv;
+    int *perm, *candi, *flag;
+    void *ctl;
+};
+static size_t ws_layout(int64_t n, void *base, Ws *o) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t at = off; off = align_up(off + bytes, 256); return at; };
+    const size_t nn = (size_t)n * n * sizeof(double);
+    size_t ow = take(nn), ol = take(nn), os = take(8 * sizeof(double)), ov = take((size_t)n * sizeof(double) * 2);
+    size_t op = take((size_t)n * sizeof(int)), oc = take(2 * 4096 * sizeof(double)), oci = take(2 * 4096 * sizeof(int));
+    size_t of = take(sizeof(int) * 4), octl = take(256);
+    if (o && base) {
+        unsigned char *b = static_cast<unsigned char *>(base);
+        o->w = reinterpret_cast<double *>(b + ow);
+        o->l = reinterpret_cast<double *>(b + ol);
+        o->stats = reinterpret_cast<double *>(b + os);
+        o->vec = reinterpret_cast<double *>(b + ov);
+        o->perm = reinterpret_cast<int *>(b + op);
+        o->candv = reinterpret_cast<double *>(b + oc);
+        o->candi = reinterpret_cast<int *>(b + oci);
+        o->flag = reinterpret_cast<int *>(b + of);
+        o->ctl = b + octl;
+    }
+    return off;
+}
+
+static int coop_blocks(const void *fn, int threads, size_t smem, int64_t want) {
+    int maxb = max_coop_blocks(fn, threads, smem);
+    if (maxb <= 0) return 0;
+    int64_t b = want < 1 ? 1 : want;
+    return (int)(b > maxb ? maxb : b);
+}
+
+static int trsv_launch(TriView M, int n, bool lower, bool unit, const double *rhs, const int *perm, double *x,
+                       cudaStream_t st) {
+    const size_t smem = (size_t)n * sizeof(double);
+    if (smem > 48 * 1024)
+        SK_CUDA(cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    trsv_kernel<<<1, 1024, smem, st>>>(M, n, lower, unit, rhs, perm, x);
+    SK_LAUNCH_CHECK("trsv_kernel");
+    return SK_OK;
+}
+
+// Cholesky factor of (S+S^T)/2 into ws.l; returns SK_OK or SK_NOT_POSITIVE_DEFINITE.
+static int chol_factor(const double *s, int n, Ws &ws, sk_status *status, cudaStream_t st) {
+    FactorCtl *ctl = static_cast<FactorCtl *>(ws.ctl);
+    SK_CUDA(cudaMemsetAsync(ctl, 0, sizeof(FactorCtl), st));
+    SK_CUDA(cudaMemsetAsync(ws.l, 0, (size_t)n * n * sizeof(double), st));
+    symmetrize<<<(unsigned)std::min<int64_t>(((int64_t)n * n + 255) / 256, 4096), 256, 0, st>>>(s, n, ws.w);
+    SK_LAUNCH_CHECK("symmetrize");
+    const int blocks = coop_blocks((const void *)chol_kernel, THREADS, 0, ((int64_t)n * n / 2 + THREADS * 8 - 1) / (THREADS * 8));
+    if (!blocks) { set_error("chol_kernel not co-resident"); return SK_ERR_CUDA; }
+    double *w = ws.w, *l = ws.l;
+    int ni = n;
+    void *args[] = {&w, &l, &ni, &ctl};
+    SK_CUDA(cudaLaunchCooperativeKernel((const void *)chol_kernel, dim3(blocks), dim3(THREADS), args, 0, st));
+    SK_LAUNCH_CHECK("chol_kernel");
+    FactorCtl h;
+    SK_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(h), cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaStreamSynchronize(st));
+    if (h.fail_code) {
+        set_error("pivot %d is %g", h.fail_col, h.fail_value);
+        return fill_status(status, h.fail_code, h.fail_col, h.fail_value, 0.0);
+    }
+    return SK_OK;
+}
+
+}  // namespace nxn
+}  // namespace sk
+
+using namespace sk;
+using namespace sk::nxn;
+
+extern "C" {
+
+size_t sk_nxn_workspace(int64_t n) { return ws_layout(n, nullptr, nullptr) + 1024; }
+
+int sk_chol_solve_f64(const double *s, int64_t n, const double *rhs, double *x, sk_status *status, void *wsp,
+                      size_t ws_bytes, sk_stream_t stream) {
+    if (!s || !rhs || !x || n <= 0 || n > 65536 || !wsp || ws_bytes < sk_nxn_workspace(n)) {
+        set_error("sk_chol_solve_f64: bad arguments");
+        return SK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    Ws ws;
+    ws_layout(n, wsp, &ws);
+    // symmetry gate (src/dense.py:332-335)
+    SK_CUDA(cudaMemsetAsync(ws.stats, 0, 4 * sizeof(double), st));
+    sym_stats<<<(unsigned)std::min<int64_t>((n * n + 255) / 256, 1024), 256, 0, st>>>(s, (int)n, ws.stats);
+    SK_LAUNCH_CHECK("sym_stats");
+    double h[4];
+    SK_CUDA(cudaMemcpyAsync(h, ws.stats, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaStreamSynchronize(st));
+    if (h[2] > 0) { set_error("s contains non-finite entries"); return fill_status(status, SK_NON_FINITE, -1, 0, 0); }
+    if (h[1] > 10.0 * 2.220446049250313e-16 * h[0]) {
+        set_error("s is not symmetric within 10*eps relative tolerance");
+        return fill_status(status, SK_NOT_SYMMETRIC, -1, h[1], h[0]);
+    }
+    int rc = chol_factor(s, (int)n, ws, status, st);
+    if (rc != SK_OK) return rc;
+    // y = L^{-1} rhs, x = L^{-T} y
+    const TriView Lv{ws.l, 1, n}, LTv{ws.l, n, 1};
+    rc = trsv_launch(Lv, (int)n, true, false, rhs, nullptr, ws.vec, st);
+    if (rc) return rc;
+    rc = trsv_launch(LTv, (int)n, false, false, ws.vec, nullptr, x, st);
+    if (rc) return rc;
+    return fill_status(status, SK_OK, -1, 0, 0);
+}
+
+int sk_lu_solve_f64(const double *g, int64_t n, const double *rhs, double *x, sk_status *status, void *wsp,
+                    size_t ws_bytes, sk_stream_t stream) {
+    if (!g || !rhs || !x || n <= 0 || n > 65536 || !wsp || ws_bytes < sk_nxn_workspace(n)) {
+        set_error("sk_lu_solve_f64: bad arguments");
+        return SK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    Ws ws;
+    ws_layout(n, wsp, &ws);
+    SK_CUDA(cudaMemsetAsync(ws.stats, 0, 4 * sizeof(double), st));
+    sym_stats<<<(unsigned)std::min<int64_t>((n * n + 255) / 256, 1024), 256, 0, st>>>(g, (int)n, ws.stats);
+    SK_LAUNCH_CHECK("sym_stats");
+    double h[4];
+    SK_CUDA(cudaMemcpyAsync(h, ws.stats, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaStreamSynchronize(st));
+    if (h[2] > 0) { set_error("a contains non-finite entries"); return fill_status(status, SK_NON_FINITE, -1, 0, 0); }
+    LuCtl c{};
+    c.thresh = (double)n * 2.220446049250313e-16 * h[0];   // n * eps * max|a|
+    LuCtl *ctl = static_cast<LuCtl *>(ws.ctl);
+    SK_CUDA(cudaMemcpyAsync(ctl, &c, sizeof(c), cudaMemcpyHostToDevice, st));
+    // column-major working copy (the reference factors an order="F" copy)
+    transpose_copy<<<(unsigned)std::min<int64_t>((n * n + 255) / 256, 4096), 256, 0, st>>>(g, (int)n, ws.w);
+    SK_LAUNCH_CHECK("transpose_copy");
+    SK_CUDA(cudaMemsetAsync(ws.l, 0, (size_t)n * n * sizeof(double), st));
+    int blocks = coop_blocks((const void *)lu_kernel, THREADS, 0, (n * n + THREADS * 8 - 1) / (THREADS * 8));
+    if (blocks > 2048) blocks = 2048;
+    if (!blocks) { set_error("lu_kernel not co-resident"); return SK_ERR_CUDA; }
+    double *w = ws.w, *lm = ws.l, *cv = ws.candv;
+    int *perm = ws.perm, *ci = ws.candi;
+    int ni = (int)n;
+    void *args[] = {&w, &lm, &perm, &ni, &cv, &ci, &ctl};
+    SK_CUDA(cudaLaunchCooperativeKernel((const void *)lu_kernel, dim3(blocks), dim3(THREADS), args, 0, st));
+    SK_LAUNCH_CHECK("lu_kernel");
+    LuCtl hc;
+    SK_CUDA(cudaMemcpyAsync(&hc, ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaStreamSynchronize(st));
+    if (hc.fail_code) {
+        set_error("pivot %d magnitude %.3e below threshold %.3e", hc.fail_col, hc.fail_value, hc.thresh);
+        return fill_status(status, hc.fail_code, hc.fail_col, hc.fail_value, hc.thresh);
+    }
+    // x = U^{-1} L^{-1} rhs[perm]
+    const TriView Lv{ws.l, 1, n}, Uv{ws.w, 1, n};
+    int rc = trsv_launch(Lv, (int)n, true, true, rhs, perm, ws.vec, st);
+    if (rc) return rc;
+    rc = trsv_launch(Uv, (int)n, false, false, ws.vec, nullptr, x, st);
+    if (rc) return rc;
+    return fill_status(status, SK_OK, -1, 0, 0);
+}
+
+int sk_trsv_f64(const double *r, int64_t ldr, int64_t n, int transposed, const double *rhs, double *x,
+                sk_status *status, void *wsp, size_t ws_bytes, sk_stream_t stream) {
+    if (!r || !rhs || !x || n <= 0 || ldr < n || n > 65536 || !wsp || ws_bytes < 2 * sizeof(double) * (size_t)n + 256) {
+        set_error("sk_trsv_f64: bad arguments");
+        return SK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    int *flag = static_cast<int *>(wsp);
+    double *tmp = reinterpret_cast<double *>(static_cast<unsigned char *>(wsp) + 256);
+    const TriView Rv{r, ldr, 1};       // R(i,k) = r[i*ldr + k]  (row-major upper)
+    const TriView RTv{r, 1, ldr};      // R^T(i,k) = R(k,i)
+    int big = INT32_MAX, first = INT32_MAX;
+    SK_CUDA(cudaMemcpyAsync(flag, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+    first_zero_diag<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Rv, (int)n, flag);
+    SK_LAUNCH_CHECK("first_zero_diag");
+    SK_CUDA(cudaMemcpyAsync(&first, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaStreamSynchronize(st));
+    if (first != INT32_MAX) {
+        set_error("zero diagonal entry at index %d", first);
+        return fill_status(status, SK_SINGULAR_TRIANGULAR, first, 0, 0);
+    }
+    SK_CUDA(cudaMemcpyAsync(tmp, rhs, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    int rc = transposed ? trsv_launch(RTv, (int)n, true, false, tmp, nullptr, x, st)
+                        : trsv_launch(Rv, (int)n, false, false, tmp, nullptr, x, st);
+    if (rc) return rc;
+    return fill_status(status, SK_OK, -1, 0, 0);
+}
+
+int sk_kappa0_from_gram(const double *g, int64_t n, double *kappa0_host, int *overflowed_host, void *wsp,
+                        size_t ws_bytes, sk_stream_t stream) {
+    if (!g || !kappa0_host || !overflowed_host || n <= 0 || n > 65536 || !wsp || ws_bytes < sk_nxn_workspace(n)) {
+        set_error("sk_kappa0_from_gram: bad arguments");
+        return SK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    Ws ws;
+    ws_layout(n, wsp, &ws);
+    *kappa0_host = NAN;
+    *overflowed_host = 1;
+    // finite check and ||G||_1 (src/precision.py:231-235)
+    SK_CUDA(cudaMemsetAsync(ws.stats, 0, 4 * sizeof(double), st));
+    sym_stats<<<(unsigned)std::min<int64_t>((n * n + 255) / 256, 1024), 256, 0, st>>>(g, (int)n, ws.stats);
+    SK_LAUNCH_CHECK("sym_stats");
+    col_abs_sums<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, (int)n, ws.vec);
+    SK_LAUNCH_CHECK("col_abs_sums");
+    double h[4];
+    SK_CUDA(cudaMemcpyAsync(h, ws.stats, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    double *cs = static_cast<double *>(malloc((size_t)n * sizeof(double)));
+    if (!cs) { set_error("host alloc"); return SK_ERR_ARG; }
+    cudaError_t e = cudaMemcpyAsync(cs, ws.vec, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { free(cs); return cuda_fail(e, "kappa0 norm1"); }
+    double norm1 = -INFINITY;   // np.abs(g).sum(axis=0).max()
+    for (int64_t j = 0; j < n; ++j) norm1 = (cs[j] > norm1 || cs[j] != cs[j]) ? cs[j] : norm1;
+    free(cs);
+    if (h[2] > 0) return SK_OK;                              // non-finite G
+    if (norm1 == 0.0 || !std::isfinite(norm1)) return SK_OK;
+    int rc = chol_factor(g, (int)n, ws, nullptr, st);
+    if (rc == SK_NOT_POSITIVE_DEFINITE) return SK_OK;        // breakdown -> overflowed
+    if (rc != SK_OK) return rc;
+    const size_t smem = 3 * (size_t)n * sizeof(double);
+    if (smem > 227 * 1024) { set_error("n too large for the single-CTA Hager kernel"); return SK_ERR_ARG; }
+    if (smem > 48 * 1024)
+        SK_CUDA(cudaFuncSetAttribute(hager_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    hager_kernel<<<1, 1024, smem, st>>>(ws.l, (int)n, ws.stats + 4);
+    SK_LAUNCH_CHECK("hager_kernel");
+    double est = 0.0;
+    SK_CUDA(cudaMemcpyAsync(&est, ws.stats + 4, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaStreamSynchronize(st));
+    const double value = (double)n * norm1 * est;
+    if (!std::isfinite(value) || value <= 0.0) return SK_OK;
+    *kappa0_host = 0.5 * log10(value);
+    *overflowed_host = 0;
+    return SK_OK;
+}
+
+}  // extern "C"

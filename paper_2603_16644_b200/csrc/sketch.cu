@@ -1,0 +1,319 @@
+// SRTT sketch  A_s = sqrt(m_pad/d) * S F D * A_level  (src/sketch.py:138-169).
+//
+// The reference demotes A to the level (src/solvers.py:191-193), flips row signs,
+// runs a full length-m orthonormal DCT-II (pocketfft) or Walsh-Hadamard transform
+// along the rows, keeps the d sampled output rows and scales them.  Only d of the
+// m transform outputs are ever used, so here the sampled rows of the transform
+// are formed directly as a GEMM against the closed-form operator
+//     F_dct[r, j] = c_r cos(pi r (2j+1) / (2M)),   F_wht[r, j] = (-1)^popc(r & j) / sqrt(M)
+// generated on the fly in shared memory, with the signs folded into the demoted
+// A tile.  This v1 kernel runs on the FP64 DMMA pipe for every level (the exact
+// product is then rounded to the level in sk_sketch_finalize, matching the
+// reference's "transform in working precision, round" to within the level's
+// unit roundoff).  Row shards pass their global row_offset, so partial sketches
+// of contiguous row blocks sum (NCCL allreduce) to the global sketch.
+//
+// DCT phases are exact: p = r (2j+1) mod 4M in integer arithmetic, then
+// sincospi(p / 2M); within a 16-wide K block the angle advances by a per-row
+// rotation e^{i t pi r / M} computed the same way, so every Omega entry is a
+// product of two correctly-reduced unit complex numbers (~2 ulp).
+#include "common.cuh"
+
+namespace sk {
+namespace sketch {
+
+constexpr int BM = 128, BN = 128, BK = 16, THREADS = 256, WM = 32, WN = 64;
+constexpr int APITCH = BK + 4;   // Omega tile [i][k], 20 = 4 (mod 16)
+constexpr int BPITCH = BN + 4;   // A tile [k][c], 132 = 4 (mod 16)
+constexpr size_t SMEM = sizeof(double) * (2 * BM * APITCH + 2 * BK * BPITCH + 2 * BM * BK);
+
+template <int LEVEL>
+__device__ __forceinline__ double demote(double v, int &over) {
+    double w;
+    if (LEVEL == 16) w = (double)__half2float(__double2half(v));
+    else if (LEVEL == 32) w = (double)__double2float_rn(v);
+    else w = v;
+    over |= (isinf(w) && isfinite(v)) ? 1 : 0;
+    return w;
+}
+
+template <int LEVEL, int TRANSFORM>
+__global__ void __launch_bounds__(THREADS, 1)
+sketch_kernel(const double *__restrict__ a, int64_t lda, int64_t m_local, int64_t row_offset,
+              int64_t mpad, int n, const double *__restrict__ signs, const int64_t *__restrict__ rows,
+              int d, int ntn, int ntiles, int64_t kchunk, double *__restrict__ part, int *overflow_flag) {
+    extern __shared__ __align__(16) double smem[];
+    double *om = smem;                          // [2][BM][APITCH]
+    double *bt = om + 2 * BM * APITCH;          // [2][BK][BPITCH]
+    double *rot = bt + 2 * BK * BPITCH;         // [BM][BK] (cos) + [BM][BK] (sin) -> per-row step rotations
+
+    const int unit = blockIdx.x;
+    const int tile = unit % ntiles, split = unit / ntiles;
+    const int ti = tile / ntn, tj = tile % ntn;
+    const int i0 = ti * BM, c0 = tj * BN;
+    const int64_t kbeg = split * kchunk;
+    const int64_t kend = min(m_local, kbeg + kchunk);
+    const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int wm = warp % (BM / WM), wn = warp / (BM / WM);
+
+    // Omega generator role: thread -> (row gi = tid/2, k half = tid%2 -> 8 columns)
+    const int gi = tid >> 1, gh = tid & 1;
+    const bool grow_ok = (i0 + gi) < d;
+    const int64_t rr = grow_ok ? rows[i0 + gi] : 0;
+    const double M = (double)mpad;
+    const int64_t fourM = 4 * mpad;
+    const double cr = (rr == 0) ? sqrt(1.0 / M) : sqrt(2.0 / M);
+    double rc[8], rs[8];   // e^{i (gh*8 + u) pi r / M}, u = 0..7, relative to the block base
+    if (TRANSFORM == SK_DCT2) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t q = (int64_t)(((uint64_t)rr * (uint64_t)(2 * u)) % (uint64_t)fourM);
+            sincospi((double)q / (2.0 * M), &rs[u], &rc[u]);
+        }
+    }
+    (void)rot;
+    int over = 0;
+
+    auto gen_omega = [&](double *dst, int64_t kb) {
+        // columns kb + gh*8 + u (local rows of A), global jg = row_offset + local
+        const int64_t jl0 = kb + gh * 8;
+        if (TRANSFORM == SK_DCT2) {
+            const int64_t jg0 = row_offset + jl0;
+            // both factors < 4M < 2^32, so the product fits in 64 bits
+            const uint64_t f1 = (uint64_t)rr % (uint64_t)fourM;
+            const uint64_t f2 = (uint64_t)(2 * jg0 + 1) % (uint64_t)fourM;
+            const int64_t p = (int64_t)((f1 * f2) % (uint64_t)fourM);
+            double sb, cb;
+            sincospi((double)p / (2.0 * M), &sb, &cb);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                double v = cr * (cb * rc[u] - sb * rs[u]);
+                if (!grow_ok || jl0 + u >= kend) v = 0.0;
+                dst[gi * APITCH + gh * 8 + u] = v;
+            }
+        } else {
+            const double inv = 1.0 / sqrt(M);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t jg = row_offset + jl0 + u;
+                double v = (__popcll((unsigned long long)(rr & jg)) & 1) ? -inv : inv;
+                if (!grow_ok || jl0 + u >= kend) v = 0.0;
+                dst[gi * APITCH + gh * 8 + u] = v;
+            }
+        }
+    };
+    // A tile loader role: thread -> (k row = tid/16, 8 columns = (tid%16)*8)
+    const int lk = tid >> 4, lc = (tid & 15) * 8;
+    double areg[8];
+    auto load_a = [&](int64_t kb) {
+        const int64_t k = kb + lk;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int c = c0 + lc + u;
+            areg[u] = (k < kend && c < n) ? a[k * lda + c] : 0.0;
+        }
+    };
+    auto store_a = [&](double *dst, int64_t kb) {
+        const int64_t k = kb + lk;
+        const double s = (k < kend) ? signs[row_offset + k] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) dst[lk * BPITCH + lc + u] = s * demote<LEVEL>(areg[u], over);
+    };
+
+    double acc[WM / 8][WN / 8][2];
+#pragma unroll
+    for (int x = 0; x < WM / 8; ++x)
+#pragma unroll
+        for (int y = 0; y < WN / 8; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+
+    if (nk > 0) {
+        load_a(kbeg);
+        gen_omega(om, kbeg);
+        store_a(bt, kbeg);
+    }
+    __syncthreads();
+    for (int kt = 0; kt < nk; ++kt) {
+        const int cur = kt & 1;
+        const bool more = kt + 1 < nk;
+        const int64_t kb_next = kbeg + (int64_t)(kt + 1) * BK;
+        if (more) load_a(kb_next);
+        const double *os = om + cur * BM * APITCH;
+        const double *bs = bt + cur * BK * BPITCH;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[WM / 8], bf[WN / 8];
+#pragma unroll
+            for (int x = 0; x < WM / 8; ++x) af[x] = os[(wm * WM + x * 8 + g) * APITCH + kk + t];
+#pragma unroll
+            for (int y = 0; y < WN / 8; ++y) bf[y] = bs[(kk + t) * BPITCH + wn * WN + y * 8 + g];
+#pragma unroll
+            for (int x = 0; x < WM / 8; ++x)
+#pragma unroll
+                for (int y = 0; y < WN / 8; ++y) dmma884(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+        }
+        if (more) {
+            gen_omega(om + (cur ^ 1) * BM * APITCH, kb_next);
+            store_a(bt + (cur ^ 1) * BK * BPITCH, kb_next);
+        }
+        __syncthreads();
+    }
+    if (over) atomicOr(overflow_flag, 1);
+
+    double *out = part + ((size_t)split * ntiles + tile) * (BM * BN);
+#pragma unroll
+    for (int x = 0; x < WM / 8; ++x)
+#pragma unroll
+        for (int y = 0; y < WN / 8; ++y) {
+            const int r = wm * WM + x * 8 + g, c = wn * WN + y * 8 + 2 * t;
+            *reinterpret_cast<double2 *>(out + r * BN + c) = make_double2(acc[x][y][0], acc[x][y][1]);
+        }
+}
+
+// out (col-major d x n, ldo) (+)= sum over splits
+__global__ void sketch_reduce(const double *__restrict__ part, int splits, int ntiles, int ntn, int d, int n,
+                              double *__restrict__ out, int64_t ldo, int accumulate) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)d * n) return;
+    const int c = (int)(idx / d), i = (int)(idx % d);   // consecutive threads -> consecutive i (col-major)
+    const int tile = (i / BM) * ntn + (c / BN);
+    const double *p = part + (size_t)tile * (BM * BN) + (i % BM) * BN + (c % BN);
+    double s = 0.0;
+    for (int k = 0; k < splits; ++k) s += p[(size_t)k * ntiles * (BM * BN)];
+    double *o = out + (int64_t)c * ldo + i;
+    *o = accumulate ? *o + s : s;
+}
+
+template <int LEVEL>
+__global__ void sketch_finalize_kernel(const double *__restrict__ sum, int64_t ldsum, int d, int n,
+                                       double scale64, void *a_s, double *out_f64) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)d * n) return;
+    const int c = (int)(idx / d), i = (int)(idx % d);
+    const double v = sum[(int64_t)c * ldsum + i];
+    double promoted;
+    if (LEVEL == 16) {
+        // transform computed in binary32 then rounded to binary16 (src/sketch.py:163-165),
+        // then the binary16 product with binary16(sqrt(m_pad/d)) (src/sketch.py:168-169)
+        const __half h = __float2half_rn(__double2float_rn(v));
+        const __half s = __float2half_rn(__double2float_rn(scale64));
+        const __half o = __float2half_rn(__fmul_rn(__half2float(h), __half2float(s)));
+        static_cast<__half *>(a_s)[idx] = o;
+        promoted = (double)__half2float(o);
+    } else if (LEVEL == 32) {
+        const float o = __fmul_rn(__double2float_rn(v), __double2float_rn(scale64));
+        static_cast<float *>(a_s)[idx] = o;
+        promoted = (double)o;
+    } else {
+        const double o = __dmul_rn(v, scale64);
+        static_cast<double *>(a_s)[idx] = o;
+        promoted = o;
+    }
+    if (out_f64) out_f64[(int64_t)i * n + c] = promoted;
+}
+
+struct Plan {
+    int ntm, ntn, ntiles, splits;
+    int64_t kchunk;
+};
+static Plan make_plan(int64_t m_local, int64_t n, int64_t d) {
+    Plan p;
+    p.ntm = (int)((d + BM - 1) / BM);
+    p.ntn = (int)((n + BN - 1) / BN);
+    p.ntiles = p.ntm * p.ntn;
+    const int sms = sm_count();
+    int64_t smax = (m_local + 1023) / 1024;
+    if (smax < 1) smax = 1;
+    int64_t target = (int64_t)32 * sms / p.ntiles;
+    if (target < 1) target = 1;
+    if (target > smax) target = smax;
+    int64_t best = target;
+    for (int64_t s = target; s >= (target * 4) / 5 && s >= 1; --s)
+        if (((int64_t)p.ntiles * s) % sms == 0) { best = s; break; }
+    p.kchunk = (m_local + best - 1) / best;
+    p.kchunk = (p.kchunk + BK - 1) / BK * BK;
+    if (p.kchunk < BK) p.kchunk = BK;
+    p.splits = (int)((m_local + p.kchunk - 1) / p.kchunk);
+    if (p.splits < 1) p.splits = 1;
+    return p;
+}
+
+}  // namespace sketch
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" {
+
+size_t sk_sketch_workspace(int64_t m_local, int64_t n, int64_t d) {
+    sketch::Plan p = sketch::make_plan(m_local, n, d);
+    return (size_t)p.splits * p.ntiles * sketch::BM * sketch::BN * sizeof(double);
+}
+
+int sk_sketch_partial(int level, int transform, const double *a, int64_t lda, int64_t m_local,
+                      int64_t row_offset, int64_t m_pad, int64_t n, const double *signs,
+                      const int64_t *rows, int64_t d, double *out, int64_t ldo, int accumulate,
+                      int *overflow_flag_dev, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    if (!a || !signs || !rows || !out || !overflow_flag_dev || m_local < 0 || n <= 0 || d <= 0 ||
+        lda < n || ldo < d || m_pad <= 0 || row_offset < 0 || row_offset + m_local > m_pad ||
+        (level != 16 && level != 32 && level != 64) || (transform != SK_DCT2 && transform != SK_WHT) ||
+        m_pad >= (int64_t(1) << 30)) {
+        set_error("sk_sketch_partial: bad arguments");
+        return SK_ERR_ARG;
+    }
+    sketch::Plan p = sketch::make_plan(m_local, n, d);
+    const size_t need = (size_t)p.splits * p.ntiles * sketch::BM * sketch::BN * sizeof(double);
+    if (!ws || ws_bytes < need) {
+        set_error("sk_sketch_partial: workspace %zu < %zu", ws_bytes, need);
+        return SK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    double *part = static_cast<double *>(ws);
+    const unsigned units = (unsigned)(p.ntiles * p.splits);
+#define SK_SKETCH(L, T)                                                                            \
+    do {                                                                                           \
+        auto kfn = sketch::sketch_kernel<L, T>;                                                    \
+        SK_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sketch::SMEM)); \
+        kfn<<<units, sketch::THREADS, sketch::SMEM, st>>>(a, lda, m_local, row_offset, m_pad, (int)n, signs, \
+                                                          rows, (int)d, p.ntn, p.ntiles, p.kchunk, part,    \
+                                                          overflow_flag_dev);                      \
+    } while (0)
+    if (transform == SK_DCT2) {
+        if (level == 16) SK_SKETCH(16, SK_DCT2);
+        else if (level == 32) SK_SKETCH(32, SK_DCT2);
+        else SK_SKETCH(64, SK_DCT2);
+    } else {
+        if (level == 16) SK_SKETCH(16, SK_WHT);
+        else if (level == 32) SK_SKETCH(32, SK_WHT);
+        else SK_SKETCH(64, SK_WHT);
+    }
+#undef SK_SKETCH
+    SK_LAUNCH_CHECK("sketch_kernel");
+    const int64_t total = d * n;
+    sketch::sketch_reduce<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(part, p.splits, p.ntiles, p.ntn,
+                                                                           (int)d, (int)n, out, ldo, accumulate);
+    SK_LAUNCH_CHECK("sketch_reduce");
+    return SK_OK;
+}
+
+int sk_sketch_finalize(int level, const double *sum, int64_t ldsum, int64_t d, int64_t n, int64_t m_pad,
+                       void *a_s_level, double *out_f64, sk_stream_t stream) {
+    if (!sum || !a_s_level || d <= 0 || n <= 0 || ldsum < d || m_pad <= 0) {
+        set_error("sk_sketch_finalize: bad arguments");
+        return SK_ERR_ARG;
+    }
+    const double scale = sqrt((double)m_pad / (double)d);   // math.sqrt(op.m_pad / op.d)
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t total = d * n;
+    const unsigned grid = (unsigned)((total + 255) / 256);
+    if (level == 16) sketch::sketch_finalize_kernel<16><<<grid, 256, 0, st>>>(sum, ldsum, (int)d, (int)n, scale, a_s_level, out_f64);
+    else if (level == 32) sketch::sketch_finalize_kernel<32><<<grid, 256, 0, st>>>(sum, ldsum, (int)d, (int)n, scale, a_s_level, out_f64);
+    else if (level == 64) sketch::sketch_finalize_kernel<64><<<grid, 256, 0, st>>>(sum, ldsum, (int)d, (int)n, scale, a_s_level, out_f64);
+    else { set_error("bad level"); return SK_ERR_ARG; }
+    SK_LAUNCH_CHECK("sketch_finalize_kernel");
+    return SK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,220 @@
+// A_p = A R^{-1}: right-side, upper-triangular FP64 solve on the DMMA pipe.
+//
+// Reference: precondition_matrix src/solvers.py:205-215, which calls
+// triangular_solve(r_s, a.T, transposed=True) src/dense.py:204-242 — forward
+// substitution over the columns of A_p, x_i = (a_i - sum_{l<i} r_li x_l) / r_ii,
+// independently for every row of A.
+//
+// B200 design: row panels are independent, so each CTA owns BMR rows and walks
+// the NB-wide column blocks left to right ("left-looking"):
+//   T      = A[rows, J] - A_p[rows, <J] . R[<J, J]     (DMMA GEMM, cp.async ring)
+//   A_p[rows, J] = substitution of T against R[J, J]    (one thread per row,
+//                                                        row in registers, R_JJ in smem)
+// The panel's earlier A_p columns are re-read from L2/HBM (compute-bound:
+// ~BMR/4 flop per byte), R stays L2-resident.  A_p may alias A (in place).
+#include "common.cuh"
+
+namespace sk {
+namespace trsm {
+
+constexpr int BMR = 128, NB = 64, BK = 16, STAGES = 3, THREADS = 256;
+constexpr int WM = 32, WN = 32;             // 4 x 2 warps
+constexpr int APITCH = BK + 4;              // 20 = 4 (mod 16): conflict-free A fragments
+constexpr int BPITCH = NB + 4;              // 68 = 4 (mod 16): conflict-free B fragments
+constexpr int TPITCH = NB + 2;              // T tile, 16B-aligned rows
+constexpr size_t SMEM = sizeof(double) * (size_t(STAGES) * BMR * APITCH + size_t(STAGES) * BK * BPITCH +
+                                          size_t(BMR) * TPITCH + size_t(NB) * NB);
+
+__device__ __forceinline__ void load_stage(double *as, double *bs, const double *__restrict__ ap,
+                                           int64_t ldap, const double *__restrict__ r, int64_t ldr,
+                                           int64_t row0, int64_t m, int k0, int kend, int j0, int n,
+                                           bool vec) {
+    const int tid = threadIdx.x;
+    if (vec) {
+        // A_p panel: BMR rows x BK cols -> BMR * BK/2 chunks
+        for (int c = tid; c < BMR * (BK / 2); c += THREADS) {
+            const int rr = c / (BK / 2), kc = (c % (BK / 2)) * 2;
+            const int64_t row = row0 + rr;
+            const int k = k0 + kc;
+            int bytes = (row < m) ? (kend - k) * 8 : 0;
+            bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
+            cp_async16(as + rr * APITCH + kc, bytes ? ap + row * ldap + k : ap, bytes);
+        }
+        // R block: BK rows x NB cols
+        for (int c = tid; c < BK * (NB / 2); c += THREADS) {
+            const int kr = c / (NB / 2), jc = (c % (NB / 2)) * 2;
+            const int k = k0 + kr, j = j0 + jc;
+            int bytes = (k < kend) ? (n - j) * 8 : 0;
+            bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
+            cp_async16(bs + kr * BPITCH + jc, bytes ? r + (int64_t)k * ldr + j : r, bytes);
+        }
+    } else {
+        for (int c = tid; c < BMR * BK; c += THREADS) {
+            const int rr = c / BK, kc = c % BK;
+            const int64_t row = row0 + rr;
+            const int k = k0 + kc;
+            const int bytes = (row < m && k < kend) ? 8 : 0;
+            cp_async8(as + rr * APITCH + kc, bytes ? ap + row * ldap + k : ap, bytes);
+        }
+        for (int c = tid; c < BK * NB; c += THREADS) {
+            const int kr = c / NB, jc = c % NB;
+            const int k = k0 + kr, j = j0 + jc;
+            const int bytes = (k < kend && j < n) ? 8 : 0;
+            cp_async8(bs + kr * BPITCH + jc, bytes ? r + (int64_t)k * ldr + j : r, bytes);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__restrict__ r,
+            int64_t ldr, double *ap, int64_t ldap, bool vec) {
+    extern __shared__ __align__(16) double smem[];
+    double *as_base = smem;
+    double *bs_base = as_base + STAGES * BMR * APITCH;
+    double *ts = bs_base + STAGES * BK * BPITCH;
+    double *rjj = ts + BMR * TPITCH;
+
+    const int64_t row0 = (int64_t)blockIdx.x * BMR;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int wm = warp % (BMR / WM), wn = warp / (BMR / WM);
+    const int nblocks = (n + NB - 1) / NB;
+
+    for (int J = 0; J < nblocks; ++J) {
+        const int j0 = J * NB;
+        const int jw = min(NB, n - j0);
+        // -- stage T = A[rows, J] and R[J,J] (identity padded) into smem
+        for (int c = tid; c < BMR * NB; c += THREADS) {
+            const int rr = c / NB, jc = c % NB;
+            const int64_t row = row0 + rr;
+            ts[rr * TPITCH + jc] = (row < m && jc < jw) ? a[row * lda + j0 + jc] : 0.0;
+        }
+        for (int c = tid; c < NB * NB; c += THREADS) {
+            const int i = c / NB, j = c % NB;
+            double v;
+            if (i < jw && j < jw) v = (j >= i) ? r[(int64_t)(j0 + i) * ldr + j0 + j] : 0.0;
+            else v = (i == j) ? 1.0 : 0.0;
+            rjj[i * NB + j] = v;
+        }
+
+        // -- GEMM part: acc = A_p[rows, 0:j0] . R[0:j0, J]
+        double acc[WM / 8][WN / 8][2];
+#pragma unroll
+        for (int x = 0; x < WM / 8; ++x)
+#pragma unroll
+            for (int y = 0; y < WN / 8; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+        const int nk = (j0 + BK - 1) / BK;
+#pragma unroll
+        for (int s = 0; s < STAGES - 1; ++s) {
+            if (s < nk)
+                load_stage(as_base + s * BMR * APITCH, bs_base + s * BK * BPITCH, ap, ldap, r, ldr,
+                           row0, m, s * BK, j0, j0, n, vec);
+            cp_async_commit();
+        }
+        for (int kt = 0; kt < nk; ++kt) {
+            cp_async_wait<STAGES - 2>();
+            __syncthreads();
+            const int nxt = kt + STAGES - 1;
+            if (nxt < nk) {
+                const int s = nxt % STAGES;
+                load_stage(as_base + s * BMR * APITCH, bs_base + s * BK * BPITCH, ap, ldap, r, ldr,
+                           row0, m, nxt * BK, j0, j0, n, vec);
+            }
+            cp_async_commit();
+            const double *as = as_base + (kt % STAGES) * BMR * APITCH;
+            const double *bs = bs_base + (kt % STAGES) * BK * BPITCH;
+#pragma unroll
+            for (int kk = 0; kk < BK; kk += 4) {
+                double af[WM / 8], bf[WN / 8];
+#pragma unroll
+                for (int x = 0; x < WM / 8; ++x) af[x] = as[(wm * WM + x * 8 + g) * APITCH + kk + t];
+#pragma unroll
+                for (int y = 0; y < WN / 8; ++y) bf[y] = bs[(kk + t) * BPITCH + wn * WN + y * 8 + g];
+#pragma unroll
+                for (int x = 0; x < WM / 8; ++x)
+#pragma unroll
+                    for (int y = 0; y < WN / 8; ++y) dmma884(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+            }
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+        // -- T -= acc
+        if (nk > 0) {
+#pragma unroll
+            for (int x = 0; x < WM / 8; ++x)
+#pragma unroll
+                for (int y = 0; y < WN / 8; ++y) {
+                    const int rr = wm * WM + x * 8 + g, cc = wn * WN + y * 8 + 2 * t;
+                    ts[rr * TPITCH + cc] -= acc[x][y][0];
+                    ts[rr * TPITCH + cc + 1] -= acc[x][y][1];
+                }
+        }
+        __syncthreads();
+        // -- substitution against R[J,J]: one thread per row, the row in registers
+        if (tid < BMR) {
+            double v[NB];
+#pragma unroll
+            for (int c = 0; c < NB; ++c) v[c] = ts[tid * TPITCH + c];
+#pragma unroll
+            for (int c = 0; c < NB; ++c) {
+                v[c] = v[c] / rjj[c * NB + c];
+#pragma unroll
+                for (int c2 = c + 1; c2 < NB; ++c2) v[c2] -= v[c] * rjj[c * NB + c2];
+            }
+#pragma unroll
+            for (int c = 0; c < NB; ++c) ts[tid * TPITCH + c] = v[c];
+        }
+        __syncthreads();
+        // -- store A_p[rows, J] (coalesced)
+        for (int c = tid; c < BMR * NB; c += THREADS) {
+            const int rr = c / NB, jc = c % NB;
+            const int64_t row = row0 + rr;
+            if (row < m && jc < jw) ap[row * ldap + j0 + jc] = ts[rr * TPITCH + jc];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void first_zero_diag(const double *__restrict__ r, int64_t ldr, int n, int *out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        if (r[(int64_t)i * ldr + i] == 0.0) atomicMin(out, i);
+}
+
+}  // namespace trsm
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" int sk_trsm_right_upper_f64(const double *a, int64_t lda, int64_t m, int64_t n, const double *r,
+                                       int64_t ldr, double *ap, int64_t ldap, sk_status *status,
+                                       sk_stream_t stream) {
+    if (!a || !r || !ap || m < 0 || n <= 0 || lda < n || ldr < n || ldap < n || n > (1 << 20)) {
+        set_error("sk_trsm_right_upper_f64: bad arguments");
+        return SK_ERR_ARG;
+    }
+    if (a != ap && lda != ldap) {
+        // allowed; nothing special
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    // exactly-zero diagonal -> SingularTriangular (src/dense.py:231-233)
+    int *dflag = nullptr;
+    SK_CUDA(cudaMallocAsync(&dflag, sizeof(int), st));
+    int big = INT32_MAX, first = INT32_MAX;
+    SK_CUDA(cudaMemcpyAsync(dflag, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+    trsm::first_zero_diag<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(r, ldr, (int)n, dflag);
+    SK_CUDA(cudaMemcpyAsync(&first, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaFreeAsync(dflag, st));
+    SK_CUDA(cudaStreamSynchronize(st));
+    if (first != INT32_MAX) {
+        set_error("zero diagonal entry at index %d", first);
+        return fill_status(status, SK_SINGULAR_TRIANGULAR, first, 0.0, 0.0);
+    }
+    if (m == 0) return fill_status(status, SK_OK, -1, 0, 0);
+    const bool vec = ((reinterpret_cast<uintptr_t>(ap) | reinterpret_cast<uintptr_t>(r)) % 16 == 0) &&
+                     (ldap % 2 == 0) && (ldr % 2 == 0);
+    SK_CUDA(cudaFuncSetAttribute(trsm::trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm::SMEM));
+    const unsigned grid = (unsigned)((m + trsm::BMR - 1) / trsm::BMR);
+    trsm::trsm_kernel<<<grid, trsm::THREADS, trsm::SMEM, st>>>(a, lda, m, (int)n, r, ldr, ap, ldap, vec);
+    SK_LAUNCH_CHECK("trsm_kernel");
+    return fill_status(status, SK_OK, -1, 0, 0);
+}

@@ -1,0 +1,256 @@
+"""Dense kernels on the device, mirroring src/dense.py of the reference.
+
+Public functions keep the reference names and argument conventions
+(`triangular_solve`, `lu_solve`, `cholesky_solve`, `cholesky_factor`,
+`householder_qr`, `householder_reduce`, `jacobi_singular_values`,
+`condition_diagnostics`, `hager_one_norm_inverse_estimate`) and accept numpy
+arrays or torch tensors.  Underscored helpers take validated device matrices and
+are what the solvers call, so a pipeline never leaves the GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import WORKSPACE, DMat, as_dmat, as_dvec, call, device, like_input, stream_handle, to_host
+from .errors import DimensionMismatch, RankDeficient
+
+
+@dataclass(frozen=True)
+class QRFactors:
+    """Thin QR factors (src/dense.py:29-34).  The device QR forms R only (the
+    solve path never needs Q); q is None unless explicitly requested."""
+
+    q: np.ndarray | None
+    r: np.ndarray
+
+
+@dataclass(frozen=True)
+class ConditionDiagnostics:
+    """Spectral summary (src/dense.py:37-54)."""
+
+    two_norm: float
+    two_norm_condition: float
+    singular_values: np.ndarray
+
+
+# --------------------------------------------------------------- device ops --
+def _gram(x: DMat | torch.Tensor, y: DMat | torch.Tensor | None = None, out: torch.Tensor | None = None,
+          accumulate: bool = False) -> torch.Tensor:
+    """G = X^T Y (SYRK when y is None or y is x) on the DMMA pipe."""
+    xt = x.t if isinstance(x, DMat) else x
+    yt = xt if y is None else (y.t if isinstance(y, DMat) else y)
+    m, n = xt.shape
+    if yt.shape != xt.shape:
+        raise DimensionMismatch(f"gram operands {tuple(xt.shape)} vs {tuple(yt.shape)}")
+    if out is None:
+        out = torch.empty((n, n), dtype=torch.float64, device=xt.device)
+    lib = _lib.lib()
+    wsb = lib.sk_gram_workspace(m, n)
+    wp, wn = WORKSPACE.get(wsb)
+    call("sk_gram_f64", xt.data_ptr(), xt.stride(0), yt.data_ptr(), yt.stride(0), m, n,
+         out.data_ptr(), out.stride(0), int(accumulate), wp, wn, stream_handle())
+    return out
+
+
+def _gemv_t(x: DMat | torch.Tensor, v: torch.Tensor, out: torch.Tensor | None = None,
+            accumulate: bool = False) -> torch.Tensor:
+    """out = X^T v (memory-bound)."""
+    xt = x.t if isinstance(x, DMat) else x
+    m, n = xt.shape
+    if out is None:
+        out = torch.empty(n, dtype=torch.float64, device=xt.device)
+    lib = _lib.lib()
+    wp, wn = WORKSPACE.get(lib.sk_gemv_t_workspace(m, n))
+    call("sk_gemv_t_f64", xt.data_ptr(), xt.stride(0), m, n, v.data_ptr(), out.data_ptr(),
+         int(accumulate), wp, wn, stream_handle())
+    return out
+
+
+def _trsm(a: DMat | torch.Tensor, r: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """A_p = A R^{-1} (R upper, device f64)."""
+    at = a.t if isinstance(a, DMat) else a
+    m, n = at.shape
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float64, device=at.device)
+    st = _lib.SkStatus()
+    call("sk_trsm_right_upper_f64", at.data_ptr(), at.stride(0), m, n, r.data_ptr(), r.stride(0),
+         out.data_ptr(), out.stride(0), C.byref(st), stream_handle())
+    return out
+
+
+def _trsv(r: torch.Tensor, rhs: torch.Tensor, transposed: bool = False) -> torch.Tensor:
+    n = r.shape[0]
+    out = torch.empty(n, dtype=torch.float64, device=r.device)
+    wp, wn = WORKSPACE.get(2 * 8 * n + 1024)
+    st = _lib.SkStatus()
+    call("sk_trsv_f64", r.data_ptr(), r.stride(0), n, int(transposed), rhs.data_ptr(), out.data_ptr(),
+         C.byref(st), wp, wn, stream_handle())
+    return out
+
+
+def _chol_solve(s: torch.Tensor, rhs: torch.Tensor) -> torch.Tensor:
+    n = s.shape[0]
+    out = torch.empty(n, dtype=torch.float64, device=s.device)
+    wp, wn = WORKSPACE.get(_lib.lib().sk_nxn_workspace(n))
+    st = _lib.SkStatus()
+    call("sk_chol_solve_f64", s.data_ptr(), n, rhs.data_ptr(), out.data_ptr(), C.byref(st), wp, wn,
+         stream_handle())
+    return out
+
+
+def _lu_solve(g: torch.Tensor, rhs: torch.Tensor) -> torch.Tensor:
+    n = g.shape[0]
+    out = torch.empty(n, dtype=torch.float64, device=g.device)
+    wp, wn = WORKSPACE.get(_lib.lib().sk_nxn_workspace(n))
+    st = _lib.SkStatus()
+    call("sk_lu_solve_f64", g.data_ptr(), n, rhs.data_ptr(), out.data_ptr(), C.byref(st), wp, wn,
+         stream_handle())
+    return out
+
+
+def _qr_r(a_s_level: torch.Tensor, level_code: int, d: int, n: int) -> torch.Tensor:
+    """R of a column-major d x n level-dtype buffer (overwritten)."""
+    r = torch.empty((n, n), dtype=torch.float64, device=a_s_level.device)
+    wp, wn = WORKSPACE.get(_lib.lib().sk_qr_workspace(level_code, d, n))
+    st = _lib.SkStatus()
+    call("sk_qr_r", level_code, a_s_level.data_ptr(), d, n, r.data_ptr(), r.stride(0), C.byref(st), wp, wn,
+         stream_handle())
+    return r
+
+
+def _householder_r64(at: torch.Tensor) -> torch.Tensor:
+    """householder_reduce(a)[2] for a device f64 row-major m x n (m >= n)."""
+    m, n = at.shape
+    if m < n:
+        raise DimensionMismatch(f"need rows >= cols, got {m} x {n}")
+    colmajor = at.t().contiguous()          # n x m row-major == m x n column-major
+    return _qr_r(colmajor, 64, m, n)
+
+
+def _jacobi_sv(at: torch.Tensor, max_sweeps: int = 30, tol: float = 1e-14) -> np.ndarray:
+    rows, n = at.shape
+    sv = (C.c_double * n)()
+    wp, wn = WORKSPACE.get(_lib.lib().sk_jacobi_workspace(rows, n))
+    call("sk_jacobi_sv_f64", at.data_ptr(), rows, n, at.stride(0), int(max_sweeps), float(tol), sv, wp, wn,
+         stream_handle())
+    return np.array(sv[:], dtype=np.float64)
+
+
+def _diagnostics_dev(at: torch.Tensor) -> ConditionDiagnostics:
+    """condition_diagnostics on a device matrix (src/dense.py:418-448)."""
+    if at.shape[0] < at.shape[1]:
+        at = at.t().contiguous()
+    m, n = at.shape
+    w = at
+    if m > n:
+        try:
+            w = _householder_r64(at)
+        except RankDeficient:
+            w = at
+    sv = _jacobi_sv(w)
+    cond = float(sv[0] / sv[-1]) if sv[-1] > 0 else float("inf")
+    return ConditionDiagnostics(two_norm=float(sv[0]), two_norm_condition=cond, singular_values=sv)
+
+
+# ----------------------------------------------------------------- public ---
+def _square_dev(a, name):
+    d = as_dmat(a, name)
+    if d.shape[0] != d.shape[1]:
+        raise ValueError(f"{name} must be square, got shape {d.shape}")
+    return d
+
+
+def triangular_solve(r, rhs, transposed=False):
+    """Solve r x = rhs (or r^T x = rhs): src/dense.py:204-242."""
+    rd = as_dmat(r, "r") if not isinstance(r, np.ndarray) or r.ndim == 2 else None
+    if rd is None or rd.shape[0] != rd.shape[1]:
+        raise ValueError(f"r must be square, got shape {np.shape(r)}")
+    n = rd.shape[0]
+    rhs_np = rhs.detach().cpu().numpy() if isinstance(rhs, torch.Tensor) else np.asarray(rhs)
+    if rhs_np.shape[0] != n:
+        raise DimensionMismatch(f"rhs length {rhs_np.shape[0]} != n = {n}")
+    cols = [rhs_np] if rhs_np.ndim == 1 else [rhs_np[:, k] for k in range(rhs_np.shape[1])]
+    outs = [to_host(_trsv(rd.t, as_dvec(c), transposed)) for c in cols]
+    x = outs[0] if rhs_np.ndim == 1 else np.stack(outs, axis=1)
+    return like_input(torch.from_numpy(x), "numpy" if not isinstance(rhs, torch.Tensor) else "torch")
+
+
+def lu_solve(a, rhs):
+    """LU with partial pivoting: src/dense.py:245-286."""
+    ad = _square_dev(a, "a")
+    n = ad.shape[0]
+    rhs_np = np.asarray(rhs.detach().cpu() if isinstance(rhs, torch.Tensor) else rhs)
+    if rhs_np.shape[0] != n:
+        raise DimensionMismatch(f"rhs length {rhs_np.shape[0]} != n = {n}")
+    cols = [rhs_np] if rhs_np.ndim == 1 else [rhs_np[:, k] for k in range(rhs_np.shape[1])]
+    outs = [to_host(_lu_solve(ad.t, as_dvec(c))) for c in cols]
+    return outs[0] if rhs_np.ndim == 1 else np.stack(outs, axis=1)
+
+
+def cholesky_solve(s, rhs):
+    """SPD solve with the 10-eps symmetry gate: src/dense.py:314-342."""
+    sd = _square_dev(s, "s")
+    n = sd.shape[0]
+    rhs_np = np.asarray(rhs.detach().cpu() if isinstance(rhs, torch.Tensor) else rhs)
+    if rhs_np.shape[0] != n:
+        raise DimensionMismatch(f"rhs length {rhs_np.shape[0]} != n = {n}")
+    cols = [rhs_np] if rhs_np.ndim == 1 else [rhs_np[:, k] for k in range(rhs_np.shape[1])]
+    outs = [to_host(_chol_solve(sd.t, as_dvec(c))) for c in cols]
+    return outs[0] if rhs_np.ndim == 1 else np.stack(outs, axis=1)
+
+
+def householder_reduce(a):
+    """R factor of a tall matrix (src/dense.py:108-161); reflectors are not
+    materialised on the host: returns (None, None, R)."""
+    ad = as_dmat(a)
+    return None, None, to_host(_householder_r64(ad.t))
+
+
+def householder_qr(a):
+    """Thin QR (src/dense.py:175-201).  R on the device; Q formed on request as
+    Q = A R^{-1} only for API completeness (the solvers never need it)."""
+    ad = as_dmat(a)
+    m, n = ad.shape
+    if m < n:
+        raise DimensionMismatch(f"need rows >= cols, got {m} x {n}")
+    r = _householder_r64(ad.t)
+    q = _trsm(ad, r)
+    return QRFactors(q=to_host(q), r=to_host(r))
+
+
+def jacobi_singular_values(a, max_sweeps=30, tol=1e-14):
+    """One-sided Jacobi singular values: src/dense.py:365-415."""
+    ad = as_dmat(a)
+    return _jacobi_sv(ad.t, max_sweeps, tol)
+
+
+def condition_diagnostics(a):
+    """src/dense.py:418-448."""
+    return _diagnostics_dev(as_dmat(a).t)
+
+
+def hager_one_norm_inverse_estimate(solve, n):
+    """Hager's estimator around a caller-supplied solve (src/dense.py:451-480).
+    The callable is the caller's; the pipeline's own estimate runs entirely on
+    the device inside sk_kappa0_from_gram."""
+    if n < 1:
+        raise ValueError(f"n must be >= 1, got {n}")
+    x = np.full(n, 1.0 / n)
+    best = 0.0
+    for _ in range(5):
+        y = np.asarray(solve(x, False), dtype=np.float64)
+        best = max(best, float(np.abs(y).sum()))
+        z = np.asarray(solve(np.where(y >= 0, 1.0, -1.0), True), dtype=np.float64)
+        j = int(np.argmax(np.abs(z)))
+        if abs(z[j]) <= float(z @ x):
+            break
+        x = np.zeros(n)
+        x[j] = 1.0
+    return best

@@ -1,0 +1,367 @@
+"""Least-squares solvers: PNE / HPNE / NE / SNE / NNE / QR and Algorithm 1.
+
+Same entry points, signatures, dataclasses and error behaviour as the reference
+(src/solvers.py).  Every m x n pass runs in libsklsq on the device:
+
+  check      sk_cast_stats                (validation + f64 + ||A||_F^2, one pass)
+  kappa0     sk_gram_f64 (SYRK) + sk_kappa0_from_gram
+  sketch     sk_sketch_partial/finalize   (on-the-fly SRTT operator, level demotion fused)
+  level QR   sk_qr_r                      (binary16 op-for-op emulation)
+  A_p        sk_trsm_right_upper_f64      (DMMA)
+  Gram       sk_gram_f64 (SYRK for PNE, GEMM-TN for HPNE/NNE) + sk_gemv_t_f64
+  n x n      sk_chol_solve_f64 / sk_lu_solve_f64 / sk_trsv_f64
+  report     sk_residual
+
+Inputs may be numpy arrays (the reference's convention) or torch tensors (CPU
+or CUDA; a CUDA tensor avoids the host->device copy).  x_hat is returned as a
+numpy array like the reference; A_p from precondition_matrix follows the input
+kind (numpy in -> numpy out, torch in -> CUDA tensor out).
+
+Diagnostics: the reference always fills Preconditioner.kappa_rs / kappa_ap with
+one-sided Jacobi (src/solvers.py:200, :214).  Here they run on the device too
+(sk_jacobi_sv_f64; kappa_ap via the R factor of A_p) and are on by default for
+API parity; pass diagnostics=False to skip them (they are not part of
+Algorithm 1 and are excluded from the bench's solve time).  With
+strict_diagnostics=False (default) a Jacobi NoConvergence is recorded as NaN
+instead of aborting the solve; strict_diagnostics=True raises
+like the reference.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .dense import (_chol_solve, _diagnostics_dev, _gemv_t, _gram, _householder_r64, _lu_solve, _trsm, _trsv)
+from .device import DMat, as_dmat, as_dvec, call, like_input, stream_handle, to_host, WORKSPACE
+from .errors import DimensionMismatch, NoConvergence, NotPositiveDefinite, RankDeficient
+from .precision import (BINARY64, PrecisionDecision, PrecisionLevel, _decide_dev, _qr_level_dev,
+                        level_from_name, next_higher)
+from .sketch import DCT2, DeviceSketch, _apply_dev, make_sketch
+from . import _lib
+
+import ctypes as C
+
+
+@dataclass
+class Preconditioner:
+    """src/solvers.py:47-59.  r_s is the promoted binary64 factor (numpy)."""
+
+    r_s: np.ndarray
+    computed_in: PrecisionLevel
+    kappa_rs: float
+    kappa_ap: float | None = None
+    sketch_descriptor: dict | None = None
+    _r_dev: torch.Tensor | None = field(default=None, repr=False, compare=False)
+
+    def r_device(self) -> torch.Tensor:
+        if self._r_dev is None or self._r_dev.device != torch.device("cuda", torch.cuda.current_device()):
+            self._r_dev = torch.from_numpy(np.ascontiguousarray(self.r_s, dtype=np.float64)).cuda()
+        return self._r_dev
+
+
+@dataclass
+class SolveReport:
+    """src/solvers.py:62-84 (+ stage_ms: per-stage device times, ours)."""
+
+    method: str
+    x_hat: np.ndarray
+    residual_norm: float
+    relative_residual: float
+    relative_error: float | None
+    wall_ms: float
+    preconditioner: Preconditioner | None = None
+    bounds: dict = field(default_factory=dict)
+    norm_is_frobenius: bool = True
+    precision_decision: PrecisionDecision | None = None
+    escalated_from: PrecisionLevel | None = None
+    stage_ms: dict = field(default_factory=dict)
+
+
+# ------------------------------------------------------------------ helpers --
+class _Stages:
+    """CUDA-event stage timer on the current stream (no host sync until read)."""
+
+    def __init__(self, enabled=True):
+        self.enabled = enabled
+        self.marks = []
+
+    def mark(self, name):
+        if self.enabled:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.marks.append((name, ev))
+
+    def result(self):
+        out = {}
+        if len(self.marks) < 2:
+            return out
+        self.marks[-1][1].synchronize()
+        for (name, e0), (_, e1) in zip(self.marks[:-1], self.marks[1:]):
+            out[name] = out.get(name, 0.0) + e0.elapsed_time(e1)
+        return out
+
+
+def _check_system(a, b):
+    """src/solvers.py:87-96 on the device."""
+    ad = as_dmat(a)
+    m, n = ad.shape
+    if isinstance(b, torch.Tensor):
+        if b.dim() != 1:
+            raise ValueError(f"b must be 1-D, got ndim={b.dim()}")
+    else:
+        bn = np.asarray(b, dtype=np.float64)
+        if bn.ndim != 1:
+            raise ValueError(f"b must be 1-D, got ndim={bn.ndim}")
+    if m < n:
+        raise DimensionMismatch(f"need rows >= cols, got {ad.shape}")
+    bd = b if isinstance(b, torch.Tensor) and b.is_cuda and b.dtype == torch.float64 else None
+    if bd is None:
+        bd = as_dvec(b)
+    if bd.shape[0] != m:
+        raise DimensionMismatch(f"b length {bd.shape[0]} != rows {m}")
+    return ad, bd.contiguous()
+
+
+def _report(method, ad: DMat, bd, x_dev, t0, x_star=None, preconditioner=None, stages=None):
+    """src/solvers.py:99-117: residual on the device, norms, relative error."""
+    m, n = ad.shape
+    out = (C.c_double * 2)()
+    wp, wn = WORKSPACE.get(_lib.lib().sk_matrix_stats_workspace(m, n))
+    call("sk_residual", ad.ptr, m, n, ad.ld, x_dev.data_ptr(), bd.data_ptr(), None, out, wp, wn,
+         stream_handle())
+    if stages is not None:
+        stages.mark("end")
+    x_hat = to_host(x_dev)
+    residual_norm = float(math.sqrt(out[0]))
+    denom = float(math.sqrt(ad.frob2)) * float(math.sqrt(out[1]))
+    relative_residual = residual_norm / denom if denom > 0 else math.inf
+    relative_error = None
+    if x_star is not None:
+        xs = np.asarray(x_star.detach().cpu() if isinstance(x_star, torch.Tensor) else x_star, dtype=np.float64)
+        relative_error = float(np.linalg.norm(x_hat - xs) / np.linalg.norm(xs))
+    return SolveReport(method=method, x_hat=x_hat, residual_norm=residual_norm,
+                       relative_residual=relative_residual, relative_error=relative_error,
+                       wall_ms=(time.perf_counter() - t0) * 1e3, preconditioner=preconditioner,
+                       stage_ms=stages.result() if stages is not None else {})
+
+
+def _kappa(at: torch.Tensor, strict: bool) -> float:
+    try:
+        return _diagnostics_dev(at).two_norm_condition
+    except NoConvergence:
+        if strict:
+            raise
+        return math.nan
+
+
+# ---------------------------------------------------------- baseline solvers --
+def solve_qr_baseline(a, b, x_star=None):
+    """src/solvers.py:120-126: Householder QR, x = R^{-1} Q^T b.  Q^T b is read
+    off the last column of the R factor of [A | b] (the same reflectors applied
+    to b), so Q is never formed."""
+    ad, bd = _check_system(a, b)
+    t0 = time.perf_counter()
+    m, n = ad.shape
+    aug = torch.cat([ad.t, bd[:, None]], dim=1)
+    if m == n:   # a zero row leaves R and Q^T b unchanged and makes room for column n
+        aug = torch.cat([aug, torch.zeros((1, n + 1), dtype=aug.dtype, device=aug.device)], dim=0)
+    r_aug = _householder_r64(aug)
+    r = r_aug[:n, :n].contiguous()
+    qtb = r_aug[:n, n].contiguous()
+    x = _trsv(r, qtb)
+    return _report("qr", ad, bd, x, t0, x_star)
+
+
+def solve_normal(a, b, x_star=None):
+    """src/solvers.py:129-138: Cholesky of A^T A, no fallback."""
+    ad, bd = _check_system(a, b)
+    t0 = time.perf_counter()
+    x = _chol_solve(_gram(ad), _gemv_t(ad, bd))
+    return _report("ne", ad, bd, x, t0, x_star)
+
+
+def solve_seminormal(a, b, x_star=None):
+    """src/solvers.py:141-148: R of A, then R^T y = A^T b, R x = y."""
+    ad, bd = _check_system(a, b)
+    t0 = time.perf_counter()
+    r = _householder_r64(ad.t)
+    y = _trsv(r, _gemv_t(ad, bd), transposed=True)
+    x = _trsv(r, y)
+    return _report("sne", ad, bd, x, t0, x_star)
+
+
+def solve_notnormal(a, b_matrix, b, x_star=None):
+    """src/solvers.py:151-165: LU of B^T A."""
+    ad, bd = _check_system(a, b)
+    bm = as_dmat(b_matrix, "b_matrix")
+    if bm.shape != ad.shape:
+        raise DimensionMismatch(f"b_matrix shape {bm.shape} != a shape {ad.shape}")
+    t0 = time.perf_counter()
+    x = _lu_solve(_gram(bm, ad), _gemv_t(bm, bd))
+    return _report("nne", ad, bd, x, t0, x_star)
+
+
+# ------------------------------------------------------------ preconditioner --
+def _build_dev(ad: DMat, d_factor, transform, level, seed, diagnostics=True, strict=False, stages=None):
+    m, n = ad.shape
+    if m < n:
+        raise DimensionMismatch(f"need rows >= cols, got {m} x {n}")
+    d = int(math.ceil(d_factor * n))
+    if d < n:
+        raise ValueError(f"d_factor {d_factor} gives d={d} < n={n}")
+    op = make_sketch(m, d, transform, seed)
+    if stages is not None:
+        stages.mark("sketch")
+    a_s, _ = _apply_dev(op, ad, level)          # Overflow on demotion (src/solvers.py:191-193)
+    if stages is not None:
+        stages.mark("level_qr")
+    r_s = _qr_level_dev(a_s, level, d, n)       # RankDeficient / Overflow
+    if bool((torch.diagonal(r_s) == 0).any().item()):
+        raise RankDeficient("sketched factor has a zero diagonal entry")
+    if stages is not None:
+        stages.mark("diag_rs")
+    kappa_rs = _kappa(r_s, strict) if diagnostics else math.nan
+    pre = Preconditioner(r_s=to_host(r_s), computed_in=level, kappa_rs=kappa_rs,
+                         sketch_descriptor=op.descriptor(), _r_dev=r_s)
+    return pre
+
+
+def build_preconditioner(a, d_factor=3.0, transform=DCT2, level=BINARY64, seed=0, *, diagnostics=True,
+                         strict_diagnostics=False):
+    """src/solvers.py:168-202."""
+    return _build_dev(as_dmat(a), d_factor, transform, level, seed, diagnostics, strict_diagnostics)
+
+
+def _precondition_dev(ad: DMat, pre: Preconditioner, diagnostics=True, strict=False, stages=None,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+    r = pre.r_device()
+    if r.shape[0] != ad.shape[1]:
+        raise DimensionMismatch(f"r_s is {tuple(r.shape)} but A has {ad.shape[1]} columns")
+    if stages is not None:
+        stages.mark("trsm")
+    a_p = _trsm(ad, r, out=out)                 # SingularTriangular on a zero diagonal
+    if stages is not None:
+        stages.mark("diag_ap")
+    pre.kappa_ap = _kappa(a_p, strict) if diagnostics else math.nan
+    return a_p
+
+
+def precondition_matrix(a, pre, *, diagnostics=True, strict_diagnostics=False):
+    """src/solvers.py:205-215: A_p = A R_s^{-1}; sets pre.kappa_ap."""
+    ad = as_dmat(a)
+    return like_input(_precondition_dev(ad, pre, diagnostics, strict_diagnostics), ad.kind)
+
+
+def _prepare_dev(ad, d_factor, transform, level, seed, diagnostics=True, strict=False, stages=None):
+    escalated_from = None
+    while True:
+        try:
+            pre = _build_dev(ad, d_factor, transform, level, seed, diagnostics, strict, stages)
+            a_p = _precondition_dev(ad, pre, diagnostics, strict, stages)
+            return pre, a_p, escalated_from
+        except RankDeficient:
+            wider = next_higher(level)
+            if escalated_from is not None or wider is None:
+                raise
+            escalated_from = level
+            level = wider
+
+
+def prepare_preconditioner(a, d_factor=3.0, transform=DCT2, level=BINARY64, seed=0, *, diagnostics=True,
+                           strict_diagnostics=False):
+    """src/solvers.py:255-279: one escalation on RankDeficient."""
+    ad = as_dmat(a)
+    pre, a_p, esc = _prepare_dev(ad, d_factor, transform, level, seed, diagnostics, strict_diagnostics)
+    return pre, like_input(a_p, ad.kind), esc
+
+
+# -------------------------------------------------------------- PNE / HPNE ---
+def _a_p_dev(a_p, ad: DMat) -> torch.Tensor:
+    if isinstance(a_p, torch.Tensor) and a_p.is_cuda and a_p.dtype == torch.float64 and a_p.is_contiguous():
+        t = a_p
+    else:
+        t = as_dmat(a_p, "a_p").t
+    if tuple(t.shape) != ad.shape:
+        raise DimensionMismatch(f"a_p shape {tuple(t.shape)} != a shape {ad.shape}")
+    return t
+
+
+def _pne_dev(ad, bd, pre, a_p, stages=None):
+    if stages is not None:
+        stages.mark("gram")
+    g = _gram(a_p)
+    rhs = _gemv_t(a_p, bd)
+    if stages is not None:
+        stages.mark("nxn")
+    try:
+        y = _chol_solve(g, rhs)
+    except NotPositiveDefinite:
+        y = _lu_solve(g, rhs)
+    return _trsv(pre.r_device(), y)
+
+
+def _hpne_dev(ad, bd, pre, a_p, stages=None):
+    if stages is not None:
+        stages.mark("gram")
+    g = _gram(a_p, ad)
+    rhs = _gemv_t(a_p, bd)
+    if stages is not None:
+        stages.mark("nxn")
+    return _lu_solve(g, rhs)
+
+
+def solve_pne(a, b, pre, x_star=None, a_p=None, *, diagnostics=True, strict_diagnostics=False):
+    """src/solvers.py:218-237: Cholesky of A_p^T A_p (LU fallback), x = R_s^{-1} y."""
+    ad, bd = _check_system(a, b)
+    t0 = time.perf_counter()
+    ap = _precondition_dev(ad, pre, diagnostics, strict_diagnostics) if a_p is None else _a_p_dev(a_p, ad)
+    x = _pne_dev(ad, bd, pre, ap)
+    return _report("pne", ad, bd, x, t0, x_star, preconditioner=pre)
+
+
+def solve_hpne(a, b, pre, x_star=None, a_p=None, *, diagnostics=True, strict_diagnostics=False):
+    """src/solvers.py:240-252: LU of A_p^T A."""
+    ad, bd = _check_system(a, b)
+    t0 = time.perf_counter()
+    ap = _precondition_dev(ad, pre, diagnostics, strict_diagnostics) if a_p is None else _a_p_dev(a_p, ad)
+    x = _hpne_dev(ad, bd, pre, ap)
+    return _report("hpne", ad, bd, x, t0, x_star, preconditioner=pre)
+
+
+def algorithm1_pipeline(a, b, method="pne", precision="auto", d_factor=3.0, transform=DCT2, seed=0,
+                        x_star=None, *, diagnostics=True, strict_diagnostics=False, stage_timing=False):
+    """Algorithm 1 end to end (src/solvers.py:282-324), entirely on the device.
+
+    Extra keyword-only options (not in the reference): diagnostics,
+    strict_diagnostics (see module docstring) and stage_timing (fills
+    SolveReport.stage_ms with CUDA-event times per stage).
+    """
+    stages = _Stages(stage_timing)
+    stages.mark("check")
+    ad, bd = _check_system(a, b)
+    if method not in ("pne", "hpne"):
+        raise ValueError(f"pipeline method must be pne or hpne, got {method!r}")
+    t0 = time.perf_counter()
+    decision = None
+    if isinstance(precision, PrecisionLevel):
+        level = precision
+    elif precision == "auto":
+        stages.mark("kappa0")
+        decision = _decide_dev(ad)
+        level = decision.selected
+    else:
+        level = level_from_name(precision)
+    pre, a_p, escalated_from = _prepare_dev(ad, d_factor, transform, level, seed, diagnostics,
+                                            strict_diagnostics, stages)
+    x = (_pne_dev if method == "pne" else _hpne_dev)(ad, bd, pre, a_p, stages)
+    stages.mark("report")
+    report = _report(method, ad, bd, x, t0, x_star, preconditioner=pre, stages=stages)
+    report.precision_decision = decision
+    report.escalated_from = escalated_from
+    report.wall_ms = (time.perf_counter() - t0) * 1e3
+    return report

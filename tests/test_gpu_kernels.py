@@ -1,0 +1,220 @@
+"""GPU parity of the individual libsklsq kernels against the oracle and the
+reference's golden vectors (tolerances stated per test)."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import restatement as R
+from tests.golden_data import ARR, META, problem
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sq():
+    import paper_2603_16644_b200 as mod
+    return mod
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    return t
+
+
+def rel(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300))
+
+
+# ---------------------------------------------------------------- Gram -------
+@pytest.mark.parametrize("m,n", [(7, 3), (300, 20), (1000, 100), (4099, 130), (20000, 257)])
+def test_gram_syrk_and_gemm(sq, torch, m, n):
+    from paper_2603_16644_b200.dense import _gram, _gemv_t
+    g = R.philox(m * 7 + n, 3)
+    x = g.standard_normal((m, n))
+    y = g.standard_normal((m, n))
+    xt = torch.from_numpy(x).cuda()
+    yt = torch.from_numpy(y).cuda()
+    gs = _gram(xt).cpu().numpy()
+    assert np.array_equal(gs, gs.T)                     # exactly symmetric (SYRK mirror)
+    assert rel(gs, x.T @ x) <= 1e-13                    # FP64: summation-order differences only
+    gg = _gram(xt, yt).cpu().numpy()
+    assert rel(gg, x.T @ y) <= 1e-13
+    v = g.standard_normal(m)
+    gv = _gemv_t(xt, torch.from_numpy(v).cuda()).cpu().numpy()
+    assert rel(gv, x.T @ v) <= 1e-13
+
+
+def test_gram_odd_leading_dimension(sq, torch):
+    from paper_2603_16644_b200.dense import _gram
+    big = torch.randn(500, 41, dtype=torch.float64, device="cuda")
+    sub = big[:, :37]                                   # ld = 41 (odd) -> 8-byte cp.async path
+    ref = sub.cpu().numpy()
+    out = _gram(sub).cpu().numpy()
+    assert rel(out, ref.T @ ref) <= 1e-13
+
+
+# ---------------------------------------------------------------- TRSM -------
+@pytest.mark.parametrize("m,n,kappa", [(300, 24, 1e2), (1000, 100, 1e6), (5000, 130, 1e3), (777, 64, 1e8)])
+def test_trsm_matches_substitution(sq, torch, m, n, kappa):
+    from paper_2603_16644_b200.dense import _trsm
+    from oracle.problems import planted_triangle
+    r = planted_triangle(n, kappa, seed=m)
+    a = R.philox(m, 3).standard_normal((m, n))
+    ref = np.ascontiguousarray(R.tri_solve(r, a.T, transposed=True).T)
+    got = _trsm(torch.from_numpy(a).cuda(), torch.from_numpy(r).cuda()).cpu().numpy()
+    # forward error of a backward-stable substitution scales with kappa(R) u
+    assert rel(got, ref) <= 50 * kappa * 2.0 ** -52
+
+
+def test_trsm_identity_is_exact_and_singular_raises(sq, torch):
+    from paper_2603_16644_b200.dense import _trsm
+    a = R.philox(1, 3).standard_normal((257, 70))
+    got = _trsm(torch.from_numpy(a).cuda(), torch.eye(70, dtype=torch.float64, device="cuda")).cpu().numpy()
+    assert np.array_equal(got, a)
+    r = np.eye(70)
+    r[33, 33] = 0.0
+    with pytest.raises(sq.SingularTriangular):
+        _trsm(torch.from_numpy(a).cuda(), torch.from_numpy(r).cuda())
+
+
+# -------------------------------------------------------------- sketch -------
+@pytest.mark.parametrize("case", [("p600_k1e2", "dct2", 120), ("p300_k10_s5", "wht", 60),
+                                  ("p300_k10_s5", "dct2", 60)])
+def test_apply_sketch_vs_reference(sq, case):
+    name, transform, d = case
+    p = problem(name)
+    op = sq.make_sketch(p.a.shape[0], d, transform, seed=17)
+    key = f"sketch/{name}/{transform}"
+    assert np.array_equal(op.signs, ARR[key + "/signs"]) and np.array_equal(op.sampled_rows, ARR[key + "/rows"])
+    for level, tol in (("binary64", 1e-13), ("binary32", 2e-6), ("binary16", 3e-3)):
+        data = p.a.astype(R.LEVEL_DTYPE[level])
+        got = sq.apply_sketch(op, data)
+        ref = ARR[f"{key}/{level}/a_s"]
+        assert got.dtype == ref.dtype
+        # reference: pocketfft transform in the working precision; ours: exact
+        # sampled transform rounded once.  Agreement to the level's roundoff.
+        assert rel(got, ref) <= tol, level
+
+
+# ----------------------------------------------------------- level QR --------
+@pytest.mark.parametrize("case", [("p600_k1e2", "dct2"), ("p300_k10_s5", "wht"), ("p300_k10_s5", "dct2")])
+def test_level_qr_on_reference_sketch(sq, case):
+    name, transform = case
+    key = f"sketch/{name}/{transform}"
+    for level in ("binary16", "binary32", "binary64"):
+        a_s = ARR[f"{key}/{level}/a_s"]
+        ref_r = ARR[f"{key}/{level}/r"]
+        got = sq.qr_in_precision(a_s, sq.level_from_name(level)).r
+        if level == "binary16":
+            # op-for-op binary16 emulation: bitwise the reference
+            assert np.array_equal(got, ref_r)
+        elif level == "binary32":
+            assert rel(got, ref_r) <= 1e-5
+        else:
+            assert rel(got, ref_r) <= 1e-12
+        assert np.all(np.tril(got, -1) == 0.0)
+
+
+def test_binary16_qr_collapse_matches_reference(sq):
+    # kappa = 1e6 sketch at binary16: the reference raises RankDeficient (tau overflow)
+    p = problem("p600_k1e6_s6")
+    op = R.draw_sketch(600, 120, "dct2", seed=6)
+    a16, _ = R.demote(p.a, "binary16")
+    a_s = R.sketch_apply(op, a16)
+    with pytest.raises(R.RankDeficient):
+        R.qr_at_level(a_s, "binary16")
+    with pytest.raises(sq.RankDeficient):
+        sq.qr_in_precision(a_s, sq.BINARY16)
+
+
+def test_qr_sign_convention(sq):
+    r = sq.qr_in_precision(np.array([[3.0, 1.0], [4.0, 2.0]]), sq.BINARY64).r
+    assert r[0, 0] == pytest.approx(-5.0, rel=1e-15)
+    r = sq.qr_in_precision(np.array([[-3.0, 1.0], [4.0, 2.0]]), sq.BINARY64).r
+    assert r[0, 0] == pytest.approx(5.0, rel=1e-15)
+    with pytest.raises(sq.RankDeficient):
+        sq.qr_in_precision(np.zeros((4, 2)), sq.BINARY64)
+    with pytest.raises(sq.RankDeficient):
+        sq.qr_in_precision(np.array([[1.0, 0.0], [1.0, 0.0], [1.0, 0.0]]), sq.BINARY64)
+
+
+# --------------------------------------------------------------- n x n -------
+def test_known_answers(sq):
+    r2 = np.array([[2.0, 1.0], [0.0, 4.0]])
+    assert np.array_equal(sq.triangular_solve(r2, np.array([5.0, 8.0])), ARR["ka/trsv"])
+    assert np.array_equal(sq.triangular_solve(r2, np.array([2.0, 9.0]), transposed=True), ARR["ka/trsv_t"])
+    perm = np.array([[0.0, 1.0, 0.0], [0.0, 0.0, 1.0], [1.0, 0.0, 0.0]])
+    assert np.array_equal(sq.lu_solve(perm, np.array([7.0, -2.0, 5.0])), ARR["ka/lu_perm"])
+    spd = ARR["ka/spd"]
+    assert rel(sq.cholesky_solve(spd, np.arange(9.0)), ARR["ka/chol_x"]) <= 1e-13
+    g = R.philox(7, 3).standard_normal((9, 9))
+    assert rel(sq.lu_solve(spd + np.triu(g), np.arange(9.0)), ARR["ka/lu_x"]) <= 1e-12
+
+
+def test_nxn_error_classes(sq):
+    with pytest.raises(sq.SingularTriangular):
+        sq.triangular_solve(np.array([[1.0, 2.0], [0.0, 0.0]]), np.array([1.0, 1.0]))
+    with pytest.raises(sq.NumericallySingular):
+        sq.lu_solve(np.array([[1.0, 2.0], [2.0, 4.0]]), np.array([1.0, 1.0]))
+    with pytest.raises(sq.NotPositiveDefinite):
+        sq.cholesky_solve(np.array([[1.0, 0.0], [0.0, -1.0]]), np.array([1.0, 1.0]))
+    with pytest.raises(ValueError):
+        sq.cholesky_solve(np.array([[1.0, 5.0], [0.0, 1.0]]), np.array([1.0, 1.0]))
+
+
+@pytest.mark.parametrize("n", [6, 40, 100, 333, 1024])
+def test_lu_and_cholesky_vs_oracle(sq, n):
+    g = R.philox(n, 3)
+    a = g.standard_normal((n, n)) + n * np.eye(n)
+    x = g.standard_normal(n)
+    got = sq.lu_solve(a, a @ x)
+    assert np.linalg.norm(got - x) <= 1e-10 * np.linalg.norm(x)
+    b = g.standard_normal((3 * n, n))
+    s = b.T @ b + np.eye(n)
+    rhs = g.standard_normal(n)
+    assert rel(sq.cholesky_solve(s, rhs), R.spd_solve(s, rhs)) <= 1e-9
+    r = np.triu(g.standard_normal((n, n))) + 4.0 * np.eye(n)
+    for tr in (False, True):
+        assert rel(sq.triangular_solve(r, rhs, transposed=tr), R.tri_solve(r, rhs, transposed=tr)) <= 1e-11
+
+
+def test_lu_pivot_sequence_bitwise_small(sq):
+    # the factorisation is op-for-op the reference's; with n <= 32 the substitution
+    # is a single sequential block too, so small systems agree to the last bit
+    g = R.philox(5, 3)
+    for n in (3, 8, 17):
+        a = g.standard_normal((n, n))
+        rhs = g.standard_normal(n)
+        assert rel(sq.lu_solve(a, rhs), R.lu_pivoted_solve(a, rhs)) <= 1e-13
+
+
+# --------------------------------------------------------------- kappa0 ------
+@pytest.mark.parametrize("name", ["p600_k1e2", "p600_k1e6", "p600_k1e10", "p2000_k1e4", "cfg1_rho1e-6"])
+def test_kappa0_decision_matches_reference(sq, name):
+    want = META["decisions"][name]
+    d = sq.decide_precision(problem(name).a)
+    assert d.selected.name == want["selected"] and d.overflowed == want["overflowed"]
+    if not want["overflowed"]:
+        assert abs(d.kappa0 - want["kappa0"]) <= 1e-6
+
+
+def test_kappa0_identity(sq):
+    k0, over = sq.estimate_log10_condition(np.eye(100))
+    assert not over and abs(k0 - 1.0) <= 1e-15
+
+
+# --------------------------------------------------------------- Jacobi ------
+def test_jacobi_and_diagnostics(sq):
+    sv = sq.jacobi_singular_values(np.diag([4.0, 0.25, 2.0]))
+    assert np.array_equal(sv, np.array([4.0, 2.0, 0.25]))
+    g = R.philox(7, 3).standard_normal((9, 9))
+    assert rel(sq.jacobi_singular_values(g), ARR["ka/jacobi_sv"]) <= 1e-13
+    from oracle.problems import planted_triangle
+    for seed, kappa in enumerate((1e2, 1e4, 1e6)):
+        r = planted_triangle(20 + 2 * seed, kappa, seed)
+        diag = sq.condition_diagnostics(r)
+        assert diag.two_norm_condition == pytest.approx(kappa, rel=1e-6)
+    with pytest.raises(sq.NoConvergence):
+        sq.jacobi_singular_values(R.philox(5, 3).standard_normal((12, 12)), max_sweeps=1, tol=1e-300)
