@@ -1,0 +1,392 @@
+"""Benchmark: Algorithm-1 solve time at 4M x 2048 (BASELINE.json config 3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = one full `algorithm1_pipeline(A, b, method, precision="auto")`
+solve (kappa0 estimate, sketch, level QR, A_p = A R^-1, Gram, n x n solve,
+residual report) on device-resident synthetic data of prescribed kappa(A) and
+residual (the GPU Algorithm-2 generator, probgen.py).  `value` is milliseconds
+per solve (lower is better) timed with CUDA events between barriers, max over
+ranks.  `e2e` is the same solve through the public API from pinned HOST
+buffers, the host->device copy of A and b and the device->host read of x_hat
+inside the timed region.  A (68.7 GB) is far larger than L2, so no flush is
+needed between steps.
+
+Multi-GPU (torchrun): rows are sharded, each rank holds m rows (weak scaling:
+m_total = N * m); partial Gram / sketch results are summed with NCCL
+all-reduce (distributed.py).
+
+`--impl reference` times the reference algorithm on the host CPU (the oracle
+port in oracle/, all host threads) on a bounded sample of the same workload and
+reports it in the same unit, extrapolated stage by stage to the full size.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "PNE/HPNE solve time at 4M×2048 (1–8 GPUs); % of roofline; rel. error"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--m", type=int, default=4 * 1024 * 1024, help="rows per GPU")
+    p.add_argument("--n", type=int, default=2048)
+    p.add_argument("--kappa", type=float, default=10.0)
+    p.add_argument("--rho", type=float, default=1e-6)
+    p.add_argument("--method", default="hpne", choices=["pne", "hpne"])
+    p.add_argument("--precision", default="auto")
+    p.add_argument("--seed", type=int, default=20261018)
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample", default="32768x256", help="oracle sample m x n for the CPU legs")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------- clocks ---
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                maxs.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": max(maxs) if maxs else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# -------------------------------------------------------------- roofline ---
+def fp64_peak():
+    """Measured cuBLAS DGEMM peak (TFLOP/s) from profiles/, else the spec estimate."""
+    path = os.path.join(HERE, "profiles", "fp64_peak.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["fp64_tflops"]), d.get("source", path)
+    except Exception:  # noqa: BLE001
+        return 37.2, "spec estimate 148 SM x 64 FMA/clk x 2 x 1.965 GHz (not measured)"
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel_key):
+    try:
+        with open(os.path.join(HERE, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh).get(kernel_key)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def stage_work(stage, m, n, d, method, level):
+    """Algorithmic work per stage: (flops, bytes, bound)."""
+    if stage == "kappa0":
+        return float(m) * n * n, 8.0 * m * n, "tensor"          # SYRK: m n^2 flops
+    if stage == "trsm":
+        return float(m) * n * n, 16.0 * m * n, "tensor"
+    if stage == "gram":
+        f = 2.0 * m * n * n if method == "hpne" else float(m) * n * n
+        return f, 16.0 * m * n if method == "hpne" else 8.0 * m * n, "tensor"
+    if stage == "sketch":
+        return 2.0 * d * m * n, 8.0 * m * n, "hbm"              # floor: one read of A
+    if stage == "report":
+        return 2.0 * m * n, 8.0 * m * n, "hbm"
+    return None
+
+
+# ------------------------------------------------------------- CPU legs ----
+def cpu_sample_run(args, sample):
+    """Time the oracle (reference algorithm, numpy/OpenBLAS on all host threads)
+    on an m_s x n_s sample and extrapolate each stage to the full size."""
+    import numpy as np
+    from oracle import restatement as R
+    from oracle.problems import planted_problem
+    ms, ns = (int(v) for v in sample.split("x"))
+    p = planted_problem(ms, ns, args.kappa, args.rho, 7)
+    tm = {}
+    t0 = time.perf_counter()
+    rep = R.pipeline(p.a, p.b, method=args.method, precision=args.precision, seed=1, x_star=p.x_star,
+                     diagnostics=False, timings=tm)
+    wall = time.perf_counter() - t0
+    M, N = args.m * args.gpus, args.n
+    fm, fn = M / ms, N / ns
+    scale = {"kappa0": fm * fn * fn, "sketch": fm * fn * math.log2(M) / math.log2(ms),
+             "level_qr": fn ** 3, "trsm": fm * fn * fn, "solve": fm * fn * fn}
+    est = sum(tm.get(k, 0.0) * s for k, s in scale.items())
+    other = max(wall - sum(tm.get(k, 0.0) for k in scale), 0.0) * fm * fn
+    return {"sample_s": wall, "stages_s": tm, "extrapolated_ms": (est + other) * 1e3,
+            "level": rep.pre.level, "rel_error": rep.relative_error}
+
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        th = [i.get("num_threads") for i in threadpool_info() if i.get("internal_api") == "openblas"]
+        if th:
+            return int(th[0])
+    except Exception:  # noqa: BLE001
+        pass
+    return os.cpu_count()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    reps = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample_run(args, args.cpu_sample)
+        if i >= args.warmup:
+            reps.append(r)
+    value = statistics.median([r["extrapolated_ms"] for r in reps])
+    sample = (f"oracle port of sketchlsq algorithm1_pipeline (numpy/OpenBLAS, diagnostics off) on a "
+              f"{args.cpu_sample} planted problem (kappa={args.kappa:g}, {args.method}, precision={args.precision}); "
+              f"measured {statistics.median([r['sample_s'] for r in reps]):.2f} s per sample, extrapolated per stage "
+              f"(m n^2 stages x (M/m_s)(N/n_s)^2, level QR x (N/n_s)^3, sketch x m log m n) to "
+              f"{args.m * args.gpus}x{args.n}")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "ms", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args),
+            "cpu_baseline": {"value": value, "unit": "ms", "cores": cpu_cores(), "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "rel_error_sample": reps[-1]["rel_error"], "level_sample": reps[-1]["level"]}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args):
+    return {"workload": (f"config 3: A {args.m * args.gpus:,} x {args.n} fp64 (rows/GPU {args.m:,}), "
+                         f"kappa(A)={args.kappa:g}, residual rho={args.rho:g}, {args.method.upper()}, "
+                         f"precision={args.precision}, d=3n DCT-II sketch"),
+            "m_total": args.m * args.gpus, "m_per_gpu": args.m, "n": args.n, "kappa": args.kappa, "rho": args.rho,
+            "method": args.method, "precision": args.precision, "d_factor": 3.0, "transform": "dct2",
+            "l2": "inputs larger than L2 (A is 8 m n bytes >> 126 MB): no flush needed",
+            "parallelism": f"row-shard x{args.gpus}"}
+
+
+# --------------------------------------------------------------- our arm ----
+def run_ours(args, rank, world):
+    import numpy as np
+    import torch
+    import paper_2603_16644_b200 as sq
+    from paper_2603_16644_b200 import _lib
+    from paper_2603_16644_b200.probgen import generate_problem_device
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    m, n = args.m, args.n
+    d = int(math.ceil(3.0 * n))
+    a, b, x_star = generate_problem_device(m, n, args.kappa, args.rho, args.seed + 7919 * rank, dev)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def solve(A, B):
+        if dist is not None:
+            from paper_2603_16644_b200.distributed import algorithm1_pipeline_sharded
+            return algorithm1_pipeline_sharded(A, B, method=args.method, precision=args.precision, seed=1,
+                                               x_star=x_star, diagnostics=False, stage_timing=True)
+        return sq.algorithm1_pipeline(A, B, method=args.method, precision=args.precision, seed=1, x_star=x_star,
+                                      diagnostics=False, stage_timing=True)
+
+    lib = _lib.lib()
+    for _ in range(args.warmup):
+        rep = solve(a, b)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    l0 = lib.sk_launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    e0.record()
+    reps = [solve(a, b) for _ in range(args.steps)]
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    launches = lib.sk_launch_count() - l0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    rep = reps[-1]
+    stages = {}
+    for r in reps:
+        for k, v in r.stage_ms.items():
+            stages[k] = stages.get(k, 0.0) + v / len(reps)
+    level = rep.preconditioner.computed_in.name
+
+    # roofline of the dominant stage (CUDA events around the stage, same stream)
+    dom = max((k for k in stages if stage_work(k, m, n, d, args.method, level)), key=lambda k: stages[k])
+    flops, bytes_, bound = stage_work(dom, m, n, d, args.method, level)
+    if bound == "tensor":
+        peak, src = fp64_peak()
+        achieved = flops / (stages[dom] * 1e-3) / 1e12
+        roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(dom), "peak_source": src,
+                "algorithmic_flops": flops, "pipe": "FP64 DMMA (mma.sync m8n8k4)"}
+    else:
+        peak, src = hbm_peak()
+        achieved = bytes_ / (stages[dom] * 1e-3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(dom), "peak_source": src,
+                "algorithmic_bytes": bytes_}
+    per_stage = {}
+    for k, v in stages.items():
+        w = stage_work(k, m, n, d, args.method, level)
+        if w and w[2] == "tensor":
+            per_stage[k] = {"ms": v, "tflops": w[0] / (v * 1e-3) / 1e12}
+        elif w:
+            per_stage[k] = {"ms": v, "gbs": w[1] / (v * 1e-3) / 1e9}
+        else:
+            per_stage[k] = {"ms": v}
+    fp64_total = (m * n * n if args.precision == "auto" else 0) + m * n * n + \
+        (2.0 if args.method == "hpne" else 1.0) * m * n * n
+    t_roof = fp64_total / (fp64_peak()[0] * 1e12) + 2 * 8.0 * m * n / (hbm_peak()[0] * 1e9)
+
+    # ---- e2e: host buffers, H2D + D2H inside the timed region ----
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        a_host = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
+        a_host.copy_(a)
+        b_host = b.to("cpu").pin_memory()
+        del a, rep, reps
+        torch.cuda.empty_cache()
+        torch.cuda.synchronize()
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.e2e_steps):
+            r2 = solve(a_host, b_host)
+        f1.record()
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = f0.elapsed_time(f1) / args.e2e_steps
+        if dist is not None:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 8 * m * n + 8 * m,
+               "d2h_bytes_per_step": 8 * n + 16, "steps": args.e2e_steps,
+               "rel_error": r2.relative_error}
+
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            s = cpu_sample_run(args, args.cpu_sample)
+            cpu = {"value": s["extrapolated_ms"], "unit": "ms", "cores": cpu_cores(), "kind": "port",
+                   "sample": (f"oracle port on a {args.cpu_sample} planted problem (kappa={args.kappa:g}, "
+                              f"{args.method}, auto): {s['sample_s']:.2f} s measured, extrapolated per stage to "
+                              f"{m * world}x{n}; sample level {s['level']}")}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": "ms", "cores": cpu_cores(), "kind": "port", "sample": f"failed: {ex!r}"}
+    line = {"metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (GPU Algorithm-2 generator, probgen.py)",
+            "config": workload_config(args), "selected_level": level,
+            "kappa0": rep_kappa0(rep), "escalated_from": rep.escalated_from.name if rep.escalated_from else None,
+            "rel_error": rep.relative_error, "relative_residual": rep.relative_residual,
+            "roofline": roof, "roofline_solve": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
+                                                 "model": "FP64 flops / measured DGEMM peak + 2 reads of A / HBM"},
+            "stages_ms": per_stage, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
+            "gpu_launches_per_step": launches / args.steps, "clocks": clk}
+    print(json.dumps(line), flush=True)
+
+
+def rep_kappa0(rep):
+    d = rep.precision_decision
+    if d is None or (isinstance(d.kappa0, float) and math.isnan(d.kappa0)):
+        return None
+    return d.kappa0
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if world != args.gpus and world == 1 and args.gpus > 1:
+        print(json.dumps({"error": "launch with torchrun for --gpus > 1"}))
+        return 2
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return 0
+    run_ours(args, rank, world)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

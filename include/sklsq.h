@@ -65,6 +65,9 @@ typedef struct sk_status {
 int sk_version(void);
 const char *sk_last_error(void);
 int sk_sm_count(int device);
+/* Number of kernels this library has launched in the process (instrumentation:
+ * the bench reports launches inside its timed region from the difference). */
+uint64_t sk_launch_count(void);
 
 /* ---- streaming passes over A (HBM-bound) --------------------------------- */
 /* _as_matrix + astype(float64) + ||A||_F^2 in one pass: src/dense.py:57-65,

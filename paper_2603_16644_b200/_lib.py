@@ -39,6 +39,7 @@ SIGNATURES = {
     "sk_version": (_i32, []),
     "sk_last_error": (C.c_char_p, []),
     "sk_sm_count": (_i32, [_i32]),
+    "sk_launch_count": (C.c_uint64, []),
     "sk_matrix_stats_workspace": (_sz, [_i64, _i64]),
     "sk_cast_stats": (_i32, [_p, _i32, _i64, _i64, _i64, _p, _i64, _pd, _p, _sz, _p]),
     "sk_level_overflow": (_i32, [_p, _i64, _i64, _i64, _i32, _pi, _p, _sz, _p]),

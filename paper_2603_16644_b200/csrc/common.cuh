@@ -27,8 +27,11 @@ inline int fill_status(sk_status *st, int code, int64_t index, double value, dou
         if (_e != cudaSuccess) return ::sk::cuda_fail(_e, #call);      \
     } while (0)
 
+void count_launch();   // every kernel launch site passes through SK_LAUNCH_CHECK
+
 #define SK_LAUNCH_CHECK(where)                                          \
     do {                                                                \
+        ::sk::count_launch();                                           \
         cudaError_t _e = cudaGetLastError();                            \
         if (_e != cudaSuccess) return ::sk::cuda_fail(_e, where);      \
     } while (0)

@@ -1,5 +1,6 @@
 // Library plumbing: versioning, thread-local error text, device facts.
 #include <cstdarg>
+#include <atomic>
 #include <mutex>
 
 #include "common.cuh"
@@ -7,6 +8,9 @@
 namespace sk {
 
 static thread_local char g_err[512] = "";
+static std::atomic<unsigned long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char *fmt, ...) {
     va_list ap;
@@ -45,6 +49,8 @@ int max_coop_blocks(const void *kernel, int threads, size_t smem) {
 extern "C" {
 
 int sk_version(void) { return 1; }
+
+uint64_t sk_launch_count(void) { return sk::g_launches.load(std::memory_order_relaxed); }
 
 const char *sk_last_error(void) { return sk::g_err; }
 

@@ -41,11 +41,18 @@ class ConditionDiagnostics:
 
 
 # --------------------------------------------------------------- device ops --
+def _rm(t: torch.Tensor) -> torch.Tensor:
+    """Row-major view with unit column stride (what the C ABI expects)."""
+    if t.dim() == 2 and (t.stride(1) != 1 or t.stride(0) < t.shape[1]):
+        return t.contiguous()
+    return t
+
+
 def _gram(x: DMat | torch.Tensor, y: DMat | torch.Tensor | None = None, out: torch.Tensor | None = None,
           accumulate: bool = False) -> torch.Tensor:
     """G = X^T Y (SYRK when y is None or y is x) on the DMMA pipe."""
-    xt = x.t if isinstance(x, DMat) else x
-    yt = xt if y is None else (y.t if isinstance(y, DMat) else y)
+    xt = _rm(x.t if isinstance(x, DMat) else x)
+    yt = xt if y is None else _rm(y.t if isinstance(y, DMat) else y)
     m, n = xt.shape
     if yt.shape != xt.shape:
         raise DimensionMismatch(f"gram operands {tuple(xt.shape)} vs {tuple(yt.shape)}")
@@ -62,7 +69,7 @@ def _gram(x: DMat | torch.Tensor, y: DMat | torch.Tensor | None = None, out: tor
 def _gemv_t(x: DMat | torch.Tensor, v: torch.Tensor, out: torch.Tensor | None = None,
             accumulate: bool = False) -> torch.Tensor:
     """out = X^T v (memory-bound)."""
-    xt = x.t if isinstance(x, DMat) else x
+    xt = _rm(x.t if isinstance(x, DMat) else x)
     m, n = xt.shape
     if out is None:
         out = torch.empty(n, dtype=torch.float64, device=xt.device)
@@ -75,7 +82,8 @@ def _gemv_t(x: DMat | torch.Tensor, v: torch.Tensor, out: torch.Tensor | None = 
 
 def _trsm(a: DMat | torch.Tensor, r: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     """A_p = A R^{-1} (R upper, device f64)."""
-    at = a.t if isinstance(a, DMat) else a
+    at = _rm(a.t if isinstance(a, DMat) else a)
+    r = _rm(r)
     m, n = at.shape
     if out is None:
         out = torch.empty((m, n), dtype=torch.float64, device=at.device)
@@ -86,6 +94,7 @@ def _trsm(a: DMat | torch.Tensor, r: torch.Tensor, out: torch.Tensor | None = No
 
 
 def _trsv(r: torch.Tensor, rhs: torch.Tensor, transposed: bool = False) -> torch.Tensor:
+    r, rhs = _rm(r), rhs.contiguous()
     n = r.shape[0]
     out = torch.empty(n, dtype=torch.float64, device=r.device)
     wp, wn = WORKSPACE.get(2 * 8 * n + 1024)
@@ -96,6 +105,7 @@ def _trsv(r: torch.Tensor, rhs: torch.Tensor, transposed: bool = False) -> torch
 
 
 def _chol_solve(s: torch.Tensor, rhs: torch.Tensor) -> torch.Tensor:
+    s, rhs = s.contiguous(), rhs.contiguous()
     n = s.shape[0]
     out = torch.empty(n, dtype=torch.float64, device=s.device)
     wp, wn = WORKSPACE.get(_lib.lib().sk_nxn_workspace(n))
@@ -106,6 +116,7 @@ def _chol_solve(s: torch.Tensor, rhs: torch.Tensor) -> torch.Tensor:
 
 
 def _lu_solve(g: torch.Tensor, rhs: torch.Tensor) -> torch.Tensor:
+    g, rhs = g.contiguous(), rhs.contiguous()
     n = g.shape[0]
     out = torch.empty(n, dtype=torch.float64, device=g.device)
     wp, wn = WORKSPACE.get(_lib.lib().sk_nxn_workspace(n))
@@ -135,6 +146,7 @@ def _householder_r64(at: torch.Tensor) -> torch.Tensor:
 
 
 def _jacobi_sv(at: torch.Tensor, max_sweeps: int = 30, tol: float = 1e-14) -> np.ndarray:
+    at = _rm(at)
     rows, n = at.shape
     sv = (C.c_double * n)()
     wp, wn = WORKSPACE.get(_lib.lib().sk_jacobi_workspace(rows, n))
