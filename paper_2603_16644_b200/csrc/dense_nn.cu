@@ -406,7 +406,7 @@ static int coop_blocks(const void *fn, int threads, size_t smem, int64_t want) {
 static int trsv_launch(TriView M, int n, bool lower, bool unit, const double *rhs, const int *perm, double *x,
                        cudaStream_t st) {
     const size_t smem = (size_t)n * sizeof(double);
-    if (smem > 48 * 1024)
+    if (smem > 40 * 1024)
         SK_CUDA(cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     trsv_kernel<<<1, 1024, smem, st>>>(M, n, lower, unit, rhs, perm, x);
     SK_LAUNCH_CHECK("trsv_kernel");
@@ -590,7 +590,7 @@ int sk_kappa0_from_gram(const double *g, int64_t n, double *kappa0_host, int *ov
     if (rc != SK_OK) return rc;
     const size_t smem = 3 * (size_t)n * sizeof(double);
     if (smem > 227 * 1024) { set_error("n too large for the single-CTA Hager kernel"); return SK_ERR_ARG; }
-    if (smem > 48 * 1024)
+    if (smem > 40 * 1024)
         SK_CUDA(cudaFuncSetAttribute(hager_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     hager_kernel<<<1, 1024, smem, st>>>(ws.l, (int)n, ws.stats + 4);
     SK_LAUNCH_CHECK("hager_kernel");

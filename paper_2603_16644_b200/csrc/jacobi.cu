@@ -161,7 +161,7 @@ int sk_jacobi_sv_f64(const double *a, int64_t rows, int64_t n, int64_t lda, int 
     int npow2 = 1;
     while (npow2 < n) npow2 <<= 1;
     const size_t smem = (size_t)npow2 * sizeof(double);
-    if (smem > 48 * 1024)
+    if (smem > 40 * 1024)
         SK_CUDA(cudaFuncSetAttribute(jac::colnorm_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     jac::colnorm_sort<<<1, 1024, smem, st>>>(w, rows, (int)n, npow2, sv);
     SK_LAUNCH_CHECK("colnorm_sort");

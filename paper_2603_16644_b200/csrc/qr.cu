@@ -224,7 +224,7 @@ int run(T *w, int64_t d, int64_t n, double inv_scale, double *r, int64_t ldr, sk
     const int scratch_per_warp = HALF ? (int)((d + 7) / 8 + 8) : 1;
     const size_t smem = (size_t)WARPS * scratch_per_warp * sizeof(T);
     auto kfn = householder_kernel<T, HALF>;
-    if (smem > 48 * 1024) SK_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 40 * 1024) SK_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int maxb = max_coop_blocks((const void *)kfn, THREADS, smem);
     if (maxb <= 0) { set_error("sk_qr_r: kernel cannot be co-resident (d too large?)"); return SK_ERR_ARG; }
     int blocks = (int)((n + WARPS - 1) / WARPS);
