@@ -286,6 +286,9 @@ def run_ours(args, rank, world):
         for k, v in r.stage_ms.items():
             stages[k] = stages.get(k, 0.0) + v / len(reps)
     level = rep.preconditioner.computed_in.name
+    summary = {"selected_level": level, "kappa0": rep_kappa0(rep),
+               "escalated_from": rep.escalated_from.name if rep.escalated_from else None,
+               "rel_error": rep.relative_error, "relative_residual": rep.relative_residual}
 
     # roofline of the dominant stage (CUDA events around the stage, same stream)
     dom = max((k for k in stages if stage_work(k, m, n, d, args.method, level)), key=lambda k: stages[k])
@@ -357,9 +360,7 @@ def run_ours(args, rank, world):
     line = {"metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (GPU Algorithm-2 generator, probgen.py)",
-            "config": workload_config(args), "selected_level": level,
-            "kappa0": rep_kappa0(rep), "escalated_from": rep.escalated_from.name if rep.escalated_from else None,
-            "rel_error": rep.relative_error, "relative_residual": rep.relative_residual,
+            "config": workload_config(args), **summary,
             "roofline": roof, "roofline_solve": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
                                                  "model": "FP64 flops / measured DGEMM peak + 2 reads of A / HBM"},
             "stages_ms": per_stage, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),

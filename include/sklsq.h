@@ -121,11 +121,19 @@ int sk_trsm_right_upper_f64(const double *a, int64_t lda, int64_t m, int64_t n, 
  * the final rounding happen in sk_sketch_finalize so that partials can be summed
  * across row shards (NCCL) first.  Overflow of the demotion is OR-ed into
  * *overflow_flag_dev (device int).  transform SK_DCT2/SK_WHT, level 16/32/64. */
-size_t sk_sketch_workspace(int64_t m_local, int64_t n, int64_t d);
+enum sk_sketch_algo { SK_SKETCH_AUTO = 0, SK_SKETCH_DMMA = 1, SK_SKETCH_TC = 2 };
+size_t sk_sketch_workspace(int level, int64_t m_local, int64_t n, int64_t d);
 int sk_sketch_partial(int level, int transform, const double *a, int64_t lda, int64_t m_local,
                       int64_t row_offset, int64_t m_pad, int64_t n, const double *signs,
                       const int64_t *rows, int64_t d, double *out, int64_t ldo, int accumulate,
                       int *overflow_flag_dev, void *ws, size_t ws_bytes, sk_stream_t stream);
+/* Same, choosing the engine: SK_SKETCH_TC = tcgen05 kind::f16 GEMM with TMEM
+ * accumulators and TMA-staged operands (binary16 only), SK_SKETCH_DMMA = FP64
+ * DMMA GEMM (any level), SK_SKETCH_AUTO = TC for binary16, else DMMA. */
+int sk_sketch_partial_ex(int level, int transform, const double *a, int64_t lda, int64_t m_local,
+                         int64_t row_offset, int64_t m_pad, int64_t n, const double *signs,
+                         const int64_t *rows, int64_t d, double *out, int64_t ldo, int accumulate,
+                         int *overflow_flag_dev, void *ws, size_t ws_bytes, sk_stream_t stream, int algo);
 
 /* Finish the sketch: A_s = level(level(sum) * level(sqrt(m_pad/d))) written as a
  * COLUMN-major d x n matrix in the level dtype (f16/f32/f64), the layout the

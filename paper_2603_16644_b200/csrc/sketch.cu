@@ -245,22 +245,56 @@ static Plan make_plan(int64_t m_local, int64_t n, int64_t d) {
 
 using namespace sk;
 
+namespace sk {
+size_t sketch_tc_workspace(int64_t m_local, int64_t n, int64_t d);
+int sketch_tc_run(int transform, const double *a, int64_t lda, int64_t m_local, int64_t row_offset, int64_t m_pad,
+                  int64_t n, const double *signs, const int64_t *rows, int64_t d, double *out, int64_t ldo,
+                  int accumulate, int *overflow_flag_dev, void *ws, size_t ws_bytes, cudaStream_t st);
+}
+
 extern "C" {
 
-size_t sk_sketch_workspace(int64_t m_local, int64_t n, int64_t d) {
+static size_t dmma_sketch_ws(int64_t m_local, int64_t n, int64_t d) {
     sketch::Plan p = sketch::make_plan(m_local, n, d);
     return (size_t)p.splits * p.ntiles * sketch::BM * sketch::BN * sizeof(double);
 }
+
+size_t sk_sketch_workspace(int level, int64_t m_local, int64_t n, int64_t d) {
+    const size_t a = dmma_sketch_ws(m_local, n, d);
+    if (level != 16) return a;
+    const size_t b = sk::sketch_tc_workspace(m_local, n, d);
+    return a > b ? a : b;
+}
+
+int sk_sketch_partial_ex(int level, int transform, const double *a, int64_t lda, int64_t m_local,
+                         int64_t row_offset, int64_t m_pad, int64_t n, const double *signs, const int64_t *rows,
+                         int64_t d, double *out, int64_t ldo, int accumulate, int *overflow_flag_dev, void *ws,
+                         size_t ws_bytes, sk_stream_t stream, int algo);
 
 int sk_sketch_partial(int level, int transform, const double *a, int64_t lda, int64_t m_local,
                       int64_t row_offset, int64_t m_pad, int64_t n, const double *signs,
                       const int64_t *rows, int64_t d, double *out, int64_t ldo, int accumulate,
                       int *overflow_flag_dev, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    return sk_sketch_partial_ex(level, transform, a, lda, m_local, row_offset, m_pad, n, signs, rows, d, out, ldo,
+                                accumulate, overflow_flag_dev, ws, ws_bytes, stream, SK_SKETCH_AUTO);
+}
+
+int sk_sketch_partial_ex(int level, int transform, const double *a, int64_t lda, int64_t m_local,
+                         int64_t row_offset, int64_t m_pad, int64_t n, const double *signs, const int64_t *rows,
+                         int64_t d, double *out, int64_t ldo, int accumulate, int *overflow_flag_dev, void *ws,
+                         size_t ws_bytes, sk_stream_t stream, int algo) {
     if (!a || !signs || !rows || !out || !overflow_flag_dev || m_local < 0 || n <= 0 || d <= 0 ||
         lda < n || ldo < d || m_pad <= 0 || row_offset < 0 || row_offset + m_local > m_pad ||
         (level != 16 && level != 32 && level != 64) || (transform != SK_DCT2 && transform != SK_WHT) ||
-        m_pad >= (int64_t(1) << 30)) {
+        m_pad >= (int64_t(1) << 30) || (algo != SK_SKETCH_AUTO && algo != SK_SKETCH_DMMA && algo != SK_SKETCH_TC)) {
         set_error("sk_sketch_partial: bad arguments");
+        return SK_ERR_ARG;
+    }
+    if (level == 16 && algo != SK_SKETCH_DMMA)
+        return sk::sketch_tc_run(transform, a, lda, m_local, row_offset, m_pad, n, signs, rows, d, out, ldo,
+                                 accumulate, overflow_flag_dev, ws, ws_bytes, (cudaStream_t)stream);
+    if (algo == SK_SKETCH_TC) {
+        set_error("sk_sketch_partial: the tensor-core path exists for binary16 only");
         return SK_ERR_ARG;
     }
     sketch::Plan p = sketch::make_plan(m_local, n, d);

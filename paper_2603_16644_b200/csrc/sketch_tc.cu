@@ -1,0 +1,385 @@
+// binary16 SRTT sketch on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+//   A_s(partial) = F_sampled * (D A16)      M = d sampled rows, N = n, K = m rows
+//
+// Reference semantics (src/sketch.py:138-169 at binary16, src/solvers.py:191-195):
+// A is demoted to binary16, signs flipped (exact), the orthonormal DCT-II / WHT is
+// taken along the rows (pocketfft in binary32 for the DCT, per-op binary16 for
+// the WHT), the d sampled rows are kept, rounded to binary16 and scaled.  Here
+// the d sampled rows of the transform are a tensor-core GEMM:
+//
+//   prep kernel   : At16[c][j] = sign_j * fp16(A[j][c])    (one HBM pass, transposed,
+//                   overflow of the demotion -> flag)      K-major operand for TMA
+//   main kernel   : persistent, warp-specialised, 1 CTA / SM
+//       warp 0      TMA producer: B tile At16[n-tile 256][k-block 64], SWIZZLE_128B
+//       warp 1      MMA issuer:   tcgen05.mma.cta_group::1.kind::f16, M128 N256 K16,
+//                                 fp32 accumulator in TMEM (256 columns)
+//       warp 2      TMEM allocator
+//       warps 4-11  operator generator: F'[r_i][j] = cos(pi r_i (2j+1) / 2M) (DCT; 1/sqrt2
+//                   for r = 0) or (-1)^popc(r_i & j) (WHT), exact integer phase
+//                   reduction once per 32 columns + fp32 rotation recurrence, rounded
+//                   to fp16 straight into the 128B-swizzled K-major A tile; then the
+//                   epilogue: tcgen05.ld -> scale sqrt(2/M) (DCT) or 1/sqrt(M) (WHT)
+//                   -> fp32 split-K partials
+//   reduce kernel : fixed-order sum of the split-K partials -> f64 (column-major d x n)
+// sk_sketch_finalize then applies the binary16 rounding and scale of the reference.
+#include "tc.cuh"
+
+namespace sk {
+
+int make_tmap_2d(CUtensorMap *map, CUtensorMapDataType dtype, const void *base, uint64_t inner, uint64_t outer,
+                 uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz) {
+    using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p) {
+            set_error("cuTensorMapEncodeTiled unavailable");
+            return SK_ERR_CUDA;
+        }
+        fn = reinterpret_cast<EncodeFn>(p);
+    }
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_stride_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, dtype, 2, const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return SK_ERR_CUDA;
+    }
+    return SK_OK;
+}
+
+namespace sktc {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int THREADS = 384, GEN_WARP0 = 4, NGEN_WARPS = 8;
+constexpr uint32_t A_BYTES = BM * BK * 2;   // 16 KB
+constexpr uint32_t B_BYTES = BN * BK * 2;   // 32 KB
+constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+constexpr int TMEM_COLS = 256;
+
+// ------------------------------------------------------------ prep kernel ---
+constexpr int PT = 64;   // 64 x 64 tile
+__global__ void __launch_bounds__(256)
+prep_f16t(const double *__restrict__ a, int64_t lda, int64_t m_local, int n, const double *__restrict__ signs,
+          int64_t row_offset, __half *__restrict__ out, int64_t ldm, int *overflow_flag) {
+    __shared__ __half tile[PT][PT + 2];
+    const int64_t j0 = (int64_t)blockIdx.x * PT;
+    const int c0 = blockIdx.y * PT;
+    int over = 0;
+#pragma unroll 4
+    for (int rep = 0; rep < (PT * PT) / 256; ++rep) {
+        const int idx = threadIdx.x + rep * 256;
+        const int r = idx / PT, c = idx % PT;
+        const int64_t j = j0 + r;
+        __half h = __float2half_rn(0.f);
+        if (j < m_local && c0 + c < n) {
+            const double v = a[j * lda + c0 + c];
+            h = __double2half(v);
+            over |= (isinf(__half2float(h)) && isfinite(v));
+            if (signs[row_offset + j] < 0) h = __hneg(h);
+        }
+        tile[c][r] = h;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rep = 0; rep < (PT * PT / 2) / 256; ++rep) {
+        const int idx = threadIdx.x + rep * 256;
+        const int c = idx / (PT / 2), r2 = (idx % (PT / 2)) * 2;
+        const int64_t j = j0 + r2;
+        if (c0 + c < n && j < ldm) {
+            __half2 v = __halves2half2(tile[c][r2], tile[c][r2 + 1]);
+            *reinterpret_cast<__half2 *>(out + (int64_t)(c0 + c) * ldm + j) = v;
+        }
+    }
+    if (__any_sync(0xffffffffu, over) && (threadIdx.x & 31) == 0) atomicOr(overflow_flag, 1);
+}
+
+struct Params {
+    const int64_t *rows;
+    int64_t mpad, row_offset, m_local, kchunk;
+    int n, d, ntn, ntiles, units;
+    int wht;
+    float epi_scale;
+    float *part;
+};
+
+__device__ __forceinline__ void unit_coords(const Params &p, int u, int &tm, int &tn, int64_t &k0, int &nkb) {
+    const int tile = u % p.ntiles, split = u / p.ntiles;
+    tm = tile / p.ntn;
+    tn = tile % p.ntn;
+    k0 = (int64_t)split * p.kchunk;
+    const int64_t k1 = min(p.m_local, k0 + p.kchunk);
+    nkb = (int)((k1 - k0 + BK - 1) / BK);
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sa = smem;
+    uint8_t *sb = smem + STAGES * A_BYTES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sb + STAGES * B_BYTES);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint64_t *tempty = tfull + 1;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1 + NGEN_WARPS);
+            tc::mbar_init(&empty[s], 1);
+        }
+        tc::mbar_init(tfull, 1);
+        tc::mbar_init(tempty, NGEN_WARPS);
+        tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&tmap_b);
+    }
+    if (warp == 2) tc::tmem_alloc<TMEM_COLS>(tslot);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0) {
+        if (lane == 0) {   // ---------------- TMA producer
+            int stage = 0;
+            unsigned phase = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                int tm, tn, nkb;
+                int64_t k0;
+                unit_coords(p, u, tm, tn, k0, nkb);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    tc::mbar_wait(&empty[stage], phase ^ 1);
+                    tc::mbar_arrive_expect_tx(&full[stage], B_BYTES);
+                    tc::tma_load_2d(sb + stage * B_BYTES, &tmap_b, &full[stage], (int)(k0 + (int64_t)kb * BK), tn * BN);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {   // ---------------- MMA issuer
+            constexpr uint32_t idesc = tc::idesc_f32acc(BM, BN, 0, 0);
+            int stage = 0;
+            unsigned phase = 0, tphase = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                int tm, tn, nkb;
+                int64_t k0;
+                unit_coords(p, u, tm, tn, k0, nkb);
+                tc::mbar_wait(tempty, tphase ^ 1);
+                tc::tc_fence_after();
+                for (int kb = 0; kb < nkb; ++kb) {
+                    tc::mbar_wait(&full[stage], phase);
+                    tc::tc_fence_after();
+                    const uint64_t ad = tc::desc_kmajor_sw128(smem_u32(sa + stage * A_BYTES));
+                    const uint64_t bd = tc::desc_kmajor_sw128(smem_u32(sb + stage * B_BYTES));
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)   // +32 bytes along K per UMMA_K = 16
+                        tc::mma_f16_ss(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) ? 1u : 0u);
+                    tc::mma_commit(&empty[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                tc::mma_commit(tfull);
+                tphase ^= 1;
+            }
+        }
+    } else if (warp >= GEN_WARP0) {
+        // ---------------- operator generator + epilogue
+        const int gt = threadIdx.x - GEN_WARP0 * 32;   // 0..255
+        const int row = gt >> 1, half = gt & 1;
+        const uint64_t M = (uint64_t)p.mpad, fourM = 4 * M;
+        const float inv2M = 1.0f / (2.0f * (float)p.mpad);
+        int stage = 0;
+        unsigned phase = 0, tphase = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            int tm, tn, nkb;
+            int64_t k0;
+            unit_coords(p, u, tm, tn, k0, nkb);
+            const int i = tm * BM + row;
+            const bool valid = i < p.d;
+            const uint64_t r = valid ? (uint64_t)p.rows[i] : 0;
+            // per-column rotation e^{i pi r / M}
+            float wsn, wcs;
+            sincospif((float)(r % (2 * M)) / (float)M, &wsn, &wcs);
+            for (int kb = 0; kb < nkb; ++kb) {
+                tc::mbar_wait(&empty[stage], phase ^ 1);
+                const int64_t jg0 = p.row_offset + k0 + (int64_t)kb * BK + half * 32;
+                uint32_t packed[16];
+                if (!p.wht) {
+                    const uint64_t f1 = r % fourM, f2 = (uint64_t)(2 * jg0 + 1) % fourM;
+                    const uint64_t ph = (f1 * f2) % fourM;
+                    float zs, zc;
+                    sincospif((float)ph * inv2M, &zs, &zc);
+#pragma unroll
+                    for (int t = 0; t < 32; t += 2) {
+                        const float v0 = zc;
+                        float nc = zc * wcs - zs * wsn, ns = zs * wcs + zc * wsn;
+                        const float v1 = nc;
+                        zc = nc * wcs - ns * wsn;
+                        zs = ns * wcs + nc * wsn;
+                        float a0 = valid ? (r == 0 ? 0.70710678118654752f : v0) : 0.f;
+                        float a1 = valid ? (r == 0 ? 0.70710678118654752f : v1) : 0.f;
+                        __half2 h = __floats2half2_rn(a0, a1);
+                        packed[t >> 1] = *reinterpret_cast<uint32_t *>(&h);
+                    }
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 32; t += 2) {
+                        const uint64_t j0 = (uint64_t)(jg0 + t), j1 = j0 + 1;
+                        float a0 = (__popcll(r & j0) & 1) ? -1.f : 1.f;
+                        float a1 = (__popcll(r & j1) & 1) ? -1.f : 1.f;
+                        if (!valid) a0 = a1 = 0.f;
+                        __half2 h = __floats2half2_rn(a0, a1);
+                        packed[t >> 1] = *reinterpret_cast<uint32_t *>(&h);
+                    }
+                }
+                uint8_t *tile = sa + stage * A_BYTES;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint4 v = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+                    *reinterpret_cast<uint4 *>(tile + tc::sw128_offset(row, half * 4 + q)) = v;
+                }
+                tc::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&full[stage]);
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+            // ---- epilogue: TMEM -> registers -> fp32 partial (column-major within the tile)
+            tc::mbar_wait(tfull, tphase);
+            tc::tc_fence_after();
+            tphase ^= 1;
+            const int lg = warp & 3, colhalf = (warp - GEN_WARP0) >> 2;
+            const int tile = u % p.ntiles, split = u / p.ntiles;
+            float *out = p.part + ((size_t)split * p.ntiles + tile) * (size_t)(BM * BN);
+#pragma unroll 1
+            for (int cb = 0; cb < 4; ++cb) {
+                const int col = colhalf * 128 + cb * 32;
+                uint32_t v[32];
+                tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)col, v);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int q = 0; q < 32; ++q) out[(size_t)(col + q) * BM + lg * 32 + lane] = __uint_as_float(v[q]) * p.epi_scale;
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tempty);
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc<TMEM_COLS>(tmem);
+    }
+}
+
+__global__ void reduce_part(const float *__restrict__ part, int splits, int ntiles, int ntn, int d, int n,
+                            double *__restrict__ out, int64_t ldo, int accumulate) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)d * n) return;
+    const int c = (int)(idx / d), i = (int)(idx % d);
+    const int tile = (i / BM) * ntn + c / BN;
+    const float *pp = part + (size_t)tile * (BM * BN) + (size_t)(c % BN) * BM + (i % BM);
+    double s = 0.0;
+    for (int k = 0; k < splits; ++k) s += (double)pp[(size_t)k * ntiles * (BM * BN)];
+    double *o = out + (int64_t)c * ldo + i;
+    *o = accumulate ? *o + s : s;
+}
+
+struct Plan {
+    int ntm, ntn, ntiles, splits, units;
+    int64_t kchunk, ldm;
+    size_t at_bytes, part_bytes;
+};
+
+Plan make_plan(int64_t m_local, int64_t n, int64_t d) {
+    Plan p;
+    p.ntm = (int)((d + BM - 1) / BM);
+    p.ntn = (int)((n + BN - 1) / BN);
+    p.ntiles = p.ntm * p.ntn;
+    const int sms = sm_count();
+    const int64_t nkb_total = (m_local + BK - 1) / BK;
+    int64_t target = (int64_t)32 * sms / p.ntiles;     // ~32 waves of units
+    if (target < 1) target = 1;
+    const int64_t smax = (nkb_total + 15) / 16;       // >= 16 K-blocks per unit
+    if (target > smax) target = smax;
+    if (target < 1) target = 1;
+    int64_t best = target;
+    for (int64_t s = target; s >= (target * 4) / 5 && s >= 1; --s)
+        if (((int64_t)p.ntiles * s) % sms == 0) { best = s; break; }
+    const int64_t kb_per = (nkb_total + best - 1) / best;
+    p.kchunk = kb_per * BK;
+    p.splits = (int)((m_local + p.kchunk - 1) / p.kchunk);
+    if (p.splits < 1) p.splits = 1;
+    p.units = p.ntiles * p.splits;
+    p.ldm = (m_local + 63) / 64 * 64;
+    p.at_bytes = align_up((size_t)n * p.ldm * sizeof(__half), 1024);
+    p.part_bytes = (size_t)p.splits * p.ntiles * BM * BN * sizeof(float);
+    return p;
+}
+
+}  // namespace sktc
+
+size_t sketch_tc_workspace(int64_t m_local, int64_t n, int64_t d) {
+    sktc::Plan p = sktc::make_plan(m_local, n, d);
+    return p.at_bytes + p.part_bytes + 1024;
+}
+
+int sketch_tc_run(int transform, const double *a, int64_t lda, int64_t m_local, int64_t row_offset, int64_t m_pad,
+                  int64_t n, const double *signs, const int64_t *rows, int64_t d, double *out, int64_t ldo,
+                  int accumulate, int *overflow_flag_dev, void *ws, size_t ws_bytes, cudaStream_t st) {
+    using namespace sktc;
+    Plan p = make_plan(m_local, n, d);
+    if (ws_bytes < p.at_bytes + p.part_bytes) {
+        set_error("sketch_tc: workspace %zu < %zu", ws_bytes, p.at_bytes + p.part_bytes);
+        return SK_ERR_ARG;
+    }
+    __half *at = static_cast<__half *>(ws);
+    float *part = reinterpret_cast<float *>(static_cast<uint8_t *>(ws) + p.at_bytes);
+    if (m_local == 0) {
+        if (!accumulate) {
+            for (int64_t c = 0; c < n; ++c) SK_CUDA(cudaMemsetAsync(out + c * ldo, 0, (size_t)d * sizeof(double), st));
+        }
+        return SK_OK;
+    }
+    dim3 pg((unsigned)((m_local + PT - 1) / PT), (unsigned)((n + PT - 1) / PT));
+    prep_f16t<<<pg, 256, 0, st>>>(a, lda, m_local, (int)n, signs, row_offset, at, p.ldm, overflow_flag_dev);
+    SK_LAUNCH_CHECK("prep_f16t");
+    CUtensorMap tmap;
+    int rc = make_tmap_2d(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, at, (uint64_t)m_local, (uint64_t)n,
+                          (uint64_t)p.ldm * sizeof(__half), BK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    Params prm;
+    prm.rows = rows;
+    prm.mpad = m_pad;
+    prm.row_offset = row_offset;
+    prm.m_local = m_local;
+    prm.kchunk = p.kchunk;
+    prm.n = (int)n;
+    prm.d = (int)d;
+    prm.ntn = p.ntn;
+    prm.ntiles = p.ntiles;
+    prm.units = p.units;
+    prm.wht = transform == SK_WHT;
+    prm.epi_scale = transform == SK_WHT ? (float)(1.0 / sqrt((double)m_pad)) : (float)sqrt(2.0 / (double)m_pad);
+    prm.part = part;
+    SK_CUDA(cudaFuncSetAttribute(sketch_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    const int grid = std::min(p.units, sm_count());
+    sketch_tc_kernel<<<grid, THREADS, SMEM, st>>>(tmap, prm);
+    SK_LAUNCH_CHECK("sketch_tc_kernel");
+    const int64_t total = d * n;
+    reduce_part<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(part, p.splits, p.ntiles, p.ntn, (int)d, (int)n, out,
+                                                                 ldo, accumulate);
+    SK_LAUNCH_CHECK("reduce_part");
+    return SK_OK;
+}
+
+}  // namespace sk

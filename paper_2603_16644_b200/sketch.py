@@ -80,10 +80,14 @@ class DeviceSketch:
         self.rows = torch.from_numpy(np.ascontiguousarray(op.sampled_rows, dtype=np.int64)).to(dev)
 
 
+ALGO = {"auto": 0, "dmma": 1, "tc": 2}
+
+
 def _sketch_sum(dsk: DeviceSketch, at: torch.Tensor, level_code: int, row_offset: int = 0,
                 out: torch.Tensor | None = None, accumulate: bool = False,
-                overflow_flag: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
-    """Unscaled partial sum (d x n, column-major) of Omega[:, rows of this block] A_block."""
+                overflow_flag: torch.Tensor | None = None, algo: str = "auto") -> tuple[torch.Tensor, torch.Tensor]:
+    """Unscaled partial sum (d x n, column-major) of Omega[:, rows of this block] A_block.
+    algo: "auto" (tcgen05 for binary16, DMMA otherwise), "tc" or "dmma"."""
     op = dsk.op
     m_local, n = at.shape
     d = op.d
@@ -92,10 +96,10 @@ def _sketch_sum(dsk: DeviceSketch, at: torch.Tensor, level_code: int, row_offset
         out = torch.zeros((n, d), dtype=torch.float64, device=dev)   # column-major d x n
     if overflow_flag is None:
         overflow_flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    wp, wn = WORKSPACE.get(_lib.lib().sk_sketch_workspace(m_local, n, d))
-    call("sk_sketch_partial", level_code, _lib.TRANSFORM_CODE[op.transform], at.data_ptr(), at.stride(0),
+    wp, wn = WORKSPACE.get(_lib.lib().sk_sketch_workspace(level_code, m_local, n, d))
+    call("sk_sketch_partial_ex", level_code, _lib.TRANSFORM_CODE[op.transform], at.data_ptr(), at.stride(0),
          m_local, row_offset, op.m_pad, n, dsk.signs.data_ptr(), dsk.rows.data_ptr(), d, out.data_ptr(),
-         d, int(accumulate), overflow_flag.data_ptr(), wp, wn, stream_handle())
+         d, int(accumulate), overflow_flag.data_ptr(), wp, wn, stream_handle(), ALGO[algo])
     return out, overflow_flag
 
 
