@@ -447,10 +447,17 @@ def hager(solve, n):
 def kappa0_estimate(a):
     """-> (kappa0, overflowed).  Everything binary64 on the full A."""
     a = as_float_matrix(a)
-    n = a.shape[1]
     w = a.astype(np.float64)
     with np.errstate(over="ignore", invalid="ignore", under="ignore"):
         g = w.T @ w
+    return kappa0_from_gram(g)
+
+
+def kappa0_from_gram(g):
+    """src/precision.py:231-251: the estimate given G = A^T A (row shards sum
+    their partial Grams first)."""
+    n = g.shape[0]
+    with np.errstate(over="ignore", invalid="ignore", under="ignore"):
         if not np.isfinite(g).all():
             return math.nan, True
         n1 = float(np.abs(g).sum(axis=0).max())

@@ -1,0 +1,209 @@
+"""Row-sharded Algorithm 1 over torch.distributed (one process per GPU).
+
+A and b are split into contiguous row blocks; rank g holds rows
+[offset_g, offset_g + m_g) and uses GLOBAL row indices for the sketch operator
+(signs, DCT phases), so partial results are exact pieces of the global ones.
+Every m-sized pass is local; the only exchanges are all-reduces of small
+results:
+
+  ||A||_F^2, ||r||^2            sum of 2 scalars
+  kappa0 Gram   A_g^T A_g       n x n   f64
+  sketch        Omega_g A_g     d x n   f64   (rounded to the level AFTER the sum)
+  demotion overflow flag        max
+  Gram + rhs    A_p,g^T [A_g|b_g] or A_p,g^T [A_p,g|b_g]   n x (n+1) f64
+
+The n x n work (kappa0 Cholesky/Hager, level QR of the sketch, LU/Cholesky) is
+replicated: every rank holds bit-identical inputs after the all-reduce, so all
+ranks take the same decisions (precision level, escalation, Cholesky->LU
+fallback) without further communication.
+
+The arithmetic is behind a small `ops` object so that the orchestration can be
+exercised on CPU with the gloo backend in the tests (with oracle arithmetic);
+production uses `DeviceOps` (libsklsq kernels + NCCL over NVLink).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .errors import DimensionMismatch, NotPositiveDefinite, RankDeficient
+from .precision import BINARY64, PrecisionDecision, PrecisionLevel, level_from_name, next_higher, select_precision
+from .sketch import DCT2, make_sketch
+from .solvers import Preconditioner, SolveReport, _Stages
+
+
+class DeviceOps:
+    """libsklsq kernels on this rank's GPU."""
+
+    def validate(self, a):
+        from .device import as_dmat
+        d = as_dmat(a)
+        return d.t, d.frob2
+
+    def vector(self, b, m):
+        from .device import as_dvec
+        return as_dvec(b, m)
+
+    def gram(self, x, y=None):
+        from .dense import _gram
+        return _gram(x, y)
+
+    def gemv_t(self, x, v):
+        from .dense import _gemv_t
+        return _gemv_t(x, v)
+
+    def sketch_partial(self, op, a_local, level, row_offset):
+        from .sketch import DeviceSketch, _sketch_sum
+        total, flag = _sketch_sum(DeviceSketch(op), a_local, level.code, row_offset=row_offset)
+        return total, flag.to(torch.float64)
+
+    def sketch_level_qr(self, total, op, level):
+        from .precision import _qr_level_dev
+        from .sketch import _sketch_finalize
+        a_s, _ = _sketch_finalize(total, op, level)
+        return _qr_level_dev(a_s, level, op.d, total.shape[0])
+
+    def trsm(self, a, r):
+        from .dense import _trsm
+        return _trsm(a, r)
+
+    def chol_solve(self, g, rhs):
+        from .dense import _chol_solve
+        return _chol_solve(g, rhs)
+
+    def lu_solve(self, g, rhs):
+        from .dense import _lu_solve
+        return _lu_solve(g, rhs)
+
+    def trsv(self, r, y):
+        from .dense import _trsv
+        return _trsv(r, y)
+
+    def kappa0_from_gram(self, g):
+        from .precision import _kappa0_from_gram
+        return _kappa0_from_gram(g)
+
+    def residual_sq(self, a, x, b):
+        """(||A_g x - b_g||^2, ||x||^2) by the sk_residual streaming kernel."""
+        import ctypes as C
+        from . import _lib
+        from .device import WORKSPACE, call, stream_handle
+        m, n = a.shape
+        out = (C.c_double * 2)()
+        wp, wn = WORKSPACE.get(_lib.lib().sk_matrix_stats_workspace(m, n))
+        call("sk_residual", a.data_ptr(), m, n, a.stride(0), x.data_ptr(), b.data_ptr(), None, out, wp, wn,
+             stream_handle())
+        return float(out[0]), float(out[1])
+
+
+def _allreduce(t: torch.Tensor, op=None) -> torch.Tensor:
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=op or dist.ReduceOp.SUM)
+    return t
+
+
+def _row_layout(m_local: int, device) -> tuple[int, int]:
+    """-> (global m, this rank's row offset) from the shard sizes."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return m_local, 0
+    world, rank = dist.get_world_size(), dist.get_rank()
+    sizes = torch.zeros(world, dtype=torch.int64, device=device)
+    sizes[rank] = m_local
+    dist.all_reduce(sizes)
+    sizes = sizes.cpu().tolist()
+    return int(sum(sizes)), int(sum(sizes[:rank]))
+
+
+def algorithm1_pipeline_sharded(a_local, b_local, method="pne", precision="auto", d_factor=3.0, transform=DCT2,
+                                seed=0, x_star=None, *, ops=None, diagnostics=False, stage_timing=False):
+    """Algorithm 1 (src/solvers.py:282-324) on row shards; returns the same
+    SolveReport on every rank.  `diagnostics` is accepted for signature parity;
+    the sharded path does not compute kappa_rs / kappa_ap (NaN)."""
+    ops = ops or DeviceOps()
+    stages = _Stages(stage_timing and torch.cuda.is_available())
+    stages.mark("check")
+    a, frob2_local = ops.validate(a_local)
+    m_local, n = a.shape
+    b = ops.vector(b_local, m_local)
+    if method not in ("pne", "hpne"):
+        raise ValueError(f"pipeline method must be pne or hpne, got {method!r}")
+    m, offset = _row_layout(m_local, a.device)
+    if m < n:
+        raise DimensionMismatch(f"need rows >= cols, got {(m, n)}")
+    t0 = time.perf_counter()
+    decision = None
+    if isinstance(precision, PrecisionLevel):
+        level = precision
+    elif precision == "auto":
+        stages.mark("kappa0")
+        g = _allreduce(ops.gram(a))
+        k0, over = ops.kappa0_from_gram(g)
+        decision = PrecisionDecision(kappa0=k0, selected=select_precision(k0, over), overflowed=over)
+        level = decision.selected
+    else:
+        level = level_from_name(precision)
+    d = int(math.ceil(d_factor * n))
+    if d < n:
+        raise ValueError(f"d_factor {d_factor} gives d={d} < n={n}")
+    op = make_sketch(m, d, transform, seed)
+    escalated_from = None
+    while True:
+        try:
+            stages.mark("sketch")
+            total, flag = ops.sketch_partial(op, a, level, offset)
+            _allreduce(total)
+            _allreduce(flag, dist.ReduceOp.MAX if dist.is_available() and dist.is_initialized() else None)
+            if float(flag.reshape(-1)[0]) > 0:
+                from .errors import Overflow
+                raise Overflow(f"input exceeds the {level.name} range")
+            stages.mark("level_qr")
+            r_s = ops.sketch_level_qr(total, op, level)
+            if bool((torch.diagonal(r_s) == 0).any()):
+                raise RankDeficient("sketched factor has a zero diagonal entry")
+            break
+        except RankDeficient:
+            wider = next_higher(level)
+            if escalated_from is not None or wider is None:
+                raise
+            escalated_from, level = level, wider
+    stages.mark("trsm")
+    a_p = ops.trsm(a, r_s)
+    stages.mark("gram")
+    if method == "pne":
+        g = _allreduce(ops.gram(a_p))
+    else:
+        g = _allreduce(ops.gram(a_p, a))
+    rhs = _allreduce(ops.gemv_t(a_p, b))
+    stages.mark("nxn")
+    if method == "pne":
+        try:
+            y = ops.chol_solve(g, rhs)
+        except NotPositiveDefinite:
+            y = ops.lu_solve(g, rhs)
+        x = ops.trsv(r_s, y)
+    else:
+        x = ops.lu_solve(g, rhs)
+    stages.mark("report")
+    rr, xx = ops.residual_sq(a, x, b)
+    sums = _allreduce(torch.tensor([rr, frob2_local], dtype=torch.float64, device=a.device))
+    stages.mark("end")
+    rr, frob2 = float(sums[0]), float(sums[1])
+    x_hat = x.detach().cpu().numpy()
+    res = math.sqrt(rr)
+    denom = math.sqrt(frob2) * math.sqrt(xx)
+    rel_err = None
+    if x_star is not None:
+        xs = np.asarray(x_star.detach().cpu() if isinstance(x_star, torch.Tensor) else x_star, dtype=np.float64)
+        rel_err = float(np.linalg.norm(x_hat - xs) / np.linalg.norm(xs))
+    pre = Preconditioner(r_s=r_s.detach().cpu().numpy(), computed_in=level, kappa_rs=math.nan, kappa_ap=math.nan,
+                         sketch_descriptor=op.descriptor(), _r_dev=r_s if r_s.is_cuda else None)
+    rep = SolveReport(method=method, x_hat=x_hat, residual_norm=res,
+                      relative_residual=res / denom if denom > 0 else math.inf, relative_error=rel_err,
+                      wall_ms=(time.perf_counter() - t0) * 1e3, preconditioner=pre,
+                      precision_decision=decision, escalated_from=escalated_from, stage_ms=stages.result())
+    return rep
