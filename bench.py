@@ -35,6 +35,9 @@ import time
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
+# A, A_p and the sketch operand are 64/64/16 GiB at config 3: avoid caching-allocator
+# fragmentation between the generator's and the solver's large blocks.
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
 METRIC = "PNE/HPNE solve time at 4M×2048 (1–8 GPUs); % of roofline; rel. error"
 
@@ -52,7 +55,7 @@ def parse():
     p.add_argument("--method", default="hpne", choices=["pne", "hpne"])
     p.add_argument("--precision", default="auto")
     p.add_argument("--seed", type=int, default=20261018)
-    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--e2e-steps", type=int, default=1)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", default="32768x256", help="oracle sample m x n for the CPU legs")
