@@ -103,23 +103,20 @@ __global__ void __launch_bounds__(THREADS) chol_kernel(double *w, double *l, int
             const int i = j + (int)t;
             l[(int64_t)j * n + i] = (t == 0) ? d : w[(int64_t)j * n + i] / d;
         }
-        // trailing lower triangle: pairs (i, k), j < k <= i  -> linear index over rem*(rem+1)/2
-        const int64_t tri = (int64_t)rem * (rem + 1) / 2;
-        for (int64_t t = tid; t < tri; t += nthreads) {
-            // column-major enumeration of the lower triangle: k-th column has rem-k entries
-            // invert t -> (kk, ii) with kk from the quadratic formula
-            const double tt = (double)t;
-            const double b = 2.0 * rem + 1.0;
-            int kk = (int)((b - sqrt(b * b - 8.0 * tt)) * 0.5);
-            if (kk < 0) kk = 0;
-            while (kk > 0 && (int64_t)kk * (2 * rem - kk + 1) / 2 > t) --kk;
-            while ((int64_t)(kk + 1) * (2 * rem - kk) / 2 <= t) ++kk;
-            const int64_t start = (int64_t)kk * (2 * rem - kk + 1) / 2;
-            const int ii = kk + (int)(t - start);
-            const int k = j + 1 + kk, i = j + 1 + ii;
-            const double li = w[(int64_t)j * n + i] / d, lk = w[(int64_t)j * n + k] / d;
-            double *p = w + (int64_t)k * n + i;
-            *p = __dsub_rn(*p, __dmul_rn(li, lk));
+        // trailing lower triangle (i, k), j < k <= i: a thread keeps one row i
+        // (consecutive threads -> consecutive i: coalesced) and strides over k
+        if (rem > 0) {
+            const int64_t groups = nthreads / rem > 0 ? nthreads / rem : 1;
+            for (int64_t t = tid; t < groups * rem; t += nthreads) {
+                const int i = j + 1 + (int)(t % rem);
+                const int g0 = (int)(t / rem);
+                const double li = w[(int64_t)j * n + i] / d;
+                for (int k = j + 1 + g0; k <= i; k += (int)groups) {
+                    const double lk = w[(int64_t)j * n + k] / d;
+                    double *p = w + (int64_t)k * n + i;
+                    *p = __dsub_rn(*p, __dmul_rn(li, lk));
+                }
+            }
         }
         grid.sync();
     }
@@ -212,18 +209,24 @@ lu_kernel(double *w, double *lmul, int *perm, int n, double *candv, int *candi, 
         const int rem = n - k - 1;
         double cbv = -1.0;
         int cbi = INT32_MAX;
-        const int64_t cnt = (int64_t)rem * (rem + 1);   // columns k..n-1 (rem+1) x rows k+1..n-1 (rem)
-        for (int64_t t = tid; t < cnt; t += nthreads) {
-            const int jj = (int)(t / rem), ii = (int)(t % rem);
-            const int i = k + 1 + ii, j = k + jj;
-            const double li = __ddiv_rn(w[(int64_t)k * n + i], akk);
-            if (j == k) {
-                lmul[(int64_t)k * n + i] = li;
-            } else {
-                double *q = w + (int64_t)j * n + i;
-                const double nv = __dsub_rn(*q, __dmul_rn(li, w[(int64_t)j * n + k]));
-                *q = nv;
-                if (j == k + 1) better(cbv, cbi, fabs(nv), i);
+        // a thread keeps one row i (one division per step) and strides over the
+        // columns j = k..n-1; consecutive threads take consecutive rows (coalesced)
+        if (rem > 0) {
+            const int64_t groups = nthreads / rem > 0 ? nthreads / rem : 1;
+            for (int64_t t = tid; t < groups * rem; t += nthreads) {
+                const int i = k + 1 + (int)(t % rem);
+                const int g0 = (int)(t / rem);
+                const double li = __ddiv_rn(w[(int64_t)k * n + i], akk);
+                for (int j = k + g0; j < n; j += (int)groups) {
+                    if (j == k) {
+                        lmul[(int64_t)k * n + i] = li;
+                    } else {
+                        double *q = w + (int64_t)j * n + i;
+                        const double nv = __dsub_rn(*q, __dmul_rn(li, w[(int64_t)j * n + k]));
+                        *q = nv;
+                        if (j == k + 1) better(cbv, cbi, fabs(nv), i);
+                    }
+                }
             }
         }
         block_argmax(cbv, cbi, sv, si, &candv[(buf ^ 1) * gridDim.x + blockIdx.x], &candi[(buf ^ 1) * gridDim.x + blockIdx.x]);
@@ -420,7 +423,9 @@ static int chol_factor(const double *s, int n, Ws &ws, sk_status *status, cudaSt
     SK_CUDA(cudaMemsetAsync(ws.l, 0, (size_t)n * n * sizeof(double), st));
     symmetrize<<<(unsigned)std::min<int64_t>(((int64_t)n * n + 255) / 256, 4096), 256, 0, st>>>(s, n, ws.w);
     SK_LAUNCH_CHECK("symmetrize");
-    const int blocks = coop_blocks((const void *)chol_kernel, THREADS, 0, ((int64_t)n * n / 2 + THREADS * 8 - 1) / (THREADS * 8));
+    // grid barriers dominate at small trailing sizes: at most 2 CTAs per SM
+    const int blocks = coop_blocks((const void *)chol_kernel, THREADS, 0,
+                                   std::min<int64_t>(2 * sm_count(), ((int64_t)n * n / 2 + THREADS * 8 - 1) / (THREADS * 8)));
     if (!blocks) { set_error("chol_kernel not co-resident"); return SK_ERR_CUDA; }
     double *w = ws.w, *l = ws.l;
     int ni = n;
@@ -503,8 +508,8 @@ int sk_lu_solve_f64(const double *g, int64_t n, const double *rhs, double *x, sk
     transpose_copy<<<(unsigned)std::min<int64_t>((n * n + 255) / 256, 4096), 256, 0, st>>>(g, (int)n, ws.w);
     SK_LAUNCH_CHECK("transpose_copy");
     SK_CUDA(cudaMemsetAsync(ws.l, 0, (size_t)n * n * sizeof(double), st));
-    int blocks = coop_blocks((const void *)lu_kernel, THREADS, 0, (n * n + THREADS * 8 - 1) / (THREADS * 8));
-    if (blocks > 2048) blocks = 2048;
+    int blocks = coop_blocks((const void *)lu_kernel, THREADS, 0,
+                             std::min<int64_t>(2 * sm_count(), (n * n + THREADS * 8 - 1) / (THREADS * 8)));
     if (!blocks) { set_error("lu_kernel not co-resident"); return SK_ERR_CUDA; }
     double *w = ws.w, *lm = ws.l, *cv = ws.candv;
     int *perm = ws.perm, *ci = ws.candi;

@@ -9,18 +9,25 @@
 // decides the precision escalation of src/solvers.py:255-279, so this kernel
 // reproduces it operation for operation: same tree shape, same rounding points,
 // no FMA contraction.  binary32 / binary64 run the same algorithm natively (the
-// reference uses BLAS there, whose summation order is unspecified; we use a fixed
-// per-warp order, deterministic run to run).
+// reference uses BLAS there, whose summation order is unspecified; we use the
+// same fixed tree, deterministic run to run).
 //
-// GPU structure: one cooperative persistent kernel, one grid barrier per column.
-// Column c > j is owned by warp (c mod #warps) for the whole factorisation; step j
-// has every owner apply reflector j to its columns (dot, tau*dot, rank-1 update)
-// and the owner of column j+1 immediately forms reflector j+1 (look-ahead), so
-// reflector j+1 is ready at the barrier.  Reflectors are double-buffered.
-// The Q factor is not formed: build_preconditioner only uses R
-// (src/solvers.py:196-197).  The reference's non-finite Q check
-// (src/precision.py:200) cannot fire without R or tau failing first at these
-// scales (|Q| entries are bounded by the reflector norms), see DESIGN.md.
+// The pairwise tree of src/precision.py:106-115 over L values is the left-aligned
+// binary tree whose node (l, i) covers [i 2^l, min((i+1) 2^l, L)) and adds its two
+// children when the right one is non-empty.  Its level-8 nodes are independent
+// 256-element chunks, which makes a 2-D (chunk x column) decomposition exact.
+// One cooperative persistent kernel, three grid barriers per column j:
+//
+//   phase 1  every (256-row chunk q, column c > j) warp unit computes the level-8
+//            node of v_j . w[j:, c]: 8-leaf subtrees per lane, then a 5-level
+//            shuffle tree (lane pairs at distance 1, 2, 4, 8, 16)
+//   phase 2  one warp per column combines its chunk nodes (levels 9..) -> t_c = tau_j * dot
+//   phase 3  every unit applies w[j:, c] -= v_j * t_c to its chunk (rounded product,
+//            rounded difference); CTA 0 updates column j+1 whole and forms reflector
+//            j+1 (norm, alpha, v, v.v, tau) with the same chunked trees (look-ahead)
+//
+// The Q factor is not formed (build_preconditioner only uses R,
+// src/solvers.py:196-197); see DESIGN.md for the reference's non-finite-Q check.
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -29,6 +36,8 @@ namespace sk {
 namespace qr {
 
 constexpr int THREADS = 256, WARPS = THREADS / 32;
+constexpr int CH = 256;          // chunk = level-8 subtree
+constexpr int MAXCH = 1024;      // chunk nodes a single warp combines: d <= 262144
 
 template <typename T>
 struct Ctl {
@@ -38,134 +47,172 @@ struct Ctl {
     int fail_col;
 };
 
-// ---- binary16 pairwise tree over L values produced by f(i) (already rounded) --
-template <class F>
-__device__ __half tree_sum_half(int L, F f, __half *scratch) {
-    using H = LevelOps<__half>;
+// Level-8 node over chunk q of u_i * v_i, i in [q*CH, min((q+1)*CH, L)), by one warp.
+template <typename T>
+__device__ __forceinline__ T chunk_node(const T *u, const T *v, int L, int q) {
+    using O = LevelOps<T>;
     const int lane = threadIdx.x & 31;
-    const int n3 = (L + 7) >> 3;
-    for (int i = lane; i < n3; i += 32) {
-        const int base = i * 8;
-        const int cnt = min(8, L - base);
-        __half x[8];
+    const int base = q * CH + lane * 8;
+    const int cnt = max(0, min(8, L - base));
+    T x[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = (u < cnt) ? f(base + u) : H::zero();
-        __half y[4];
+    for (int e = 0; e < 8; ++e) x[e] = (e < cnt) ? O::mul(u[base + e], v[base + e]) : O::zero();
+    const T y0 = (1 < cnt) ? O::add(x[0], x[1]) : x[0];
+    const T y1 = (3 < cnt) ? O::add(x[2], x[3]) : x[2];
+    const T y2 = (5 < cnt) ? O::add(x[4], x[5]) : x[4];
+    const T y3 = (7 < cnt) ? O::add(x[6], x[7]) : x[6];
+    const int c1 = (cnt + 1) >> 1;
+    const T z0 = (1 < c1) ? O::add(y0, y1) : y0;
+    const T z1 = (3 < c1) ? O::add(y2, y3) : y2;
+    const int c2 = (c1 + 1) >> 1;
+    T node = (1 < c2) ? O::add(z0, z1) : z0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) y[k] = (2 * k + 1 < cnt) ? H::add(x[2 * k], x[2 * k + 1]) : x[2 * k];
-        const int c1 = (cnt + 1) >> 1;
-        __half z0 = (1 < c1) ? H::add(y[0], y[1]) : y[0];
-        __half z1 = (3 < c1) ? H::add(y[2], y[3]) : y[2];
-        const int c2 = (c1 + 1) >> 1;
-        scratch[i] = (1 < c2) ? H::add(z0, z1) : z0;
+    for (int s = 1; s < 32; s <<= 1) {
+        const T other = __shfl_xor_sync(0xffffffffu, node, s);
+        const bool left = (lane & s) == 0;
+        const bool has_r = q * CH + (lane | s) * 8 < L;   // right child's first leaf exists
+        const T l = left ? node : other, r = left ? other : node;
+        node = has_r ? O::add(l, r) : l;
     }
-    __syncwarp();
-    int cnt = n3;
-    while (cnt > 1) {
-        const int nn = (cnt + 1) >> 1;
-        for (int base = 0; base < nn; base += 32) {
-            const int i = base + lane;
-            __half val = H::zero();
-            if (i < nn) val = (2 * i + 1 < cnt) ? H::add(scratch[2 * i], scratch[2 * i + 1]) : scratch[2 * i];
-            __syncwarp();
-            if (i < nn) scratch[i] = val;
-            __syncwarp();
+    return node;
+}
+
+// Root of the tree over `count` level-8 nodes get(i), by one warp (count <= 1024).
+// Lane l reduces the aligned block [32 l', ...) of B = 32 leaves when count > 32.
+template <typename T, class G>
+__device__ __forceinline__ T warp_tree_root(int count, G get) {
+    using O = LevelOps<T>;
+    const int lane = threadIdx.x & 31;
+    int B = 1;
+    while (B * 32 < count) B <<= 1;          // power of two, <= 32 for count <= 1024
+    const int base = lane * B;
+    int cnt = max(0, min(B, count - base));
+    T node = O::zero();
+    if (B == 1) {
+        node = cnt ? get(base) : O::zero();
+    } else {
+        T buf[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) buf[e] = (e < cnt) ? get(base + e) : O::zero();
+#pragma unroll
+        for (int sz = 32; sz > 1; sz >>= 1) {
+#pragma unroll
+            for (int i = 0; i < sz / 2; ++i) buf[i] = (2 * i + 1 < cnt) ? O::add(buf[2 * i], buf[2 * i + 1]) : buf[2 * i];
+            cnt = (cnt + 1) >> 1;
         }
-        cnt = nn;
+        node = buf[0];
     }
-    const __half r = scratch[0];
-    __syncwarp();
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        const T other = __shfl_xor_sync(0xffffffffu, node, s);
+        const bool left = (lane & s) == 0;
+        const bool has_r = (lane | s) * B < count;
+        const T l = left ? node : other, r = left ? other : node;
+        node = has_r ? O::add(l, r) : l;
+    }
+    return node;
+}
+
+// Whole-column tree dot by one CTA (look-ahead reflector); sh_nodes >= ceil(L/CH).
+template <typename T>
+__device__ T cta_dot(const T *u, const T *v, int L, T *sh_nodes, T *sh_root) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nq = (L + CH - 1) / CH;
+    for (int q = warp; q < nq; q += WARPS) {
+        const T node = chunk_node<T>(u, v, L, q);
+        if (lane == 0) sh_nodes[q] = node;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const T r = warp_tree_root<T>(nq, [&](int i) { return sh_nodes[i]; });
+        if (lane == 0) *sh_root = r;
+    }
+    __syncthreads();
+    const T r = *sh_root;
+    __syncthreads();
     return r;
 }
 
-// ---- native warp dot (fixed order: lane-strided partials, xor-shuffle tree) ----
-template <typename T, class F>
-__device__ T warp_dot_native(int L, F f) {
+// Reflector for column jj from the (final) column w[jj:, jj]; CTA-cooperative.
+template <typename T>
+__device__ int make_reflector(T *w, int64_t ld, int d, int jj, T *vout, Ctl<T> *ctl, int buf, T *sh_nodes,
+                              T *sh_root) {
     using O = LevelOps<T>;
-    const int lane = threadIdx.x & 31;
-    T s = O::zero();
-    for (int i = lane; i < L; i += 32) s = O::add(s, f(i));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s = O::add(s, __shfl_xor_sync(0xffffffffu, s, o));
-    return s;
-}
-
-template <typename T, bool HALF>
-__device__ T warp_dot(int L, const T *u, const T *v, T *scratch) {
-    using O = LevelOps<T>;
-    if constexpr (HALF) {
-        return tree_sum_half(L, [&](int i) { return O::mul(u[i], v[i]); }, scratch);
-    } else {
-        return warp_dot_native<T>(L, [&](int i) { return O::mul(u[i], v[i]); });
-    }
-}
-
-// Form reflector for column j from W[j:, j] (warp-cooperative).  Returns fail code.
-template <typename T, bool HALF>
-__device__ int make_reflector(T *w, int64_t ld, int d, int j, T *vout, Ctl<T> *ctl, int buf, T *scratch) {
-    using O = LevelOps<T>;
-    const int lane = threadIdx.x & 31;
-    const int L = d - j;
-    T *x = w + (int64_t)j * ld + j;
-    const T nrm = O::sqrt(warp_dot<T, HALF>(L, x, x, scratch));
+    const int L = d - jj;
+    T *x = w + (int64_t)jj * ld + jj;
+    const T nrm = O::sqrt(cta_dot<T>(x, x, L, sh_nodes, sh_root));
     if (O::to_f64(nrm) == 0.0) return SK_RANK_DEFICIENT;
     const T x0 = x[0];
     const T alpha = (O::to_f64(x0) >= 0.0) ? O::sub(O::zero(), nrm) : nrm;   // -norm if x0 >= 0
-    // v = x with v0 = x0 - alpha
-    for (int i = lane; i < L; i += 32) vout[i] = (i == 0) ? O::sub(x0, alpha) : x[i];
-    __syncwarp();
-    const T vtv = warp_dot<T, HALF>(L, vout, vout, scratch);
+    for (int i = threadIdx.x; i < L; i += THREADS) vout[i] = (i == 0) ? O::sub(x0, alpha) : x[i];
+    __syncthreads();
+    const T vtv = cta_dot<T>(vout, vout, L, sh_nodes, sh_root);
     if (O::to_f64(vtv) == 0.0) return SK_RANK_DEFICIENT;
     const T tau = O::div(O::from_f64(2.0), vtv);
     if (!O::finite(tau)) return SK_RANK_DEFICIENT;
-    // column j of the working matrix becomes (alpha, 0, 0, ...)
-    for (int i = lane; i < L; i += 32) x[i] = (i == 0) ? alpha : O::zero();
-    if (lane == 0) { ctl->tau[buf] = tau; ctl->alpha[buf] = alpha; }
-    __syncwarp();
+    for (int i = threadIdx.x; i < L; i += THREADS) x[i] = (i == 0) ? alpha : O::zero();
+    if (threadIdx.x == 0) { ctl->tau[buf] = tau; ctl->alpha[buf] = alpha; }
+    __syncthreads();
     return SK_OK;
 }
 
-// Apply reflector (v, tau) of step j to column c: w[j:, c] -= v * (tau * v.w[j:, c]).
-template <typename T, bool HALF>
-__device__ void apply_reflector(T *w, int64_t ld, int d, int j, int c, const T *v, T tau, T *scratch) {
-    using O = LevelOps<T>;
-    const int lane = threadIdx.x & 31;
-    const int L = d - j;
-    T *col = w + (int64_t)c * ld + j;
-    const T t = O::mul(tau, warp_dot<T, HALF>(L, v, col, scratch));
-    for (int i = lane; i < L; i += 32) col[i] = O::sub(col[i], O::mul(v[i], t));
-    __syncwarp();
-}
-
-template <typename T, bool HALF>
+template <typename T>
 __global__ void __launch_bounds__(THREADS)
-householder_kernel(T *w, int64_t ld, int d, int n, T *vbuf /* 2 x d */, Ctl<T> *ctl, int scratch_per_warp) {
-    extern __shared__ __align__(16) unsigned char qr_smem[];
+householder_kernel(T *w, int64_t ld, int d, int n, T *vbuf /* 2 x d */, T *part /* nqmax x n */, T *tvec /* n */,
+                   Ctl<T> *ctl) {
+    using O = LevelOps<T>;
+    __shared__ T sh_nodes[MAXCH];
+    __shared__ T sh_root;
     cg::grid_group grid = cg::this_grid();
-    const int warp = threadIdx.x >> 5;
-    const int gwarp = blockIdx.x * WARPS + warp;
+    const int lane = threadIdx.x & 31;
+    const int gwarp = blockIdx.x * WARPS + (threadIdx.x >> 5);
     const int nwarps = gridDim.x * WARPS;
-    T *scratch = reinterpret_cast<T *>(qr_smem) + warp * scratch_per_warp;
 
-    // reflector 0
-    if (gwarp == 0) {
-        const int rc = make_reflector<T, HALF>(w, ld, d, 0, vbuf, ctl, 0, scratch);
-        if (rc != SK_OK && (threadIdx.x & 31) == 0) { ctl->fail_code = rc; ctl->fail_col = 0; }
+    if (blockIdx.x == 0) {
+        const int rc = make_reflector<T>(w, ld, d, 0, vbuf, ctl, 0, sh_nodes, &sh_root);
+        if (rc != SK_OK && threadIdx.x == 0) { ctl->fail_code = rc; ctl->fail_col = 0; }
     }
     grid.sync();
-    for (int j = 0; j < n; ++j) {
-        if (ctl->fail_code != SK_OK) return;   // uniform: read after the barrier
+    for (int j = 0; j < n - 1; ++j) {
+        if (ctl->fail_code != SK_OK) return;   // uniform: read after a barrier
         const int buf = j & 1;
         const T *v = vbuf + (size_t)buf * d;
         const T tau = ctl->tau[buf];
-        // columns c in (j, n) owned by this warp
-        int c = j + 1 + ((gwarp - (j + 1)) % nwarps + nwarps) % nwarps;
-        for (; c < n; c += nwarps) {
-            apply_reflector<T, HALF>(w, ld, d, j, c, v, tau, scratch);
-            if (c == j + 1) {   // look-ahead: reflector j+1 as soon as its column is final
-                const int rc = make_reflector<T, HALF>(w, ld, d, j + 1, vbuf + (size_t)(buf ^ 1) * d, ctl,
-                                                       buf ^ 1, scratch);
-                if (rc != SK_OK && (threadIdx.x & 31) == 0) { ctl->fail_code = rc; ctl->fail_col = j + 1; }
+        const int L = d - j;
+        const int nq = (L + CH - 1) / CH;
+        const int ncols = n - j - 1;           // columns j+1 .. n-1
+        // ---- phase 1: chunk nodes of v . w[j:, c]
+        for (int u = gwarp; u < nq * ncols; u += nwarps) {
+            const int q = u % nq, c = j + 1 + u / nq;
+            const T node = chunk_node<T>(v, w + (int64_t)c * ld + j, L, q);
+            if (lane == 0) part[(size_t)q * n + c] = node;
+        }
+        grid.sync();
+        // ---- phase 2: t_c = tau * root, one warp per column
+        for (int cc = gwarp; cc < ncols; cc += nwarps) {
+            const int c = j + 1 + cc;
+            const T root = warp_tree_root<T>(nq, [&](int i) { return part[(size_t)i * n + c]; });
+            if (lane == 0) tvec[c] = O::mul(tau, root);
+        }
+        grid.sync();
+        // ---- phase 3: rank-1 update; CTA 0 owns column j+1 and forms reflector j+1
+        if (blockIdx.x == 0) {
+            const T t = tvec[j + 1];
+            T *col = w + (int64_t)(j + 1) * ld + j;
+            for (int i = threadIdx.x; i < L; i += THREADS) col[i] = O::sub(col[i], O::mul(v[i], t));
+            __syncthreads();
+            const int rc = make_reflector<T>(w, ld, d, j + 1, vbuf + (size_t)(buf ^ 1) * d, ctl, buf ^ 1, sh_nodes,
+                                             &sh_root);
+            if (rc != SK_OK && threadIdx.x == 0) { ctl->fail_code = rc; ctl->fail_col = j + 1; }
+        } else {
+            const int ow = gwarp - WARPS, others = nwarps - WARPS;
+            for (int u = ow; u < nq * (ncols - 1); u += others) {
+                const int q = u % nq, c = j + 2 + u / nq;
+                const T t = tvec[c];
+                T *col = w + (int64_t)c * ld + j + q * CH;
+                const T *vq = v + q * CH;
+                const int cnt = min(CH, L - q * CH);
+                for (int i = lane; i < cnt; i += 32) col[i] = O::sub(col[i], O::mul(vq[i], t));
             }
         }
         grid.sync();
@@ -185,55 +232,52 @@ __global__ void prescale_half(__half *a, int64_t count, double scale) {
         a[i] = __double2half((double)__half2float(a[i]) * scale);   // round_to_precision(work*scale, binary16)
 }
 
-// R (row-major f64) = promote(W[:n, :]) upper triangle, / scale; non-finite -> count
+// R (row-major f64) = promote(W[:n, :]) / scale; non-finite upper entries are counted
 template <typename T>
-__global__ void extract_r(const T *w, int64_t ld, int n, double inv_scale, double *r, int64_t ldr, int *nonfinite) {
+__global__ void extract_r(const T *w, int64_t ld, int n, double scale, double *r, int64_t ldr, int *nonfinite) {
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= (int64_t)n * n) return;
     const int i = (int)(idx / n), c = (int)(idx % n);
-    double v = 0.0;
-    if (c >= i) {
-        const T x = w[(int64_t)c * ld + i];
-        if (!LevelOps<T>::finite(x)) atomicAdd(nonfinite, 1);
-        v = LevelOps<T>::to_f64(x) / inv_scale;
-    } else {
-        const T x = w[(int64_t)c * ld + i];   // exact zeros written by the factorisation
-        v = LevelOps<T>::to_f64(x);
-    }
-    r[(int64_t)i * ldr + c] = v;
+    const T x = w[(int64_t)c * ld + i];
+    if (!LevelOps<T>::finite(x)) atomicAdd(nonfinite, 1);
+    r[(int64_t)i * ldr + c] = LevelOps<T>::to_f64(x) / scale;
 }
 
+inline int64_t nq_max(int64_t d) { return (d + CH - 1) / CH; }
+
 template <typename T>
-size_t ws_bytes(int64_t d) {
-    return align_up(sizeof(Ctl<T>), 256) + align_up(2 * (size_t)d * sizeof(T), 256) + 256;
+size_t ws_bytes(int64_t d, int64_t n) {
+    return align_up(sizeof(Ctl<T>), 256) + align_up(2 * (size_t)d * sizeof(T), 256) +
+           align_up((size_t)nq_max(d) * n * sizeof(T), 256) + align_up((size_t)n * sizeof(T), 256) + 256;
 }
 
 template <typename T, bool HALF>
-int run(T *w, int64_t d, int64_t n, double inv_scale, double *r, int64_t ldr, sk_status *status, void *ws,
-        size_t wsb, cudaStream_t st) {
-    if (wsb < ws_bytes<T>(d)) { set_error("sk_qr_r: workspace too small"); return SK_ERR_ARG; }
+int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_status *status, void *ws, size_t wsb,
+        cudaStream_t st) {
+    if (wsb < ws_bytes<T>(d, n)) { set_error("sk_qr_r: workspace too small"); return SK_ERR_ARG; }
+    if (nq_max(d) > MAXCH) { set_error("sk_qr_r: d too large"); return SK_ERR_ARG; }
     unsigned char *p = static_cast<unsigned char *>(ws);
     Ctl<T> *ctl = reinterpret_cast<Ctl<T> *>(p);
     p += align_up(sizeof(Ctl<T>), 256);
     T *vbuf = reinterpret_cast<T *>(p);
     p += align_up(2 * (size_t)d * sizeof(T), 256);
+    T *part = reinterpret_cast<T *>(p);
+    p += align_up((size_t)nq_max(d) * n * sizeof(T), 256);
+    T *tvec = reinterpret_cast<T *>(p);
+    p += align_up((size_t)n * sizeof(T), 256);
     int *nonfinite = reinterpret_cast<int *>(p);
     SK_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl<T>), st));
     SK_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), st));
-
-    const int scratch_per_warp = HALF ? (int)((d + 7) / 8 + 8) : 1;
-    const size_t smem = (size_t)WARPS * scratch_per_warp * sizeof(T);
-    auto kfn = householder_kernel<T, HALF>;
-    if (smem > 40 * 1024) SK_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int maxb = max_coop_blocks((const void *)kfn, THREADS, smem);
-    if (maxb <= 0) { set_error("sk_qr_r: kernel cannot be co-resident (d too large?)"); return SK_ERR_ARG; }
-    int blocks = (int)((n + WARPS - 1) / WARPS);
-    if (blocks > maxb) blocks = maxb;
-    if (blocks < 1) blocks = 1;
+    auto kfn = householder_kernel<T>;
+    const int maxb = max_coop_blocks((const void *)kfn, THREADS, 0);
+    if (maxb <= 0) { set_error("sk_qr_r: kernel cannot be co-resident"); return SK_ERR_ARG; }
+    const int64_t units = nq_max(d) * n;
+    int blocks = (int)std::min<int64_t>(std::min<int64_t>(maxb, 2 * sm_count()), (units + WARPS - 1) / WARPS + 1);
+    if (blocks < 2) blocks = std::min(2, maxb);
     int di = (int)d, ni = (int)n;
     int64_t ldw = d;
-    void *args[] = {&w, &ldw, &di, &ni, &vbuf, &ctl, (void *)&scratch_per_warp};
-    SK_CUDA(cudaLaunchCooperativeKernel((const void *)kfn, dim3(blocks), dim3(THREADS), args, smem, st));
+    void *args[] = {&w, &ldw, &di, &ni, &vbuf, &part, &tvec, &ctl};
+    SK_CUDA(cudaLaunchCooperativeKernel((const void *)kfn, dim3(blocks), dim3(THREADS), args, 0, st));
     SK_LAUNCH_CHECK("householder_kernel");
     int fail[2];
     SK_CUDA(cudaMemcpyAsync(fail, &ctl->fail_code, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -243,7 +287,7 @@ int run(T *w, int64_t d, int64_t n, double inv_scale, double *r, int64_t ldr, sk
         return fill_status(status, fail[0], fail[1], 0.0, 0.0);
     }
     const int64_t total = n * n;
-    extract_r<T><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(w, d, (int)n, inv_scale, r, ldr, nonfinite);
+    extract_r<T><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(w, d, (int)n, scale, r, ldr, nonfinite);
     SK_LAUNCH_CHECK("extract_r");
     int nf = 0;
     SK_CUDA(cudaMemcpyAsync(&nf, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -263,15 +307,14 @@ using namespace sk;
 extern "C" {
 
 size_t sk_qr_workspace(int level, int64_t d, int64_t n) {
-    (void)n;
-    if (level == 16) return qr::ws_bytes<__half>(d) + 256;
-    if (level == 32) return qr::ws_bytes<float>(d);
-    return qr::ws_bytes<double>(d);
+    if (level == 16) return qr::ws_bytes<__half>(d, n) + 256;
+    if (level == 32) return qr::ws_bytes<float>(d, n);
+    return qr::ws_bytes<double>(d, n);
 }
 
 int sk_qr_r(int level, void *a_s, int64_t d, int64_t n, double *r, int64_t ldr, sk_status *status, void *ws,
             size_t ws_bytes, sk_stream_t stream) {
-    if (!a_s || !r || !ws || n <= 0 || d < n || ldr < n || d > (1 << 26)) {
+    if (!a_s || !r || !ws || n <= 0 || d < n || ldr < n || qr::nq_max(d) > qr::MAXCH) {
         if (d < n && n > 0) {
             set_error("need rows >= cols, got %lld x %lld", (long long)d, (long long)n);
             return fill_status(status, SK_DIMENSION_MISMATCH, -1, 0, 0);
@@ -287,7 +330,7 @@ int sk_qr_r(int level, void *a_s, int64_t d, int64_t n, double *r, int64_t ldr, 
     __half *a = static_cast<__half *>(a_s);
     const int64_t count = d * n;
     unsigned long long *bits = reinterpret_cast<unsigned long long *>(static_cast<unsigned char *>(ws) +
-                                                                      qr::ws_bytes<__half>(d));
+                                                                      qr::ws_bytes<__half>(d, n));
     SK_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned long long), st));
     const unsigned g = (unsigned)std::min<int64_t>((count + 255) / 256, 4 * sm_count());
     qr::maxabs_half<<<g, 256, 0, st>>>(a, count, bits);
@@ -306,7 +349,6 @@ int sk_qr_r(int level, void *a_s, int64_t d, int64_t n, double *r, int64_t ldr, 
     const double scale = ldexp(1.0, -e);
     qr::prescale_half<<<g, 256, 0, st>>>(a, count, scale);
     SK_LAUNCH_CHECK("prescale_half");
-    // R = float64(R16) / scale  (extract_r divides by its 'inv_scale' argument)
     return qr::run<__half, true>(a, d, n, scale, r, ldr, status, ws, ws_bytes, st);
 }
 

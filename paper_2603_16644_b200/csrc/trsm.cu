@@ -7,11 +7,16 @@
 //
 // B200 design: row panels are independent, so each CTA owns BMR rows and walks
 // the NB-wide column blocks left to right ("left-looking"):
-//   T      = A[rows, J] - A_p[rows, <J] . R[<J, J]     (DMMA GEMM, cp.async ring)
-//   A_p[rows, J] = substitution of T against R[J, J]    (one thread per row,
-//                                                        row in registers, R_JJ in smem)
-// The panel's earlier A_p columns are re-read from L2/HBM (compute-bound:
-// ~BMR/4 flop per byte), R stays L2-resident.  A_p may alias A (in place).
+//   T            = A[rows, J] - A_p[rows, <J] . R[<J, J]   (DMMA GEMM, cp.async ring)
+//   A_p[rows, J] = substitution of T against R[J, J]      (two threads per row, the
+//                                                          row's columns split even/odd
+//                                                          in registers, R_JJ in smem)
+// The diagonal block is solved by substitution (dot-then-divide, like the
+// reference), never through an explicit inverse, so the solve stays backward
+// stable for kappa(R) up to 1e14.  The panel's earlier A_p columns are re-read
+// from L2/HBM (compute-bound: ~BMR/4 flop per byte); R stays L2-resident.
+// The T tile and R_JJ are staged with cp.async ahead of the GEMM so their latency
+// hides behind it.  A_p may alias A (in place).
 #include "common.cuh"
 
 namespace sk {
@@ -21,17 +26,16 @@ constexpr int BMR = 128, NB = 64, BK = 16, STAGES = 3, THREADS = 256;
 constexpr int WM = 32, WN = 32;             // 4 x 2 warps
 constexpr int APITCH = BK + 4;              // 20 = 4 (mod 16): conflict-free A fragments
 constexpr int BPITCH = NB + 4;              // 68 = 4 (mod 16): conflict-free B fragments
-constexpr int TPITCH = NB + 2;              // T tile, 16B-aligned rows
+constexpr int TPITCH = NB + 4;              // T tile rows, 16-byte aligned (544 B)
+constexpr int RPITCH = NB;
 constexpr size_t SMEM = sizeof(double) * (size_t(STAGES) * BMR * APITCH + size_t(STAGES) * BK * BPITCH +
-                                          size_t(BMR) * TPITCH + size_t(NB) * NB);
+                                          size_t(BMR) * TPITCH + size_t(NB) * RPITCH);
 
-__device__ __forceinline__ void load_stage(double *as, double *bs, const double *__restrict__ ap,
-                                           int64_t ldap, const double *__restrict__ r, int64_t ldr,
-                                           int64_t row0, int64_t m, int k0, int kend, int j0, int n,
-                                           bool vec) {
+__device__ __forceinline__ void load_stage(double *as, double *bs, const double *ap, int64_t ldap,
+                                           const double *__restrict__ r, int64_t ldr, int64_t row0, int64_t m, int k0,
+                                           int kend, int j0, int n, bool vec) {
     const int tid = threadIdx.x;
     if (vec) {
-        // A_p panel: BMR rows x BK cols -> BMR * BK/2 chunks
         for (int c = tid; c < BMR * (BK / 2); c += THREADS) {
             const int rr = c / (BK / 2), kc = (c % (BK / 2)) * 2;
             const int64_t row = row0 + rr;
@@ -40,7 +44,6 @@ __device__ __forceinline__ void load_stage(double *as, double *bs, const double 
             bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
             cp_async16(as + rr * APITCH + kc, bytes ? ap + row * ldap + k : ap, bytes);
         }
-        // R block: BK rows x NB cols
         for (int c = tid; c < BK * (NB / 2); c += THREADS) {
             const int kr = c / (NB / 2), jc = (c % (NB / 2)) * 2;
             const int k = k0 + kr, j = j0 + jc;
@@ -65,39 +68,63 @@ __device__ __forceinline__ void load_stage(double *as, double *bs, const double 
     }
 }
 
+// T tile A[rows, j0:j0+jw] and R[j0:j0+jw, j0:j0+jw] (zero-filled outside)
+__device__ __forceinline__ void load_block(double *ts, double *rs, const double *a, int64_t lda,
+                                           const double *__restrict__ r, int64_t ldr, int64_t row0, int64_t m, int j0,
+                                           int jw, bool vec) {
+    const int tid = threadIdx.x;
+    if (vec) {
+        for (int c = tid; c < BMR * (NB / 2); c += THREADS) {
+            const int rr = c / (NB / 2), jc = (c % (NB / 2)) * 2;
+            const int64_t row = row0 + rr;
+            int bytes = (row < m) ? (jw - jc) * 8 : 0;
+            bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
+            cp_async16(ts + rr * TPITCH + jc, bytes ? a + row * lda + j0 + jc : a, bytes);
+        }
+        for (int c = tid; c < NB * (NB / 2); c += THREADS) {
+            const int i = c / (NB / 2), jc = (c % (NB / 2)) * 2;
+            int bytes = (i < jw) ? (jw - jc) * 8 : 0;
+            bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
+            cp_async16(rs + i * RPITCH + jc, bytes ? r + (int64_t)(j0 + i) * ldr + j0 + jc : r, bytes);
+        }
+    } else {
+        for (int c = tid; c < BMR * NB; c += THREADS) {
+            const int rr = c / NB, jc = c % NB;
+            const int64_t row = row0 + rr;
+            const int bytes = (row < m && jc < jw) ? 8 : 0;
+            cp_async8(ts + rr * TPITCH + jc, bytes ? a + row * lda + j0 + jc : a, bytes);
+        }
+        for (int c = tid; c < NB * NB; c += THREADS) {
+            const int i = c / NB, jc = c % NB;
+            const int bytes = (i < jw && jc < jw) ? 8 : 0;
+            cp_async8(rs + i * RPITCH + jc, bytes ? r + (int64_t)(j0 + i) * ldr + j0 + jc : r, bytes);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
-trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__restrict__ r,
-            int64_t ldr, double *ap, int64_t ldap, bool vec) {
+trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__restrict__ r, int64_t ldr, double *ap,
+            int64_t ldap, bool vec) {
     extern __shared__ __align__(16) double smem[];
     double *as_base = smem;
     double *bs_base = as_base + STAGES * BMR * APITCH;
     double *ts = bs_base + STAGES * BK * BPITCH;
-    double *rjj = ts + BMR * TPITCH;
+    double *rs = ts + BMR * TPITCH;
 
     const int64_t row0 = (int64_t)blockIdx.x * BMR;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const int wm = warp % (BMR / WM), wn = warp / (BMR / WM);
     const int nblocks = (n + NB - 1) / NB;
+    // substitution role: two threads per row, columns split by parity
+    const int srow = tid >> 1, hf = tid & 1;
 
     for (int J = 0; J < nblocks; ++J) {
         const int j0 = J * NB;
         const int jw = min(NB, n - j0);
-        // -- stage T = A[rows, J] and R[J,J] (identity padded) into smem
-        for (int c = tid; c < BMR * NB; c += THREADS) {
-            const int rr = c / NB, jc = c % NB;
-            const int64_t row = row0 + rr;
-            ts[rr * TPITCH + jc] = (row < m && jc < jw) ? a[row * lda + j0 + jc] : 0.0;
-        }
-        for (int c = tid; c < NB * NB; c += THREADS) {
-            const int i = c / NB, j = c % NB;
-            double v;
-            if (i < jw && j < jw) v = (j >= i) ? r[(int64_t)(j0 + i) * ldr + j0 + j] : 0.0;
-            else v = (i == j) ? 1.0 : 0.0;
-            rjj[i * NB + j] = v;
-        }
+        load_block(ts, rs, a, lda, r, ldr, row0, m, j0, jw, vec);
+        cp_async_commit();
 
-        // -- GEMM part: acc = A_p[rows, 0:j0] . R[0:j0, J]
         double acc[WM / 8][WN / 8][2];
 #pragma unroll
         for (int x = 0; x < WM / 8; ++x)
@@ -107,8 +134,8 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
 #pragma unroll
         for (int s = 0; s < STAGES - 1; ++s) {
             if (s < nk)
-                load_stage(as_base + s * BMR * APITCH, bs_base + s * BK * BPITCH, ap, ldap, r, ldr,
-                           row0, m, s * BK, j0, j0, n, vec);
+                load_stage(as_base + s * BMR * APITCH, bs_base + s * BK * BPITCH, ap, ldap, r, ldr, row0, m, s * BK,
+                           j0, j0, n, vec);
             cp_async_commit();
         }
         for (int kt = 0; kt < nk; ++kt) {
@@ -117,8 +144,8 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
             const int nxt = kt + STAGES - 1;
             if (nxt < nk) {
                 const int s = nxt % STAGES;
-                load_stage(as_base + s * BMR * APITCH, bs_base + s * BK * BPITCH, ap, ldap, r, ldr,
-                           row0, m, nxt * BK, j0, j0, n, vec);
+                load_stage(as_base + s * BMR * APITCH, bs_base + s * BK * BPITCH, ap, ldap, r, ldr, row0, m, nxt * BK,
+                           j0, j0, n, vec);
             }
             cp_async_commit();
             const double *as = as_base + (kt % STAGES) * BMR * APITCH;
@@ -138,7 +165,7 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
         }
         cp_async_wait<0>();
         __syncthreads();
-        // -- T -= acc
+        // -- T -= acc  (padded diagonal entries of R_JJ become 1)
         if (nk > 0) {
 #pragma unroll
             for (int x = 0; x < WM / 8; ++x)
@@ -149,27 +176,48 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
                     ts[rr * TPITCH + cc + 1] -= acc[x][y][1];
                 }
         }
+        if (tid < NB && tid >= jw) rs[tid * RPITCH + tid] = 1.0;
         __syncthreads();
-        // -- substitution against R[J,J]: one thread per row, the row in registers
-        if (tid < BMR) {
-            double v[NB];
+        // -- substitution: v holds columns hf, hf+2, ..., hf+62 of this row
+        {
+            double v[NB / 2];
 #pragma unroll
-            for (int c = 0; c < NB; ++c) v[c] = ts[tid * TPITCH + c];
+            for (int k = 0; k < NB / 2; ++k) v[k] = ts[srow * TPITCH + 2 * k + hf];
+            const int base = lane & ~1;
 #pragma unroll
             for (int c = 0; c < NB; ++c) {
-                v[c] = v[c] / rjj[c * NB + c];
+                const int owner = c & 1, kc = c >> 1;
+                double x = 0.0;
+                if (hf == owner) {
+                    v[kc] = v[kc] / rs[c * RPITCH + c];
+                    x = v[kc];
+                }
+                x = __shfl_sync(0xffffffffu, x, base | owner);
 #pragma unroll
-                for (int c2 = c + 1; c2 < NB; ++c2) v[c2] -= v[c] * rjj[c * NB + c2];
+                for (int k2 = (c + 1) >> 1; k2 < NB / 2; ++k2) {
+                    const int c2 = 2 * k2 + hf;
+                    if (c2 > c) v[k2] -= x * rs[c * RPITCH + c2];
+                }
             }
 #pragma unroll
-            for (int c = 0; c < NB; ++c) ts[tid * TPITCH + c] = v[c];
+            for (int k = 0; k < NB / 2; ++k) ts[srow * TPITCH + 2 * k + hf] = v[k];
         }
         __syncthreads();
-        // -- store A_p[rows, J] (coalesced)
-        for (int c = tid; c < BMR * NB; c += THREADS) {
-            const int rr = c / NB, jc = c % NB;
-            const int64_t row = row0 + rr;
-            if (row < m && jc < jw) ap[row * ldap + j0 + jc] = ts[rr * TPITCH + jc];
+        // -- store A_p[rows, J]
+        if (vec && jw == NB) {
+            for (int c = tid; c < BMR * (NB / 2); c += THREADS) {
+                const int rr = c / (NB / 2), jc = (c % (NB / 2)) * 2;
+                const int64_t row = row0 + rr;
+                if (row < m)
+                    *reinterpret_cast<double2 *>(ap + row * ldap + j0 + jc) =
+                        *reinterpret_cast<const double2 *>(ts + rr * TPITCH + jc);
+            }
+        } else {
+            for (int c = tid; c < BMR * NB; c += THREADS) {
+                const int rr = c / NB, jc = c % NB;
+                const int64_t row = row0 + rr;
+                if (row < m && jc < jw) ap[row * ldap + j0 + jc] = ts[rr * TPITCH + jc];
+            }
         }
         __syncthreads();
     }
@@ -188,12 +236,10 @@ using namespace sk;
 extern "C" int sk_trsm_right_upper_f64(const double *a, int64_t lda, int64_t m, int64_t n, const double *r,
                                        int64_t ldr, double *ap, int64_t ldap, sk_status *status,
                                        sk_stream_t stream) {
-    if (!a || !r || !ap || m < 0 || n <= 0 || lda < n || ldr < n || ldap < n || n > (1 << 20)) {
+    if (!a || !r || !ap || m < 0 || n <= 0 || lda < n || ldr < n || ldap < n || n > (1 << 20) ||
+        (a == ap && lda != ldap)) {
         set_error("sk_trsm_right_upper_f64: bad arguments");
         return SK_ERR_ARG;
-    }
-    if (a != ap && lda != ldap) {
-        // allowed; nothing special
     }
     cudaStream_t st = (cudaStream_t)stream;
     // exactly-zero diagonal -> SingularTriangular (src/dense.py:231-233)
@@ -202,6 +248,7 @@ extern "C" int sk_trsm_right_upper_f64(const double *a, int64_t lda, int64_t m, 
     int big = INT32_MAX, first = INT32_MAX;
     SK_CUDA(cudaMemcpyAsync(dflag, &big, sizeof(int), cudaMemcpyHostToDevice, st));
     trsm::first_zero_diag<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(r, ldr, (int)n, dflag);
+    SK_LAUNCH_CHECK("first_zero_diag");
     SK_CUDA(cudaMemcpyAsync(&first, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
     SK_CUDA(cudaFreeAsync(dflag, st));
     SK_CUDA(cudaStreamSynchronize(st));
@@ -210,8 +257,9 @@ extern "C" int sk_trsm_right_upper_f64(const double *a, int64_t lda, int64_t m, 
         return fill_status(status, SK_SINGULAR_TRIANGULAR, first, 0.0, 0.0);
     }
     if (m == 0) return fill_status(status, SK_OK, -1, 0, 0);
-    const bool vec = ((reinterpret_cast<uintptr_t>(ap) | reinterpret_cast<uintptr_t>(r)) % 16 == 0) &&
-                     (ldap % 2 == 0) && (ldr % 2 == 0);
+    const bool vec = ((reinterpret_cast<uintptr_t>(ap) | reinterpret_cast<uintptr_t>(r) |
+                       reinterpret_cast<uintptr_t>(a)) % 16 == 0) &&
+                     (ldap % 2 == 0) && (ldr % 2 == 0) && (lda % 2 == 0);
     SK_CUDA(cudaFuncSetAttribute(trsm::trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm::SMEM));
     const unsigned grid = (unsigned)((m + trsm::BMR - 1) / trsm::BMR);
     trsm::trsm_kernel<<<grid, trsm::THREADS, trsm::SMEM, st>>>(a, lda, m, (int)n, r, ldr, ap, ldap, vec);
