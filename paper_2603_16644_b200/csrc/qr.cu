@@ -133,20 +133,34 @@ __device__ T cta_dot(const T *u, const T *v, int L, T *sh_nodes, T *sh_root) {
     return r;
 }
 
-// Reflector for column jj from the (final) column w[jj:, jj]; CTA-cooperative.
+// Reflector for column jj given the chunk nodes of x.x in sh_nodes[0..nq), x = w[jj:, jj]
+// (final).  v.v differs from x.x only in element 0, so only chunk 0 is recomputed.
 template <typename T>
-__device__ int make_reflector(T *w, int64_t ld, int d, int jj, T *vout, Ctl<T> *ctl, int buf, T *sh_nodes,
-                              T *sh_root) {
+__device__ int reflect_from_nodes(T *x, int L, T *vout, Ctl<T> *ctl, int buf, T *sh_nodes, T *sh_root) {
     using O = LevelOps<T>;
-    const int L = d - jj;
-    T *x = w + (int64_t)jj * ld + jj;
-    const T nrm = O::sqrt(cta_dot<T>(x, x, L, sh_nodes, sh_root));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nq = (L + CH - 1) / CH;
+    if (warp == 0) {
+        const T r = warp_tree_root<T>(nq, [&](int i) { return sh_nodes[i]; });
+        if (lane == 0) *sh_root = r;
+    }
+    __syncthreads();
+    const T nrm = O::sqrt(*sh_root);
     if (O::to_f64(nrm) == 0.0) return SK_RANK_DEFICIENT;
     const T x0 = x[0];
     const T alpha = (O::to_f64(x0) >= 0.0) ? O::sub(O::zero(), nrm) : nrm;   // -norm if x0 >= 0
     for (int i = threadIdx.x; i < L; i += THREADS) vout[i] = (i == 0) ? O::sub(x0, alpha) : x[i];
     __syncthreads();
-    const T vtv = cta_dot<T>(vout, vout, L, sh_nodes, sh_root);
+    if (warp == 0) {
+        const T node0 = chunk_node<T>(vout, vout, L, 0);
+        if (lane == 0) sh_nodes[0] = node0;
+        __syncwarp();
+        const T r = warp_tree_root<T>(nq, [&](int i) { return sh_nodes[i]; });
+        if (lane == 0) *sh_root = r;
+    }
+    __syncthreads();
+    const T vtv = *sh_root;
+    __syncthreads();
     if (O::to_f64(vtv) == 0.0) return SK_RANK_DEFICIENT;
     const T tau = O::div(O::from_f64(2.0), vtv);
     if (!O::finite(tau)) return SK_RANK_DEFICIENT;
@@ -154,6 +168,47 @@ __device__ int make_reflector(T *w, int64_t ld, int d, int jj, T *vout, Ctl<T> *
     if (threadIdx.x == 0) { ctl->tau[buf] = tau; ctl->alpha[buf] = alpha; }
     __syncthreads();
     return SK_OK;
+}
+
+// CTA 0's look-ahead: apply reflector j (v, t) to column j+1 and, in the same pass,
+// compute the chunk nodes of the updated x = w[j+1:, j+1] for reflector j+1.
+template <typename T>
+__device__ int update_and_reflect(T *colj, int L, const T *v, T t, T *vout, Ctl<T> *ctl, int buf, T *sh_nodes,
+                                  T *sh_root) {
+    using O = LevelOps<T>;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) colj[0] = O::sub(colj[0], O::mul(v[0], t));   // R entry (row j)
+    T *x = colj + 1;
+    const T *vx = v + 1;
+    const int Lx = L - 1, nq = (Lx + CH - 1) / CH;
+    for (int q = warp; q < nq; q += WARPS) {
+        const int base = q * CH + lane * 8;
+        const int cnt = max(0, min(8, Lx - base));
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if (e < cnt) x[base + e] = O::sub(x[base + e], O::mul(vx[base + e], t));
+        __syncwarp();
+        const T node = chunk_node<T>(x, x, Lx, q);
+        if (lane == 0) sh_nodes[q] = node;
+    }
+    __syncthreads();
+    return reflect_from_nodes<T>(x, Lx, vout, ctl, buf, sh_nodes, sh_root);
+}
+
+// Reflector for column jj from the (final) column w[jj:, jj]; CTA-cooperative.
+template <typename T>
+__device__ int make_reflector(T *w, int64_t ld, int d, int jj, T *vout, Ctl<T> *ctl, int buf, T *sh_nodes,
+                              T *sh_root) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int L = d - jj;
+    T *x = w + (int64_t)jj * ld + jj;
+    const int nq = (L + CH - 1) / CH;
+    for (int q = warp; q < nq; q += WARPS) {
+        const T node = chunk_node<T>(x, x, L, q);
+        if (lane == 0) sh_nodes[q] = node;
+    }
+    __syncthreads();
+    return reflect_from_nodes<T>(x, L, vout, ctl, buf, sh_nodes, sh_root);
 }
 
 template <typename T>
@@ -188,27 +243,27 @@ householder_kernel(T *w, int64_t ld, int d, int n, T *vbuf /* 2 x d */, T *part 
             if (lane == 0) part[(size_t)q * n + c] = node;
         }
         grid.sync();
-        // ---- phase 2: t_c = tau * root, one warp per column
-        for (int cc = gwarp; cc < ncols; cc += nwarps) {
-            const int c = j + 1 + cc;
-            const T root = warp_tree_root<T>(nq, [&](int i) { return part[(size_t)i * n + c]; });
-            if (lane == 0) tvec[c] = O::mul(tau, root);
-        }
-        grid.sync();
-        // ---- phase 3: rank-1 update; CTA 0 owns column j+1 and forms reflector j+1
+        // ---- phases 2+3: every unit recomputes t_c = tau * root from the chunk nodes
+        // of its column (identically), then applies the rank-1 update to its chunk;
+        // CTA 0 owns column j+1 and forms reflector j+1
+        (void)tvec;
         if (blockIdx.x == 0) {
-            const T t = tvec[j + 1];
-            T *col = w + (int64_t)(j + 1) * ld + j;
-            for (int i = threadIdx.x; i < L; i += THREADS) col[i] = O::sub(col[i], O::mul(v[i], t));
+            T t;
+            if (threadIdx.x < 32) {
+                const T root = warp_tree_root<T>(nq, [&](int i) { return part[(size_t)i * n + j + 1]; });
+                if (lane == 0) sh_root = O::mul(tau, root);
+            }
             __syncthreads();
-            const int rc = make_reflector<T>(w, ld, d, j + 1, vbuf + (size_t)(buf ^ 1) * d, ctl, buf ^ 1, sh_nodes,
-                                             &sh_root);
+            t = sh_root;
+            __syncthreads();
+            const int rc = update_and_reflect<T>(w + (int64_t)(j + 1) * ld + j, L, v, t,
+                                                 vbuf + (size_t)(buf ^ 1) * d, ctl, buf ^ 1, sh_nodes, &sh_root);
             if (rc != SK_OK && threadIdx.x == 0) { ctl->fail_code = rc; ctl->fail_col = j + 1; }
         } else {
             const int ow = gwarp - WARPS, others = nwarps - WARPS;
             for (int u = ow; u < nq * (ncols - 1); u += others) {
                 const int q = u % nq, c = j + 2 + u / nq;
-                const T t = tvec[c];
+                const T t = O::mul(tau, warp_tree_root<T>(nq, [&](int i) { return part[(size_t)i * n + c]; }));
                 T *col = w + (int64_t)c * ld + j + q * CH;
                 const T *vq = v + q * CH;
                 const int cnt = min(CH, L - q * CH);

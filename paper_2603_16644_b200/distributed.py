@@ -200,8 +200,8 @@ def algorithm1_pipeline_sharded(a_local, b_local, method="pne", precision="auto"
     if x_star is not None:
         xs = np.asarray(x_star.detach().cpu() if isinstance(x_star, torch.Tensor) else x_star, dtype=np.float64)
         rel_err = float(np.linalg.norm(x_hat - xs) / np.linalg.norm(xs))
-    pre = Preconditioner(r_s=r_s.detach().cpu().numpy(), computed_in=level, kappa_rs=math.nan, kappa_ap=math.nan,
-                         sketch_descriptor=op.descriptor(), _r_dev=r_s if r_s.is_cuda else None)
+    pre = Preconditioner(r_s=r_s if r_s.is_cuda else r_s.detach().cpu().numpy(), computed_in=level,
+                         kappa_rs=math.nan, kappa_ap=math.nan, sketch_descriptor=op.descriptor())
     rep = SolveReport(method=method, x_hat=x_hat, residual_norm=res,
                       relative_residual=res / denom if denom > 0 else math.inf, relative_error=rel_err,
                       wall_ms=(time.perf_counter() - t0) * 1e3, preconditioner=pre,

@@ -47,21 +47,43 @@ from . import _lib
 import ctypes as C
 
 
-@dataclass
 class Preconditioner:
-    """src/solvers.py:47-59.  r_s is the promoted binary64 factor (numpy)."""
+    """src/solvers.py:47-59: the promoted binary64 factor and its diagnostics.
 
-    r_s: np.ndarray
-    computed_in: PrecisionLevel
-    kappa_rs: float
-    kappa_ap: float | None = None
-    sketch_descriptor: dict | None = None
-    _r_dev: torch.Tensor | None = field(default=None, repr=False, compare=False)
+    Same fields as the reference dataclass.  r_s may be given as a numpy array or
+    a CUDA tensor; the device copy stays resident for the solve and the numpy view
+    (`.r_s`) is materialised lazily on first access, so the pipeline never pays
+    an n x n device->host copy it does not need."""
+
+    def __init__(self, r_s, computed_in, kappa_rs, kappa_ap=None, sketch_descriptor=None):
+        if isinstance(r_s, torch.Tensor) and r_s.is_cuda:
+            self._r_dev, self._r_host = r_s, None
+        else:
+            self._r_dev, self._r_host = None, np.asarray(r_s)
+        self.computed_in = computed_in
+        self.kappa_rs = kappa_rs
+        self.kappa_ap = kappa_ap
+        self.sketch_descriptor = sketch_descriptor
+
+    @property
+    def r_s(self) -> np.ndarray:
+        if self._r_host is None:
+            self._r_host = to_host(self._r_dev)
+        return self._r_host
+
+    @r_s.setter
+    def r_s(self, value):
+        self._r_dev, self._r_host = None, np.asarray(value)
 
     def r_device(self) -> torch.Tensor:
         if self._r_dev is None or self._r_dev.device != torch.device("cuda", torch.cuda.current_device()):
             self._r_dev = torch.from_numpy(np.ascontiguousarray(self.r_s, dtype=np.float64)).cuda()
         return self._r_dev
+
+    def __repr__(self):
+        return (f"Preconditioner(r_s=<{tuple(self.r_device().shape if self._r_host is None else self._r_host.shape)}>, "
+                f"computed_in={self.computed_in!r}, kappa_rs={self.kappa_rs!r}, kappa_ap={self.kappa_ap!r}, "
+                f"sketch_descriptor={self.sketch_descriptor!r})")
 
 
 @dataclass
@@ -226,8 +248,7 @@ def _build_dev(ad: DMat, d_factor, transform, level, seed, diagnostics=True, str
     if stages is not None:
         stages.mark("diag_rs")
     kappa_rs = _kappa(r_s, strict) if diagnostics else math.nan
-    pre = Preconditioner(r_s=to_host(r_s), computed_in=level, kappa_rs=kappa_rs,
-                         sketch_descriptor=op.descriptor(), _r_dev=r_s)
+    pre = Preconditioner(r_s=r_s, computed_in=level, kappa_rs=kappa_rs, sketch_descriptor=op.descriptor())
     return pre
 
 
