@@ -111,10 +111,20 @@ __global__ void __launch_bounds__(THREADS) chol_kernel(double *w, double *l, int
                 const int i = j + 1 + (int)(t % rem);
                 const int g0 = (int)(t / rem);
                 const double li = w[(int64_t)j * n + i] / d;
-                for (int k = j + 1 + g0; k <= i; k += (int)groups) {
-                    const double lk = w[(int64_t)j * n + k] / d;
-                    double *p = w + (int64_t)k * n + i;
-                    *p = __dsub_rn(*p, __dmul_rn(li, lk));
+                constexpr int U = 8;
+                const int G = (int)groups;
+                for (int kb = j + 1 + g0; kb <= i; kb += U * G) {
+                    double wv[U], wk[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int k = kb + u * G;
+                        if (k <= i) { wv[u] = w[(int64_t)k * n + i]; wk[u] = w[(int64_t)j * n + k]; }
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int k = kb + u * G;
+                        if (k <= i) w[(int64_t)k * n + i] = __dsub_rn(wv[u], __dmul_rn(li, wk[u] / d));
+                    }
                 }
             }
         }
@@ -217,14 +227,25 @@ lu_kernel(double *w, double *lmul, int *perm, int n, double *candv, int *candi, 
                 const int i = k + 1 + (int)(t % rem);
                 const int g0 = (int)(t / rem);
                 const double li = __ddiv_rn(w[(int64_t)k * n + i], akk);
-                for (int j = k + g0; j < n; j += (int)groups) {
-                    if (j == k) {
-                        lmul[(int64_t)k * n + i] = li;
-                    } else {
-                        double *q = w + (int64_t)j * n + i;
-                        const double nv = __dsub_rn(*q, __dmul_rn(li, w[(int64_t)j * n + k]));
-                        *q = nv;
-                        if (j == k + 1) better(cbv, cbi, fabs(nv), i);
+                if (g0 == 0) lmul[(int64_t)k * n + i] = li;
+                // columns j = k+1+g0 + u*groups, 8 at a time: loads first (memory-level parallelism)
+                constexpr int U = 8;
+                const int G = (int)groups;
+                for (int jb = k + 1 + g0; jb < n; jb += U * G) {
+                    double wv[U], uk[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int j = jb + u * G;
+                        if (j < n) { wv[u] = w[(int64_t)j * n + i]; uk[u] = w[(int64_t)j * n + k]; }
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int j = jb + u * G;
+                        if (j < n) {
+                            const double nv = __dsub_rn(wv[u], __dmul_rn(li, uk[u]));
+                            w[(int64_t)j * n + i] = nv;
+                            if (j == k + 1) better(cbv, cbi, fabs(nv), i);
+                        }
                     }
                 }
             }

@@ -35,7 +35,7 @@ namespace cg = cooperative_groups;
 namespace sk {
 namespace qr {
 
-constexpr int THREADS = 256, WARPS = THREADS / 32;
+constexpr int THREADS = 1024, WARPS = THREADS / 32;   // one CTA per SM, 32 warps to hide L2 latency
 constexpr int CH = 256;          // chunk = level-8 subtree
 constexpr int MAXCH = 1024;      // chunk nodes a single warp combines: d <= 262144
 
@@ -237,10 +237,17 @@ householder_kernel(T *w, int64_t ld, int d, int n, T *vbuf /* 2 x d */, T *part 
         const int nq = (L + CH - 1) / CH;
         const int ncols = n - j - 1;           // columns j+1 .. n-1
         // ---- phase 1: chunk nodes of v . w[j:, c]
-        for (int u = gwarp; u < nq * ncols; u += nwarps) {
+        for (int u = gwarp; u < nq * ncols; u += 2 * nwarps) {   // two independent units in flight
+            const int u2 = u + nwarps;
             const int q = u % nq, c = j + 1 + u / nq;
+            const int q2 = u2 % nq, c2 = j + 1 + u2 / nq;
+            const bool has2 = u2 < nq * ncols;
             const T node = chunk_node<T>(v, w + (int64_t)c * ld + j, L, q);
-            if (lane == 0) part[(size_t)q * n + c] = node;
+            const T node2 = has2 ? chunk_node<T>(v, w + (int64_t)c2 * ld + j, L, q2) : O::zero();
+            if (lane == 0) {
+                part[(size_t)q * n + c] = node;
+                if (has2) part[(size_t)q2 * n + c2] = node2;
+            }
         }
         grid.sync();
         // ---- phases 2+3: every unit recomputes t_c = tau * root from the chunk nodes
@@ -327,7 +334,7 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
     const int maxb = max_coop_blocks((const void *)kfn, THREADS, 0);
     if (maxb <= 0) { set_error("sk_qr_r: kernel cannot be co-resident"); return SK_ERR_ARG; }
     const int64_t units = nq_max(d) * n;
-    int blocks = (int)std::min<int64_t>(std::min<int64_t>(maxb, 2 * sm_count()), (units + WARPS - 1) / WARPS + 1);
+    int blocks = (int)std::min<int64_t>(std::min<int64_t>(maxb, sm_count()), (units + WARPS - 1) / WARPS + 1);
     if (blocks < 2) blocks = std::min(2, maxb);
     int di = (int)d, ni = (int)n;
     int64_t ldw = d;

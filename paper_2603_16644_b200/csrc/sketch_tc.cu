@@ -206,29 +206,41 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
             const int i = tm * BM + row;
             const bool valid = i < p.d;
             const uint64_t r = valid ? (uint64_t)p.rows[i] : 0;
-            // per-column rotation e^{i pi r / M}
-            float wsn, wcs;
-            sincospif((float)(r % (2 * M)) / (float)M, &wsn, &wcs);
+            const uint64_t f1 = r % fourM;
+            // per-row offset table e^{i pi r (2t) / 2M}, t = 0..31 (exact integer phases)
+            float wc[32], ws[32];
+            if (!p.wht) {
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                    const uint64_t q = (f1 * (uint64_t)(2 * t)) % fourM;
+                    sincospif((float)q * inv2M, &ws[t], &wc[t]);
+                }
+            }
+            // phase of this thread's first column, advanced exactly by r*2*BK per K-block
+            uint64_t ph = (f1 * ((uint64_t)(2 * (p.row_offset + k0 + half * 32) + 1) % fourM)) % fourM;
+            const uint64_t dph = (f1 * (uint64_t)(2 * BK)) % fourM;
             for (int kb = 0; kb < nkb; ++kb) {
                 tc::mbar_wait(&empty[stage], phase ^ 1);
                 const int64_t jg0 = p.row_offset + k0 + (int64_t)kb * BK + half * 32;
                 uint32_t packed[16];
                 if (!p.wht) {
-                    const uint64_t f1 = r % fourM, f2 = (uint64_t)(2 * jg0 + 1) % fourM;
-                    const uint64_t ph = (f1 * f2) % fourM;
                     float zs, zc;
                     sincospif((float)ph * inv2M, &zs, &zc);
+                    ph += dph;
+                    if (ph >= fourM) ph -= fourM;
+                    if (r == 0 || !valid) {
+                        const float c = valid ? 0.70710678118654752f : 0.f;
+                        __half2 h = __floats2half2_rn(c, c);
 #pragma unroll
-                    for (int t = 0; t < 32; t += 2) {
-                        const float v0 = zc;
-                        float nc = zc * wcs - zs * wsn, ns = zs * wcs + zc * wsn;
-                        const float v1 = nc;
-                        zc = nc * wcs - ns * wsn;
-                        zs = ns * wcs + nc * wsn;
-                        float a0 = valid ? (r == 0 ? 0.70710678118654752f : v0) : 0.f;
-                        float a1 = valid ? (r == 0 ? 0.70710678118654752f : v1) : 0.f;
-                        __half2 h = __floats2half2_rn(a0, a1);
-                        packed[t >> 1] = *reinterpret_cast<uint32_t *>(&h);
+                        for (int t = 0; t < 16; ++t) packed[t] = *reinterpret_cast<uint32_t *>(&h);
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 32; t += 2) {
+                            const float v0 = zc * wc[t] - zs * ws[t];
+                            const float v1 = zc * wc[t + 1] - zs * ws[t + 1];
+                            __half2 h = __floats2half2_rn(v0, v1);
+                            packed[t >> 1] = *reinterpret_cast<uint32_t *>(&h);
+                        }
                     }
                 } else {
 #pragma unroll
