@@ -28,8 +28,12 @@ constexpr int APITCH = BK + 4;              // 20 = 4 (mod 16): conflict-free A 
 constexpr int BPITCH = NB + 4;              // 68 = 4 (mod 16): conflict-free B fragments
 constexpr int TPITCH = NB + 4;              // T tile rows, 16-byte aligned (544 B)
 constexpr int RPITCH = NB;
-constexpr size_t SMEM = sizeof(double) * (size_t(STAGES) * BMR * APITCH + size_t(STAGES) * BK * BPITCH +
-                                          size_t(BMR) * TPITCH + size_t(NB) * RPITCH);
+// The T tile and R_JJ alias the GEMM staging ring (they are loaded after the GEMM),
+// which keeps a CTA at ~102 KB so two CTAs share an SM: one CTA's substitution and
+// staging latency hides behind the other's DMMA work.
+constexpr size_t RING = sizeof(double) * (size_t(STAGES) * BMR * APITCH + size_t(STAGES) * BK * BPITCH);
+constexpr size_t TILE = sizeof(double) * (size_t(BMR) * TPITCH + size_t(NB) * RPITCH);
+constexpr size_t SMEM = RING > TILE ? RING : TILE;
 
 __device__ __forceinline__ void load_stage(double *as, double *bs, const double *ap, int64_t ldap,
                                            const double *__restrict__ r, int64_t ldr, int64_t row0, int64_t m, int k0,
@@ -102,13 +106,13 @@ __device__ __forceinline__ void load_block(double *ts, double *rs, const double 
     }
 }
 
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, 2)
 trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__restrict__ r, int64_t ldr, double *ap,
             int64_t ldap, bool vec) {
     extern __shared__ __align__(16) double smem[];
     double *as_base = smem;
     double *bs_base = as_base + STAGES * BMR * APITCH;
-    double *ts = bs_base + STAGES * BK * BPITCH;
+    double *ts = smem;                   // aliases the ring (used after the GEMM)
     double *rs = ts + BMR * TPITCH;
 
     const int64_t row0 = (int64_t)blockIdx.x * BMR;
@@ -122,8 +126,6 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
     for (int J = 0; J < nblocks; ++J) {
         const int j0 = J * NB;
         const int jw = min(NB, n - j0);
-        load_block(ts, rs, a, lda, r, ldr, row0, m, j0, jw, vec);
-        cp_async_commit();
 
         double acc[WM / 8][WN / 8][2];
 #pragma unroll
@@ -163,6 +165,10 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
                     for (int y = 0; y < WN / 8; ++y) dmma884(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
             }
         }
+        cp_async_wait<0>();
+        __syncthreads();                 // ring free: stage T and R_JJ into it
+        load_block(ts, rs, a, lda, r, ldr, row0, m, j0, jw, vec);
+        cp_async_commit();
         cp_async_wait<0>();
         __syncthreads();
         // -- T -= acc  (padded diagonal entries of R_JJ become 1)
