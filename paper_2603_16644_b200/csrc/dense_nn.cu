@@ -188,11 +188,27 @@ lu_kernel(double *w, double *lmul, int *perm, int n, double *candv, int *candi, 
     grid.sync();
     for (int k = 0; k < n; ++k) {
         const int buf = k & 1;
-        // every thread reduces the block candidates in block order (deterministic)
-        double bv = -1.0;
-        int p = INT32_MAX;
-        for (int b = 0; b < (int)gridDim.x; ++b) better(bv, p, candv[buf * gridDim.x + b], candi[buf * gridDim.x + b]);
-        const double piv = bv;
+        // warp 0 of every block reduces the block candidates (the (value, lowest index)
+        // order is total, so the result is deterministic) and broadcasts through smem
+        __shared__ double s_piv;
+        __shared__ int s_p;
+        if (threadIdx.x < 32) {
+            double bv = -1.0;
+            int bi = INT32_MAX;
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += 32)
+                better(bv, bi, candv[buf * gridDim.x + b], candi[buf * gridDim.x + b]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                better(bv, bi, ov, oi);
+            }
+            if (threadIdx.x == 0) { s_piv = bv; s_p = bi; }
+        }
+        __syncthreads();
+        const double piv = s_piv;
+        const int p = s_p;
+        __syncthreads();
         if (piv < thresh || piv == 0.0 || !(piv == piv)) {
             if (tid == 0) { ctl->fail_code = SK_NUMERICALLY_SINGULAR; ctl->fail_col = k; ctl->fail_value = piv; }
             return;

@@ -267,15 +267,39 @@ householder_kernel(T *w, int64_t ld, int d, int n, T *vbuf /* 2 x d */, T *part 
                                                  vbuf + (size_t)(buf ^ 1) * d, ctl, buf ^ 1, sh_nodes, &sh_root);
             if (rc != SK_OK && threadIdx.x == 0) { ctl->fail_code = rc; ctl->fail_col = j + 1; }
         } else {
-            const int ow = gwarp - WARPS, others = nwarps - WARPS;
-            for (int u = ow; u < nq * (ncols - 1); u += others) {
-                const int q = u % nq, c = j + 2 + u / nq;
-                const T t = O::mul(tau, warp_tree_root<T>(nq, [&](int i) { return part[(size_t)i * n + c]; }));
-                T *col = w + (int64_t)c * ld + j + q * CH;
-                const T *vq = v + q * CH;
-                const int cnt = min(CH, L - q * CH);
-                for (int i = lane; i < cnt; i += 32) col[i] = O::sub(col[i], O::mul(vq[i], t));
+            // CTA-major: CTA b >= 1 owns columns j+2+k*(G-1)+(b-1); its warps first
+            // compute t_c for all owned columns in parallel, then update (column, chunk)
+            // units with two in flight per warp.
+            const int G1 = gridDim.x - 1, b1 = blockIdx.x - 1;
+            const int rest = ncols - 1;                               // columns j+2 .. n-1
+            const int mine = rest > b1 ? (rest - b1 + G1 - 1) / G1 : 0;
+            const int warp = threadIdx.x >> 5;
+            for (int k = warp; k < mine; k += WARPS) {
+                const int c = j + 2 + b1 + k * G1;
+                const T root = warp_tree_root<T>(nq, [&](int i) { return part[(size_t)i * n + c]; });
+                if (lane == 0) sh_nodes[k] = O::mul(tau, root);
             }
+            __syncthreads();
+            const int units = mine * nq;
+            for (int u = warp; u < units; u += 2 * WARPS) {
+                const int u2 = u + WARPS;
+                const bool has2 = u2 < units;
+                const int k1 = u / nq, q1 = u % nq, k2 = u2 / nq, q2 = u2 % nq;
+                T *col1 = w + (int64_t)(j + 2 + b1 + k1 * G1) * ld + j + q1 * CH;
+                T *col2 = w + (int64_t)(j + 2 + b1 + (has2 ? k2 : k1) * G1) * ld + j + (has2 ? q2 : q1) * CH;
+                const T t1 = sh_nodes[k1], t2 = has2 ? sh_nodes[k2] : O::zero();
+                const int cnt1 = min(CH, L - q1 * CH), cnt2 = has2 ? min(CH, L - q2 * CH) : 0;
+                const T *v1 = v + q1 * CH, *v2 = v + (has2 ? q2 : q1) * CH;
+#pragma unroll 4
+                for (int i = lane; i < CH; i += 32) {
+                    T a1 = O::zero(), a2 = O::zero(), x1 = O::zero(), x2 = O::zero();
+                    if (i < cnt1) { a1 = col1[i]; x1 = v1[i]; }
+                    if (i < cnt2) { a2 = col2[i]; x2 = v2[i]; }
+                    if (i < cnt1) col1[i] = O::sub(a1, O::mul(x1, t1));
+                    if (i < cnt2) col2[i] = O::sub(a2, O::mul(x2, t2));
+                }
+            }
+            __syncthreads();
         }
         grid.sync();
     }
