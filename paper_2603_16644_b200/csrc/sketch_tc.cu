@@ -58,12 +58,14 @@ int make_tmap_2d(CUtensorMap *map, CUtensorMapDataType dtype, const void *base, 
 
 namespace sktc {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int THREADS = 384, GEN_WARP0 = 4, NGEN_WARPS = 8;
-constexpr uint32_t A_BYTES = BM * BK * 2;   // 16 KB
+// A CTA owns 256 sampled rows (two M=128 UMMA accumulators, 2 x 256 TMEM columns)
+// against one 256-column B tile, so every B byte staged from L2 feeds 256 rows.
+constexpr int BM = 256, UMMA_M = 128, BN = 256, BK = 64, STAGES = 3;
+constexpr int THREADS = 640, GEN_WARP0 = 4, NGEN_WARPS = 16;
+constexpr uint32_t A_BYTES = BM * BK * 2;   // 32 KB (two 16 KB UMMA operands)
 constexpr uint32_t B_BYTES = BN * BK * 2;   // 32 KB
 constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
-constexpr int TMEM_COLS = 256;
+constexpr int TMEM_COLS = 512;
 
 // ------------------------------------------------------------ prep kernel ---
 constexpr int PT = 64;   // 64 x 64 tile
@@ -167,7 +169,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
         }
     } else if (warp == 1) {
         if (lane == 0) {   // ---------------- MMA issuer
-            constexpr uint32_t idesc = tc::idesc_f32acc(BM, BN, 0, 0);
+            constexpr uint32_t idesc = tc::idesc_f32acc(UMMA_M, BN, 0, 0);
             int stage = 0;
             unsigned phase = 0, tphase = 0;
             for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
@@ -179,11 +181,14 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
                 for (int kb = 0; kb < nkb; ++kb) {
                     tc::mbar_wait(&full[stage], phase);
                     tc::tc_fence_after();
-                    const uint64_t ad = tc::desc_kmajor_sw128(smem_u32(sa + stage * A_BYTES));
+                    const uint64_t ad0 = tc::desc_kmajor_sw128(smem_u32(sa + stage * A_BYTES));
+                    const uint64_t ad1 = tc::desc_kmajor_sw128(smem_u32(sa + stage * A_BYTES + A_BYTES / 2));
                     const uint64_t bd = tc::desc_kmajor_sw128(smem_u32(sb + stage * B_BYTES));
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)   // +32 bytes along K per UMMA_K = 16
-                        tc::mma_f16_ss(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) ? 1u : 0u);
+                    for (int k = 0; k < BK / 16; ++k) {   // +32 bytes along K per UMMA_K = 16
+                        tc::mma_f16_ss(tmem, ad0 + 2 * k, bd + 2 * k, idesc, (kb | k) ? 1u : 0u);
+                        tc::mma_f16_ss(tmem + BN, ad1 + 2 * k, bd + 2 * k, idesc, (kb | k) ? 1u : 0u);
+                    }
                     tc::mma_commit(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -222,42 +227,39 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
             for (int kb = 0; kb < nkb; ++kb) {
                 tc::mbar_wait(&empty[stage], phase ^ 1);
                 const int64_t jg0 = p.row_offset + k0 + (int64_t)kb * BK + half * 32;
-                uint32_t packed[16];
+                uint8_t *tile = sa + stage * A_BYTES;
+                // 32 operator values of this (row, half) -> four 16-byte swizzled chunks,
+                // each stored as soon as its 8 values are rounded (few live registers)
+                float zs = 0.f, zc = 0.f;
                 if (!p.wht) {
-                    float zs, zc;
                     sincospif((float)ph * inv2M, &zs, &zc);
                     ph += dph;
                     if (ph >= fourM) ph -= fourM;
-                    if (r == 0 || !valid) {
-                        const float c = valid ? 0.70710678118654752f : 0.f;
-                        __half2 h = __floats2half2_rn(c, c);
-#pragma unroll
-                        for (int t = 0; t < 16; ++t) packed[t] = *reinterpret_cast<uint32_t *>(&h);
-                    } else {
-#pragma unroll
-                        for (int t = 0; t < 32; t += 2) {
-                            const float v0 = zc * wc[t] - zs * ws[t];
-                            const float v1 = zc * wc[t + 1] - zs * ws[t + 1];
-                            __half2 h = __floats2half2_rn(v0, v1);
-                            packed[t >> 1] = *reinterpret_cast<uint32_t *>(&h);
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int t = 0; t < 32; t += 2) {
-                        const uint64_t j0 = (uint64_t)(jg0 + t), j1 = j0 + 1;
-                        float a0 = (__popcll(r & j0) & 1) ? -1.f : 1.f;
-                        float a1 = (__popcll(r & j1) & 1) ? -1.f : 1.f;
-                        if (!valid) a0 = a1 = 0.f;
-                        __half2 h = __floats2half2_rn(a0, a1);
-                        packed[t >> 1] = *reinterpret_cast<uint32_t *>(&h);
-                    }
                 }
-                uint8_t *tile = sa + stage * A_BYTES;
+                const bool flat = !p.wht && (r == 0 || !valid);
+                const float cflat = valid ? 0.70710678118654752f : 0.f;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    uint4 v = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
-                    *reinterpret_cast<uint4 *>(tile + tc::sw128_offset(row, half * 4 + q)) = v;
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int t = q * 8 + 2 * e;
+                        float a0, a1;
+                        if (p.wht) {
+                            const uint64_t j0 = (uint64_t)(jg0 + t), j1 = j0 + 1;
+                            a0 = valid ? ((__popcll(r & j0) & 1) ? -1.f : 1.f) : 0.f;
+                            a1 = valid ? ((__popcll(r & j1) & 1) ? -1.f : 1.f) : 0.f;
+                        } else if (flat) {
+                            a0 = a1 = cflat;
+                        } else {
+                            a0 = zc * wc[t] - zs * ws[t];
+                            a1 = zc * wc[t + 1] - zs * ws[t + 1];
+                        }
+                        __half2 h = __floats2half2_rn(a0, a1);
+                        pk[e] = *reinterpret_cast<uint32_t *>(&h);
+                    }
+                    *reinterpret_cast<uint4 *>(tile + tc::sw128_offset(row, half * 4 + q)) =
+                        make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }
                 tc::fence_proxy_async_smem();
                 __syncwarp();
@@ -268,17 +270,20 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
             tc::mbar_wait(tfull, tphase);
             tc::tc_fence_after();
             tphase ^= 1;
-            const int lg = warp & 3, colhalf = (warp - GEN_WARP0) >> 2;
+            // warp w reads TMEM lanes 32*(w%4)..; the 16 warps split 2 accumulators x 2 column halves
+            const int lg = warp & 3, quarter = (warp - GEN_WARP0) >> 2;
+            const int acc = quarter >> 1, colhalf = quarter & 1;
             const int tile = u % p.ntiles, split = u / p.ntiles;
             float *out = p.part + ((size_t)split * p.ntiles + tile) * (size_t)(BM * BN);
+            const int orow = acc * UMMA_M + lg * 32 + lane;
 #pragma unroll 1
             for (int cb = 0; cb < 4; ++cb) {
                 const int col = colhalf * 128 + cb * 32;
                 uint32_t v[32];
-                tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)col, v);
+                tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * BN + col), v);
                 tc::tmem_ld_wait();
 #pragma unroll
-                for (int q = 0; q < 32; ++q) out[(size_t)(col + q) * BM + lg * 32 + lane] = __uint_as_float(v[q]) * p.epi_scale;
+                for (int q = 0; q < 32; ++q) out[(size_t)(col + q) * BM + orow] = __uint_as_float(v[q]) * p.epi_scale;
             }
             tc::tc_fence_before();
             __syncwarp();

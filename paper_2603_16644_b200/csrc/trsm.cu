@@ -133,11 +133,15 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
 #pragma unroll
             for (int y = 0; y < WN / 8; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
         const int nk = (j0 + BK - 1) / BK;
+        // Each CTA starts its K sweep at a different block (rotation by blockIdx): the
+        // concurrently resident panels are 2 MB apart, so walking the same columns in
+        // lockstep would hammer the same L2/HBM channels.
+        const int rot = nk ? (int)(blockIdx.x % (unsigned)nk) : 0;
 #pragma unroll
         for (int s = 0; s < STAGES - 1; ++s) {
             if (s < nk)
-                load_stage(as_base + s * BMR * APITCH, bs_base + s * BK * BPITCH, ap, ldap, r, ldr, row0, m, s * BK,
-                           j0, j0, n, vec);
+                load_stage(as_base + s * BMR * APITCH, bs_base + s * BK * BPITCH, ap, ldap, r, ldr, row0, m,
+                           ((s + rot) % nk) * BK, j0, j0, n, vec);
             cp_async_commit();
         }
         for (int kt = 0; kt < nk; ++kt) {
@@ -146,8 +150,8 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
             const int nxt = kt + STAGES - 1;
             if (nxt < nk) {
                 const int s = nxt % STAGES;
-                load_stage(as_base + s * BMR * APITCH, bs_base + s * BK * BPITCH, ap, ldap, r, ldr, row0, m, nxt * BK,
-                           j0, j0, n, vec);
+                load_stage(as_base + s * BMR * APITCH, bs_base + s * BK * BPITCH, ap, ldap, r, ldr, row0, m,
+                           ((nxt + rot) % nk) * BK, j0, j0, n, vec);
             }
             cp_async_commit();
             const double *as = as_base + (kt % STAGES) * BMR * APITCH;
