@@ -230,3 +230,19 @@ def test_torch_cuda_inputs_stay_on_device(sq):
     pre = sq.build_preconditioner(at, seed=3)
     a_p = sq.precondition_matrix(at, pre)
     assert isinstance(a_p, torch.Tensor) and a_p.is_cuda
+
+
+def test_sharded_pipeline_single_rank_device_ops(sq):
+    """distributed.algorithm1_pipeline_sharded with the production DeviceOps on one
+    GPU (no process group: every all-reduce is the identity)."""
+    from paper_2603_16644_b200.distributed import algorithm1_pipeline_sharded
+    for kappa, method, prec in ((1e2, "hpne", "auto"), (1e6, "pne", "half")):
+        p = planted_problem(600, 40, kappa, 1e-8, 6)
+        got = algorithm1_pipeline_sharded(p.a, p.b, method=method, precision=prec, seed=6, x_star=p.x_star)
+        ref = R.pipeline(p.a, p.b, method=method, precision=prec, seed=6, x_star=p.x_star, diagnostics=False)
+        assert got.preconditioner.computed_in.name == ref.pre.level
+        assert (got.escalated_from.name if got.escalated_from else None) == ref.escalated_from
+        assert got.relative_error <= max(10 * ref.relative_error, ERR_FLOOR)
+        one = sq.algorithm1_pipeline(p.a, p.b, method=method, precision=prec, seed=6, x_star=p.x_star,
+                                     diagnostics=False)
+        assert np.linalg.norm(got.x_hat - one.x_hat) <= 1e-12 * np.linalg.norm(one.x_hat)
