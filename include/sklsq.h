@@ -78,6 +78,13 @@ int sk_cast_stats(const void *src, int src_dtype, int64_t rows, int64_t cols, in
                   double *dst, int64_t ld_dst, double *stats_host,
                   void *ws, size_t ws_bytes, sk_stream_t stream);
 
+/* Stream-ordered variant for row chunks arriving while earlier chunks are being
+ * processed: stats_dev[0] += #non-finite, stats_dev[1] += sum of squares (device
+ * doubles, caller-zeroed), no host synchronisation. */
+int sk_cast_stats_async(const void *src, int src_dtype, int64_t rows, int64_t cols, int64_t ld_src,
+                        double *dst, int64_t ld_dst, double *stats_dev, void *ws, size_t ws_bytes,
+                        sk_stream_t stream);
+
 /* round_to_precision(A, level).overflowed without materialising the rounding:
  * src/precision.py:90-103, src/solvers.py:191-193.  *overflowed_host = 0/1. */
 int sk_level_overflow(const double *a, int64_t rows, int64_t cols, int64_t lda, int level,

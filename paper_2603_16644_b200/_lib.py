@@ -42,6 +42,7 @@ SIGNATURES = {
     "sk_launch_count": (C.c_uint64, []),
     "sk_matrix_stats_workspace": (_sz, [_i64, _i64]),
     "sk_cast_stats": (_i32, [_p, _i32, _i64, _i64, _i64, _p, _i64, _pd, _p, _sz, _p]),
+    "sk_cast_stats_async": (_i32, [_p, _i32, _i64, _i64, _i64, _p, _i64, _p, _p, _sz, _p]),
     "sk_level_overflow": (_i32, [_p, _i64, _i64, _i64, _i32, _pi, _p, _sz, _p]),
     "sk_residual": (_i32, [_p, _i64, _i64, _i64, _p, _p, _p, _pd, _p, _sz, _p]),
     "sk_gram_workspace": (_sz, [_i64, _i64]),

@@ -71,6 +71,16 @@ __global__ void sum_parts(const double *part, int nblocks, int width, double *ou
     if (lane == 0) out[slot] = s;
 }
 
+// out[slot] += fixed-order sum of the per-block partials (streamed chunks accumulate)
+__global__ void accumulate_parts(const double *part, int nblocks, int width, double *out) {
+    const int slot = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (slot >= width) return;
+    double s = 0.0;
+    for (int b = lane; b < nblocks; b += 32) s += part[(int64_t)b * width + slot];
+    s = warp_sum(s);
+    if (lane == 0) out[slot] += s;
+}
+
 template <int LEVEL>
 __global__ void __launch_bounds__(THREADS)
 overflow_kernel(const double *a, int64_t rows, int64_t cols, int64_t lda, int *flag) {
@@ -170,6 +180,25 @@ int sk_cast_stats(const void *src, int src_dtype, int64_t rows, int64_t cols, in
     SK_LAUNCH_CHECK("sum_parts");
     SK_CUDA(cudaMemcpyAsync(stats_host, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     SK_CUDA(cudaStreamSynchronize(st));
+    return SK_OK;
+}
+
+int sk_cast_stats_async(const void *src, int src_dtype, int64_t rows, int64_t cols, int64_t ld_src, double *dst,
+                        int64_t ld_dst, double *stats_dev, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    if (!src || !stats_dev || rows < 0 || cols <= 0 || ld_src < cols || (dst && ld_dst < cols) || !ws ||
+        ws_bytes < sk_matrix_stats_workspace(rows, cols) ||
+        (src_dtype != SK_F16 && src_dtype != SK_F32 && src_dtype != SK_F64)) {
+        set_error("sk_cast_stats_async: bad arguments");
+        return SK_ERR_ARG;
+    }
+    if (rows == 0) return SK_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nb = blocks_for(rows * cols);
+    double *part = static_cast<double *>(ws);
+    cast_stats_kernel<<<nb, THREADS, 0, st>>>(src, src_dtype, rows, cols, ld_src, dst, ld_dst, part);
+    SK_LAUNCH_CHECK("cast_stats_kernel");
+    accumulate_parts<<<1, 64, 0, st>>>(part, nb, 2, stats_dev);
+    SK_LAUNCH_CHECK("accumulate_parts");
     return SK_OK;
 }
 

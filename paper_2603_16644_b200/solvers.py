@@ -128,6 +128,15 @@ class _Stages:
         return out
 
 
+def _host_f64_matrix(a):
+    """A 2-D float64 host matrix as a CPU torch tensor (no copy), else None."""
+    if isinstance(a, torch.Tensor):
+        return a if (not a.is_cuda and a.dim() == 2 and a.dtype == torch.float64 and a.is_contiguous()) else None
+    if isinstance(a, np.ndarray) and a.ndim == 2 and a.dtype == np.float64 and a.flags.c_contiguous:
+        return torch.from_numpy(a)
+    return None
+
+
 def _check_system(a, b):
     """src/solvers.py:87-96 on the device."""
     ad = as_dmat(a)
@@ -228,18 +237,83 @@ def solve_notnormal(a, b_matrix, b, x_star=None):
     return _report("nne", ad, bd, x, t0, x_star)
 
 
+# ------------------------------------------------------- streamed ingestion --
+STREAM_MIN_BYTES = 1 << 30      # host matrices at least this large are streamed in row chunks
+STREAM_CHUNKS = 16
+
+
+def _ingest_streamed(a_cpu: torch.Tensor, want_gram: bool, sketch_plan=None):
+    """Host -> device copy of A in row chunks on a side stream, overlapped with the
+    per-chunk work that does not need all of A: validation + ||A||_F^2, the kappa0
+    SYRK (accumulated chunk by chunk) and the (speculative) sketch partial sums
+    with global row offsets.  Returns (DMat, G or None, sketch (total, flag) or None)."""
+    from .device import device as _device
+    from .sketch import _sketch_sum
+    dev = _device()
+    m, n = a_cpu.shape
+    out = torch.empty((m, n), dtype=torch.float64, device=dev)
+    compute = torch.cuda.current_stream()
+    copier = torch.cuda.Stream(device=dev)
+    copier.wait_stream(compute)          # `out` may reuse memory still read by queued kernels
+    rows = max(64, -(-m // STREAM_CHUNKS))
+    rows = -(-rows // 64) * 64
+    chunks = [(r0, min(m, r0 + rows)) for r0 in range(0, m, rows)]
+    events = []
+    with torch.cuda.stream(copier):
+        for r0, r1 in chunks:
+            out[r0:r1].copy_(a_cpu[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copier)
+            events.append(ev)
+    stats = torch.zeros(2, dtype=torch.float64, device=dev)
+    g = torch.zeros((n, n), dtype=torch.float64, device=dev) if want_gram else None
+    sk_total = sk_flag = None
+    if sketch_plan is not None:
+        dsk, level_code = sketch_plan
+        sk_total = torch.zeros((n, dsk.op.d), dtype=torch.float64, device=dev)
+        sk_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib = _lib.lib()
+    for i, (r0, r1) in enumerate(chunks):
+        compute.wait_event(events[i])
+        part = out[r0:r1]
+        wp, wn = WORKSPACE.get(lib.sk_matrix_stats_workspace(r1 - r0, n))
+        call("sk_cast_stats_async", part.data_ptr(), 8, r1 - r0, n, n, None, n, stats.data_ptr(), wp, wn,
+             stream_handle())
+        if g is not None:
+            _gram(part, out=g, accumulate=i > 0)
+        if sketch_plan is not None:
+            _sketch_sum(dsk, part, level_code, row_offset=r0, out=sk_total, accumulate=i > 0,
+                        overflow_flag=sk_flag)
+    out.record_stream(copier)
+    st = stats.cpu()
+    if st[0] > 0:
+        raise ValueError("a contains non-finite entries")
+    ad = DMat(out, float(st[1]), "numpy")
+    return ad, g, ((sk_total, sk_flag) if sketch_plan is not None else None)
+
+
 # ------------------------------------------------------------ preconditioner --
-def _build_dev(ad: DMat, d_factor, transform, level, seed, diagnostics=True, strict=False, stages=None):
+def _build_dev(ad: DMat, d_factor, transform, level, seed, diagnostics=True, strict=False, stages=None,
+               presketch=None):
     m, n = ad.shape
     if m < n:
         raise DimensionMismatch(f"need rows >= cols, got {m} x {n}")
     d = int(math.ceil(d_factor * n))
     if d < n:
         raise ValueError(f"d_factor {d_factor} gives d={d} < n={n}")
-    op = make_sketch(m, d, transform, seed)
     if stages is not None:
         stages.mark("sketch")
-    a_s, _ = _apply_dev(op, ad, level)          # Overflow on demotion (src/solvers.py:191-193)
+    if presketch is not None and presketch[0] == (level.name, d, transform, seed):
+        # the streamed ingestion already accumulated this exact sketch
+        from .errors import Overflow
+        from .sketch import _sketch_finalize
+        _, op, total, flag = presketch
+        if int(flag.item()):
+            raise Overflow(f"input exceeds the {level.name} range")
+        a_s, _ = _sketch_finalize(total, op, level)
+    else:
+        op = make_sketch(m, d, transform, seed)
+        a_s, _ = _apply_dev(op, ad, level)      # Overflow on demotion (src/solvers.py:191-193)
     if stages is not None:
         stages.mark("level_qr")
     r_s = _qr_level_dev(a_s, level, d, n)       # RankDeficient / Overflow
@@ -278,11 +352,12 @@ def precondition_matrix(a, pre, *, diagnostics=True, strict_diagnostics=False):
     return like_input(_precondition_dev(ad, pre, diagnostics, strict_diagnostics), ad.kind)
 
 
-def _prepare_dev(ad, d_factor, transform, level, seed, diagnostics=True, strict=False, stages=None):
+def _prepare_dev(ad, d_factor, transform, level, seed, diagnostics=True, strict=False, stages=None,
+                 presketch=None):
     escalated_from = None
     while True:
         try:
-            pre = _build_dev(ad, d_factor, transform, level, seed, diagnostics, strict, stages)
+            pre = _build_dev(ad, d_factor, transform, level, seed, diagnostics, strict, stages, presketch)
             a_p = _precondition_dev(ad, pre, diagnostics, strict, stages)
             return pre, a_p, escalated_from
         except RankDeficient:
@@ -364,21 +439,49 @@ def algorithm1_pipeline(a, b, method="pne", precision="auto", d_factor=3.0, tran
     """
     stages = _Stages(stage_timing)
     stages.mark("check")
-    ad, bd = _check_system(a, b)
     if method not in ("pne", "hpne"):
         raise ValueError(f"pipeline method must be pne or hpne, got {method!r}")
+    if not isinstance(precision, PrecisionLevel) and precision != "auto":
+        level_from_name(precision)      # ValueError before any work, like the reference
+    host = _host_f64_matrix(a)
+    presketch = None
+    gram_auto = None
+    if host is not None and host.numel() * 8 >= STREAM_MIN_BYTES and host.shape[0] >= host.shape[1]:
+        # Streamed ingestion: the H2D copy of A overlaps with validation, the kappa0
+        # Gram and the sketch (the real one for a fixed level, a speculative binary16
+        # one under "auto", reused if kappa0 selects binary16).
+        from .precision import BINARY16
+        from .sketch import DeviceSketch
+        m, n = host.shape
+        fixed = precision if isinstance(precision, PrecisionLevel) else (
+            None if precision == "auto" else level_from_name(precision))
+        spec_level = fixed or BINARY16
+        d = int(math.ceil(d_factor * n))
+        op = make_sketch(m, d, transform, seed) if d >= n else None
+        plan = (DeviceSketch(op), spec_level.code) if op is not None else None
+        ad, gram_auto, sk = _ingest_streamed(host, want_gram=precision == "auto", sketch_plan=plan)
+        if sk is not None:
+            presketch = ((spec_level.name, d, transform, seed), op, sk[0], sk[1])
+        bd = as_dvec(b, m)
+    else:
+        ad, bd = _check_system(a, b)
     t0 = time.perf_counter()
     decision = None
     if isinstance(precision, PrecisionLevel):
         level = precision
     elif precision == "auto":
         stages.mark("kappa0")
-        decision = _decide_dev(ad)
+        if gram_auto is not None:
+            from .precision import _kappa0_from_gram, select_precision
+            k0, over = _kappa0_from_gram(gram_auto)
+            decision = PrecisionDecision(kappa0=k0, selected=select_precision(k0, over), overflowed=over)
+        else:
+            decision = _decide_dev(ad)
         level = decision.selected
     else:
         level = level_from_name(precision)
     pre, a_p, escalated_from = _prepare_dev(ad, d_factor, transform, level, seed, diagnostics,
-                                            strict_diagnostics, stages)
+                                            strict_diagnostics, stages, presketch)
     x = (_pne_dev if method == "pne" else _hpne_dev)(ad, bd, pre, a_p, stages)
     stages.mark("report")
     report = _report(method, ad, bd, x, t0, x_star, preconditioner=pre, stages=stages)

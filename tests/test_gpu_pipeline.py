@@ -232,6 +232,26 @@ def test_torch_cuda_inputs_stay_on_device(sq):
     assert isinstance(a_p, torch.Tensor) and a_p.is_cuda
 
 
+@pytest.mark.parametrize("kappa,prec,level", [(1e2, "auto", "binary16"), (1e6, "auto", "binary32"),
+                                              (1e2, "single", "binary32"), (1e10, "auto", "binary64")])
+def test_streamed_host_ingestion_matches(sq, monkeypatch, kappa, prec, level):
+    """Host input above STREAM_MIN_BYTES is copied in row chunks that overlap the
+    kappa0 Gram and the (speculative) sketch; decisions and accuracy must match."""
+    from paper_2603_16644_b200 import solvers as S
+    p = planted_problem(3000, 40, kappa, 1e-8, 5)
+    ref = R.pipeline(p.a, p.b, method="hpne", precision=prec, seed=5, x_star=p.x_star, diagnostics=False)
+    monkeypatch.setattr(S, "STREAM_MIN_BYTES", 0)
+    monkeypatch.setattr(S, "STREAM_CHUNKS", 7)
+    got = sq.algorithm1_pipeline(p.a, p.b, method="hpne", precision=prec, seed=5, x_star=p.x_star,
+                                 diagnostics=False)
+    assert got.preconditioner.computed_in.name == ref.pre.level == level
+    assert got.relative_error <= max(10 * ref.relative_error, ERR_FLOOR)
+    bad = p.a.copy()
+    bad[2999, 39] = np.inf
+    with pytest.raises(ValueError):
+        sq.algorithm1_pipeline(bad, p.b, precision=prec)
+
+
 def test_sharded_pipeline_single_rank_device_ops(sq):
     """distributed.algorithm1_pipeline_sharded with the production DeviceOps on one
     GPU (no process group: every all-reduce is the identity)."""
