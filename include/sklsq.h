@@ -169,6 +169,12 @@ size_t sk_nxn_workspace(int64_t n);
 int sk_chol_solve_f64(const double *s, int64_t n, const double *rhs, double *x,
                       sk_status *status, void *ws, size_t ws_bytes, sk_stream_t stream);
 
+/* Upper Cholesky factor R = L^T (row-major n x n, zeros below) of (S + S^T)/2:
+ * cholesky_factor src/dense.py:289-311 (pivot <= 0 or non-finite ->
+ * SK_NOT_POSITIVE_DEFINITE).  Used for the Gram route to kappa(A_p) on tall A_p. */
+int sk_chol_factor_f64(const double *s, int64_t n, double *r, sk_status *status, void *ws, size_t ws_bytes,
+                       sk_stream_t stream);
+
 /* x = G^{-1} rhs by LU with partial pivoting: lu_solve src/dense.py:245-286
  * (lowest index on ties; pivot < n eps max|G| -> SK_NUMERICALLY_SINGULAR). */
 int sk_lu_solve_f64(const double *g, int64_t n, const double *rhs, double *x,

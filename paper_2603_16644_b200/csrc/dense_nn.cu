@@ -521,6 +521,22 @@ int sk_chol_solve_f64(const double *s, int64_t n, const double *rhs, double *x, 
     return fill_status(status, SK_OK, -1, 0, 0);
 }
 
+int sk_chol_factor_f64(const double *s, int64_t n, double *r, sk_status *status, void *wsp, size_t ws_bytes,
+                       sk_stream_t stream) {
+    if (!s || !r || n <= 0 || n > 65536 || !wsp || ws_bytes < sk_nxn_workspace(n)) {
+        set_error("sk_chol_factor_f64: bad arguments");
+        return SK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    Ws ws;
+    ws_layout(n, wsp, &ws);
+    int rc = chol_factor(s, (int)n, ws, status, st);
+    if (rc != SK_OK) return rc;
+    // ws.l is L column-major, i.e. exactly R = L^T row-major
+    SK_CUDA(cudaMemcpyAsync(r, ws.l, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return fill_status(status, SK_OK, -1, 0, 0);
+}
+
 int sk_lu_solve_f64(const double *g, int64_t n, const double *rhs, double *x, sk_status *status, void *wsp,
                     size_t ws_bytes, sk_stream_t stream) {
     if (!g || !rhs || !x || n <= 0 || n > 65536 || !wsp || ws_bytes < sk_nxn_workspace(n)) {

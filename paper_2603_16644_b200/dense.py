@@ -155,13 +155,39 @@ def _jacobi_sv(at: torch.Tensor, max_sweeps: int = 30, tol: float = 1e-14) -> np
     return np.array(sv[:], dtype=np.float64)
 
 
+TALL_QR_MAX_ROWS = 262144     # the column Householder kernel's chunk-tree limit
+
+
+def _chol_factor(s: torch.Tensor) -> torch.Tensor:
+    """Upper R with R^T R = (S + S^T)/2 (NotPositiveDefinite on breakdown)."""
+    s = s.contiguous()
+    n = s.shape[0]
+    r = torch.empty((n, n), dtype=torch.float64, device=s.device)
+    wp, wn = WORKSPACE.get(_lib.lib().sk_nxn_workspace(n))
+    st = _lib.SkStatus()
+    call("sk_chol_factor_f64", s.data_ptr(), n, r.data_ptr(), C.byref(st), wp, wn, stream_handle())
+    return r
+
+
 def _diagnostics_dev(at: torch.Tensor) -> ConditionDiagnostics:
-    """condition_diagnostics on a device matrix (src/dense.py:418-448)."""
+    """condition_diagnostics on a device matrix (src/dense.py:418-448).
+
+    The reference reduces a tall matrix to its n x n Householder R before Jacobi.
+    Beyond TALL_QR_MAX_ROWS rows (e.g. A_p at m = 4M) the R factor is taken from the
+    Cholesky factor of the Gram A^T A (same singular values in exact arithmetic);
+    that is accurate while kappa(A) << 1e8, which holds for the preconditioned A_p
+    this is used on (kappa(A_p) = O(1))."""
     if at.shape[0] < at.shape[1]:
         at = at.t().contiguous()
     m, n = at.shape
     w = at
-    if m > n:
+    if m > TALL_QR_MAX_ROWS:
+        try:
+            w = _chol_factor(_gram(at))
+        except Exception:   # noqa: BLE001  (breakdown: kappa out of the Gram route's range)
+            sv = np.full(n, np.nan)
+            return ConditionDiagnostics(two_norm=math.nan, two_norm_condition=math.nan, singular_values=sv)
+    elif m > n:
         try:
             w = _householder_r64(at)
         except RankDeficient:

@@ -227,3 +227,18 @@ def test_jacobi_and_diagnostics(sq):
         assert diag.two_norm_condition == pytest.approx(kappa, rel=1e-6)
     with pytest.raises(sq.NoConvergence):
         sq.jacobi_singular_values(R.philox(5, 3).standard_normal((12, 12)), max_sweeps=1, tol=1e-300)
+
+
+def test_tall_diagnostics_gram_route(sq, monkeypatch):
+    """Beyond the column-Householder row limit, kappa of a well-conditioned tall
+    matrix comes from the Cholesky factor of its Gram; it must agree with the QR route."""
+    from paper_2603_16644_b200 import dense as D
+    import torch
+    a = R.philox(11, 3).standard_normal((5000, 48)) @ np.diag(np.linspace(1.0, 30.0, 48))
+    qr_route = sq.condition_diagnostics(a)
+    monkeypatch.setattr(D, "TALL_QR_MAX_ROWS", 1000)
+    gram_route = sq.condition_diagnostics(a)
+    assert gram_route.two_norm_condition == pytest.approx(qr_route.two_norm_condition, rel=1e-10)
+    assert gram_route.two_norm == pytest.approx(qr_route.two_norm, rel=1e-12)
+    r = D._chol_factor(torch.from_numpy(a.T @ a).cuda()).cpu().numpy()
+    assert np.all(np.tril(r, -1) == 0) and rel(r.T @ r, a.T @ a) <= 1e-13
