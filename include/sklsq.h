@@ -128,8 +128,10 @@ int sk_trsm_right_upper_f64(const double *a, int64_t lda, int64_t m, int64_t n, 
  * the final rounding happen in sk_sketch_finalize so that partials can be summed
  * across row shards (NCCL) first.  Overflow of the demotion is OR-ed into
  * *overflow_flag_dev (device int).  transform SK_DCT2/SK_WHT, level 16/32/64. */
-enum sk_sketch_algo { SK_SKETCH_AUTO = 0, SK_SKETCH_DMMA = 1, SK_SKETCH_TC = 2 };
+enum sk_sketch_algo { SK_SKETCH_AUTO = 0, SK_SKETCH_DMMA = 1, SK_SKETCH_TC = 2, SK_SKETCH_FFT = 3 };
 size_t sk_sketch_workspace(int level, int64_t m_local, int64_t n, int64_t d);
+/* Exact workspace for one (level, transform, row shard of an m_pad-row operator). */
+size_t sk_sketch_workspace_ex(int level, int transform, int64_t m_local, int64_t m_pad, int64_t n, int64_t d);
 int sk_sketch_partial(int level, int transform, const double *a, int64_t lda, int64_t m_local,
                       int64_t row_offset, int64_t m_pad, int64_t n, const double *signs,
                       const int64_t *rows, int64_t d, double *out, int64_t ldo, int accumulate,

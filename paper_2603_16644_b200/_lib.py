@@ -51,6 +51,7 @@ SIGNATURES = {
     "sk_gemv_t_f64": (_i32, [_p, _i64, _i64, _i64, _p, _p, _i32, _p, _sz, _p]),
     "sk_trsm_right_upper_f64": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _p, _i64, _ps, _p]),
     "sk_sketch_workspace": (_sz, [_i32, _i64, _i64, _i64]),
+    "sk_sketch_workspace_ex": (_sz, [_i32, _i32, _i64, _i64, _i64, _i64]),
     "sk_sketch_partial": (_i32, [_i32, _i32, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _i64,
                                  _p, _i64, _i32, _p, _p, _sz, _p]),
     "sk_sketch_partial_ex": (_i32, [_i32, _i32, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _i64,

@@ -246,6 +246,11 @@ static Plan make_plan(int64_t m_local, int64_t n, int64_t d) {
 using namespace sk;
 
 namespace sk {
+bool sketch_fft_supported(int64_t m_pad);
+size_t sketch_fft_workspace(int64_t m_pad, int64_t n, int64_t d);
+int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int64_t row_offset, int64_t m_pad,
+                   int64_t n, const double *signs, const int64_t *rows, int64_t d, double *out, int64_t ldo,
+                   int accumulate, int *overflow_flag_dev, void *ws, size_t ws_bytes, cudaStream_t st);
 size_t sketch_tc_workspace(int64_t m_local, int64_t n, int64_t d);
 int sketch_tc_run(int transform, const double *a, int64_t lda, int64_t m_local, int64_t row_offset, int64_t m_pad,
                   int64_t n, const double *signs, const int64_t *rows, int64_t d, double *out, int64_t ldo,
@@ -260,10 +265,20 @@ static size_t dmma_sketch_ws(int64_t m_local, int64_t n, int64_t d) {
 }
 
 size_t sk_sketch_workspace(int level, int64_t m_local, int64_t n, int64_t d) {
+    (void)level;
+    // independent of the row shard's size for the FFT path, so callers pass m_pad
+    // as m_local to size it; take the max over engines
     const size_t a = dmma_sketch_ws(m_local, n, d);
-    if (level != 16) return a;
     const size_t b = sk::sketch_tc_workspace(m_local, n, d);
-    return a > b ? a : b;
+    const size_t c = sk::sketch_fft_workspace(m_local, n, d);
+    return std::max(a, std::max(b, c));
+}
+
+size_t sk_sketch_workspace_ex(int level, int transform, int64_t m_local, int64_t m_pad, int64_t n, int64_t d) {
+    size_t w = dmma_sketch_ws(m_local, n, d);
+    if (level == 16) w = std::max(w, sk::sketch_tc_workspace(m_local, n, d));
+    if (level != 16 && transform == SK_DCT2) w = std::max(w, sk::sketch_fft_workspace(m_pad, n, d));
+    return w;
 }
 
 int sk_sketch_partial_ex(int level, int transform, const double *a, int64_t lda, int64_t m_local,
@@ -296,6 +311,15 @@ int sk_sketch_partial_ex(int level, int transform, const double *a, int64_t lda,
     if (algo == SK_SKETCH_TC) {
         set_error("sk_sketch_partial: the tensor-core path exists for binary16 only");
         return SK_ERR_ARG;
+    }
+    const bool fft_ok = transform == SK_DCT2 && sk::sketch_fft_supported(m_pad);
+    if (algo == SK_SKETCH_FFT || (algo == SK_SKETCH_AUTO && fft_ok)) {
+        if (!fft_ok || level == 16) {
+            set_error("sk_sketch_partial: the FFT path needs binary32/64, DCT-II and m_pad %% 4096 == 0");
+            return SK_ERR_ARG;
+        }
+        return sk::sketch_fft_run(level, a, lda, m_local, row_offset, m_pad, n, signs, rows, d, out, ldo, accumulate,
+                                  overflow_flag_dev, ws, ws_bytes, (cudaStream_t)stream);
     }
     sketch::Plan p = sketch::make_plan(m_local, n, d);
     const size_t need = (size_t)p.splits * p.ntiles * sketch::BM * sketch::BN * sizeof(double);

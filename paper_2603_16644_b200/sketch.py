@@ -80,7 +80,7 @@ class DeviceSketch:
         self.rows = torch.from_numpy(np.ascontiguousarray(op.sampled_rows, dtype=np.int64)).to(dev)
 
 
-ALGO = {"auto": 0, "dmma": 1, "tc": 2}
+ALGO = {"auto": 0, "dmma": 1, "tc": 2, "fft": 3}
 
 
 def _sketch_sum(dsk: DeviceSketch, at: torch.Tensor, level_code: int, row_offset: int = 0,
@@ -96,7 +96,8 @@ def _sketch_sum(dsk: DeviceSketch, at: torch.Tensor, level_code: int, row_offset
         out = torch.zeros((n, d), dtype=torch.float64, device=dev)   # column-major d x n
     if overflow_flag is None:
         overflow_flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    wp, wn = WORKSPACE.get(_lib.lib().sk_sketch_workspace(level_code, m_local, n, d))
+    wp, wn = WORKSPACE.get(_lib.lib().sk_sketch_workspace_ex(level_code, _lib.TRANSFORM_CODE[op.transform],
+                                                             m_local, op.m_pad, n, d))
     call("sk_sketch_partial_ex", level_code, _lib.TRANSFORM_CODE[op.transform], at.data_ptr(), at.stride(0),
          m_local, row_offset, op.m_pad, n, dsk.signs.data_ptr(), dsk.rows.data_ptr(), d, out.data_ptr(),
          d, int(accumulate), overflow_flag.data_ptr(), wp, wn, stream_handle(), ALGO[algo])
