@@ -301,7 +301,7 @@ int sk_sketch_partial_ex(int level, int transform, const double *a, int64_t lda,
     if (!a || !signs || !rows || !out || !overflow_flag_dev || m_local < 0 || n <= 0 || d <= 0 ||
         lda < n || ldo < d || m_pad <= 0 || row_offset < 0 || row_offset + m_local > m_pad ||
         (level != 16 && level != 32 && level != 64) || (transform != SK_DCT2 && transform != SK_WHT) ||
-        m_pad >= (int64_t(1) << 30) || (algo != SK_SKETCH_AUTO && algo != SK_SKETCH_DMMA && algo != SK_SKETCH_TC)) {
+        m_pad >= (int64_t(1) << 30) || algo < SK_SKETCH_AUTO || algo > SK_SKETCH_FFT) {
         set_error("sk_sketch_partial: bad arguments");
         return SK_ERR_ARG;
     }

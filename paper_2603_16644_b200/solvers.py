@@ -457,7 +457,9 @@ def algorithm1_pipeline(a, b, method="pne", precision="auto", d_factor=3.0, tran
             None if precision == "auto" else level_from_name(precision))
         spec_level = fixed or BINARY16
         d = int(math.ceil(d_factor * n))
-        op = make_sketch(m, d, transform, seed) if d >= n else None
+        # only the tensor-core (binary16) sketch is chunk-friendly; the FFT sketch of
+        # binary32/64 transforms all M rows per call, so it runs once after ingestion
+        op = make_sketch(m, d, transform, seed) if (d >= n and spec_level is BINARY16) else None
         plan = (DeviceSketch(op), spec_level.code) if op is not None else None
         ad, gram_auto, sk = _ingest_streamed(host, want_gram=precision == "auto", sketch_plan=plan)
         if sk is not None:
