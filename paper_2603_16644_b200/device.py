@@ -163,7 +163,7 @@ def as_dvec(b, length: int | None = None) -> torch.Tensor:
 
 
 def to_host(t: torch.Tensor) -> np.ndarray:
-    return t.detach().to("cpu").numpy()
+    return t.detach().contiguous().to("cpu").numpy()
 
 
 def like_input(t: torch.Tensor, kind: str):

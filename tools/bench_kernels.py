@@ -36,6 +36,10 @@ if want("gemm"):
     res["gemm"] = t(lambda: D._gram(a, ap_buf)); res["gemm_tflops"] = 2 * m * n * n / (min(res["gemm"]) * 1e-3) / 1e12
 if want("trsm"):
     res["trsm"] = t(lambda: D._trsm(a, r, out=ap_buf)); res["trsm_tflops"] = m * n * n / (min(res["trsm"]) * 1e-3) / 1e12
+    del ap_buf
+    torch.cuda.empty_cache()
+    res["trsm_padded"] = t(lambda: D._trsm(a, r)); res["trsm_padded_tflops"] = m * n * n / (min(res["trsm_padded"]) * 1e-3) / 1e12
+    ap_buf = torch.empty_like(a)
 if want("sketch"):
     op = sq.make_sketch(m, d, "dct2", seed=1); dsk = S.DeviceSketch(op)
     res["sketch_tc"] = t(lambda: S._sketch_sum(dsk, a, 16, algo="tc"))
