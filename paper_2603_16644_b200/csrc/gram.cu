@@ -19,7 +19,15 @@ namespace sk {
 
 namespace gram {
 
-constexpr int BM = 128, BN = 128, BK = 16, WM = 32, WN = 64, STAGES = 4;
+// K-step / ring depth: 32 x 3 measured best on B200 (1M x 2048: SYRK 30.4, GEMM 32.7
+// TFLOP/s vs 30.1 / 32.5 for 16 x 4 and 28.0 / 30.5 for 8 x 8; tools/ab_gram.sh)
+#ifndef SK_GRAM_BK
+#define SK_GRAM_BK 32
+#endif
+#ifndef SK_GRAM_STAGES
+#define SK_GRAM_STAGES 3
+#endif
+constexpr int BM = 128, BN = 128, BK = SK_GRAM_BK, WM = 32, WN = 64, STAGES = SK_GRAM_STAGES;
 constexpr int THREADS = 256;
 constexpr int PITCH = BM + 4;  // doubles; 132 = 4 (mod 16) -> conflict-free fragment loads
 constexpr size_t SMEM = size_t(STAGES) * BK * PITCH * 2 * sizeof(double);

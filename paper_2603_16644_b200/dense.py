@@ -143,12 +143,27 @@ def _qr_r(a_s_level: torch.Tensor, level_code: int, d: int, n: int) -> torch.Ten
 
 
 def _householder_r64(at: torch.Tensor) -> torch.Tensor:
-    """householder_reduce(a)[2] for a device f64 row-major m x n (m >= n)."""
+    """householder_reduce(a)[2] for a device f64 row-major m x n (m >= n).
+
+    Up to TALL_QR_MAX_ROWS rows this is the column Householder kernel (the
+    reference's algorithm and sign convention).  Taller matrices use TSQR: the R
+    factors of row blocks are stacked and reduced again (a tree of Householder
+    QRs).  R is unique up to the signs of its rows; every caller (seminormal
+    equations, the Q^T b column of the QR baseline, singular values) is invariant
+    to those signs."""
     m, n = at.shape
     if m < n:
         raise DimensionMismatch(f"need rows >= cols, got {m} x {n}")
-    colmajor = at.t().contiguous()          # n x m row-major == m x n column-major
-    return _qr_r(colmajor, 64, m, n)
+    if m <= TALL_QR_MAX_ROWS:
+        colmajor = at.t().contiguous()          # n x m row-major == m x n column-major
+        return _qr_r(colmajor, 64, m, n)
+    rows = max(n, TALL_QR_MAX_ROWS // 2)
+    rs = [_householder_r64(at[r0:min(m, r0 + rows)]) for r0 in range(0, m, rows)
+          if min(m, r0 + rows) - r0 >= n]
+    tail = m % rows
+    if tail and tail < n:                       # a short last block joins the stack as rows
+        rs.append(at[m - tail:].contiguous())
+    return _householder_r64(torch.cat(rs, dim=0))
 
 
 def _jacobi_sv(at: torch.Tensor, max_sweeps: int = 30, tol: float = 1e-14) -> np.ndarray:
@@ -162,6 +177,7 @@ def _jacobi_sv(at: torch.Tensor, max_sweeps: int = 30, tol: float = 1e-14) -> np
 
 
 TALL_QR_MAX_ROWS = 262144     # the column Householder kernel's chunk-tree limit
+GRAM_DIAGNOSTICS = True       # tall kappa diagnostics via the Gram (fast); False: via TSQR (robust)
 
 
 def _chol_factor(s: torch.Tensor) -> torch.Tensor:
@@ -187,7 +203,7 @@ def _diagnostics_dev(at: torch.Tensor) -> ConditionDiagnostics:
         at = at.t().contiguous()
     m, n = at.shape
     w = at
-    if m > TALL_QR_MAX_ROWS:
+    if m > TALL_QR_MAX_ROWS and GRAM_DIAGNOSTICS:
         try:
             w = _chol_factor(_gram(at))
         except Exception:   # noqa: BLE001  (breakdown: kappa out of the Gram route's range)

@@ -242,3 +242,21 @@ def test_tall_diagnostics_gram_route(sq, monkeypatch):
     assert gram_route.two_norm == pytest.approx(qr_route.two_norm, rel=1e-12)
     r = D._chol_factor(torch.from_numpy(a.T @ a).cuda()).cpu().numpy()
     assert np.all(np.tril(r, -1) == 0) and rel(r.T @ r, a.T @ a) <= 1e-13
+
+
+def test_tsqr_for_tall_matrices(sq, monkeypatch):
+    """Above the column-Householder row limit, R comes from TSQR (R of stacked
+    block R factors); seminormal / QR-baseline solutions must be unchanged."""
+    from paper_2603_16644_b200 import dense as D
+    from oracle.problems import planted_problem
+    p = planted_problem(5000, 30, 1e6, 1e-6, 3)
+    ref_sne = R.solve_sne(p.a, p.b, x_star=p.x_star)
+    ref_qr = R.solve_qr(p.a, p.b, x_star=p.x_star)
+    monkeypatch.setattr(D, "TALL_QR_MAX_ROWS", 700)
+    got_sne = sq.solve_seminormal(p.a, p.b, x_star=p.x_star)
+    got_qr = sq.solve_qr_baseline(p.a, p.b, x_star=p.x_star)
+    assert got_sne.relative_error <= max(10 * ref_sne.relative_error, 1e-14)
+    assert got_qr.relative_error <= max(10 * ref_qr.relative_error, 1e-14)
+    r_tsqr = np.abs(sq.householder_reduce(p.a)[2])
+    r_ref = np.abs(R.householder_steps(p.a)[2])
+    assert rel(r_tsqr, r_ref) <= 1e-9     # unique up to row signs
