@@ -27,7 +27,7 @@
 namespace sk {
 namespace skfft {
 
-constexpr int N2 = 2048;          // M2: FFT length of pass A
+constexpr int N2 = 1024;          // M2: FFT length of pass A
 constexpr int A_THREADS = 512;    // 4 FFTs per CTA (2 j1 x 2 column pairs)
 constexpr int B_THREADS = 256;
 constexpr int B_PAIRS = 4;        // column pairs per pass-B CTA
@@ -51,7 +51,9 @@ __device__ __forceinline__ void dft4(double2 &x0, double2 &x1, double2 &x2, doub
 // forward R-point DFT in registers, R = 16 (4 x 4) or 8 (4 x 2); tw = e^{-2 pi i t / N2} table
 template <int R>
 __device__ __forceinline__ void dft_small(double2 (&v)[R], const double2 *tw) {
-    if constexpr (R == 16) {
+    if constexpr (R == 4) {
+        dft4(v[0], v[1], v[2], v[3]);
+    } else if constexpr (R == 16) {
         // n = 4 n1 + n2: 4-point over n1, twiddle W16^{n2 k1}, 4-point over n2
 #pragma unroll
         for (int n2 = 0; n2 < 4; ++n2) dft4(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);
@@ -134,32 +136,33 @@ struct PassAParams {
     int *overflow;
 };
 
-// grid: (M1/2, ncols/4)
+// grid: (M1/2, ncols/8).  A CTA owns j1 in {2 a2, 2 a2 + 1} and 8 columns (4 complex
+// pairs): every gathered row segment is a full 64-byte line, every Y store 32 bytes.
 __global__ void __launch_bounds__(A_THREADS) fft_pass_a(const PassAParams p) {
     extern __shared__ __align__(16) double2 fa_smem[];
     double2 *tw = fa_smem;                  // N2 twiddles
-    double2 *x = fa_smem + N2;              // 4 FFTs: f = jj * 2 + pp
-    const int a2 = blockIdx.x;              // j1 in {2 a2, 2 a2 + 1}
-    const int q = blockIdx.y;               // column quad
+    double2 *x = fa_smem + N2;              // 8 FFTs: f = jj * 4 + pp
+    const int a2 = blockIdx.x;
+    const int q = blockIdx.y;               // column octet
     for (int t = threadIdx.x; t < N2; t += blockDim.x) {
         double s, c;
         sincospi(-2.0 * (double)t / (double)N2, &s, &c);
         tw[t] = make_double2(c, s);
     }
-    // ---- gather: v_{j1 + M1 j2} for the two j1 and four columns
-    const int cbase = p.c0 + 4 * q;
+    // ---- gather: v_{j1 + M1 j2} for the two j1 and eight columns
+    const int cbase = p.c0 + 8 * q;
     for (int e = threadIdx.x; e < 2 * N2; e += blockDim.x) {
         const int jj = e / N2, j2 = e % N2;
         const int64_t j1 = 2 * (int64_t)a2 + jj;
         const int64_t row = (j2 < N2 / 2) ? (2 * j1 + 2 * p.M1 * (int64_t)j2)
                                           : (2 * p.M - 1 - 2 * j1 - 2 * p.M1 * (int64_t)j2);
         const int64_t lr = row - p.row_offset;
-        double v[4] = {0.0, 0.0, 0.0, 0.0};
+        double v[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         if (lr >= 0 && lr < p.m_local) {
             const double sg = p.signs[row];
             const double *src = p.a + lr * p.lda + cbase;
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < 8; ++u)
                 if (cbase + u < p.n) {
                     double w = src[u];
                     if (p.level == 32) {   // round_to_precision(A, binary32) (src/precision.py:90-103)
@@ -170,18 +173,18 @@ __global__ void __launch_bounds__(A_THREADS) fft_pass_a(const PassAParams p) {
                     v[u] = sg * w;
                 }
         }
-        x[(jj * 2 + 0) * N2 + j2] = make_double2(v[0], v[1]);
-        x[(jj * 2 + 1) * N2 + j2] = make_double2(v[2], v[3]);
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) x[(jj * 4 + pp) * N2 + j2] = make_double2(v[2 * pp], v[2 * pp + 1]);
     }
     __syncthreads();
-    // 4 FFTs x 2048 points: radix-16 stages have 512 butterflies (1 per thread),
-    // the radix-8 stage 1024 (2 per thread)
+    // 8 FFTs x 1024 points: radix-16 stages have 512 butterflies (1 per thread),
+    // the radix-4 stage 2048 (4 per thread)
     stockham_stage<16, 1>(x, 1, tw);
     stockham_stage<16, 1>(x, 16, tw);
-    stockham_stage<8, 2>(x, 256, tw);
+    stockham_stage<4, 4>(x, 256, tw);
     // ---- twiddle e^{-2 pi i j1 k2 / M} and store Y[pair][k2][j1 pair]
-    const int pair0 = 2 * q;                // pair index within the block
-    for (int e = threadIdx.x; e < 2 * N2; e += blockDim.x) {
+    const int pair0 = 4 * q;                // pair index within the block
+    for (int e = threadIdx.x; e < 4 * N2; e += blockDim.x) {
         const int pp = e / N2, k2 = e % N2;
         double2 out[2];
 #pragma unroll
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(A_THREADS) fft_pass_a(const PassAParams p) {
             const int64_t ph = (j1 * (int64_t)k2) % p.M;
             double s, c;
             sincospi(-2.0 * (double)ph / (double)p.M, &s, &c);
-            out[jj] = cmul(x[(jj * 2 + pp) * N2 + k2], make_double2(c, s));
+            out[jj] = cmul(x[(jj * 4 + pp) * N2 + k2], make_double2(c, s));
         }
         double2 *dst = p.y + ((size_t)(pair0 + pp) * N2 + k2) * p.M1 + 2 * a2;
         *reinterpret_cast<double4 *>(dst) = make_double4(out[0].x, out[0].y, out[1].x, out[1].y);
@@ -281,7 +284,7 @@ bool sketch_fft_supported(int64_t m_pad) { return m_pad >= 2 * skfft::N2 && m_pa
 size_t sketch_fft_workspace(int64_t m_pad, int64_t n, int64_t d) {
     using namespace skfft;
     if (!sketch_fft_supported(m_pad)) return 0;
-    const int64_t cb = std::min<int64_t>(COLBLOCK, (n + 3) / 4 * 4);
+    const int64_t cb = std::min<int64_t>(COLBLOCK, (n + 7) / 8 * 8);
     const size_t ybytes = (size_t)(cb / 2) * m_pad * sizeof(double2);
     const size_t zbytes = (size_t)d * 2 * (cb / 2) * sizeof(double2);
     const size_t req = (size_t)(N2 + 1) * sizeof(int) + (size_t)2 * d * (2 * sizeof(int) + sizeof(int64_t));
@@ -295,7 +298,7 @@ int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int
     if (!sketch_fft_supported(m_pad)) { set_error("sketch_fft: M must be a multiple of 4096"); return SK_ERR_ARG; }
     if (ws_bytes < sketch_fft_workspace(m_pad, n, d)) { set_error("sketch_fft: workspace too small"); return SK_ERR_ARG; }
     const int64_t M = m_pad, M1 = M / N2;
-    const int64_t cb = std::min<int64_t>(COLBLOCK, (n + 3) / 4 * 4);
+    const int64_t cb = std::min<int64_t>(COLBLOCK, (n + 7) / 8 * 8);
     uint8_t *p = static_cast<uint8_t *>(ws);
     double2 *y = reinterpret_cast<double2 *>(p);
     p += align_up((size_t)(cb / 2) * M * sizeof(double2), 256);
@@ -330,16 +333,16 @@ int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int
     SK_CUDA(cudaMemcpyAsync(d_s, hs.data(), (size_t)2 * d * sizeof(int), cudaMemcpyHostToDevice, st));
     SK_CUDA(cudaMemcpyAsync(d_w, hw.data(), (size_t)2 * d * sizeof(int), cudaMemcpyHostToDevice, st));
     SK_CUDA(cudaMemcpyAsync(d_k1, hk1.data(), (size_t)2 * d * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    const size_t smem_a = (size_t)(N2 + 4 * N2) * sizeof(double2);
+    const size_t smem_a = (size_t)(N2 + 8 * N2) * sizeof(double2);
     const size_t smem_b = (size_t)M1 * sizeof(double2);
     if (smem_b > 200 * 1024) { set_error("sketch_fft: M too large for pass B (M1 %lld)", (long long)M1); return SK_ERR_ARG; }
     SK_CUDA(cudaFuncSetAttribute(fft_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
     SK_CUDA(cudaFuncSetAttribute(fft_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
     for (int64_t c0 = 0; c0 < n; c0 += cb) {
-        const int ncols = (int)std::min<int64_t>(cb, (n - c0 + 3) / 4 * 4);
+        const int ncols = (int)std::min<int64_t>(cb, (n - c0 + 7) / 8 * 8);
         const int npairs = ncols / 2;
         PassAParams pa{a, lda, m_local, row_offset, M, M1, signs, (int)c0, ncols, (int)n, y, level, overflow_flag_dev};
-        fft_pass_a<<<dim3((unsigned)(M1 / 2), (unsigned)(ncols / 4)), A_THREADS, smem_a, st>>>(pa);
+        fft_pass_a<<<dim3((unsigned)(M1 / 2), (unsigned)(ncols / 8)), A_THREADS, smem_a, st>>>(pa);
         SK_LAUNCH_CHECK("fft_pass_a");
         PassBParams pb{y, M1, d_ptr, d_s, d_w, d_k1, npairs, zbuf, (int)d};
         fft_pass_b<<<dim3((unsigned)N2, (unsigned)((npairs + B_PAIRS - 1) / B_PAIRS)), B_THREADS, smem_b, st>>>(pb);

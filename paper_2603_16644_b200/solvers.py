@@ -387,11 +387,29 @@ def _a_p_dev(a_p, ad: DMat) -> torch.Tensor:
     return t
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def _gram_and_rhs(x, y, bd):
+    """G = X^T Y (DMMA, compute-bound) and rhs = X^T b (HBM-bound) on two streams so
+    the streaming GEMV hides under the Gram."""
+    cur = torch.cuda.current_stream()
+    side = _SIDE_STREAMS.get(cur.device.index)
+    if side is None:
+        side = _SIDE_STREAMS.setdefault(cur.device.index, torch.cuda.Stream(device=cur.device))
+    side.wait_stream(cur)
+    with torch.cuda.stream(side):
+        rhs = _gemv_t(x, bd)
+    g = _gram(x, y)
+    cur.wait_stream(side)
+    rhs.record_stream(cur)
+    return g, rhs
+
+
 def _pne_dev(ad, bd, pre, a_p, stages=None):
     if stages is not None:
         stages.mark("gram")
-    g = _gram(a_p)
-    rhs = _gemv_t(a_p, bd)
+    g, rhs = _gram_and_rhs(a_p, None, bd)
     if stages is not None:
         stages.mark("nxn")
     try:
@@ -404,8 +422,7 @@ def _pne_dev(ad, bd, pre, a_p, stages=None):
 def _hpne_dev(ad, bd, pre, a_p, stages=None):
     if stages is not None:
         stages.mark("gram")
-    g = _gram(a_p, ad)
-    rhs = _gemv_t(a_p, bd)
+    g, rhs = _gram_and_rhs(a_p, ad, bd)
     if stages is not None:
         stages.mark("nxn")
     return _lu_solve(g, rhs)
