@@ -16,16 +16,20 @@
 // binary tree whose node (l, i) covers [i 2^l, min((i+1) 2^l, L)) and adds its two
 // children when the right one is non-empty.  Its level-8 nodes are independent
 // 256-element chunks, which makes a 2-D (chunk x column) decomposition exact.
-// One cooperative persistent kernel, three grid barriers per column j:
+// One cooperative persistent kernel, two grid barriers per column j:
 //
 //   phase 1  every (256-row chunk q, column c > j) warp unit computes the level-8
 //            node of v_j . w[j:, c]: 8-leaf subtrees per lane, then a 5-level
 //            shuffle tree (lane pairs at distance 1, 2, 4, 8, 16)
-//   phase 2  one warp per column combines its chunk nodes (levels 9..) -> t_c = tau_j * dot
-//   phase 3  every unit applies w[j:, c] -= v_j * t_c to its chunk (rounded product,
-//            rounded difference); CTA 0 updates column j+1 whole and forms reflector
-//            j+1 (norm, alpha, v, v.v, tau) with the same chunked trees (look-ahead)
+//   phase 2  every unit recomputes t_c = tau_j * root (levels 9.. over the chunk
+//            nodes, identical in every unit) and applies w[j:, c] -= v_j * t_c to its
+//            chunk (rounded product, rounded difference); CTA 0 updates column j+1 and,
+//            in the same pass, the chunk nodes of x = w[j+1:, j+1] -> reflector j+1
 //
+// The reflector is kept in compact form, like LAPACK: v_j is column j below the
+// diagonal with only v_0 = x_0 - alpha held apart (ctl), and alpha_j goes to a
+// side array; R's diagonal and exact-zero lower triangle are produced by
+// extract_r.  v.v differs from x.x only in element 0, so only chunk 0 is redone.
 // The Q factor is not formed (build_preconditioner only uses R,
 // src/solvers.py:196-197); see DESIGN.md for the reference's non-finite-Q check.
 #include "common.cuh"
@@ -42,21 +46,31 @@ constexpr int MAXCH = 1024;      // chunk nodes a single warp combines: d <= 262
 template <typename T>
 struct Ctl {
     T tau[2];
-    T alpha[2];
+    T v0[2];
     int fail_code;
     int fail_col;
 };
 
 // Level-8 node over chunk q of u_i * v_i, i in [q*CH, min((q+1)*CH, L)), by one warp.
+// ov: bit 0 replaces u[0] by v0, bit 1 replaces v[0] by v0 (compact reflector).
 template <typename T>
-__device__ __forceinline__ T chunk_node(const T *u, const T *v, int L, int q) {
+__device__ __forceinline__ T chunk_node(const T *u, const T *v, int L, int q, int ov = 0, T v0 = T()) {
     using O = LevelOps<T>;
     const int lane = threadIdx.x & 31;
     const int base = q * CH + lane * 8;
     const int cnt = max(0, min(8, L - base));
     T x[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) x[e] = (e < cnt) ? O::mul(u[base + e], v[base + e]) : O::zero();
+    for (int e = 0; e < 8; ++e) {
+        if (e < cnt) {
+            const bool first = (base + e) == 0;
+            const T a = (first && (ov & 1)) ? v0 : u[base + e];
+            const T b = (first && (ov & 2)) ? v0 : v[base + e];
+            x[e] = O::mul(a, b);
+        } else {
+            x[e] = O::zero();
+        }
+    }
     const T y0 = (1 < cnt) ? O::add(x[0], x[1]) : x[0];
     const T y1 = (3 < cnt) ? O::add(x[2], x[3]) : x[2];
     const T y2 = (5 < cnt) ? O::add(x[4], x[5]) : x[4];
@@ -78,13 +92,13 @@ __device__ __forceinline__ T chunk_node(const T *u, const T *v, int L, int q) {
 }
 
 // Root of the tree over `count` level-8 nodes get(i), by one warp (count <= 1024).
-// Lane l reduces the aligned block [32 l', ...) of B = 32 leaves when count > 32.
+// Lane l reduces the aligned block [l B, (l+1) B) of B leaves (B a power of two).
 template <typename T, class G>
 __device__ __forceinline__ T warp_tree_root(int count, G get) {
     using O = LevelOps<T>;
     const int lane = threadIdx.x & 31;
     int B = 1;
-    while (B * 32 < count) B <<= 1;          // power of two, <= 32 for count <= 1024
+    while (B * 32 < count) B <<= 1;
     const int base = lane * B;
     int cnt = max(0, min(B, count - base));
     T node = O::zero();
@@ -113,126 +127,86 @@ __device__ __forceinline__ T warp_tree_root(int count, G get) {
     return node;
 }
 
-// Whole-column tree dot by one CTA (look-ahead reflector); sh_nodes >= ceil(L/CH).
+// Reflector for column jj given the chunk nodes of x.x in sh_nodes[0..nq), x = w[jj:, jj].
 template <typename T>
-__device__ T cta_dot(const T *u, const T *v, int L, T *sh_nodes, T *sh_root) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nq = (L + CH - 1) / CH;
-    for (int q = warp; q < nq; q += WARPS) {
-        const T node = chunk_node<T>(u, v, L, q);
-        if (lane == 0) sh_nodes[q] = node;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        const T r = warp_tree_root<T>(nq, [&](int i) { return sh_nodes[i]; });
-        if (lane == 0) *sh_root = r;
-    }
-    __syncthreads();
-    const T r = *sh_root;
-    __syncthreads();
-    return r;
-}
-
-// Reflector for column jj given the chunk nodes of x.x in sh_nodes[0..nq), x = w[jj:, jj]
-// (final).  v.v differs from x.x only in element 0, so only chunk 0 is recomputed.
-template <typename T>
-__device__ int reflect_from_nodes(T *x, int L, T *vout, Ctl<T> *ctl, int buf, T *sh_nodes, T *sh_root) {
-    using O = LevelOps<T>;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nq = (L + CH - 1) / CH;
-    if (warp == 0) {
-        const T r = warp_tree_root<T>(nq, [&](int i) { return sh_nodes[i]; });
-        if (lane == 0) *sh_root = r;
-    }
-    __syncthreads();
-    const T nrm = O::sqrt(*sh_root);
-    if (O::to_f64(nrm) == 0.0) return SK_RANK_DEFICIENT;
-    const T x0 = x[0];
-    const T alpha = (O::to_f64(x0) >= 0.0) ? O::sub(O::zero(), nrm) : nrm;   // -norm if x0 >= 0
-    for (int i = threadIdx.x; i < L; i += THREADS) vout[i] = (i == 0) ? O::sub(x0, alpha) : x[i];
-    __syncthreads();
-    if (warp == 0) {
-        const T node0 = chunk_node<T>(vout, vout, L, 0);
-        if (lane == 0) sh_nodes[0] = node0;
-        __syncwarp();
-        const T r = warp_tree_root<T>(nq, [&](int i) { return sh_nodes[i]; });
-        if (lane == 0) *sh_root = r;
-    }
-    __syncthreads();
-    const T vtv = *sh_root;
-    __syncthreads();
-    if (O::to_f64(vtv) == 0.0) return SK_RANK_DEFICIENT;
-    const T tau = O::div(O::from_f64(2.0), vtv);
-    if (!O::finite(tau)) return SK_RANK_DEFICIENT;
-    for (int i = threadIdx.x; i < L; i += THREADS) x[i] = (i == 0) ? alpha : O::zero();
-    if (threadIdx.x == 0) { ctl->tau[buf] = tau; ctl->alpha[buf] = alpha; }
-    __syncthreads();
-    return SK_OK;
-}
-
-// CTA 0's look-ahead: apply reflector j (v, t) to column j+1 and, in the same pass,
-// compute the chunk nodes of the updated x = w[j+1:, j+1] for reflector j+1.
-template <typename T>
-__device__ int update_and_reflect(T *colj, int L, const T *v, T t, T *vout, Ctl<T> *ctl, int buf, T *sh_nodes,
+__device__ int reflect_from_nodes(const T *x, int L, Ctl<T> *ctl, int buf, T *alphas, int jj, T *sh_nodes,
                                   T *sh_root) {
     using O = LevelOps<T>;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) colj[0] = O::sub(colj[0], O::mul(v[0], t));   // R entry (row j)
-    T *x = colj + 1;
-    const T *vx = v + 1;
-    const int Lx = L - 1, nq = (Lx + CH - 1) / CH;
-    for (int q = warp; q < nq; q += WARPS) {
-        const int base = q * CH + lane * 8;
-        const int cnt = max(0, min(8, Lx - base));
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-            if (e < cnt) x[base + e] = O::sub(x[base + e], O::mul(vx[base + e], t));
-        __syncwarp();
-        const T node = chunk_node<T>(x, x, Lx, q);
-        if (lane == 0) sh_nodes[q] = node;
+    const int nq = (L + CH - 1) / CH;
+    __shared__ T sh_v0, sh_tau, sh_alpha;
+    __shared__ int sh_rc;
+    if (warp == 0) {
+        const T nrm = O::sqrt(warp_tree_root<T>(nq, [&](int i) { return sh_nodes[i]; }));
+        int rc = SK_OK;
+        T alpha = O::zero(), v0 = O::zero(), tau = O::zero();
+        if (O::to_f64(nrm) == 0.0) {
+            rc = SK_RANK_DEFICIENT;
+        } else {
+            const T x0 = x[0];
+            alpha = (O::to_f64(x0) >= 0.0) ? O::sub(O::zero(), nrm) : nrm;   // -norm if x0 >= 0
+            v0 = O::sub(x0, alpha);
+            const T node0 = chunk_node<T>(x, x, L, 0, 3, v0);                 // v.v: chunk 0 redone
+            if (lane == 0) sh_nodes[0] = node0;
+            __syncwarp();
+            const T vtv = warp_tree_root<T>(nq, [&](int i) { return sh_nodes[i]; });
+            if (O::to_f64(vtv) == 0.0) {
+                rc = SK_RANK_DEFICIENT;
+            } else {
+                tau = O::div(O::from_f64(2.0), vtv);
+                if (!O::finite(tau)) rc = SK_RANK_DEFICIENT;
+            }
+        }
+        if (lane == 0) { sh_rc = rc; sh_v0 = v0; sh_tau = tau; sh_alpha = alpha; }
     }
     __syncthreads();
-    return reflect_from_nodes<T>(x, Lx, vout, ctl, buf, sh_nodes, sh_root);
+    const int rc = sh_rc;
+    if (rc == SK_OK && threadIdx.x == 0) {
+        ctl->tau[buf] = sh_tau;
+        ctl->v0[buf] = sh_v0;
+        alphas[jj] = sh_alpha;
+    }
+    (void)sh_root;
+    __syncthreads();
+    return rc;
 }
 
-// Reflector for column jj from the (final) column w[jj:, jj]; CTA-cooperative.
 template <typename T>
-__device__ int make_reflector(T *w, int64_t ld, int d, int jj, T *vout, Ctl<T> *ctl, int buf, T *sh_nodes,
+__device__ int make_reflector(const T *w, int64_t ld, int d, int jj, Ctl<T> *ctl, int buf, T *alphas, T *sh_nodes,
                               T *sh_root) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int L = d - jj;
-    T *x = w + (int64_t)jj * ld + jj;
+    const T *x = w + (int64_t)jj * ld + jj;
     const int nq = (L + CH - 1) / CH;
     for (int q = warp; q < nq; q += WARPS) {
         const T node = chunk_node<T>(x, x, L, q);
         if (lane == 0) sh_nodes[q] = node;
     }
     __syncthreads();
-    return reflect_from_nodes<T>(x, L, vout, ctl, buf, sh_nodes, sh_root);
+    return reflect_from_nodes<T>(x, L, ctl, buf, alphas, jj, sh_nodes, sh_root);
 }
 
 template <typename T>
 __global__ void __launch_bounds__(THREADS)
-householder_kernel(T *w, int64_t ld, int d, int n, T *vbuf /* 2 x d */, T *part /* nqmax x n */, T *tvec /* n */,
-                   Ctl<T> *ctl) {
+householder_kernel(T *w, int64_t ld, int d, int n, T *alphas /* n */, T *part /* nqmax x n */, Ctl<T> *ctl) {
     using O = LevelOps<T>;
     __shared__ T sh_nodes[MAXCH];
     __shared__ T sh_root;
     cg::grid_group grid = cg::this_grid();
-    const int lane = threadIdx.x & 31;
-    const int gwarp = blockIdx.x * WARPS + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gwarp = blockIdx.x * WARPS + warp;
     const int nwarps = gridDim.x * WARPS;
 
     if (blockIdx.x == 0) {
-        const int rc = make_reflector<T>(w, ld, d, 0, vbuf, ctl, 0, sh_nodes, &sh_root);
+        const int rc = make_reflector<T>(w, ld, d, 0, ctl, 0, alphas, sh_nodes, &sh_root);
         if (rc != SK_OK && threadIdx.x == 0) { ctl->fail_code = rc; ctl->fail_col = 0; }
     }
     grid.sync();
     for (int j = 0; j < n - 1; ++j) {
         if (ctl->fail_code != SK_OK) return;   // uniform: read after a barrier
         const int buf = j & 1;
-        const T *v = vbuf + (size_t)buf * d;
-        const T tau = ctl->tau[buf];
+        const T *v = w + (int64_t)j * ld + j;  // compact reflector: v[0] is ctl->v0
+        const T tau = ctl->tau[buf], v0 = ctl->v0[buf];
         const int L = d - j;
         const int nq = (L + CH - 1) / CH;
         const int ncols = n - j - 1;           // columns j+1 .. n-1
@@ -242,38 +216,47 @@ householder_kernel(T *w, int64_t ld, int d, int n, T *vbuf /* 2 x d */, T *part 
             const int q = u % nq, c = j + 1 + u / nq;
             const int q2 = u2 % nq, c2 = j + 1 + u2 / nq;
             const bool has2 = u2 < nq * ncols;
-            const T node = chunk_node<T>(v, w + (int64_t)c * ld + j, L, q);
-            const T node2 = has2 ? chunk_node<T>(v, w + (int64_t)c2 * ld + j, L, q2) : O::zero();
+            const T node = chunk_node<T>(v, w + (int64_t)c * ld + j, L, q, 1, v0);
+            const T node2 = has2 ? chunk_node<T>(v, w + (int64_t)c2 * ld + j, L, q2, 1, v0) : O::zero();
             if (lane == 0) {
                 part[(size_t)q * n + c] = node;
                 if (has2) part[(size_t)q2 * n + c2] = node2;
             }
         }
         grid.sync();
-        // ---- phases 2+3: every unit recomputes t_c = tau * root from the chunk nodes
-        // of its column (identically), then applies the rank-1 update to its chunk;
-        // CTA 0 owns column j+1 and forms reflector j+1
-        (void)tvec;
+        // ---- phase 2
         if (blockIdx.x == 0) {
-            T t;
-            if (threadIdx.x < 32) {
+            // column j+1: t, update (rows j..), chunk nodes of x = w[j+1:, j+1], reflector j+1
+            if (warp == 0) {
                 const T root = warp_tree_root<T>(nq, [&](int i) { return part[(size_t)i * n + j + 1]; });
                 if (lane == 0) sh_root = O::mul(tau, root);
             }
             __syncthreads();
-            t = sh_root;
+            const T t = sh_root;
+            T *colj = w + (int64_t)(j + 1) * ld + j;
+            if (threadIdx.x == 0) colj[0] = O::sub(colj[0], O::mul(v0, t));   // R entry (row j)
+            T *x = colj + 1;
+            const T *vx = v + 1;
+            const int Lx = L - 1, nqx = (Lx + CH - 1) / CH;
+            for (int q = warp; q < nqx; q += WARPS) {
+                const int base = q * CH + lane * 8;
+                const int cnt = max(0, min(8, Lx - base));
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    if (e < cnt) x[base + e] = O::sub(x[base + e], O::mul(vx[base + e], t));
+                __syncwarp();
+                const T node = chunk_node<T>(x, x, Lx, q);
+                if (lane == 0) sh_nodes[q] = node;
+            }
             __syncthreads();
-            const int rc = update_and_reflect<T>(w + (int64_t)(j + 1) * ld + j, L, v, t,
-                                                 vbuf + (size_t)(buf ^ 1) * d, ctl, buf ^ 1, sh_nodes, &sh_root);
+            const int rc = reflect_from_nodes<T>(x, Lx, ctl, buf ^ 1, alphas, j + 1, sh_nodes, &sh_root);
             if (rc != SK_OK && threadIdx.x == 0) { ctl->fail_code = rc; ctl->fail_col = j + 1; }
         } else {
-            // CTA-major: CTA b >= 1 owns columns j+2+k*(G-1)+(b-1); its warps first
-            // compute t_c for all owned columns in parallel, then update (column, chunk)
-            // units with two in flight per warp.
+            // CTA-major: CTA b >= 1 owns columns j+2+k*(G-1)+(b-1); its warps compute t_c for
+            // all owned columns in parallel, then update (column, chunk) units, two in flight
             const int G1 = gridDim.x - 1, b1 = blockIdx.x - 1;
             const int rest = ncols - 1;                               // columns j+2 .. n-1
             const int mine = rest > b1 ? (rest - b1 + G1 - 1) / G1 : 0;
-            const int warp = threadIdx.x >> 5;
             for (int k = warp; k < mine; k += WARPS) {
                 const int c = j + 2 + b1 + k * G1;
                 const T root = warp_tree_root<T>(nq, [&](int i) { return part[(size_t)i * n + c]; });
@@ -293,8 +276,8 @@ householder_kernel(T *w, int64_t ld, int d, int n, T *vbuf /* 2 x d */, T *part 
 #pragma unroll 4
                 for (int i = lane; i < CH; i += 32) {
                     T a1 = O::zero(), a2 = O::zero(), x1 = O::zero(), x2 = O::zero();
-                    if (i < cnt1) { a1 = col1[i]; x1 = v1[i]; }
-                    if (i < cnt2) { a2 = col2[i]; x2 = v2[i]; }
+                    if (i < cnt1) { a1 = col1[i]; x1 = (q1 == 0 && i == 0) ? v0 : v1[i]; }
+                    if (i < cnt2) { a2 = col2[i]; x2 = (q2 == 0 && i == 0) ? v0 : v2[i]; }
                     if (i < cnt1) col1[i] = O::sub(a1, O::mul(x1, t1));
                     if (i < cnt2) col2[i] = O::sub(a2, O::mul(x2, t2));
                 }
@@ -318,13 +301,17 @@ __global__ void prescale_half(__half *a, int64_t count, double scale) {
         a[i] = __double2half((double)__half2float(a[i]) * scale);   // round_to_precision(work*scale, binary16)
 }
 
-// R (row-major f64) = promote(W[:n, :]) / scale; non-finite upper entries are counted
+// R (row-major f64) = promote(upper part, alphas on the diagonal, exact zeros below) / scale;
+// non-finite entries are counted (src/precision.py:200 checks the binary16 R)
 template <typename T>
-__global__ void extract_r(const T *w, int64_t ld, int n, double scale, double *r, int64_t ldr, int *nonfinite) {
+__global__ void extract_r(const T *w, int64_t ld, const T *alphas, int n, double scale, double *r, int64_t ldr,
+                          int *nonfinite) {
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= (int64_t)n * n) return;
     const int i = (int)(idx / n), c = (int)(idx % n);
-    const T x = w[(int64_t)c * ld + i];
+    T x = LevelOps<T>::zero();
+    if (i < c) x = w[(int64_t)c * ld + i];
+    else if (i == c) x = alphas[c];
     if (!LevelOps<T>::finite(x)) atomicAdd(nonfinite, 1);
     r[(int64_t)i * ldr + c] = LevelOps<T>::to_f64(x) / scale;
 }
@@ -333,8 +320,8 @@ inline int64_t nq_max(int64_t d) { return (d + CH - 1) / CH; }
 
 template <typename T>
 size_t ws_bytes(int64_t d, int64_t n) {
-    return align_up(sizeof(Ctl<T>), 256) + align_up(2 * (size_t)d * sizeof(T), 256) +
-           align_up((size_t)nq_max(d) * n * sizeof(T), 256) + align_up((size_t)n * sizeof(T), 256) + 256;
+    return align_up(sizeof(Ctl<T>), 256) + align_up((size_t)n * sizeof(T), 256) +
+           align_up((size_t)nq_max(d) * n * sizeof(T), 256) + 256;
 }
 
 template <typename T, bool HALF>
@@ -345,12 +332,10 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
     unsigned char *p = static_cast<unsigned char *>(ws);
     Ctl<T> *ctl = reinterpret_cast<Ctl<T> *>(p);
     p += align_up(sizeof(Ctl<T>), 256);
-    T *vbuf = reinterpret_cast<T *>(p);
-    p += align_up(2 * (size_t)d * sizeof(T), 256);
+    T *alphas = reinterpret_cast<T *>(p);
+    p += align_up((size_t)n * sizeof(T), 256);
     T *part = reinterpret_cast<T *>(p);
     p += align_up((size_t)nq_max(d) * n * sizeof(T), 256);
-    T *tvec = reinterpret_cast<T *>(p);
-    p += align_up((size_t)n * sizeof(T), 256);
     int *nonfinite = reinterpret_cast<int *>(p);
     SK_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl<T>), st));
     SK_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), st));
@@ -362,7 +347,7 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
     if (blocks < 2) blocks = std::min(2, maxb);
     int di = (int)d, ni = (int)n;
     int64_t ldw = d;
-    void *args[] = {&w, &ldw, &di, &ni, &vbuf, &part, &tvec, &ctl};
+    void *args[] = {&w, &ldw, &di, &ni, &alphas, &part, &ctl};
     SK_CUDA(cudaLaunchCooperativeKernel((const void *)kfn, dim3(blocks), dim3(THREADS), args, 0, st));
     SK_LAUNCH_CHECK("householder_kernel");
     int fail[2];
@@ -373,7 +358,7 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
         return fill_status(status, fail[0], fail[1], 0.0, 0.0);
     }
     const int64_t total = n * n;
-    extract_r<T><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(w, d, (int)n, scale, r, ldr, nonfinite);
+    extract_r<T><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(w, d, alphas, (int)n, scale, r, ldr, nonfinite);
     SK_LAUNCH_CHECK("extract_r");
     int nf = 0;
     SK_CUDA(cudaMemcpyAsync(&nf, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(A_THREADS) fft_pass_a(const PassAParams p) {
 #pragma unroll
         for (int jj = 0; jj < 2; ++jj) {
             const int64_t j1 = 2 * (int64_t)a2 + jj;
-            const int64_t ph = (j1 * (int64_t)k2) % p.M;
+            const int64_t ph = j1 * (int64_t)k2;     // < M1 * N2 = M: no reduction needed
             double s, c;
             sincospi(-2.0 * (double)ph / (double)p.M, &s, &c);
             out[jj] = cmul(x[(jj * 4 + pp) * N2 + k2], make_double2(c, s));
@@ -235,8 +235,13 @@ __global__ void __launch_bounds__(B_THREADS) fft_pass_b(const PassBParams p) {
         const int64_t k1 = p.req_k1[rq];
         double2 acc = make_double2(0.0, 0.0);
         const double2 *yrow = p.y + ((size_t)(pbase + pp) * N2 + k2) * M1;   // reused by the k2's requests (L1/L2)
+        // twiddle index (j1 k1) mod M1, advanced incrementally (no 64-bit modulo per term)
+        int idx = (int)(((int64_t)lane * k1) % M1);
+        const int step = (int)((32 * k1) % M1);
         for (int j1 = lane; j1 < M1; j1 += 32) {
-            const double2 w = tw[(int)(((int64_t)j1 * k1) % M1)];
+            const double2 w = tw[idx];
+            idx += step;
+            if (idx >= M1) idx -= M1;
             const double2 yv = yrow[j1];
             acc.x += w.x * yv.x - w.y * yv.y;
             acc.y += w.x * yv.y + w.y * yv.x;
