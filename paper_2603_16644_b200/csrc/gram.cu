@@ -19,16 +19,27 @@ namespace sk {
 
 namespace gram {
 
-// K-step / ring depth: 32 x 3 measured best on B200 (1M x 2048: SYRK 30.4, GEMM 32.7
-// TFLOP/s vs 30.1 / 32.5 for 16 x 4 and 28.0 / 30.5 for 8 x 8; tools/ab_gram.sh)
+// Tile configuration, measured on B200 with tools/ab_gram.sh at 1M x 2048 (SYRK / GEMM
+// TFLOP/s): 64x64 tiles, 4 warps of 32x32, BK 16, 4 stages, 3 CTAs per SM: 33.3 / 34.2
+// (96% of cuBLAS DGEMM); 128x128 / 8 warps / BK 32 x 3: 30.4 / 32.7; BK 16 x 4: 30.1 /
+// 32.5; 64x64 BK 8 x 6: 32.4 / 33.3.  More resident CTAs hide the DMMA / barrier
+// latencies that one 8-warp CTA per SM could not.
 #ifndef SK_GRAM_BK
-#define SK_GRAM_BK 32
+#define SK_GRAM_BK 16
 #endif
 #ifndef SK_GRAM_STAGES
-#define SK_GRAM_STAGES 3
+#define SK_GRAM_STAGES 4
 #endif
-constexpr int BM = 128, BN = 128, BK = SK_GRAM_BK, WM = 32, WN = 64, STAGES = SK_GRAM_STAGES;
-constexpr int THREADS = 256;
+#ifndef SK_GRAM_BM
+#define SK_GRAM_BM 64
+#define SK_GRAM_WM 32
+#define SK_GRAM_WN 32
+#define SK_GRAM_THREADS 128
+#define SK_GRAM_MINB 3
+#endif
+constexpr int BM = SK_GRAM_BM, BN = SK_GRAM_BM, BK = SK_GRAM_BK, WM = SK_GRAM_WM, WN = SK_GRAM_WN,
+              STAGES = SK_GRAM_STAGES;
+constexpr int THREADS = SK_GRAM_THREADS;
 constexpr int PITCH = BM + 4;  // doubles; 132 = 4 (mod 16) -> conflict-free fragment loads
 constexpr size_t SMEM = size_t(STAGES) * BK * PITCH * 2 * sizeof(double);
 
@@ -85,7 +96,7 @@ __device__ __forceinline__ void load_stage(double *xs, double *ys, const double 
 // One work unit = (tile, split).  unit = split * ntiles + tile so that CTAs that
 // are resident together share a K range (L2 reuse of the X/Y row block).
 template <bool VEC16, bool SYRK>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, SK_GRAM_MINB)
 gram_tn_kernel(const double *__restrict__ x, int64_t ldx, const double *__restrict__ y, int64_t ldy,
                int64_t m, int n, int ntn, int ntiles, int64_t kchunk, double *__restrict__ part) {
     extern __shared__ __align__(16) double smem[];
@@ -203,13 +214,20 @@ static Plan make_plan(int64_t m, int64_t n, bool syrk) {
     const int64_t min_chunk = 1024;  // rows per split: keeps each unit long enough
     int64_t smax = (m + min_chunk - 1) / min_chunk;
     if (smax < 1) smax = 1;
-    // aim for ~64 waves of one CTA per SM, exact multiple of the SM count if possible
-    int64_t target = (int64_t)64 * sms / p.ntiles;
+    // ~16 waves of resident CTAs; among nearby split counts pick the one whose last
+    // wave is fullest (units = tiles x splits spread over sms x SK_GRAM_MINB slots)
+    const int64_t slots = (int64_t)sms * SK_GRAM_MINB;
+    int64_t target = 16 * slots / p.ntiles;
     if (target < 1) target = 1;
     if (target > smax) target = smax;
     int64_t best = target;
-    for (int64_t s = target; s >= (target * 4) / 5 && s >= 1; --s)
-        if (((int64_t)p.ntiles * s) % sms == 0) { best = s; break; }
+    double best_fill = -1.0;
+    for (int64_t s = std::max<int64_t>(1, target / 2); s <= std::min<int64_t>(smax, 2 * target); ++s) {
+        const int64_t units = (int64_t)p.ntiles * s;
+        const int64_t waves = (units + slots - 1) / slots;
+        const double fill = (double)units / (double)(waves * slots);
+        if (fill > best_fill + 1e-9 || (fill > best_fill - 1e-9 && s > best)) { best_fill = fill; best = s; }
+    }
     p.splits = (int)best;
     p.kchunk = (m + p.splits - 1) / p.splits;
     p.kchunk = (p.kchunk + BK - 1) / BK * BK;

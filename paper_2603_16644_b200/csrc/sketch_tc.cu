@@ -213,13 +213,16 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
             const uint64_t r = valid ? (uint64_t)p.rows[i] : 0;
             const uint64_t f1 = r % fourM;
             // per-row offset table e^{i pi r (2t) / 2M}, t = 0..31 (exact integer phases)
-            float wc[32], ws[32];
+            // 16-entry table (registers): columns 16..31 use the base rotated by e^{i 16 delta}
+            float wc[16], ws[16], wc16 = 1.f, ws16 = 0.f;
             if (!p.wht) {
 #pragma unroll
-                for (int t = 0; t < 32; ++t) {
+                for (int t = 0; t < 16; ++t) {
                     const uint64_t q = (f1 * (uint64_t)(2 * t)) % fourM;
                     sincospif((float)q * inv2M, &ws[t], &wc[t]);
                 }
+                const uint64_t q16 = (f1 * (uint64_t)32) % fourM;
+                sincospif((float)q16 * inv2M, &ws16, &wc16);
             }
             // phase of this thread's first column, advanced exactly by r*2*BK per K-block
             uint64_t ph = (f1 * ((uint64_t)(2 * (p.row_offset + k0 + half * 32) + 1) % fourM)) % fourM;
@@ -236,6 +239,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
                     ph += dph;
                     if (ph >= fourM) ph -= fourM;
                 }
+                const float zc2 = zc * wc16 - zs * ws16, zs2 = zs * wc16 + zc * ws16;
                 const bool flat = !p.wht && (r == 0 || !valid);
                 const float cflat = valid ? 0.70710678118654752f : 0.f;
 #pragma unroll
@@ -251,9 +255,12 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
                             a1 = valid ? ((__popcll(r & j1) & 1) ? -1.f : 1.f) : 0.f;
                         } else if (flat) {
                             a0 = a1 = cflat;
-                        } else {
+                        } else if (t < 16) {
                             a0 = zc * wc[t] - zs * ws[t];
                             a1 = zc * wc[t + 1] - zs * ws[t + 1];
+                        } else {
+                            a0 = zc2 * wc[t - 16] - zs2 * ws[t - 16];
+                            a1 = zc2 * wc[t - 15] - zs2 * ws[t - 15];
                         }
                         __half2 h = __floats2half2_rn(a0, a1);
                         pk[e] = *reinterpret_cast<uint32_t *>(&h);
