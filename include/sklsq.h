@@ -171,6 +171,11 @@ size_t sk_nxn_workspace(int64_t n);
 int sk_chol_solve_f64(const double *s, int64_t n, const double *rhs, double *x,
                       sk_status *status, void *ws, size_t ws_bytes, sk_stream_t stream);
 
+/* out_host[0] = #non-finite entries of G (n x n), out_host[1] = trace(G).  With
+ * G = A^T A this validates A (non-finite A => non-finite G) and gives ||A||_F^2,
+ * which lets the kappa0 pass replace the separate validation pass over A. */
+int sk_gram_check(const double *g, int64_t n, double *out_host, void *ws, size_t ws_bytes, sk_stream_t stream);
+
 /* Upper Cholesky factor R = L^T (row-major n x n, zeros below) of (S + S^T)/2:
  * cholesky_factor src/dense.py:289-311 (pivot <= 0 or non-finite ->
  * SK_NOT_POSITIVE_DEFINITE).  Used for the Gram route to kappa(A_p) on tall A_p. */

@@ -61,6 +61,7 @@ SIGNATURES = {
     "sk_qr_r": (_i32, [_i32, _p, _i64, _i64, _p, _i64, _ps, _p, _sz, _p]),
     "sk_nxn_workspace": (_sz, [_i64]),
     "sk_chol_solve_f64": (_i32, [_p, _i64, _p, _p, _ps, _p, _sz, _p]),
+    "sk_gram_check": (_i32, [_p, _i64, _pd, _p, _sz, _p]),
     "sk_chol_factor_f64": (_i32, [_p, _i64, _p, _ps, _p, _sz, _p]),
     "sk_lu_solve_f64": (_i32, [_p, _i64, _p, _p, _ps, _p, _sz, _p]),
     "sk_trsv_f64": (_i32, [_p, _i64, _i64, _i32, _p, _p, _ps, _p, _sz, _p]),

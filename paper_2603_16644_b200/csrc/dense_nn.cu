@@ -50,6 +50,20 @@ __global__ void sym_stats(const double *a, int n, double *out) {
         atomicAdd(out + 2, nf);
     }
 }
+__global__ void trace_kernel(const double *a, int n, double *out) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += a[(int64_t)i * n + i];
+    s = warp_sum(s);
+    __shared__ double sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sh[k];
+        *out = t;
+    }
+}
+
 __global__ void col_abs_sums(const double *a, int n, double *colsum) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
@@ -129,6 +143,127 @@ __global__ void __launch_bounds__(THREADS) chol_kernel(double *w, double *l, int
             }
         }
         grid.sync();
+    }
+}
+
+// Blocked right-looking Cholesky, in place on the lower triangle of W (col-major),
+// panels of CB = 32 columns, three grid barriers per panel (64 panels at n = 2048
+// instead of one barrier per column):
+//   1. CTA 0 factors the 32 x 32 diagonal block in shared memory (pivot > 0 and
+//      finite, else NotPositiveDefinite at that column)
+//   2. every CTA solves its rows of the panel against the diagonal block
+//   3. every CTA applies the rank-32 update to 32 x 32 tiles of the trailing lower
+//      triangle
+// Same quantities as the column algorithm, blocked summation order.
+constexpr int CB = 32;
+
+__global__ void __launch_bounds__(THREADS) chol_blocked_kernel(double *w, int n, FactorCtl *ctl) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double dblk[CB][CB + 1];
+    __shared__ double ti[CB][CB + 1], tk[CB][CB + 1];
+    const int tid = threadIdx.x;
+    for (int J = 0; J < n; J += CB) {
+        const int jb = min(CB, n - J);
+        // ---- 1. diagonal block
+        if (blockIdx.x == 0) {
+            for (int e = tid; e < CB * CB; e += blockDim.x) {
+                const int i = e / CB, k = e % CB;
+                dblk[i][k] = (i < jb && k < jb && k <= i) ? w[(int64_t)(J + k) * n + J + i] : 0.0;
+            }
+            __syncthreads();
+            if (tid < 32) {
+                const int lane = tid;
+                int fail = -1;
+                double fval = 0.0;
+                for (int j = 0; j < jb; ++j) {
+                    const double c0 = dblk[j][j];
+                    if (!(c0 > 0.0) || !isfinite(c0)) { fail = j; fval = c0; break; }
+                    const double d = sqrt(c0);
+                    __syncwarp();
+                    if (lane == 0) dblk[j][j] = d;
+                    if (lane > j && lane < jb) dblk[lane][j] = dblk[lane][j] / d;
+                    __syncwarp();
+                    if (lane > j && lane < jb)
+                        for (int k = j + 1; k <= lane; ++k)
+                            dblk[lane][k] = __dsub_rn(dblk[lane][k], __dmul_rn(dblk[lane][j], dblk[k][j]));
+                    __syncwarp();
+                }
+                if (lane == 0 && fail >= 0) {
+                    ctl->fail_code = SK_NOT_POSITIVE_DEFINITE;
+                    ctl->fail_col = J + fail;
+                    ctl->fail_value = fval;
+                }
+            }
+            __syncthreads();
+            for (int e = tid; e < CB * CB; e += blockDim.x) {
+                const int i = e / CB, k = e % CB;
+                if (i < jb && k < jb && k <= i) w[(int64_t)(J + k) * n + J + i] = dblk[i][k];
+            }
+        }
+        grid.sync();
+        if (ctl->fail_code) return;
+        // ---- 2. panel rows below the diagonal block: x = w_row * L_JJ^{-T}
+        for (int e = tid; e < CB * CB; e += blockDim.x) {
+            const int i = e / CB, k = e % CB;
+            dblk[i][k] = (i < jb && k < jb && k <= i) ? w[(int64_t)(J + k) * n + J + i] : 0.0;
+        }
+        __syncthreads();
+        for (int64_t r = J + jb + blockIdx.x * (int64_t)blockDim.x + tid; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+            double x[CB];
+#pragma unroll
+            for (int k = 0; k < CB; ++k) x[k] = (k < jb) ? w[(int64_t)(J + k) * n + r] : 0.0;
+#pragma unroll
+            for (int k = 0; k < CB; ++k) {
+                if (k < jb) {
+                    double s = x[k];
+#pragma unroll
+                    for (int l = 0; l < k; ++l) s = __dsub_rn(s, __dmul_rn(x[l], dblk[k][l]));
+                    x[k] = s / dblk[k][k];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < CB; ++k)
+                if (k < jb) w[(int64_t)(J + k) * n + r] = x[k];
+        }
+        grid.sync();
+        // ---- 3. trailing update of the lower triangle, 32 x 32 tiles
+        const int t0 = J + jb;
+        const int nt = (n - t0 + CB - 1) / CB;
+        const int ntri = nt * (nt + 1) / 2;
+        for (int tix = blockIdx.x; tix < ntri; tix += gridDim.x) {
+            int bi = (int)((sqrt(8.0 * tix + 1.0) - 1.0) * 0.5);
+            while ((bi + 1) * (bi + 2) / 2 <= tix) ++bi;
+            while (bi * (bi + 1) / 2 > tix) --bi;
+            const int bk = tix - bi * (bi + 1) / 2;
+            const int i0 = t0 + bi * CB, k0 = t0 + bk * CB;
+            __syncthreads();
+            for (int e = tid; e < CB * CB; e += blockDim.x) {
+                const int rr = e % CB, l = e / CB;
+                ti[rr][l] = (i0 + rr < n && l < jb) ? w[(int64_t)(J + l) * n + i0 + rr] : 0.0;
+                tk[rr][l] = (k0 + rr < n && l < jb) ? w[(int64_t)(J + l) * n + k0 + rr] : 0.0;
+            }
+            __syncthreads();
+            for (int e = tid; e < CB * CB; e += blockDim.x) {
+                const int rr = e % CB, cc = e / CB;
+                const int i = i0 + rr, k = k0 + cc;
+                if (i < n && k < n && k <= i) {
+                    double s = 0.0;
+#pragma unroll 8
+                    for (int l = 0; l < CB; ++l) s += ti[rr][l] * tk[cc][l];
+                    double *p = w + (int64_t)k * n + i;
+                    *p = *p - s;
+                }
+            }
+        }
+        grid.sync();
+    }
+}
+
+__global__ void lower_to_l(const double *w, int n, double *l) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(idx / n), i = (int)(idx % n);   // col-major: l[i + k n]
+        l[idx] = (i >= k) ? w[idx] : 0.0;
     }
 }
 
@@ -460,15 +595,17 @@ static int chol_factor(const double *s, int n, Ws &ws, sk_status *status, cudaSt
     SK_CUDA(cudaMemsetAsync(ws.l, 0, (size_t)n * n * sizeof(double), st));
     symmetrize<<<(unsigned)std::min<int64_t>(((int64_t)n * n + 255) / 256, 4096), 256, 0, st>>>(s, n, ws.w);
     SK_LAUNCH_CHECK("symmetrize");
-    // grid barriers dominate at small trailing sizes: at most 2 CTAs per SM
-    const int blocks = coop_blocks((const void *)chol_kernel, THREADS, 0,
-                                   std::min<int64_t>(2 * sm_count(), ((int64_t)n * n / 2 + THREADS * 8 - 1) / (THREADS * 8)));
+    // blocked: one CTA per SM (3 grid barriers per 32-column panel)
+    const int blocks = coop_blocks((const void *)chol_blocked_kernel, THREADS, 0,
+                                   std::min<int64_t>(sm_count(), ((int64_t)n * n / 2 + 1023) / 1024 + 1));
     if (!blocks) { set_error("chol_kernel not co-resident"); return SK_ERR_CUDA; }
-    double *w = ws.w, *l = ws.l;
+    double *w = ws.w;
     int ni = n;
-    void *args[] = {&w, &l, &ni, &ctl};
-    SK_CUDA(cudaLaunchCooperativeKernel((const void *)chol_kernel, dim3(blocks), dim3(THREADS), args, 0, st));
-    SK_LAUNCH_CHECK("chol_kernel");
+    void *args[] = {&w, &ni, &ctl};
+    SK_CUDA(cudaLaunchCooperativeKernel((const void *)chol_blocked_kernel, dim3(blocks), dim3(THREADS), args, 0, st));
+    SK_LAUNCH_CHECK("chol_blocked_kernel");
+    lower_to_l<<<(unsigned)std::min<int64_t>(((int64_t)n * n + 255) / 256, 4096), 256, 0, st>>>(ws.w, n, ws.l);
+    SK_LAUNCH_CHECK("lower_to_l");
     FactorCtl h;
     SK_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(h), cudaMemcpyDeviceToHost, st));
     SK_CUDA(cudaStreamSynchronize(st));
@@ -519,6 +656,26 @@ int sk_chol_solve_f64(const double *s, int64_t n, const double *rhs, double *x, 
     rc = trsv_launch(LTv, (int)n, false, false, ws.vec, nullptr, x, st);
     if (rc) return rc;
     return fill_status(status, SK_OK, -1, 0, 0);
+}
+
+int sk_gram_check(const double *g, int64_t n, double *out_host, void *wsp, size_t ws_bytes, sk_stream_t stream) {
+    if (!g || !out_host || n <= 0 || !wsp || ws_bytes < 64) {
+        set_error("sk_gram_check: bad arguments");
+        return SK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    double *stats = static_cast<double *>(wsp);
+    SK_CUDA(cudaMemsetAsync(stats, 0, 4 * sizeof(double), st));
+    sym_stats<<<(unsigned)std::min<int64_t>((n * n + 255) / 256, 1024), 256, 0, st>>>(g, (int)n, stats);
+    SK_LAUNCH_CHECK("sym_stats");
+    trace_kernel<<<1, 256, 0, st>>>(g, (int)n, stats + 3);
+    SK_LAUNCH_CHECK("trace_kernel");
+    double h[4];
+    SK_CUDA(cudaMemcpyAsync(h, stats, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    SK_CUDA(cudaStreamSynchronize(st));
+    out_host[0] = h[2];
+    out_host[1] = h[3];
+    return SK_OK;
 }
 
 int sk_chol_factor_f64(const double *s, int64_t n, double *r, sk_status *status, void *wsp, size_t ws_bytes,

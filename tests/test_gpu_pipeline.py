@@ -252,6 +252,24 @@ def test_streamed_host_ingestion_matches(sq, monkeypatch, kappa, prec, level):
         sq.algorithm1_pipeline(bad, p.b, precision=prec)
 
 
+def test_device_auto_path_validates_through_the_gram(sq):
+    """Device-resident A under "auto" is validated by the kappa0 Gram (non-finite A
+    makes G non-finite) and ||A||_F^2 comes from trace(G)."""
+    import torch
+    p = planted_problem(2000, 50, 1e4, 1e-8, 3)
+    rep = sq.algorithm1_pipeline(torch.from_numpy(p.a).cuda(), torch.from_numpy(p.b).cuda(), method="pne",
+                                 precision="auto", seed=3, x_star=p.x_star)
+    ref = R.pipeline(p.a, p.b, method="pne", precision="auto", seed=3, x_star=p.x_star, diagnostics=False)
+    assert rep.relative_residual == pytest.approx(ref.relative_residual, rel=1e-8)
+    assert rep.relative_error <= max(10 * ref.relative_error, ERR_FLOOR)
+    bad = p.a.copy()
+    bad[1234, 7] = np.nan
+    with pytest.raises(ValueError):
+        sq.algorithm1_pipeline(torch.from_numpy(bad).cuda(), torch.from_numpy(p.b).cuda(), precision="auto")
+    with pytest.raises(sq.DimensionMismatch):
+        sq.algorithm1_pipeline(torch.from_numpy(p.a).cuda(), torch.from_numpy(p.b[:-3]).cuda(), precision="auto")
+
+
 def test_sharded_pipeline_single_rank_device_ops(sq):
     """distributed.algorithm1_pipeline_sharded with the production DeviceOps on one
     GPU (no process group: every all-reduce is the identity)."""
