@@ -35,10 +35,30 @@ constexpr size_t RING = sizeof(double) * (size_t(STAGES) * BMR * APITCH + size_t
 constexpr size_t TILE = sizeof(double) * (size_t(BMR) * TPITCH + size_t(NB) * RPITCH);
 constexpr size_t SMEM = RING > TILE ? RING : TILE;
 
+// R_JJ in shared memory with each row split by column parity: element (i, j) at
+// i*RPITCH + (j&1)*NB/2 + j/2, so a substitution thread's half-row is contiguous.
+__device__ __forceinline__ int ridx(int i, int j) { return i * RPITCH + (j & 1) * (NB / 2) + (j >> 1); }
+
 __device__ __forceinline__ void load_stage(double *as, double *bs, const double *ap, int64_t ldap,
                                            const double *__restrict__ r, int64_t ldr, int64_t row0, int64_t m, int k0,
                                            int kend, int j0, int n, bool vec) {
     const int tid = threadIdx.x;
+    if (vec && row0 + BMR <= m && k0 + BK <= kend && j0 + NB <= n) {
+        // interior tile: no bounds arithmetic (the common case)
+#pragma unroll
+        for (int i = 0; i < (BMR * (BK / 2)) / THREADS; ++i) {
+            const int c = tid + i * THREADS;
+            const int rr = c / (BK / 2), kc = (c % (BK / 2)) * 2;
+            cp_async16(as + rr * APITCH + kc, ap + (row0 + rr) * ldap + k0 + kc, 16);
+        }
+#pragma unroll
+        for (int i = 0; i < (BK * (NB / 2)) / THREADS; ++i) {
+            const int c = tid + i * THREADS;
+            const int kr = c / (NB / 2), jc = (c % (NB / 2)) * 2;
+            cp_async16(bs + kr * BPITCH + jc, r + (int64_t)(k0 + kr) * ldr + j0 + jc, 16);
+        }
+        return;
+    }
     if (vec) {
         for (int c = tid; c < BMR * (BK / 2); c += THREADS) {
             const int rr = c / (BK / 2), kc = (c % (BK / 2)) * 2;
@@ -85,11 +105,10 @@ __device__ __forceinline__ void load_block(double *ts, double *rs, const double 
             bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
             cp_async16(ts + rr * TPITCH + jc, bytes ? a + row * lda + j0 + jc : a, bytes);
         }
-        for (int c = tid; c < NB * (NB / 2); c += THREADS) {
-            const int i = c / (NB / 2), jc = (c % (NB / 2)) * 2;
-            int bytes = (i < jw) ? (jw - jc) * 8 : 0;
-            bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
-            cp_async16(rs + i * RPITCH + jc, bytes ? r + (int64_t)(j0 + i) * ldr + j0 + jc : r, bytes);
+        for (int c = tid; c < NB * NB; c += THREADS) {
+            const int i = c / NB, jc = c % NB;
+            const int bytes = (i < jw && jc < jw) ? 8 : 0;
+            cp_async8(rs + ridx(i, jc), bytes ? r + (int64_t)(j0 + i) * ldr + j0 + jc : r, bytes);
         }
     } else {
         for (int c = tid; c < BMR * NB; c += THREADS) {
@@ -101,7 +120,7 @@ __device__ __forceinline__ void load_block(double *ts, double *rs, const double 
         for (int c = tid; c < NB * NB; c += THREADS) {
             const int i = c / NB, jc = c % NB;
             const int bytes = (i < jw && jc < jw) ? 8 : 0;
-            cp_async8(rs + i * RPITCH + jc, bytes ? r + (int64_t)(j0 + i) * ldr + j0 + jc : r, bytes);
+            cp_async8(rs + ridx(i, jc), bytes ? r + (int64_t)(j0 + i) * ldr + j0 + jc : r, bytes);
         }
     }
 }
@@ -136,12 +155,14 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
         // Each CTA starts its K sweep at a different block (rotation by blockIdx): the
         // concurrently resident panels are 2 MB apart, so walking the same columns in
         // lockstep would hammer the same L2/HBM channels.
-        const int rot = nk ? (int)(blockIdx.x % (unsigned)nk) : 0;
+        int kload = nk ? (int)(blockIdx.x % (unsigned)nk) : 0;   // next K block to stage (rotated)
 #pragma unroll
         for (int s = 0; s < STAGES - 1; ++s) {
-            if (s < nk)
+            if (s < nk) {
                 load_stage(as_base + s * BMR * APITCH, bs_base + s * BK * BPITCH, ap, ldap, r, ldr, row0, m,
-                           ((s + rot) % nk) * BK, j0, j0, n, vec);
+                           kload * BK, j0, j0, n, vec);
+                if (++kload == nk) kload = 0;
+            }
             cp_async_commit();
         }
         for (int kt = 0; kt < nk; ++kt) {
@@ -151,7 +172,8 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
             if (nxt < nk) {
                 const int s = nxt % STAGES;
                 load_stage(as_base + s * BMR * APITCH, bs_base + s * BK * BPITCH, ap, ldap, r, ldr, row0, m,
-                           ((nxt + rot) % nk) * BK, j0, j0, n, vec);
+                           kload * BK, j0, j0, n, vec);
+                if (++kload == nk) kload = 0;
             }
             cp_async_commit();
             const double *as = as_base + (kt % STAGES) * BMR * APITCH;
@@ -186,7 +208,7 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
                     ts[rr * TPITCH + cc + 1] -= acc[x][y][1];
                 }
         }
-        if (tid < NB && tid >= jw) rs[tid * RPITCH + tid] = 1.0;
+        if (tid < NB && tid >= jw) rs[ridx(tid, tid)] = 1.0;
         __syncthreads();
         // -- substitution: v holds columns hf, hf+2, ..., hf+62 of this row
         {
@@ -199,14 +221,17 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
                 const int owner = c & 1, kc = c >> 1;
                 double x = 0.0;
                 if (hf == owner) {
-                    v[kc] = v[kc] / rs[c * RPITCH + c];
+                    v[kc] = v[kc] / rs[ridx(c, c)];
                     x = v[kc];
                 }
                 x = __shfl_sync(0xffffffffu, x, base | owner);
+                // this thread's half of row c of R_JJ is contiguous: 16-byte loads
+                const double *rrow = rs + c * RPITCH + hf * (NB / 2);
 #pragma unroll
-                for (int k2 = (c + 1) >> 1; k2 < NB / 2; ++k2) {
-                    const int c2 = 2 * k2 + hf;
-                    if (c2 > c) v[k2] -= x * rs[c * RPITCH + c2];
+                for (int kp = ((c + 1) >> 1) >> 1; kp < NB / 4; ++kp) {
+                    const double2 rv = *reinterpret_cast<const double2 *>(rrow + 2 * kp);
+                    if (4 * kp + hf > c) v[2 * kp] -= x * rv.x;
+                    if (4 * kp + 2 + hf > c) v[2 * kp + 1] -= x * rv.y;
                 }
             }
 #pragma unroll
