@@ -8,10 +8,14 @@
 // the WHT), the d sampled rows are kept, rounded to binary16 and scaled.  Here
 // the d sampled rows of the transform are a tensor-core GEMM:
 //
-//   prep kernel   : At16[c][j] = sign_j * fp16(A[j][c])    (one HBM pass, transposed,
-//                   overflow of the demotion -> flag)      K-major operand for TMA
-//   main kernel   : persistent, warp-specialised, 1 CTA / SM
-//       warp 0      TMA producer: B tile At16[n-tile 256][k-block 64], SWIZZLE_128B
+//   prep kernel   : A16[j][c] = sign_j * fp16(A[j][c])     (one streaming HBM pass in A's
+//                   own row order, overflow of the demotion -> flag); the tensor cores
+//                   read it as an MN-major B operand
+//   main kernel   : persistent, warp-specialised, 1 CTA / SM; CTA b keeps sampled-row
+//                   tile b % ntm and walks (column tile, K split) groups with the other
+//                   ntm - 1 CTAs of its slot, so B chunks are shared through L2
+//       warp 0      TMA producer: B tile A16[k-block 64][n-tile 256] as four 64 x 64
+//                   SWIZZLE_128B boxes
 //       warp 1      MMA issuer:   tcgen05.mma.cta_group::1.kind::f16, M128 N256 K16,
 //                                 fp32 accumulator in TMEM (256 columns)
 //       warp 2      TMEM allocator
@@ -68,37 +72,52 @@ constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
 constexpr int TMEM_COLS = 512;
 
 // ------------------------------------------------------------ prep kernel ---
-constexpr int PT = 64;   // 64 x 64 tile
+// A16[j][c] = sign_j * fp16(A[j][c]) in A's own row-major order (ld = n rounded up to 8):
+// a pure streaming cast, 16-byte loads and stores.  The tensor cores read it MN-major.
+constexpr int PV = 8;   // columns per thread item
 __global__ void __launch_bounds__(256)
-prep_f16t(const double *__restrict__ a, int64_t lda, int64_t m_local, int n, const double *__restrict__ signs,
-          int64_t row_offset, __half *__restrict__ out, int64_t ldm, int *overflow_flag) {
-    __shared__ __half tile[PT][PT + 2];
-    const int64_t j0 = (int64_t)blockIdx.x * PT;
-    const int c0 = blockIdx.y * PT;
+prep_f16r(const double *__restrict__ a, int64_t lda, int64_t m_local, int n, const double *__restrict__ signs,
+          int64_t row_offset, __half *__restrict__ out, int64_t ldn, int vec, int *overflow_flag) {
+    const int cpr = (n + PV - 1) / PV;
+    const int rpi = cpr >= 256 ? 1 : 256 / cpr;       // rows per block iteration
+    const int sub = cpr >= 256 ? 0 : threadIdx.x / cpr;
+    const int cfirst = cpr >= 256 ? threadIdx.x : threadIdx.x % cpr;
+    const int cstep = cpr >= 256 ? 256 : cpr;
     int over = 0;
-#pragma unroll 4
-    for (int rep = 0; rep < (PT * PT) / 256; ++rep) {
-        const int idx = threadIdx.x + rep * 256;
-        const int r = idx / PT, c = idx % PT;
-        const int64_t j = j0 + r;
-        __half h = __float2half_rn(0.f);
-        if (j < m_local && c0 + c < n) {
-            const double v = a[j * lda + c0 + c];
-            h = __double2half(v);
-            over |= (isinf(__half2float(h)) && isfinite(v));
-            if (signs[row_offset + j] < 0) h = __hneg(h);
-        }
-        tile[c][r] = h;
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int rep = 0; rep < (PT * PT / 2) / 256; ++rep) {
-        const int idx = threadIdx.x + rep * 256;
-        const int c = idx / (PT / 2), r2 = (idx % (PT / 2)) * 2;
-        const int64_t j = j0 + r2;
-        if (c0 + c < n && j < ldm) {
-            __half2 v = __halves2half2(tile[c][r2], tile[c][r2 + 1]);
-            *reinterpret_cast<__half2 *>(out + (int64_t)(c0 + c) * ldm + j) = v;
+    for (int64_t j0 = (int64_t)blockIdx.x * rpi; j0 < m_local; j0 += (int64_t)gridDim.x * rpi) {
+        const int64_t j = j0 + sub;
+        if (sub >= rpi || j >= m_local) continue;
+        const bool neg = signs[row_offset + j] < 0;
+        const double *src = a + j * lda;
+        __half *dst = out + j * ldn;
+        for (int ch = cfirst; ch < cpr; ch += cstep) {
+            const int c0 = ch * PV;
+            double v[PV];
+            if (vec && c0 + PV <= n) {
+#pragma unroll
+                for (int q = 0; q < PV / 2; ++q) {
+                    const double2 t = __ldcs(reinterpret_cast<const double2 *>(src + c0) + q);
+                    v[2 * q] = t.x;
+                    v[2 * q + 1] = t.y;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < PV; ++q) v[q] = c0 + q < n ? src[c0 + q] : 0.0;
+            }
+            uint32_t pk[PV / 2];
+#pragma unroll
+            for (int e = 0; e < PV / 2; ++e) {
+                __half h0 = __double2half(v[2 * e]), h1 = __double2half(v[2 * e + 1]);
+                over |= (isinf(__half2float(h0)) && isfinite(v[2 * e])) |
+                        (isinf(__half2float(h1)) && isfinite(v[2 * e + 1]));
+                if (neg) {
+                    h0 = __hneg(h0);
+                    h1 = __hneg(h1);
+                }
+                __half2 h = __halves2half2(h0, h1);
+                pk[e] = *reinterpret_cast<uint32_t *>(&h);
+            }
+            *reinterpret_cast<uint4 *>(dst + c0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
     }
     if (__any_sync(0xffffffffu, over) && (threadIdx.x & 31) == 0) atomicOr(overflow_flag, 1);
@@ -107,16 +126,18 @@ prep_f16t(const double *__restrict__ a, int64_t lda, int64_t m_local, int n, con
 struct Params {
     const int64_t *rows;
     int64_t mpad, row_offset, m_local, kchunk;
-    int n, d, ntn, ntiles, units;
+    int n, d, ntm, ntn, ntiles, groups, nslots;
     int wht;
     float epi_scale;
     float *part;
 };
 
-__device__ __forceinline__ void unit_coords(const Params &p, int u, int &tm, int &tn, int64_t &k0, int &nkb) {
-    const int tile = u % p.ntiles, split = u / p.ntiles;
-    tm = tile / p.ntn;
-    tn = tile % p.ntn;
+// CTA b owns sampled-row tile tm = b % ntm for the whole launch and walks the groups
+// (tn, split) g = slot, slot + nslots, ...: the ntm CTAs of one slot stream the same
+// B chunk at the same time, so each B byte comes from HBM once and from L2 ntm - 1 times.
+__device__ __forceinline__ void group_coords(const Params &p, int g, int &tn, int &split, int64_t &k0, int &nkb) {
+    tn = g % p.ntn;
+    split = g / p.ntn;
     k0 = (int64_t)split * p.kchunk;
     const int64_t k1 = min(p.m_local, k0 + p.kchunk);
     nkb = (int)((k1 - k0 + BK - 1) / BK);
@@ -135,6 +156,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
     uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tm = blockIdx.x % p.ntm, slot = blockIdx.x / p.ntm;
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             tc::mbar_init(&full[s], 1 + NGEN_WARPS);
@@ -155,27 +177,31 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
         if (lane == 0) {   // ---------------- TMA producer
             int stage = 0;
             unsigned phase = 0;
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-                int tm, tn, nkb;
+            for (int g = slot; g < p.groups; g += p.nslots) {
+                int tn, split, nkb;
                 int64_t k0;
-                unit_coords(p, u, tm, tn, k0, nkb);
+                group_coords(p, g, tn, split, k0, nkb);
                 for (int kb = 0; kb < nkb; ++kb) {
                     tc::mbar_wait(&empty[stage], phase ^ 1);
                     tc::mbar_arrive_expect_tx(&full[stage], B_BYTES);
-                    tc::tma_load_2d(sb + stage * B_BYTES, &tmap_b, &full[stage], (int)(k0 + (int64_t)kb * BK), tn * BN);
+                    const int krow = (int)(k0 + (int64_t)kb * BK);
+#pragma unroll
+                    for (int q = 0; q < BN / 64; ++q)   // four 64-column x 64-row SW128 boxes
+                        tc::tma_load_2d(sb + stage * B_BYTES + q * (B_BYTES / (BN / 64)), &tmap_b, &full[stage],
+                                        tn * BN + q * 64, krow);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {   // ---------------- MMA issuer
-            constexpr uint32_t idesc = tc::idesc_f32acc(UMMA_M, BN, 0, 0);
+            constexpr uint32_t idesc = tc::idesc_f32acc(UMMA_M, BN, 0, 0, 0, 1);   // B MN-major
             int stage = 0;
             unsigned phase = 0, tphase = 0;
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-                int tm, tn, nkb;
+            for (int g = slot; g < p.groups; g += p.nslots) {
+                int tn, split, nkb;
                 int64_t k0;
-                unit_coords(p, u, tm, tn, k0, nkb);
+                group_coords(p, g, tn, split, k0, nkb);
                 tc::mbar_wait(tempty, tphase ^ 1);
                 tc::tc_fence_after();
                 for (int kb = 0; kb < nkb; ++kb) {
@@ -183,11 +209,12 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
                     tc::tc_fence_after();
                     const uint64_t ad0 = tc::desc_kmajor_sw128(smem_u32(sa + stage * A_BYTES));
                     const uint64_t ad1 = tc::desc_kmajor_sw128(smem_u32(sa + stage * A_BYTES + A_BYTES / 2));
-                    const uint64_t bd = tc::desc_kmajor_sw128(smem_u32(sb + stage * B_BYTES));
+                    // B: 64-column blocks 8 KB apart (LBO), 8-row K groups 1 KB apart (SBO)
+                    const uint64_t bd = tc::desc_mnmajor_sw128(smem_u32(sb + stage * B_BYTES), B_BYTES / (BN / 64), 1024);
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {   // +32 bytes along K per UMMA_K = 16
-                        tc::mma_f16_ss(tmem, ad0 + 2 * k, bd + 2 * k, idesc, (kb | k) ? 1u : 0u);
-                        tc::mma_f16_ss(tmem + BN, ad1 + 2 * k, bd + 2 * k, idesc, (kb | k) ? 1u : 0u);
+                    for (int k = 0; k < BK / 16; ++k) {   // A: +32 bytes along K; B: +16 rows = 2 KB
+                        tc::mma_f16_ss(tmem, ad0 + 2 * k, bd + 128 * k, idesc, (kb | k) ? 1u : 0u);
+                        tc::mma_f16_ss(tmem + BN, ad1 + 2 * k, bd + 128 * k, idesc, (kb | k) ? 1u : 0u);
                     }
                     tc::mma_commit(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -204,26 +231,26 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
         const float inv2M = 1.0f / (2.0f * (float)p.mpad);
         int stage = 0;
         unsigned phase = 0, tphase = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-            int tm, tn, nkb;
-            int64_t k0;
-            unit_coords(p, u, tm, tn, k0, nkb);
-            const int i = tm * BM + row;
-            const bool valid = i < p.d;
-            const uint64_t r = valid ? (uint64_t)p.rows[i] : 0;
-            const uint64_t f1 = r % fourM;
-            // per-row offset table e^{i pi r (2t) / 2M}, t = 0..31 (exact integer phases)
-            // 16-entry table (registers): columns 16..31 use the base rotated by e^{i 16 delta}
-            float wc[16], ws[16], wc16 = 1.f, ws16 = 0.f;
-            if (!p.wht) {
+        const int i = tm * BM + row;
+        const bool valid = i < p.d;
+        const uint64_t r = valid ? (uint64_t)p.rows[i] : 0;
+        const uint64_t f1 = r % fourM;
+        // per-row offset table e^{i pi r (2t) / 2M}, t = 0..31 (exact integer phases)
+        // 16-entry table (registers): columns 16..31 use the base rotated by e^{i 16 delta}
+        float wc[16], ws[16], wc16 = 1.f, ws16 = 0.f;
+        if (!p.wht) {
 #pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                    const uint64_t q = (f1 * (uint64_t)(2 * t)) % fourM;
-                    sincospif((float)q * inv2M, &ws[t], &wc[t]);
-                }
-                const uint64_t q16 = (f1 * (uint64_t)32) % fourM;
-                sincospif((float)q16 * inv2M, &ws16, &wc16);
+            for (int t = 0; t < 16; ++t) {
+                const uint64_t q = (f1 * (uint64_t)(2 * t)) % fourM;
+                sincospif((float)q * inv2M, &ws[t], &wc[t]);
             }
+            const uint64_t q16 = (f1 * (uint64_t)32) % fourM;
+            sincospif((float)q16 * inv2M, &ws16, &wc16);
+        }
+        for (int g = slot; g < p.groups; g += p.nslots) {
+            int tn, split, nkb;
+            int64_t k0;
+            group_coords(p, g, tn, split, k0, nkb);
             // phase of this thread's first column, advanced exactly by r*2*BK per K-block
             uint64_t ph = (f1 * ((uint64_t)(2 * (p.row_offset + k0 + half * 32) + 1) % fourM)) % fourM;
             const uint64_t dph = (f1 * (uint64_t)(2 * BK)) % fourM;
@@ -280,7 +307,7 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
             // warp w reads TMEM lanes 32*(w%4)..; the 16 warps split 2 accumulators x 2 column halves
             const int lg = warp & 3, quarter = (warp - GEN_WARP0) >> 2;
             const int acc = quarter >> 1, colhalf = quarter & 1;
-            const int tile = u % p.ntiles, split = u / p.ntiles;
+            const int tile = tm * p.ntn + tn;
             float *out = p.part + ((size_t)split * p.ntiles + tile) * (size_t)(BM * BN);
             const int orow = acc * UMMA_M + lg * 32 + lane;
 #pragma unroll 1
@@ -319,8 +346,8 @@ __global__ void reduce_part(const float *__restrict__ part, int splits, int ntil
 }
 
 struct Plan {
-    int ntm, ntn, ntiles, splits, units;
-    int64_t kchunk, ldm;
+    int ntm, ntn, ntiles, splits, groups, nslots, grid;
+    int64_t kchunk, ldn;
     size_t at_bytes, part_bytes;
 };
 
@@ -330,22 +357,25 @@ Plan make_plan(int64_t m_local, int64_t n, int64_t d) {
     p.ntn = (int)((n + BN - 1) / BN);
     p.ntiles = p.ntm * p.ntn;
     const int sms = sm_count();
+    p.nslots = sms >= p.ntm ? sms / p.ntm : 1;
+    p.grid = p.ntm * p.nslots;
     const int64_t nkb_total = (m_local + BK - 1) / BK;
-    int64_t target = (int64_t)32 * sms / p.ntiles;     // ~32 waves of units
+    // ~32 groups per slot; the split count is nudged so that every slot gets the same
+    // number of groups (ntn * splits divisible by nslots)
+    int64_t target = (int64_t)32 * p.nslots / p.ntn;
     if (target < 1) target = 1;
-    const int64_t smax = (nkb_total + 15) / 16;       // >= 16 K-blocks per unit
+    const int64_t smax = std::max<int64_t>(1, (nkb_total + 15) / 16);   // >= 16 K-blocks per group
     if (target > smax) target = smax;
-    if (target < 1) target = 1;
     int64_t best = target;
-    for (int64_t s = target; s >= (target * 4) / 5 && s >= 1; --s)
-        if (((int64_t)p.ntiles * s) % sms == 0) { best = s; break; }
+    for (int64_t s = target; s < target + p.nslots && s <= smax; ++s)
+        if (((int64_t)p.ntn * s) % p.nslots == 0) { best = s; break; }
     const int64_t kb_per = (nkb_total + best - 1) / best;
     p.kchunk = kb_per * BK;
     p.splits = (int)((m_local + p.kchunk - 1) / p.kchunk);
     if (p.splits < 1) p.splits = 1;
-    p.units = p.ntiles * p.splits;
-    p.ldm = (m_local + 63) / 64 * 64;
-    p.at_bytes = align_up((size_t)n * p.ldm * sizeof(__half), 1024);
+    p.groups = p.ntn * p.splits;
+    p.ldn = (n + 7) / 8 * 8;
+    p.at_bytes = align_up((size_t)m_local * p.ldn * sizeof(__half), 1024);
     p.part_bytes = (size_t)p.splits * p.ntiles * BM * BN * sizeof(float);
     return p;
 }
@@ -374,12 +404,13 @@ int sketch_tc_run(int transform, const double *a, int64_t lda, int64_t m_local, 
         }
         return SK_OK;
     }
-    dim3 pg((unsigned)((m_local + PT - 1) / PT), (unsigned)((n + PT - 1) / PT));
-    prep_f16t<<<pg, 256, 0, st>>>(a, lda, m_local, (int)n, signs, row_offset, at, p.ldm, overflow_flag_dev);
-    SK_LAUNCH_CHECK("prep_f16t");
+    const int vec = ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (lda % 2 == 0);
+    prep_f16r<<<sm_count() * 8, 256, 0, st>>>(a, lda, m_local, (int)n, signs, row_offset, at, p.ldn, vec,
+                                              overflow_flag_dev);
+    SK_LAUNCH_CHECK("prep_f16r");
     CUtensorMap tmap;
-    int rc = make_tmap_2d(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, at, (uint64_t)m_local, (uint64_t)n,
-                          (uint64_t)p.ldm * sizeof(__half), BK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    int rc = make_tmap_2d(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, at, (uint64_t)n, (uint64_t)m_local,
+                          (uint64_t)p.ldn * sizeof(__half), 64, BK, CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
     Params prm;
     prm.rows = rows;
@@ -389,15 +420,16 @@ int sketch_tc_run(int transform, const double *a, int64_t lda, int64_t m_local, 
     prm.kchunk = p.kchunk;
     prm.n = (int)n;
     prm.d = (int)d;
+    prm.ntm = p.ntm;
     prm.ntn = p.ntn;
     prm.ntiles = p.ntiles;
-    prm.units = p.units;
+    prm.groups = p.groups;
+    prm.nslots = p.nslots;
     prm.wht = transform == SK_WHT;
     prm.epi_scale = transform == SK_WHT ? (float)(1.0 / sqrt((double)m_pad)) : (float)sqrt(2.0 / (double)m_pad);
     prm.part = part;
     SK_CUDA(cudaFuncSetAttribute(sketch_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-    const int grid = std::min(p.units, sm_count());
-    sketch_tc_kernel<<<grid, THREADS, SMEM, st>>>(tmap, prm);
+    sketch_tc_kernel<<<p.grid, THREADS, SMEM, st>>>(tmap, prm);
     SK_LAUNCH_CHECK("sketch_tc_kernel");
     const int64_t total = d * n;
     reduce_part<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(part, p.splits, p.ntiles, p.ntn, (int)d, (int)n, out,

@@ -90,11 +90,23 @@ __device__ __forceinline__ uint64_t desc_kmajor_sw128(uint32_t smem_addr) {
     d |= (uint64_t)2u << 61;                 // SWIZZLE_128B
     return d;
 }
-// kind::f16 / kind::tf32 instruction descriptor: fp32 accumulate, K-major A and B.
-// a_fmt/b_fmt: 0 = F16, 1 = BF16, 2 = TF32.
-__host__ __device__ constexpr uint32_t idesc_f32acc(int m, int n, int a_fmt, int b_fmt) {
-    return (1u << 4) | ((uint32_t)a_fmt << 7) | ((uint32_t)b_fmt << 10) | ((uint32_t)(n >> 3) << 17) |
-           ((uint32_t)(m >> 4) << 24);
+// MN-major SWIZZLE_128B operand: 64-element (128 B) MN rows, 8 K rows per 1024-B swizzle
+// atom; LBO = byte stride between 64-wide MN blocks, SBO = byte stride between 8-row K
+// groups (canonical ((8,n),(8,k)) : ((1,LBO),(8,SBO)) in 16-byte units).
+__device__ __forceinline__ uint64_t desc_mnmajor_sw128(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1u << 46;
+    d |= (uint64_t)2u << 61;
+    return d;
+}
+// kind::f16 / kind::tf32 instruction descriptor: fp32 accumulate, K-major A and B unless
+// a_mn / b_mn select MN-major (bits 15 / 16).  a_fmt/b_fmt: 0 = F16, 1 = BF16, 2 = TF32.
+__host__ __device__ constexpr uint32_t idesc_f32acc(int m, int n, int a_fmt, int b_fmt, int a_mn = 0, int b_mn = 0) {
+    return (1u << 4) | ((uint32_t)a_fmt << 7) | ((uint32_t)b_fmt << 10) | ((uint32_t)a_mn << 15) |
+           ((uint32_t)b_mn << 16) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 __device__ __forceinline__ void mma_f16_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                            uint32_t accumulate) {
