@@ -129,6 +129,12 @@ int sk_trsm_right_upper_f64(const double *a, int64_t lda, int64_t m, int64_t n, 
  * across row shards (NCCL) first.  Overflow of the demotion is OR-ed into
  * *overflow_flag_dev (device int).  transform SK_DCT2/SK_WHT, level 16/32/64. */
 enum sk_sketch_algo { SK_SKETCH_AUTO = 0, SK_SKETCH_DMMA = 1, SK_SKETCH_TC = 2, SK_SKETCH_FFT = 3 };
+/* The sign vector of make_sketch (src/sketch.py:89-112):
+ *   rng.stream(seed, LANE).integers(0, 2, count) * 2.0 - 1.0     (src/rng.py:23-34)
+ * drawn on the device, bitwise numpy's: Philox4x64-10 with key (key_lo, key_hi),
+ * output block b at counter b + 1, each 64-bit word split into two 32-bit draws
+ * (low half first), draw j -> +1 if its top bit is set else -1. */
+int sk_sketch_signs(uint64_t key_lo, uint64_t key_hi, int64_t count, double *signs, sk_stream_t stream);
 size_t sk_sketch_workspace(int level, int64_t m_local, int64_t n, int64_t d);
 /* Exact workspace for one (level, transform, row shard of an m_pad-row operator). */
 size_t sk_sketch_workspace_ex(int level, int transform, int64_t m_local, int64_t m_pad, int64_t n, int64_t d);

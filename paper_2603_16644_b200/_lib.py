@@ -56,6 +56,7 @@ SIGNATURES = {
                                  _p, _i64, _i32, _p, _p, _sz, _p]),
     "sk_sketch_partial_ex": (_i32, [_i32, _i32, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _i64,
                                     _p, _i64, _i32, _p, _p, _sz, _p, _i32]),
+    "sk_sketch_signs": (_i32, [C.c_uint64, C.c_uint64, _i64, _p, _p]),
     "sk_sketch_finalize": (_i32, [_i32, _p, _i64, _i64, _i64, _i64, _p, _p, _p]),
     "sk_qr_workspace": (_sz, [_i32, _i64, _i64]),
     "sk_qr_r": (_i32, [_i32, _p, _i64, _i64, _p, _i64, _ps, _p, _sz, _p]),

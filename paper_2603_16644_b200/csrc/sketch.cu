@@ -375,3 +375,55 @@ int sk_sketch_finalize(int level, const double *sum, int64_t ldsum, int64_t d, i
 }
 
 }  // extern "C"
+
+namespace sk {
+namespace sketch {
+// numpy's Philox (Philox4x64, 10 rounds): one thread per 4-word output block.
+__global__ void __launch_bounds__(256)
+signs_kernel(uint64_t k0, uint64_t k1, int64_t count, double *__restrict__ signs) {
+    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b * 8 >= count) return;
+    uint64_t c0 = (uint64_t)b + 1, c1 = 0, c2 = 0, c3 = 0, ka = k0, kb = k1;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t lo0 = 0xD2E7470EE14C6C93ull * c0, hi0 = __umul64hi(0xD2E7470EE14C6C93ull, c0);
+        const uint64_t lo1 = 0xCA5A826395121157ull * c2, hi1 = __umul64hi(0xCA5A826395121157ull, c2);
+        const uint64_t n0 = hi1 ^ c1 ^ ka, n2 = hi0 ^ c3 ^ kb;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+        ka += 0x9E3779B97F4A7C15ull;
+        kb += 0xBB67AE8584CAA73Bull;
+    }
+    const uint64_t w[4] = {c0, c1, c2, c3};
+    double s[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        s[2 * q] = (w[q] & 0x80000000ull) ? 1.0 : -1.0;              // low 32-bit draw
+        s[2 * q + 1] = (w[q] & 0x8000000000000000ull) ? 1.0 : -1.0;  // high 32-bit draw
+    }
+    const int64_t j0 = b * 8;
+    if (j0 + 8 <= count) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            reinterpret_cast<double2 *>(signs + j0)[q] = make_double2(s[2 * q], s[2 * q + 1]);
+    } else {
+        for (int q = 0; q < 8 && j0 + q < count; ++q) signs[j0 + q] = s[q];
+    }
+}
+}  // namespace sketch
+}  // namespace sk
+
+extern "C" int sk_sketch_signs(uint64_t key_lo, uint64_t key_hi, int64_t count, double *signs, sk_stream_t stream) {
+    if (count < 0 || (count > 0 && (!signs || (reinterpret_cast<uintptr_t>(signs) & 15)))) {
+        set_error("sk_sketch_signs: bad arguments (signs must be 16-byte aligned)");
+        return SK_ERR_ARG;
+    }
+    if (count == 0) return SK_OK;
+    const int64_t blocks = (count + 7) / 8;
+    sketch::signs_kernel<<<(unsigned)((blocks + 255) / 256), 256, 0, (cudaStream_t)stream>>>(key_lo, key_hi, count,
+                                                                                           signs);
+    SK_LAUNCH_CHECK("signs_kernel");
+    return SK_OK;
+}

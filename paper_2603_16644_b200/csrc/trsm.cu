@@ -258,9 +258,33 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
     }
 }
 
-__global__ void first_zero_diag(const double *__restrict__ r, int64_t ldr, int n, int *out) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        if (r[(int64_t)i * ldr + i] == 0.0) atomicMin(out, i);
+// one block: index of the first exactly-zero diagonal entry (INT32_MAX if none),
+// written straight into mapped pinned host memory
+__global__ void __launch_bounds__(1024) first_zero_diag(const double *__restrict__ r, int64_t ldr, int n, int *out) {
+    __shared__ int wmin[32];
+    int best = INT32_MAX;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        if (r[(int64_t)i * ldr + i] == 0.0) { best = i; break; }
+    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        best = wmin[threadIdx.x];
+        for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (threadIdx.x == 0) *reinterpret_cast<volatile int *>(out) = best;
+    }
+}
+
+// one mapped pinned int per host thread (calls on one thread are serialised by the
+// synchronize that reads it)
+int *zero_diag_slot() {
+    thread_local int *slot = nullptr;
+    if (!slot) {
+        void *p = nullptr;
+        if (cudaHostAlloc(&p, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return nullptr;
+        slot = static_cast<int *>(p);
+    }
+    return slot;
 }
 
 }  // namespace trsm
@@ -277,19 +301,21 @@ extern "C" int sk_trsm_right_upper_f64(const double *a, int64_t lda, int64_t m, 
         return SK_ERR_ARG;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    // exactly-zero diagonal -> SingularTriangular (src/dense.py:231-233)
-    int *dflag = nullptr;
-    SK_CUDA(cudaMallocAsync(&dflag, sizeof(int), st));
-    int big = INT32_MAX, first = INT32_MAX;
-    SK_CUDA(cudaMemcpyAsync(dflag, &big, sizeof(int), cudaMemcpyHostToDevice, st));
-    trsm::first_zero_diag<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(r, ldr, (int)n, dflag);
+    // exactly-zero diagonal -> SingularTriangular (src/dense.py:231-233).  No stream-
+    // ordered allocation here: a cudaMallocAsync / cudaFreeAsync pair per call made the
+    // following synchronize wait on pool trimming (measured 0.2-900 ms per call).
+    int *first = trsm::zero_diag_slot();
+    if (!first) {
+        set_error("sk_trsm_right_upper_f64: pinned status slot unavailable");
+        return SK_ERR_CUDA;
+    }
+    trsm::first_zero_diag<<<1, 1024, 0, st>>>(r, ldr, (int)n, first);
     SK_LAUNCH_CHECK("first_zero_diag");
-    SK_CUDA(cudaMemcpyAsync(&first, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
-    SK_CUDA(cudaFreeAsync(dflag, st));
     SK_CUDA(cudaStreamSynchronize(st));
-    if (first != INT32_MAX) {
-        set_error("zero diagonal entry at index %d", first);
-        return fill_status(status, SK_SINGULAR_TRIANGULAR, first, 0.0, 0.0);
+    const int first_zero = *reinterpret_cast<volatile int *>(first);
+    if (first_zero != INT32_MAX) {
+        set_error("zero diagonal entry at index %d", first_zero);
+        return fill_status(status, SK_SINGULAR_TRIANGULAR, first_zero, 0.0, 0.0);
     }
     if (m == 0) return fill_status(status, SK_OK, -1, 0, 0);
     const bool vec = ((reinterpret_cast<uintptr_t>(ap) | reinterpret_cast<uintptr_t>(r) |

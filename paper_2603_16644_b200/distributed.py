@@ -57,9 +57,18 @@ class DeviceOps:
         from .dense import _gemv_t
         return _gemv_t(x, v)
 
+    def make_operator(self, m, d, transform, seed):
+        # signs drawn on the device (bitwise make_sketch's), rows on the host
+        from .sketch import _make_sketch_dev
+        op, self._dsk = _make_sketch_dev(m, d, transform, seed)
+        return op
+
     def sketch_partial(self, op, a_local, level, row_offset):
         from .sketch import DeviceSketch, _sketch_sum
-        total, flag = _sketch_sum(DeviceSketch(op), a_local, level.code, row_offset=row_offset)
+        dsk = getattr(self, "_dsk", None)
+        if dsk is None or dsk.op is not op:
+            dsk = DeviceSketch(op)
+        total, flag = _sketch_sum(dsk, a_local, level.code, row_offset=row_offset)
         return total, flag.to(torch.float64)
 
     def sketch_level_qr(self, total, op, level):
@@ -150,7 +159,8 @@ def algorithm1_pipeline_sharded(a_local, b_local, method="pne", precision="auto"
     d = int(math.ceil(d_factor * n))
     if d < n:
         raise ValueError(f"d_factor {d_factor} gives d={d} < n={n}")
-    op = make_sketch(m, d, transform, seed)
+    mk = getattr(ops, "make_operator", None)
+    op = mk(m, d, transform, seed) if mk is not None else make_sketch(m, d, transform, seed)
     escalated_from = None
     while True:
         try:

@@ -40,6 +40,8 @@ class SketchOperator:
 
     @property
     def m_pad(self):
+        if self.signs is None:   # device-drawn operator (_make_sketch_dev): signs live on the GPU
+            return _next_pow2(self.m) if self.transform == WHT else self.m
         return self.signs.shape[0]
 
     def descriptor(self):
@@ -65,6 +67,23 @@ def make_sketch(m, d, transform=DCT2, seed=0):
                           sampled_rows=rows)
 
 
+def _make_sketch_dev(m, d, transform=DCT2, seed=0):
+    """make_sketch for the device pipeline: the d sampled rows are drawn on the host
+    (same Philox lane, d draws), the m_pad signs on the device by sk_sketch_signs
+    (bitwise the host draw, no m_pad-long host loop or copy).  Returns
+    (SketchOperator with signs=None, DeviceSketch)."""
+    if transform not in TRANSFORMS:
+        raise ValueError(f"unknown transform {transform!r}, expected {TRANSFORMS}")
+    if m < 1 or d < 1:
+        raise ValueError(f"need m >= 1 and d >= 1, got m={m}, d={d}")
+    m_pad = _next_pow2(m) if transform == WHT else m
+    if d > m_pad:
+        raise ValueError(f"sample count d={d} exceeds padded height {m_pad}")
+    rows = rng.stream(seed, rng.LANE_SKETCH_ROWS).integers(0, m_pad, d)
+    op = SketchOperator(m=int(m), d=int(d), transform=transform, seed=int(seed), signs=None, sampled_rows=rows)
+    return op, DeviceSketch(op)
+
+
 def sketch_from_descriptor(desc):
     """src/sketch.py:115-118."""
     return make_sketch(int(desc["m"]), int(desc["d"]), desc["transform"], int(desc["seed"]))
@@ -76,7 +95,13 @@ class DeviceSketch:
     def __init__(self, op: SketchOperator):
         dev = device()
         self.op = op
-        self.signs = torch.from_numpy(np.ascontiguousarray(op.signs, dtype=np.float64)).to(dev)
+        if op.signs is None:
+            self.signs = torch.empty(op.m_pad, dtype=torch.float64, device=dev)
+            key_lo = int(op.seed) & rng.MASK64
+            key_hi = int(rng.LANE_SKETCH_SIGNS) & rng.MASK64
+            call("sk_sketch_signs", key_lo, key_hi, op.m_pad, self.signs.data_ptr(), stream_handle())
+        else:
+            self.signs = torch.from_numpy(np.ascontiguousarray(op.signs, dtype=np.float64)).to(dev)
         self.rows = torch.from_numpy(np.ascontiguousarray(op.sampled_rows, dtype=np.int64)).to(dev)
 
 

@@ -41,7 +41,7 @@ from .device import DMat, as_dmat, as_dvec, call, like_input, stream_handle, to_
 from .errors import DimensionMismatch, NoConvergence, NotPositiveDefinite, RankDeficient
 from .precision import (BINARY64, PrecisionDecision, PrecisionLevel, _decide_dev, _qr_level_dev,
                         level_from_name, next_higher)
-from .sketch import DCT2, DeviceSketch, _apply_dev, make_sketch
+from .sketch import DCT2, DeviceSketch, _apply_dev, _make_sketch_dev, make_sketch
 from . import _lib
 
 import ctypes as C
@@ -312,8 +312,8 @@ def _build_dev(ad: DMat, d_factor, transform, level, seed, diagnostics=True, str
             raise Overflow(f"input exceeds the {level.name} range")
         a_s, _ = _sketch_finalize(total, op, level)
     else:
-        op = make_sketch(m, d, transform, seed)
-        a_s, _ = _apply_dev(op, ad, level)      # Overflow on demotion (src/solvers.py:191-193)
+        op, dsk = _make_sketch_dev(m, d, transform, seed)
+        a_s, _ = _apply_dev(op, ad, level, dsk)   # Overflow on demotion (src/solvers.py:191-193)
     if stages is not None:
         stages.mark("level_qr")
     r_s = _qr_level_dev(a_s, level, d, n)       # RankDeficient / Overflow
@@ -476,8 +476,8 @@ def algorithm1_pipeline(a, b, method="pne", precision="auto", d_factor=3.0, tran
         d = int(math.ceil(d_factor * n))
         # only the tensor-core (binary16) sketch is chunk-friendly; the FFT sketch of
         # binary32/64 transforms all M rows per call, so it runs once after ingestion
-        op = make_sketch(m, d, transform, seed) if (d >= n and spec_level is BINARY16) else None
-        plan = (DeviceSketch(op), spec_level.code) if op is not None else None
+        op, dsk = _make_sketch_dev(m, d, transform, seed) if (d >= n and spec_level is BINARY16) else (None, None)
+        plan = (dsk, spec_level.code) if op is not None else None
         ad, gram_auto, sk = _ingest_streamed(host, want_gram=precision == "auto", sketch_plan=plan)
         if sk is not None:
             presketch = ((spec_level.name, d, transform, seed), op, sk[0], sk[1])

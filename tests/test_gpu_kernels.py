@@ -98,6 +98,21 @@ def test_apply_sketch_vs_reference(sq, case):
         assert rel(got, ref) <= tol, level
 
 
+@pytest.mark.parametrize("m,transform,seed", [(1, "dct2", 0), (7, "dct2", 3), (9, "wht", 17), (600, "dct2", 17),
+                                              (300, "wht", 17), (1000003, "dct2", -5), (65536, "wht", 2**63 + 11)])
+def test_device_signs_bitwise_host_philox(sq, torch, m, transform, seed):
+    """sk_sketch_signs reproduces make_sketch's numpy Philox draw bit for bit."""
+    from paper_2603_16644_b200.sketch import _make_sketch_dev
+    d = min(m, 5)
+    host = sq.make_sketch(m, d, transform, seed=seed)
+    op, dsk = _make_sketch_dev(m, d, transform, seed)
+    assert op.m_pad == host.m_pad
+    assert np.array_equal(op.sampled_rows, host.sampled_rows)
+    assert np.array_equal(dsk.signs.cpu().numpy(), host.signs)
+    if m == 600:   # golden operator of the reference
+        assert np.array_equal(dsk.signs.cpu().numpy(), ARR["sketch/p600_k1e2/dct2/signs"])
+
+
 # ----------------------------------------------------------- level QR --------
 @pytest.mark.parametrize("case", [("p600_k1e2", "dct2"), ("p300_k10_s5", "wht"), ("p300_k10_s5", "dct2")])
 def test_level_qr_on_reference_sketch(sq, case):
