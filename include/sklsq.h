@@ -213,6 +213,34 @@ size_t sk_jacobi_workspace(int64_t rows, int64_t n);
 int sk_jacobi_sv_f64(const double *a, int64_t rows, int64_t n, int64_t lda, int max_sweeps,
                      double tol, double *sv_host, void *ws, size_t ws_bytes, sk_stream_t stream);
 
+/* ---- the SURVEY §8(b) contract names ------------------------------------- */
+/* Gram plus rhs in one call: G = X^T Y (SYRK when Y == X) and, if v != NULL,
+ * rhs = X^T v.  solve_pne / solve_hpne / solve_notnormal: `g, rhs = a_p.T @ a_p,
+ * a_p.T @ b` src/solvers.py:230-231, `a_p.T @ a, a_p.T @ b` :251, `b_matrix.T @ a`
+ * :164. */
+size_t sk_gemm_tn_workspace(int64_t m, int64_t n);
+int sk_gemm_tn_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
+                   const double *v, double *g, int64_t ldg, double *rhs, void *ws, size_t ws_bytes,
+                   sk_stream_t stream);
+/* G = X^T X (exactly symmetric): `a.T @ a` src/precision.py:230, src/solvers.py:137. */
+int sk_syrk_f64(const double *x, int64_t ldx, int64_t m, int64_t n, double *g, int64_t ldg, void *ws,
+                size_t ws_bytes, sk_stream_t stream);
+/* kappa0 straight from A: estimate_log10_condition src/precision.py:205-251 (SYRK +
+ * sk_kappa0_from_gram). */
+size_t sk_kappa0_workspace(int64_t m, int64_t n);
+int sk_kappa0_f64(const double *a, int64_t lda, int64_t m, int64_t n, double *kappa0_host, int *overflowed_host,
+                  void *ws, size_t ws_bytes, sk_stream_t stream);
+/* The contract's names for sk_sketch_partial (accumulate = 0), sk_level_overflow and
+ * sk_residual (apply_sketch src/sketch.py:138-169, the Overflow check
+ * src/solvers.py:191-193, _report src/solvers.py:99-117). */
+int sk_sketch(int level, int transform, const double *a, int64_t lda, int64_t m_local, int64_t row_offset,
+              int64_t m_pad, int64_t n, const double *signs, const int64_t *rows, int64_t d, double *out_partial,
+              int64_t ldo, int *overflow_flag_dev, void *ws, size_t ws_bytes, sk_stream_t stream);
+int sk_demote_check(const double *a, int64_t rows, int64_t cols, int64_t lda, int level, int *overflowed_host,
+                    void *ws, size_t ws_bytes, sk_stream_t stream);
+int sk_residual_norms(const double *a, int64_t rows, int64_t cols, int64_t lda, const double *x, const double *b,
+                      double *r, double *out_host, void *ws, size_t ws_bytes, sk_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,3 +69,27 @@ def planted_problem(m, n, kappa, rho, seed):
             raise RuntimeError("residual draws collapsed into range(a)")
         b = b + (rho / ne) * e
     return Problem(a, b, x_star, float(rho), float(kappa), int(seed))
+
+
+def planted_problem_lapack(m, n, kappa, rho, seed):
+    """Algorithm 2 (src/probgen.py:78-123) with LAPACK QR in place of the reference's
+    Python Householder: the same problem distribution (Q1 orthonormal, R with log-spaced
+    singular values 1 .. 1/kappa, x* unit, e orthogonal to range(A), ||e|| = rho), NOT
+    bitwise the reference's draw.  For test sizes where the restated generator takes
+    minutes (m x n >= 1e6); GPU and oracle are then compared on this same A, b."""
+    if not m > n >= 1:
+        raise ValueError(f"need m > n >= 1, got m={m}, n={n}")
+    q1 = np.linalg.qr(philox(mix64(seed, 1), LANE_GAUSS).standard_normal((m, n)))[0]
+    sv = 10.0 ** np.linspace(0.0, -math.log10(kappa), n)
+    u = np.linalg.qr(philox(mix64(seed, 2, 1), LANE_GAUSS).standard_normal((n, n)))[0]
+    v = np.linalg.qr(philox(mix64(seed, 2, 2), LANE_GAUSS).standard_normal((n, n)))[0]
+    r = np.linalg.qr((u * sv) @ v.T, mode="r")
+    a = q1 @ r
+    g = philox(mix64(seed, 3), LANE_GAUSS).standard_normal(n)
+    x_star = g / np.linalg.norm(g)
+    b = a @ x_star
+    if rho > 0:
+        w = philox(mix64(seed, 4, 0), LANE_GAUSS).standard_normal(m)
+        e = w - q1 @ (q1.T @ w)
+        b = b + (rho / np.linalg.norm(e)) * e
+    return Problem(np.ascontiguousarray(a), b, x_star, float(rho), float(kappa), int(seed))

@@ -69,6 +69,14 @@ SIGNATURES = {
     "sk_kappa0_from_gram": (_i32, [_p, _i64, _pd, _pi, _p, _sz, _p]),
     "sk_jacobi_workspace": (_sz, [_i64, _i64]),
     "sk_jacobi_sv_f64": (_i32, [_p, _i64, _i64, _i64, _i32, _d, _pd, _p, _sz, _p]),
+    "sk_gemm_tn_workspace": (_sz, [_i64, _i64]),
+    "sk_gemm_tn_f64": (_i32, [_p, _i64, _p, _i64, _i64, _i64, _p, _p, _i64, _p, _p, _sz, _p]),
+    "sk_syrk_f64": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _p, _sz, _p]),
+    "sk_kappa0_workspace": (_sz, [_i64, _i64]),
+    "sk_kappa0_f64": (_i32, [_p, _i64, _i64, _i64, _pd, _pi, _p, _sz, _p]),
+    "sk_sketch": (_i32, [_i32, _i32, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _i64, _p, _i64, _p, _p, _sz, _p]),
+    "sk_demote_check": (_i32, [_p, _i64, _i64, _i64, _i32, _pi, _p, _sz, _p]),
+    "sk_residual_norms": (_i32, [_p, _i64, _i64, _i64, _p, _p, _p, _pd, _p, _sz, _p]),
 }
 
 _LOCK = threading.Lock()

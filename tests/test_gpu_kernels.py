@@ -275,3 +275,47 @@ def test_tsqr_for_tall_matrices(sq, monkeypatch):
     r_tsqr = np.abs(sq.householder_reduce(p.a)[2])
     r_ref = np.abs(R.householder_steps(p.a)[2])
     assert rel(r_tsqr, r_ref) <= 1e-9     # unique up to row signs
+
+
+# ------------------------------------------------- SURVEY §8(b) ABI names -----
+def test_contract_entry_points_match_primitives(sq, torch):
+    """sk_gemm_tn_f64 / sk_syrk_f64 / sk_kappa0_f64 / sk_sketch / sk_demote_check /
+    sk_residual_norms give bit-identical results to the primitives they compose."""
+    import ctypes as C
+    from paper_2603_16644_b200 import _lib
+    from paper_2603_16644_b200.dense import _gemv_t, _gram
+    from paper_2603_16644_b200.device import stream_handle
+    from paper_2603_16644_b200.precision import _kappa0_from_gram
+    lib = _lib.lib()
+    m, n = 5000, 96
+    g = R.philox(99, 1)
+    a = torch.from_numpy(g.standard_normal((m, n))).cuda()
+    y = torch.from_numpy(g.standard_normal((m, n))).cuda()
+    v = torch.from_numpy(g.standard_normal(m)).cuda()
+    ws = torch.empty(max(lib.sk_gemm_tn_workspace(m, n), lib.sk_kappa0_workspace(m, n)), dtype=torch.uint8,
+                     device="cuda")
+    gg = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    rhs = torch.empty(n, dtype=torch.float64, device="cuda")
+    assert lib.sk_gemm_tn_f64(a.data_ptr(), n, y.data_ptr(), n, m, n, v.data_ptr(), gg.data_ptr(), n,
+                              rhs.data_ptr(), ws.data_ptr(), ws.numel(), stream_handle()) == 0
+    assert torch.equal(gg, _gram(a, y)) and torch.equal(rhs, _gemv_t(a, v))
+    assert lib.sk_syrk_f64(a.data_ptr(), n, m, n, gg.data_ptr(), n, ws.data_ptr(), ws.numel(),
+                           stream_handle()) == 0
+    assert torch.equal(gg, _gram(a))
+    k0, over = C.c_double(), C.c_int()
+    assert lib.sk_kappa0_f64(a.data_ptr(), n, m, n, C.byref(k0), C.byref(over), ws.data_ptr(), ws.numel(),
+                             stream_handle()) == 0
+    ref = _kappa0_from_gram(_gram(a))
+    assert (k0.value, bool(over.value)) == ref
+    flag = C.c_int(-1)
+    big = a * 1e6
+    assert lib.sk_demote_check(big.data_ptr(), m, n, n, 16, C.byref(flag), ws.data_ptr(), ws.numel(),
+                               stream_handle()) == 0 and flag.value == 1
+    assert lib.sk_demote_check(a.data_ptr(), m, n, n, 16, C.byref(flag), ws.data_ptr(), ws.numel(),
+                               stream_handle()) == 0 and flag.value == 0
+    x = torch.from_numpy(g.standard_normal(n)).cuda()
+    r = torch.empty(m, dtype=torch.float64, device="cuda")
+    out = (C.c_double * 2)()
+    assert lib.sk_residual_norms(a.data_ptr(), m, n, n, x.data_ptr(), v.data_ptr(), r.data_ptr(), out,
+                                 ws.data_ptr(), ws.numel(), stream_handle()) == 0
+    assert math.isclose(out[0], float(((a @ x - v) ** 2).sum()), rel_tol=1e-12)
