@@ -83,16 +83,21 @@ def _gemv_t(x: DMat | torch.Tensor, v: torch.Tensor, out: torch.Tensor | None = 
 APITCH_PAD = 8   # doubles of row padding for A_p (64 bytes)
 
 
+def _new_ap(m: int, n: int, device) -> torch.Tensor:
+    """An m x n f64 output for the TRSM, row pitch padded off a power of two (the
+    TRSM re-reads A_p panels of many CTAs at once; 2^k-byte row strides map them
+    onto the same memory channels)."""
+    pad = APITCH_PAD if (n * 8) % 4096 == 0 and m > 4096 else 0
+    return torch.empty((m, n + pad), dtype=torch.float64, device=device)[:, :n]
+
+
 def _trsm(a: DMat | torch.Tensor, r: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     """A_p = A R^{-1} (R upper, device f64)."""
     at = _rm(a.t if isinstance(a, DMat) else a)
     r = _rm(r)
     m, n = at.shape
     if out is None:
-        # pad the row pitch off a power of two: the TRSM re-reads A_p panels of many
-        # CTAs at once, and 2^k-byte row strides map them onto the same memory channels
-        pad = APITCH_PAD if (n * 8) % 4096 == 0 and m > 4096 else 0
-        out = torch.empty((m, n + pad), dtype=torch.float64, device=at.device)[:, :n]
+        out = _new_ap(m, n, at.device)
     st = _lib.SkStatus()
     call("sk_trsm_right_upper_f64", at.data_ptr(), at.stride(0), m, n, r.data_ptr(), r.stride(0),
          out.data_ptr(), out.stride(0), C.byref(st), stream_handle())

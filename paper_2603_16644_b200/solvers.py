@@ -30,6 +30,7 @@ like the reference.
 from __future__ import annotations
 
 import math
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -352,13 +353,46 @@ def precondition_matrix(a, pre, *, diagnostics=True, strict_diagnostics=False):
     return like_input(_precondition_dev(ad, pre, diagnostics, strict_diagnostics), ad.kind)
 
 
+class _ApScratch:
+    """One reusable A_p buffer per device for algorithm1_pipeline, where A_p never
+    leaves the call: a fresh 68.7 GB allocation per solve (config 3) costs a
+    variable 0-300 ms of page mapping.  `release_scratch()` drops it."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._bufs = {}
+
+    def take(self, m, n, device):
+        from .dense import _new_ap
+        key = (torch.device(device).index, m, n)
+        with self._lock:
+            t = self._bufs.pop(key, None)
+        return key, (t if t is not None else _new_ap(m, n, device))
+
+    def give(self, key, t):
+        with self._lock:
+            self._bufs = {key: t}          # keep at most one (the most recent shape)
+
+    def release(self):
+        with self._lock:
+            self._bufs = {}
+
+
+_AP_SCRATCH = _ApScratch()
+
+
+def release_scratch():
+    """Free the cached A_p buffer of algorithm1_pipeline."""
+    _AP_SCRATCH.release()
+
+
 def _prepare_dev(ad, d_factor, transform, level, seed, diagnostics=True, strict=False, stages=None,
-                 presketch=None):
+                 presketch=None, out=None):
     escalated_from = None
     while True:
         try:
             pre = _build_dev(ad, d_factor, transform, level, seed, diagnostics, strict, stages, presketch)
-            a_p = _precondition_dev(ad, pre, diagnostics, strict, stages)
+            a_p = _precondition_dev(ad, pre, diagnostics, strict, stages, out=out)
             return pre, a_p, escalated_from
         except RankDeficient:
             wider = next_higher(level)
@@ -515,9 +549,14 @@ def algorithm1_pipeline(a, b, method="pne", precision="auto", d_factor=3.0, tran
         level = decision.selected
     else:
         level = level_from_name(precision)
-    pre, a_p, escalated_from = _prepare_dev(ad, d_factor, transform, level, seed, diagnostics,
-                                            strict_diagnostics, stages, presketch)
-    x = (_pne_dev if method == "pne" else _hpne_dev)(ad, bd, pre, a_p, stages)
+    m_rows, n_cols = ad.shape
+    ap_key, ap_buf = _AP_SCRATCH.take(m_rows, n_cols, ad.t.device)
+    try:
+        pre, a_p, escalated_from = _prepare_dev(ad, d_factor, transform, level, seed, diagnostics,
+                                                strict_diagnostics, stages, presketch, out=ap_buf)
+        x = (_pne_dev if method == "pne" else _hpne_dev)(ad, bd, pre, a_p, stages)
+    finally:
+        _AP_SCRATCH.give(ap_key, ap_buf)
     stages.mark("report")
     report = _report(method, ad, bd, x, t0, x_star, preconditioner=pre, stages=stages)
     report.precision_decision = decision
