@@ -107,6 +107,16 @@ int sk_gram_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int6
                 double *g, int64_t ldg, int accumulate, void *ws, size_t ws_bytes,
                 sk_stream_t stream);
 
+/* Same product on the INT8 tensor cores (tcgen05 kind::i8, Ozaki scheme II): X and Y
+ * scaled per column to t-bit integers (t = 51 at m = 4M rows), 16 exact modular
+ * INT8 GEMMs, Chinese-remainder reconstruction in 128-bit integers.  The only
+ * rounding is the t-bit scaling: |G - X^T Y|_ij <= 2^-t (2^e_i sum|Y_j| + 2^f_j
+ * sum|X_i|) / 2, with 2^e_i > max|X_i|.  SYRK when Y == X (exactly symmetric).
+ * Workspace from sk_gram_ozaki_workspace(m, n, syrk). */
+size_t sk_gram_ozaki_workspace(int64_t m, int64_t n, int syrk);
+int sk_gram_ozaki_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
+                      double *g, int64_t ldg, void *ws, size_t ws_bytes, sk_stream_t stream);
+
 /* out (n) = X^T v (X m x n row-major): `a_p.T @ b` src/solvers.py:231/251. */
 size_t sk_gemv_t_workspace(int64_t m, int64_t n);
 int sk_gemv_t_f64(const double *x, int64_t ldx, int64_t m, int64_t n, const double *v,

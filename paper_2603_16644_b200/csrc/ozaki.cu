@@ -1,0 +1,513 @@
+// FP64 Gram products G = X^T Y on the INT8 tensor cores (tcgen05 kind::i8):
+// Ozaki scheme II, i.e. exact integer products modulo 16 coprime moduli and a
+// Chinese-remainder reconstruction.
+//
+// Same call sites as gram.cu (`a.T @ a` src/precision.py:230, `a_p.T @ a_p`
+// src/solvers.py:230, `a_p.T @ a` :251, `b_matrix.T @ a` :164).  B200 has ~3.1 POPS
+// of dense INT8 against 35 TFLOP/s of FP64 DMMA; 16 INT8 products replace one FP64
+// product.
+//
+//   1. column scales: e_i with max_k |X[k,i]| < 2^e_i (one pass over X and Y)
+//   2. per K-chunk of rows: X'[k,i] = rint(X[k,i] 2^(t - e_i)), |X'| <= 2^t, an exact
+//      integer; its residues modulo p_1..p_16 (odd, pairwise coprime, <= 255) as
+//      signed bytes in [-127, 127], 16 planes per operand, row-major like X
+//   3. per (modulus, K split <= 131072 rows, 256x256 output tile): one tcgen05 INT8
+//      GEMM with int32 accumulation in TMEM (|sum| < 131072 * 127^2 < 2^31: exact);
+//      both operands MN-major, TMA-staged with 128-byte swizzle
+//   4. residues of the int32 partials summed modulo p
+//   5. Garner mixed-radix reconstruction of C' = X'^T Y' (|C'| < M/2, M = prod p ~
+//      2^125.3) in 128-bit integers, G = C' 2^(e_i + f_j - 2t).
+//
+// Error: only step 2 rounds (|X' - X 2^(t-e)| <= 1/2), so |G - X^T Y|_ij <=
+// 2^-t (2^e_i sum_k |Y_kj| + 2^f_j sum_k |X_ki|) / 2 (+ the final rounding), with t
+// = 51 at m = 4M rows: the FP64 GEMM bound is gamma_K sum_k |X_ki||Y_kj|.  The
+// SYRK path computes lower tiles only; C' is exactly symmetric, so G is too.
+#include "tc.cuh"
+
+namespace sk {
+namespace oz {
+
+constexpr int NMOD = 16;
+// the moduli as a constexpr function (folds to immediates inside unrolled loops)
+__host__ __device__ constexpr int pm(int k) {
+    return k == 0 ? 255 : k == 1 ? 253 : k == 2 ? 251 : k == 3 ? 247 : k == 4 ? 241 : k == 5 ? 239 : k == 6 ? 233
+         : k == 7 ? 229 : k == 8 ? 227 : k == 9 ? 223 : k == 10 ? 217 : k == 11 ? 211 : k == 12 ? 199
+         : k == 13 ? 197 : k == 14 ? 193 : 191;
+}
+
+__host__ __device__ constexpr uint32_t c1_of(int k) { return (uint32_t)((1ull << 17) % (uint64_t)pm(k)); }
+__host__ __device__ constexpr uint32_t c2_of(int k) { return (uint32_t)((1ull << 34) % (uint64_t)pm(k)); }
+__host__ __device__ constexpr uint32_t magic_of(int k) {
+    return (uint32_t)(((1ull << 32) + pm(k) - 1) / (uint64_t)pm(k));
+}
+constexpr int inv_mod(int a, int p) {
+    int t = 0, nt = 1, r = p, nr = a % p;
+    while (nr != 0) {
+        const int q = r / nr, tt = t - q * nt, rr = r - q * nr;
+        t = nt; nt = tt; r = nr; nr = rr;
+    }
+    return t < 0 ? t + p : t;
+}
+// (p_0 ... p_{k-1})^{-1} mod p_k for Garner's mixed radix
+constexpr int garner_of(int k) {
+    int prod = 1;
+    for (int j = 0; j < k; ++j) prod = (int)(((int64_t)prod * pm(j)) % pm(k));
+    return inv_mod(prod, pm(k));
+}
+
+constexpr int BM = 256, UMMA_M = 128, BN = 256, BK = 128, STAGES = 3, UMMA_K = 32;
+constexpr int THREADS = 384, EPI_WARP0 = 4;                 // warps 4..11 drain TMEM
+constexpr uint32_t BOX_BYTES = 128 * BK;                     // one 128-col x BK-row int8 box
+constexpr uint32_t A_BYTES = 2 * BOX_BYTES, B_BYTES = 2 * BOX_BYTES;
+constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+constexpr int64_t KSPLIT_MAX = 131072;                       // int32-exact accumulation length
+
+// ---------------------------------------------------------- column scales ---
+// colmax bits (non-negative doubles order like their bit patterns) -> atomicMax
+__global__ void __launch_bounds__(256) colmax_kernel(const double *__restrict__ x, int64_t ldx, int64_t m, int n,
+                                                     unsigned long long *__restrict__ out) {
+    const int c = blockIdx.y * 256 + threadIdx.x;
+    if (c >= n) return;
+    double mx = 0.0;
+    for (int64_t r = blockIdx.x; r < m; r += gridDim.x) mx = fmax(mx, fabs(x[r * ldx + c]));
+    atomicMax(out + c, (unsigned long long)__double_as_longlong(mx));
+}
+
+// e = exponent with max < 2^e; scale = 2^(t - e) (inputs), out_exp for the product
+__global__ void scales_kernel(const unsigned long long *__restrict__ bits, int n, int t, double *__restrict__ scale,
+                              int *__restrict__ expo) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    const double mx = __longlong_as_double((long long)bits[c]);
+    int e = 0;
+    if (mx > 0.0) {
+        frexp(mx, &e);            // mx = f 2^e, f in [0.5, 1) -> mx < 2^e
+    }
+    expo[c] = e;
+    scale[c] = ldexp(1.0, t - e);
+}
+
+// ------------------------------------------------------------- residues -----
+__device__ __forceinline__ int residue(uint32_t l0, uint32_t l1, uint32_t l2, int k, bool neg) {
+    const uint32_t p = (uint32_t)pm(k);
+    const uint32_t v = l2 * c2_of(k) + l1 * c1_of(k) + l0;   // < 2^27
+    int r = (int)(v - p * __umulhi(v, magic_of(k)));           // r_true or r_true - p
+    r += r < 0 ? (int)p : 0;
+    r -= r > (int)(p - 1) / 2 ? (int)p : 0;
+    return neg ? -r : r;
+}
+
+// 16 consecutive columns of one row per thread -> 16 planes of 16 bytes
+__global__ void __launch_bounds__(256)
+residues_kernel(const double *__restrict__ x, int64_t ldx, int64_t rows, int n, const double *__restrict__ scale,
+                int8_t *__restrict__ out, int64_t ldr, int64_t plane, int vec) {
+    const int groups = (n + 15) / 16;
+    const int64_t total = rows * groups;
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = it / groups;
+        const int c0 = (int)(it - r * groups) * 16;
+        const double *src = x + r * ldx + c0;
+        double v[16];
+        if (vec && c0 + 16 <= n) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const double2 d = __ldcs(reinterpret_cast<const double2 *>(src) + q);
+                v[2 * q] = d.x;
+                v[2 * q + 1] = d.y;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = c0 + q < n ? src[q] : 0.0;
+        }
+        uint32_t l0[16], l1[16], l2[16];
+        uint32_t negm = 0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const double s = c0 + q < n ? scale[c0 + q] : 0.0;
+            const long long iv = __double2ll_rn(v[q] * s);
+            const unsigned long long u = (unsigned long long)(iv < 0 ? -iv : iv);
+            negm |= (iv < 0 ? 1u : 0u) << q;
+            l0[q] = (uint32_t)(u & 0x1FFFFull);
+            l1[q] = (uint32_t)((u >> 17) & 0x1FFFFull);
+            l2[q] = (uint32_t)(u >> 34);
+        }
+        int8_t *dst = out + r * ldr + c0;
+#pragma unroll
+        for (int k = 0; k < NMOD; ++k) {
+            uint32_t w[4];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                uint32_t word = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int q = 4 * q4 + b;
+                    const int rr = residue(l0[q], l1[q], l2[q], k, (negm >> q) & 1u);
+                    word |= ((uint32_t)(rr & 0xFF)) << (8 * b);
+                }
+                w[q4] = word;
+            }
+            *reinterpret_cast<uint4 *>(dst + k * plane) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- GEMM ------
+struct GemmParams {
+    int ntn, ntiles, splits, units, syrk;
+    int64_t rows, kchunk;
+    int32_t *part;              // [mod][split][tile][BN cols][BM rows]
+};
+
+// lower-triangular tile list for SYRK: tile index -> (tm, tn) with tm >= tn
+__device__ __forceinline__ void tile_coords(const GemmParams &p, int tile, int &tm, int &tn) {
+    if (!p.syrk) {
+        tm = tile / p.ntn;
+        tn = tile % p.ntn;
+    } else {
+        int r = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+        while ((r + 1) * (r + 2) / 2 <= tile) ++r;
+        while (r * (r + 1) / 2 > tile) --r;
+        tm = r;
+        tn = tile - r * (r + 1) / 2;
+    }
+}
+
+__device__ __forceinline__ void tma_load_3d(void *smem_dst, const CUtensorMap *map, uint64_t *bar, int x, int y,
+                                            int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
+            const GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sa = smem;
+    uint8_t *sb = smem + STAGES * A_BYTES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sb + STAGES * B_BYTES);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint64_t *tempty = tfull + 1;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int NEPI = (THREADS / 32) - EPI_WARP0;
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        tc::mbar_init(tfull, 1);
+        tc::mbar_init(tempty, NEPI);
+        tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&tmap_x);
+        tc::tma_prefetch_desc(&tmap_y);
+    }
+    if (warp == 2) tc::tmem_alloc<512>(tslot);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    auto unit_coords = [&](int u, int &mod, int &split, int &tile, int64_t &k0, int &nkb) {
+        tile = u % p.ntiles;
+        const int rest = u / p.ntiles;
+        split = rest % p.splits;
+        mod = rest / p.splits;
+        k0 = (int64_t)split * p.kchunk;
+        const int64_t k1 = min(p.rows, k0 + p.kchunk);
+        nkb = (int)((k1 - k0 + BK - 1) / BK);
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {   // ------------------------------------------ TMA producer
+            int stage = 0;
+            unsigned phase = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                int mod, split, tile, nkb, tm, tn;
+                int64_t k0;
+                unit_coords(u, mod, split, tile, k0, nkb);
+                tile_coords(p, tile, tm, tn);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    tc::mbar_wait(&empty[stage], phase ^ 1);
+                    tc::mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
+                    const int krow = (int)(k0 + (int64_t)kb * BK);
+                    uint8_t *a_dst = sa + stage * A_BYTES, *b_dst = sb + stage * B_BYTES;
+                    tma_load_3d(a_dst, &tmap_x, &full[stage], tm * BM, krow, mod);
+                    tma_load_3d(a_dst + BOX_BYTES, &tmap_x, &full[stage], tm * BM + 128, krow, mod);
+                    tma_load_3d(b_dst, &tmap_y, &full[stage], tn * BN, krow, mod);
+                    tma_load_3d(b_dst + BOX_BYTES, &tmap_y, &full[stage], tn * BN + 128, krow, mod);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {   // --------------------------------------------- MMA issuer
+            constexpr uint32_t idesc = tc::idesc_s32acc_s8(UMMA_M, BN, 1, 1);
+            int stage = 0;
+            unsigned phase = 0, tphase = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                int mod, split, tile, nkb;
+                int64_t k0;
+                unit_coords(u, mod, split, tile, k0, nkb);
+                tc::mbar_wait(tempty, tphase ^ 1);
+                tc::tc_fence_after();
+                for (int kb = 0; kb < nkb; ++kb) {
+                    tc::mbar_wait(&full[stage], phase);
+                    tc::tc_fence_after();
+                    const uint32_t a0 = smem_u32(sa + stage * A_BYTES), b0 = smem_u32(sb + stage * B_BYTES);
+                    // MN-major SW128: 128-element MN blocks BOX_BYTES apart, 8-row K groups 1 KB apart
+                    const uint64_t ad0 = tc::desc_mnmajor_sw128(a0, BOX_BYTES, 1024);
+                    const uint64_t ad1 = tc::desc_mnmajor_sw128(a0 + BOX_BYTES, BOX_BYTES, 1024);
+                    const uint64_t bd = tc::desc_mnmajor_sw128(b0, BOX_BYTES, 1024);
+#pragma unroll
+                    for (int k = 0; k < BK / UMMA_K; ++k) {   // +32 K rows = 4 KB per step
+                        const uint64_t adv = (uint64_t)((UMMA_K * 128) >> 4) * k;
+                        tc::mma_i8_ss(tmem, ad0 + adv, bd + adv, idesc, (kb | k) ? 1u : 0u);
+                        tc::mma_i8_ss(tmem + BN, ad1 + adv, bd + adv, idesc, (kb | k) ? 1u : 0u);
+                    }
+                    tc::mma_commit(&empty[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                tc::mma_commit(tfull);
+                tphase ^= 1;
+            }
+        }
+    } else if (warp >= EPI_WARP0) {
+        // ------------------------------------------------------------- epilogue
+        // warp w drains TMEM lanes 32*(w%4); warps 4-7 accumulator 0, 8-11 accumulator 1
+        const int lg = warp & 3, acc = (warp - EPI_WARP0) >> 2;
+        unsigned tphase = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            int mod, split, tile, nkb;
+            int64_t k0;
+            unit_coords(u, mod, split, tile, k0, nkb);
+            tc::mbar_wait(tfull, tphase);
+            tc::tc_fence_after();
+            tphase ^= 1;
+            int32_t *out = p.part + (((size_t)mod * p.splits + split) * p.ntiles + tile) * (size_t)(BM * BN);
+            const int orow = acc * UMMA_M + lg * 32 + lane;
+#pragma unroll 1
+            for (int cb = 0; cb < BN / 32; ++cb) {
+                uint32_t v[32];
+                tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int q = 0; q < 32; ++q) out[(size_t)(cb * 32 + q) * BM + orow] = (int32_t)v[q];
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tempty);
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc<512>(tmem);
+    }
+}
+
+// ------------------------------------------------------ modular reduction ----
+// acc[mod][i][j] = (acc + sum_split part) mod p, in [0, p); SYRK: lower tiles only
+__global__ void reduce_kernel(const int32_t *__restrict__ part, int splits, int ntiles, int ntn, int syrk, int n,
+                              int32_t *__restrict__ acc) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nn = (int64_t)n * n;
+    if (idx >= nn * NMOD) return;
+    const int mod = (int)(idx / nn);
+    const int64_t e = idx - (int64_t)mod * nn;
+    const int i = (int)(e / n), j = (int)(e % n);
+    const int tm = i / BM, tn = j / BN;
+    if (syrk && tm < tn) return;
+    const int tile = syrk ? tm * (tm + 1) / 2 + tn : tm * ntn + tn;
+    const int32_t *pp = part + ((size_t)mod * splits * ntiles + tile) * (size_t)(BM * BN) + (size_t)(j % BN) * BM +
+                        (i % BM);
+    int64_t s = acc[idx];
+    for (int k = 0; k < splits; ++k) s += pp[(size_t)k * ntiles * (BM * BN)];
+    int32_t p = 0;
+#pragma unroll
+    for (int k = 0; k < NMOD; ++k)
+        if (k == mod) p = pm(k);
+    int32_t r = (int32_t)(s % p);
+    acc[idx] = r < 0 ? r + p : r;
+}
+
+// ------------------------------------------------------- reconstruction -----
+__global__ void crt_kernel(const int32_t *__restrict__ acc, int n, int syrk, const int *__restrict__ ex,
+                           const int *__restrict__ ey, int t, double *__restrict__ g, int64_t ldg) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nn = (int64_t)n * n;
+    if (idx >= nn) return;
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    const int64_t src = (syrk && (i / BM) < (j / BN)) ? (int64_t)j * n + i : idx;   // mirror: C' symmetric
+    int r[NMOD];
+#pragma unroll
+    for (int k = 0; k < NMOD; ++k) r[k] = acc[(int64_t)k * nn + src];
+    // Garner: x = v0 + v1 p0 + v2 p0 p1 + ...
+    int v[NMOD];
+#pragma unroll
+    for (int k = 0; k < NMOD; ++k) {
+        // x_{k} mod p_k from the digits so far (Horner, mod p_k)
+        int acc_k = 0;
+#pragma unroll
+        for (int j2 = k - 1; j2 >= 0; --j2) acc_k = (acc_k * pm(j2) + v[j2]) % pm(k);
+        int d = (r[k] - acc_k) % pm(k);
+        d = d < 0 ? d + pm(k) : d;
+        v[k] = (int)(((int64_t)d * garner_of(k)) % pm(k));
+    }
+    unsigned __int128 x = 0;
+#pragma unroll
+    for (int k = NMOD - 1; k >= 0; --k) x = x * (unsigned)pm(k) + (unsigned)v[k];
+    unsigned __int128 mprod = 1;
+#pragma unroll
+    for (int k = 0; k < NMOD; ++k) mprod *= (unsigned)pm(k);
+    const bool neg = x > (mprod >> 1);
+    const unsigned __int128 mag = neg ? mprod - x : x;
+    const double hi = (double)(unsigned long long)(mag >> 64), lo = (double)(unsigned long long)mag;
+    double val = fma(hi, 18446744073709551616.0, lo);
+    val = neg ? -val : val;
+    g[(int64_t)i * ldg + j] = ldexp(val, ex[i] + ey[j] - 2 * t);
+}
+
+// -------------------------------------------------------------- planning ----
+struct Plan {
+    int ntm, ntn, ntiles, t;
+    int64_t chunk, kchunk, ldr;
+    int splits;
+    size_t res_bytes, part_bytes, acc_bytes, aux_bytes;
+};
+
+int choose_t(int64_t m) {
+    double lg = 0.0;
+    for (int k = 0; k < NMOD; ++k) lg += log2((double)pm(k));
+    // |C'| <= m 2^(2t) must stay below M/2
+    const int t = (int)floor((lg - 1.0 - log2((double)std::max<int64_t>(m, 1)) - 0.01) / 2.0);
+    return std::min(t, 51);
+}
+
+Plan make_plan(int64_t m, int64_t n, bool syrk) {
+    Plan p;
+    p.ntm = (int)((n + BM - 1) / BM);
+    p.ntn = p.ntm;
+    p.ntiles = syrk ? p.ntm * (p.ntm + 1) / 2 : p.ntm * p.ntn;
+    p.t = choose_t(m);
+    p.ldr = (n + 15) / 16 * 16;
+    p.kchunk = KSPLIT_MAX;
+    p.chunk = std::min<int64_t>((m + BK - 1) / BK * BK, 2 * KSPLIT_MAX);
+    p.splits = (int)((p.chunk + p.kchunk - 1) / p.kchunk);
+    const int ops = syrk ? 1 : 2;
+    p.res_bytes = (size_t)ops * NMOD * p.chunk * p.ldr;
+    p.part_bytes = (size_t)NMOD * p.splits * p.ntiles * BM * BN * sizeof(int32_t);
+    p.acc_bytes = (size_t)NMOD * n * n * sizeof(int32_t);
+    p.aux_bytes = (size_t)4 * n * 8 + 4096;
+    return p;
+}
+
+size_t align_up256(size_t b) { return (b + 255) & ~size_t(255); }
+
+}  // namespace oz
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" {
+
+size_t sk_gram_ozaki_workspace(int64_t m, int64_t n, int syrk) {
+    oz::Plan p = oz::make_plan(m, n, syrk != 0);
+    return oz::align_up256(p.res_bytes) + oz::align_up256(p.part_bytes) + oz::align_up256(p.acc_bytes) +
+           oz::align_up256(p.aux_bytes) + 1024;
+}
+
+int sk_gram_ozaki_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n, double *g,
+                      int64_t ldg, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    if (!x || !y || !g || m < 0 || n <= 0 || ldx < n || ldy < n || ldg < n || n > 65536) {
+        set_error("sk_gram_ozaki_f64: bad arguments");
+        return SK_ERR_ARG;
+    }
+    const bool syrk = (x == y) && (ldx == ldy);
+    if (!ws || ws_bytes < sk_gram_ozaki_workspace(m, n, syrk)) {
+        set_error("sk_gram_ozaki_f64: workspace %zu < %zu", ws_bytes, sk_gram_ozaki_workspace(m, n, syrk));
+        return SK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    oz::Plan p = oz::make_plan(m, n, syrk);
+    uint8_t *w = static_cast<uint8_t *>(ws);
+    int8_t *res = reinterpret_cast<int8_t *>(w);
+    w += oz::align_up256(p.res_bytes);
+    int32_t *part = reinterpret_cast<int32_t *>(w);
+    w += oz::align_up256(p.part_bytes);
+    int32_t *acc = reinterpret_cast<int32_t *>(w);
+    w += oz::align_up256(p.acc_bytes);
+    unsigned long long *bits = reinterpret_cast<unsigned long long *>(w);   // 2n
+    double *scale = reinterpret_cast<double *>(bits + 2 * n);                // 2n
+    int *expo = reinterpret_cast<int *>(scale + 2 * n);                      // 2n
+
+    SK_CUDA(cudaMemsetAsync(bits, 0, (size_t)2 * n * sizeof(unsigned long long), st));
+    SK_CUDA(cudaMemsetAsync(acc, 0, p.acc_bytes, st));
+    const int sms = sm_count();
+    const dim3 cg((unsigned)std::min<int64_t>(std::max<int64_t>(m, 1), (int64_t)sms * 4), (unsigned)((n + 255) / 256));
+    if (m > 0) {
+        oz::colmax_kernel<<<cg, 256, 0, st>>>(x, ldx, m, (int)n, bits);
+        SK_LAUNCH_CHECK("oz colmax");
+        if (!syrk) {
+            oz::colmax_kernel<<<cg, 256, 0, st>>>(y, ldy, m, (int)n, bits + n);
+            SK_LAUNCH_CHECK("oz colmax");
+        }
+    }
+    const unsigned sgrid = (unsigned)((n + 255) / 256);
+    oz::scales_kernel<<<sgrid, 256, 0, st>>>(bits, (int)n, p.t, scale, expo);
+    oz::scales_kernel<<<sgrid, 256, 0, st>>>(syrk ? bits : bits + n, (int)n, p.t, scale + n, expo + n);
+    SK_LAUNCH_CHECK("oz scales");
+
+    const int vx = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ldx % 2 == 0);
+    const int vy = ((reinterpret_cast<uintptr_t>(y) & 15) == 0) && (ldy % 2 == 0);
+    const int64_t plane = p.chunk * p.ldr;
+    int8_t *res_x = res, *res_y = syrk ? res : res + (size_t)oz::NMOD * plane;
+    SK_CUDA(cudaFuncSetAttribute(oz::gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz::SMEM));
+    for (int64_t r0 = 0; r0 < m; r0 += p.chunk) {
+        const int64_t rows = std::min(p.chunk, m - r0);
+        const int64_t items = rows * ((n + 15) / 16);
+        const unsigned rgrid = (unsigned)std::min<int64_t>((items + 255) / 256, (int64_t)sms * 8);
+        oz::residues_kernel<<<rgrid, 256, 0, st>>>(x + r0 * ldx, ldx, rows, (int)n, scale, res_x, p.ldr, plane, vx);
+        SK_LAUNCH_CHECK("oz residues");
+        if (!syrk) {
+            oz::residues_kernel<<<rgrid, 256, 0, st>>>(y + r0 * ldy, ldy, rows, (int)n, scale + n, res_y, p.ldr,
+                                                       plane, vy);
+            SK_LAUNCH_CHECK("oz residues");
+        }
+        CUtensorMap tx, ty;
+        int rc = make_tmap_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, res_x, (uint64_t)n, (uint64_t)rows, oz::NMOD,
+                              (uint64_t)p.ldr, (uint64_t)plane, 128, oz::BK, CU_TENSOR_MAP_SWIZZLE_128B);
+        if (rc) return rc;
+        rc = make_tmap_3d(&ty, CU_TENSOR_MAP_DATA_TYPE_UINT8, res_y, (uint64_t)n, (uint64_t)rows, oz::NMOD,
+                          (uint64_t)p.ldr, (uint64_t)plane, 128, oz::BK, CU_TENSOR_MAP_SWIZZLE_128B);
+        if (rc) return rc;
+        oz::GemmParams gp;
+        gp.ntn = p.ntn;
+        gp.ntiles = p.ntiles;
+        gp.splits = (int)((rows + p.kchunk - 1) / p.kchunk);
+        gp.units = oz::NMOD * gp.splits * p.ntiles;
+        gp.syrk = syrk;
+        gp.rows = rows;
+        gp.kchunk = p.kchunk;
+        gp.part = part;
+        oz::gemm_kernel<<<std::min(gp.units, sms), oz::THREADS, oz::SMEM, st>>>(tx, ty, gp);
+        SK_LAUNCH_CHECK("oz gemm");
+        const int64_t tot = (int64_t)oz::NMOD * n * n;
+        oz::reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(part, gp.splits, p.ntiles, p.ntn, syrk,
+                                                                         (int)n, acc);
+        SK_LAUNCH_CHECK("oz reduce");
+    }
+    const int64_t nn = n * n;
+    oz::crt_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(acc, (int)n, syrk, expo, expo + n, p.t, g, ldg);
+    SK_LAUNCH_CHECK("oz crt");
+    return SK_OK;
+}
+
+}  // extern "C"

@@ -48,9 +48,21 @@ def _rm(t: torch.Tensor) -> torch.Tensor:
     return t
 
 
+GRAM_ENGINE = "auto"       # "dmma" (FP64 DMMA), "ozaki" (INT8 tensor cores), "auto"
+OZAKI_MIN_WORK = 1 << 33   # m * n^2 above which "auto" takes the INT8 engine
+
+
+def _gram_engine(m: int, n: int, accumulate: bool, engine: str | None) -> str:
+    e = engine or GRAM_ENGINE
+    if e == "auto":
+        e = "ozaki" if (not accumulate and n >= 128 and m * n * n >= OZAKI_MIN_WORK) else "dmma"
+    return e
+
+
 def _gram(x: DMat | torch.Tensor, y: DMat | torch.Tensor | None = None, out: torch.Tensor | None = None,
-          accumulate: bool = False) -> torch.Tensor:
-    """G = X^T Y (SYRK when y is None or y is x) on the DMMA pipe."""
+          accumulate: bool = False, engine: str | None = None) -> torch.Tensor:
+    """G = X^T Y (SYRK when y is None or y is x): FP64 DMMA, or the INT8 tensor-core
+    Ozaki engine (sk_gram_ozaki_f64) for large products."""
     xt = _rm(x.t if isinstance(x, DMat) else x)
     yt = xt if y is None else _rm(y.t if isinstance(y, DMat) else y)
     m, n = xt.shape
@@ -59,6 +71,12 @@ def _gram(x: DMat | torch.Tensor, y: DMat | torch.Tensor | None = None, out: tor
     if out is None:
         out = torch.empty((n, n), dtype=torch.float64, device=xt.device)
     lib = _lib.lib()
+    if _gram_engine(m, n, accumulate, engine) == "ozaki":
+        syrk = xt.data_ptr() == yt.data_ptr() and xt.stride(0) == yt.stride(0)
+        wp, wn = WORKSPACE.get(lib.sk_gram_ozaki_workspace(m, n, int(syrk)))
+        call("sk_gram_ozaki_f64", xt.data_ptr(), xt.stride(0), yt.data_ptr(), yt.stride(0), m, n,
+             out.data_ptr(), out.stride(0), wp, wn, stream_handle())
+        return out
     wsb = lib.sk_gram_workspace(m, n)
     wp, wn = WORKSPACE.get(wsb)
     call("sk_gram_f64", xt.data_ptr(), xt.stride(0), yt.data_ptr(), yt.stride(0), m, n,

@@ -1,0 +1,76 @@
+"""INT8 tensor-core (Ozaki scheme II) FP64 Gram against an extended-precision
+reference and against the FP64 DMMA Gram.
+
+Bound checked: the engine's only rounding is the per-column t-bit scaling, so
+|G - X^T Y|_ij <= 2^-t (2^e_i sum|Y_j| + 2^f_j sum|X_i|) / 2 + one final rounding;
+we assert the looser "no worse than 4x the DMMA GEMM's error, or 1e-15 of |X|^T|Y|"."""
+import numpy as np
+import pytest
+
+from oracle import restatement as R
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    return t
+
+
+def _exact(x, y):
+    xl, yl = x.astype(np.longdouble), y.astype(np.longdouble)
+    return xl.T @ yl
+
+
+def _check(torch, x, y, syrk):
+    from paper_2603_16644_b200.dense import _gram
+    xt = torch.from_numpy(x).cuda()
+    yt = xt if syrk else torch.from_numpy(y).cuda()
+    g_oz = _gram(xt, None if syrk else yt, engine="ozaki").cpu().numpy()
+    g_dm = _gram(xt, None if syrk else yt, engine="dmma").cpu().numpy()
+    ex = _exact(x, x if syrk else y)
+    absb = (np.abs(x).T @ np.abs(x if syrk else y))
+    e_oz = float(np.max(np.abs(g_oz - ex) / np.maximum(absb, 1e-300)))
+    e_dm = float(np.max(np.abs(g_dm - ex) / np.maximum(absb, 1e-300)))
+    assert np.all(np.isfinite(g_oz))
+    assert e_oz <= max(4 * e_dm, 1e-15), (e_oz, e_dm)
+    if syrk:
+        assert np.array_equal(g_oz, g_oz.T)
+    return e_oz, e_dm
+
+
+@pytest.mark.parametrize("m,n,syrk", [(1000, 128, True), (1000, 128, False), (5000, 300, True),
+                                      (5000, 300, False), (6000, 520, False), (300000, 24, True),
+                                      (300000, 20, False), (77, 256, False)])
+def test_ozaki_gram_random(torch, m, n, syrk):
+    g = R.philox(m + 7 * n, 3)
+    x = g.standard_normal((m, n))
+    y = g.standard_normal((m, n))
+    _check(torch, x, y, syrk)
+
+
+def test_ozaki_gram_scaled_columns_and_rows(torch):
+    g = R.philox(11, 3)
+    m, n = 40000, 200
+    x = g.standard_normal((m, n)) * (10.0 ** g.uniform(-8, 8, n))[None, :]
+    x *= (10.0 ** g.uniform(-3, 3, m))[:, None]
+    y = g.standard_normal((m, n)) * (10.0 ** g.uniform(-8, 8, n))[None, :]
+    _check(torch, x, x, True)
+    _check(torch, x, y, False)
+
+
+def test_ozaki_gram_special_values(torch):
+    from paper_2603_16644_b200.dense import _gram
+    m, n = 3000, 130
+    x = np.zeros((m, n))
+    x[:, 5] = 1.0                      # constant column
+    x[7, 9] = -3.5                     # a single entry
+    x[:, 20] = R.philox(1, 3).standard_normal(m)
+    g_oz = _gram(torch.from_numpy(x).cuda(), engine="ozaki").cpu().numpy()
+    ref = x.T @ x
+    exact = np.ones((n, n), dtype=bool)
+    exact[20, :] = exact[:, 20] = False
+    assert np.array_equal(g_oz[exact], ref[exact])   # zeros, small integers, single products
+    assert abs(g_oz[20, 20] - ref[20, 20]) <= 1e-15 * ref[20, 20]
+    assert abs(g_oz[5, 20] - ref[5, 20]) <= 1e-15 * np.abs(x[:, 20]).sum()

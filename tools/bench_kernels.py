@@ -34,6 +34,11 @@ if want("syrk"):
     res["syrk"] = t(lambda: D._gram(a)); res["syrk_tflops"] = m * n * n / (min(res["syrk"]) * 1e-3) / 1e12
 if want("gemm"):
     res["gemm"] = t(lambda: D._gram(a, ap_buf)); res["gemm_tflops"] = 2 * m * n * n / (min(res["gemm"]) * 1e-3) / 1e12
+if want("ozaki"):
+    res["oz_syrk"] = t(lambda: D._gram(a, engine="ozaki"))
+    res["oz_syrk_tflops"] = m * n * n / (min(res["oz_syrk"]) * 1e-3) / 1e12
+    res["oz_gemm"] = t(lambda: D._gram(a, ap_buf, engine="ozaki"))
+    res["oz_gemm_tflops"] = 2 * m * n * n / (min(res["oz_gemm"]) * 1e-3) / 1e12
 if want("trsm"):
     res["trsm"] = t(lambda: D._trsm(a, r, out=ap_buf)); res["trsm_tflops"] = m * n * n / (min(res["trsm"]) * 1e-3) / 1e12
     del ap_buf
