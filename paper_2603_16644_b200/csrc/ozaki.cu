@@ -69,7 +69,14 @@ __global__ void __launch_bounds__(256) colmax_kernel(const double *__restrict__ 
     const int c = blockIdx.y * 256 + threadIdx.x;
     if (c >= n) return;
     double mx = 0.0;
-    for (int64_t r = blockIdx.x; r < m; r += gridDim.x) mx = fmax(mx, fabs(x[r * ldx + c]));
+    const int64_t g = gridDim.x;
+    int64_t r = blockIdx.x;
+    for (; r + 3 * g < m; r += 4 * g) {   // four independent loads in flight
+        const double a0 = x[r * ldx + c], a1 = x[(r + g) * ldx + c], a2 = x[(r + 2 * g) * ldx + c],
+                     a3 = x[(r + 3 * g) * ldx + c];
+        mx = fmax(fmax(mx, fmax(fabs(a0), fabs(a1))), fmax(fabs(a2), fabs(a3)));
+    }
+    for (; r < m; r += g) mx = fmax(mx, fabs(x[r * ldx + c]));
     atomicMax(out + c, (unsigned long long)__double_as_longlong(mx));
 }
 
@@ -88,66 +95,86 @@ __global__ void scales_kernel(const unsigned long long *__restrict__ bits, int n
 }
 
 // ------------------------------------------------------------- residues -----
-__device__ __forceinline__ int residue(uint32_t l0, uint32_t l1, uint32_t l2, int k, bool neg) {
-    const uint32_t p = (uint32_t)pm(k);
-    const uint32_t v = l2 * c2_of(k) + l1 * c1_of(k) + l0;   // < 2^27
-    int r = (int)(v - p * __umulhi(v, magic_of(k)));           // r_true or r_true - p
-    r += r < 0 ? (int)p : 0;
-    r -= r > (int)(p - 1) / 2 ? (int)p : 0;
-    return neg ? -r : r;
+// X' = h3 2^39 + h2 2^26 + h1 2^13 + h0 with balanced 13-bit limbs |h| <= 2^12 (exact
+// FP64 splitting), so X' mod p = (h3 c3 + h2 c2 + h1 c1 + h0) mod p with centred
+// c_j = 2^(13 j) mod p in [-127, 127]: |v| <= 1.56e6, exact in FP32.  q = round(v / p)
+// by the 1.5 2^23 magic (v inv_p is within 5e-4 of v / p, and v / p is at least 1/510
+// from a half-integer since p is odd), r = v - q p exact and already centred.
+__host__ __device__ constexpr int centred_pow2_mod(int e, int k) {
+    const int r = (int)((1ull << e) % (uint64_t)pm(k));
+    return r > (pm(k) - 1) / 2 ? r - pm(k) : r;
+}
+constexpr float FMAGIC = 12582912.0f;   // 1.5 * 2^23
+
+__device__ __forceinline__ uint32_t residue_byte(float h0, float h1, float h2, float h3, int k) {
+    const float v = fmaf(h3, (float)centred_pow2_mod(39, k),
+                         fmaf(h2, (float)centred_pow2_mod(26, k), fmaf(h1, (float)centred_pow2_mod(13, k), h0)));
+    const float q = fmaf(v, 1.0f / (float)pm(k), FMAGIC) - FMAGIC;
+    const float r = fmaf(-q, (float)pm(k), v);
+    return __float_as_uint(r + FMAGIC);     // low byte = r as a two's-complement int8
 }
 
-// 16 consecutive columns of one row per thread -> 16 planes of 16 bytes
-__global__ void __launch_bounds__(256)
+// 8 consecutive columns of one row per thread -> 16 planes of 8 bytes.  Rows are
+// walked grid-stride; a block covers 256 column groups (one row of n = 2048, or
+// several rows of narrower matrices), so no 64-bit division per item.
+constexpr int RV = 8;
+__global__ void __launch_bounds__(256, 4)
 residues_kernel(const double *__restrict__ x, int64_t ldx, int64_t rows, int n, const double *__restrict__ scale,
                 int8_t *__restrict__ out, int64_t ldr, int64_t plane, int vec) {
-    const int groups = (n + 15) / 16;
-    const int64_t total = rows * groups;
-    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total;
-         it += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = it / groups;
-        const int c0 = (int)(it - r * groups) * 16;
-        const double *src = x + r * ldx + c0;
-        double v[16];
-        if (vec && c0 + 16 <= n) {
+    const int cpr = (n + RV - 1) / RV;
+    const int rpi = cpr >= 256 ? 1 : 256 / cpr;
+    const int sub = cpr >= 256 ? 0 : threadIdx.x / cpr;
+    const int cfirst = cpr >= 256 ? threadIdx.x : threadIdx.x % cpr;
+    const int cstep = cpr >= 256 ? 256 : cpr;
+    for (int64_t r0 = (int64_t)blockIdx.x * rpi; r0 < rows; r0 += (int64_t)gridDim.x * rpi) {
+        const int64_t r = r0 + sub;
+        if (sub >= rpi || r >= rows) continue;
+        for (int ch = cfirst; ch < cpr; ch += cstep) {
+            const int c0 = ch * RV;
+            const double *src = x + r * ldx + c0;
+            double v[RV];
+            if (vec && c0 + RV <= n) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const double2 d = __ldcs(reinterpret_cast<const double2 *>(src) + q);
-                v[2 * q] = d.x;
-                v[2 * q + 1] = d.y;
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < 16; ++q) v[q] = c0 + q < n ? src[q] : 0.0;
-        }
-        uint32_t l0[16], l1[16], l2[16];
-        uint32_t negm = 0;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const double s = c0 + q < n ? scale[c0 + q] : 0.0;
-            const long long iv = __double2ll_rn(v[q] * s);
-            const unsigned long long u = (unsigned long long)(iv < 0 ? -iv : iv);
-            negm |= (iv < 0 ? 1u : 0u) << q;
-            l0[q] = (uint32_t)(u & 0x1FFFFull);
-            l1[q] = (uint32_t)((u >> 17) & 0x1FFFFull);
-            l2[q] = (uint32_t)(u >> 34);
-        }
-        int8_t *dst = out + r * ldr + c0;
-#pragma unroll
-        for (int k = 0; k < NMOD; ++k) {
-            uint32_t w[4];
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-                uint32_t word = 0;
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int q = 4 * q4 + b;
-                    const int rr = residue(l0[q], l1[q], l2[q], k, (negm >> q) & 1u);
-                    word |= ((uint32_t)(rr & 0xFF)) << (8 * b);
+                for (int q = 0; q < RV / 2; ++q) {
+                    const double2 d = __ldcs(reinterpret_cast<const double2 *>(src) + q);
+                    v[2 * q] = d.x;
+                    v[2 * q + 1] = d.y;
                 }
-                w[q4] = word;
+            } else {
+#pragma unroll
+                for (int q = 0; q < RV; ++q) v[q] = c0 + q < n ? src[q] : 0.0;
             }
-            *reinterpret_cast<uint4 *>(dst + k * plane) = make_uint4(w[0], w[1], w[2], w[3]);
+            float h0[RV], h1[RV], h2[RV], h3[RV];
+#pragma unroll
+            for (int q = 0; q < RV; ++q) {
+                const double s = c0 + q < n ? __ldg(scale + c0 + q) : 0.0;
+                const double xs = rint(v[q] * s);                 // |xs| <= 2^t <= 2^51, exact
+                const double a3 = rint(xs * 0x1p-39);
+                const double r3 = fma(-a3, 0x1p39, xs);
+                const double a2 = rint(r3 * 0x1p-26);
+                const double r2 = fma(-a2, 0x1p26, r3);
+                const double a1 = rint(r2 * 0x1p-13);
+                h3[q] = (float)a3;
+                h2[q] = (float)a2;
+                h1[q] = (float)a1;
+                h0[q] = (float)fma(-a1, 0x1p13, r2);
+            }
+            int8_t *dst = out + r * ldr + c0;
+#pragma unroll
+            for (int k = 0; k < NMOD; ++k) {
+                uint32_t w[2];
+#pragma unroll
+                for (int q4 = 0; q4 < 2; ++q4) {
+                    uint32_t b[4];
+#pragma unroll
+                    for (int bb = 0; bb < 4; ++bb) {
+                        const int q = 4 * q4 + bb;
+                        b[bb] = residue_byte(h0[q], h1[q], h2[q], h3[q], k);
+                    }
+                    w[q4] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+                }
+                *reinterpret_cast<uint2 *>(dst + k * plane) = make_uint2(w[0], w[1]);
+            }
         }
     }
 }
@@ -399,10 +426,10 @@ Plan make_plan(int64_t m, int64_t n, bool syrk) {
     p.t = choose_t(m);
     p.ldr = (n + 15) / 16 * 16;
     p.kchunk = KSPLIT_MAX;
-    p.chunk = std::min<int64_t>((m + BK - 1) / BK * BK, 2 * KSPLIT_MAX);
+    p.chunk = std::min<int64_t>((m + BK - 1) / BK * BK, KSPLIT_MAX);
     p.splits = (int)((p.chunk + p.kchunk - 1) / p.kchunk);
     const int ops = syrk ? 1 : 2;
-    p.res_bytes = (size_t)ops * NMOD * p.chunk * p.ldr;
+    p.res_bytes = (size_t)2 * ops * NMOD * p.chunk * p.ldr;   // double-buffered chunks
     p.part_bytes = (size_t)NMOD * p.splits * p.ntiles * BM * BN * sizeof(int32_t);
     p.acc_bytes = (size_t)NMOD * n * n * sizeof(int32_t);
     p.aux_bytes = (size_t)4 * n * 8 + 4096;
@@ -410,6 +437,30 @@ Plan make_plan(int64_t m, int64_t n, bool syrk) {
 }
 
 size_t align_up256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// per (host thread, device) side stream + events of the residue/GEMM pipeline
+struct SidePipe {
+    bool ok = false;
+    cudaStream_t side = nullptr;
+    cudaEvent_t start = nullptr, res_done[2] = {nullptr, nullptr}, gemm_done[2] = {nullptr, nullptr};
+};
+
+SidePipe &side_pipe() {
+    thread_local SidePipe pipes[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    SidePipe &sp = pipes[dev & 63];
+    if (!sp.ok) {
+        bool ok = cudaStreamCreateWithFlags(&sp.side, cudaStreamNonBlocking) == cudaSuccess;
+        ok = ok && cudaEventCreateWithFlags(&sp.start, cudaEventDisableTiming) == cudaSuccess;
+        for (int i = 0; i < 2; ++i) {
+            ok = ok && cudaEventCreateWithFlags(&sp.res_done[i], cudaEventDisableTiming) == cudaSuccess;
+            ok = ok && cudaEventCreateWithFlags(&sp.gemm_done[i], cudaEventDisableTiming) == cudaSuccess;
+        }
+        sp.ok = ok;
+    }
+    return sp;
+}
 
 }  // namespace oz
 }  // namespace sk
@@ -468,19 +519,38 @@ int sk_gram_ozaki_f64(const double *x, int64_t ldx, const double *y, int64_t ldy
     const int vx = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ldx % 2 == 0);
     const int vy = ((reinterpret_cast<uintptr_t>(y) & 15) == 0) && (ldy % 2 == 0);
     const int64_t plane = p.chunk * p.ldr;
-    int8_t *res_x = res, *res_y = syrk ? res : res + (size_t)oz::NMOD * plane;
+    const size_t buf_bytes = (size_t)(syrk ? 1 : 2) * oz::NMOD * plane;
     SK_CUDA(cudaFuncSetAttribute(oz::gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz::SMEM));
-    for (int64_t r0 = 0; r0 < m; r0 += p.chunk) {
+    // Two-stream pipeline: the residues of chunk c+1 (ALU-bound, side stream) run
+    // while the INT8 GEMM of chunk c (tensor-bound, caller's stream) runs; chunks
+    // alternate between two residue buffers.
+    oz::SidePipe &sp = oz::side_pipe();
+    if (!sp.ok) {
+        set_error("sk_gram_ozaki_f64: side stream unavailable");
+        return SK_ERR_CUDA;
+    }
+    SK_CUDA(cudaEventRecord(sp.start, st));
+    SK_CUDA(cudaStreamWaitEvent(sp.side, sp.start, 0));
+    int chunk_idx = 0;
+    for (int64_t r0 = 0; r0 < m; r0 += p.chunk, ++chunk_idx) {
+        const int buf = chunk_idx & 1;
+        int8_t *res_x = res + buf * buf_bytes;
+        int8_t *res_y = syrk ? res_x : res_x + (size_t)oz::NMOD * plane;
         const int64_t rows = std::min(p.chunk, m - r0);
-        const int64_t items = rows * ((n + 15) / 16);
-        const unsigned rgrid = (unsigned)std::min<int64_t>((items + 255) / 256, (int64_t)sms * 8);
-        oz::residues_kernel<<<rgrid, 256, 0, st>>>(x + r0 * ldx, ldx, rows, (int)n, scale, res_x, p.ldr, plane, vx);
+        const int cpr = (int)((n + oz::RV - 1) / oz::RV);
+        const int rpi = cpr >= 256 ? 1 : 256 / cpr;
+        const unsigned rgrid = (unsigned)std::min<int64_t>((rows + rpi - 1) / rpi, (int64_t)sms * 16);
+        if (chunk_idx >= 2) SK_CUDA(cudaStreamWaitEvent(sp.side, sp.gemm_done[buf], 0));
+        oz::residues_kernel<<<rgrid, 256, 0, sp.side>>>(x + r0 * ldx, ldx, rows, (int)n, scale, res_x, p.ldr, plane,
+                                                        vx);
         SK_LAUNCH_CHECK("oz residues");
         if (!syrk) {
-            oz::residues_kernel<<<rgrid, 256, 0, st>>>(y + r0 * ldy, ldy, rows, (int)n, scale + n, res_y, p.ldr,
-                                                       plane, vy);
+            oz::residues_kernel<<<rgrid, 256, 0, sp.side>>>(y + r0 * ldy, ldy, rows, (int)n, scale + n, res_y,
+                                                            p.ldr, plane, vy);
             SK_LAUNCH_CHECK("oz residues");
         }
+        SK_CUDA(cudaEventRecord(sp.res_done[buf], sp.side));
+        SK_CUDA(cudaStreamWaitEvent(st, sp.res_done[buf], 0));
         CUtensorMap tx, ty;
         int rc = make_tmap_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, res_x, (uint64_t)n, (uint64_t)rows, oz::NMOD,
                               (uint64_t)p.ldr, (uint64_t)plane, 128, oz::BK, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -499,6 +569,7 @@ int sk_gram_ozaki_f64(const double *x, int64_t ldx, const double *y, int64_t ldy
         gp.part = part;
         oz::gemm_kernel<<<std::min(gp.units, sms), oz::THREADS, oz::SMEM, st>>>(tx, ty, gp);
         SK_LAUNCH_CHECK("oz gemm");
+        SK_CUDA(cudaEventRecord(sp.gemm_done[buf], st));
         const int64_t tot = (int64_t)oz::NMOD * n * n;
         oz::reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(part, gp.splits, p.ntiles, p.ntn, syrk,
                                                                          (int)n, acc);

@@ -60,6 +60,35 @@ def test_ozaki_gram_scaled_columns_and_rows(torch):
     _check(torch, x, y, False)
 
 
+@pytest.fixture
+def int8_gram(monkeypatch):
+    """Every Gram of the solvers on the INT8 engine, whatever its size."""
+    from paper_2603_16644_b200 import dense
+    monkeypatch.setattr(dense, "GRAM_ENGINE", "ozaki")
+
+
+def _golden_keys():
+    from tests.golden_data import META
+    return sorted(META["runs"])
+
+
+@pytest.mark.parametrize("key", _golden_keys())
+def test_pipeline_golden_runs_on_int8_gram(int8_gram, key):
+    """The reference's golden pipeline runs (level, escalation, error, kappa0) hold with
+    the kappa0 SYRK and the PNE / HPNE Grams on the INT8 engine."""
+    import paper_2603_16644_b200 as sq
+    from tests.test_gpu_pipeline import test_pipeline_vs_reference_runs
+    test_pipeline_vs_reference_runs(sq, key)
+
+
+@pytest.mark.parametrize("kappa", [1e2, 1e6, 1e10, 1e14])
+@pytest.mark.parametrize("rho", [1e-14, 1e-6, 1e-1])
+def test_config5_grid_on_int8_gram(int8_gram, kappa, rho):
+    import paper_2603_16644_b200 as sq
+    from tests.test_gpu_configs import test_config5_grid_scaled
+    test_config5_grid_scaled(sq, kappa, rho)
+
+
 def test_ozaki_gram_special_values(torch):
     from paper_2603_16644_b200.dense import _gram
     m, n = 3000, 130
