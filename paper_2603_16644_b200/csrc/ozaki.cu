@@ -181,9 +181,9 @@ residues_kernel(const double *__restrict__ x, int64_t ldx, int64_t rows, int n, 
 
 // ---------------------------------------------------------------- GEMM ------
 struct GemmParams {
-    int ntn, ntiles, splits, units, syrk;
+    int ntn, ntiles, splits, units, syrk, n;
     int64_t rows, kchunk;
-    int32_t *part;              // [mod][split][tile][BN cols][BM rows]
+    int32_t *acc;               // [mod][n][n] residues in [0, p)
 };
 
 // lower-triangular tile list for SYRK: tile index -> (tm, tn) with tm >= tn
@@ -317,15 +317,46 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ 
             tc::mbar_wait(tfull, tphase);
             tc::tc_fence_after();
             tphase ^= 1;
-            int32_t *out = p.part + (((size_t)mod * p.splits + split) * p.ntiles + tile) * (size_t)(BM * BN);
-            const int orow = acc * UMMA_M + lg * 32 + lane;
+            // acc[mod][row][col] = (acc + C_partial) mod p, in [0, p): one unit per
+            // (modulus, tile) per launch, so no two CTAs touch the same entries
+            int tm, tn;
+            tile_coords(p, tile, tm, tn);
+            const int pmod = pm(mod);
+            const int row = tm * BM + acc * UMMA_M + lg * 32 + lane;
+            int32_t *dst_row = p.acc + (size_t)mod * p.n * p.n + (size_t)row * p.n + (size_t)tn * BN;
 #pragma unroll 1
             for (int cb = 0; cb < BN / 32; ++cb) {
                 uint32_t v[32];
                 tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
                 tc::tmem_ld_wait();
+                if (row < p.n) {
+                    int32_t *dst = dst_row + cb * 32;
+                    const int cols = min(32, p.n - (tn * BN + cb * 32));
+                    if (cols == 32 && (p.n & 3) == 0) {
 #pragma unroll
-                for (int q = 0; q < 32; ++q) out[(size_t)(cb * 32 + q) * BM + orow] = (int32_t)v[q];
+                        for (int q4 = 0; q4 < 8; ++q4) {
+                            int4 o = reinterpret_cast<int4 *>(dst)[q4];
+                            int *oo = reinterpret_cast<int *>(&o);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                int s = (int)v[4 * q4 + e] % pmod + oo[e];
+                                s += s < 0 ? pmod : 0;
+                                s -= s >= pmod ? pmod : 0;
+                                oo[e] = s;
+                            }
+                            reinterpret_cast<int4 *>(dst)[q4] = o;
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) {
+                            if (q >= cols) break;
+                            int s = (int)v[q] % pmod + dst[q];
+                            s += s < 0 ? pmod : 0;
+                            s -= s >= pmod ? pmod : 0;
+                            dst[q] = s;
+                        }
+                    }
+                }
             }
             tc::tc_fence_before();
             __syncwarp();
@@ -430,7 +461,7 @@ Plan make_plan(int64_t m, int64_t n, bool syrk) {
     p.splits = (int)((p.chunk + p.kchunk - 1) / p.kchunk);
     const int ops = syrk ? 1 : 2;
     p.res_bytes = (size_t)2 * ops * NMOD * p.chunk * p.ldr;   // double-buffered chunks
-    p.part_bytes = (size_t)NMOD * p.splits * p.ntiles * BM * BN * sizeof(int32_t);
+    p.part_bytes = 0;   // the GEMM epilogue accumulates modulo p straight into acc
     p.acc_bytes = (size_t)NMOD * n * n * sizeof(int32_t);
     p.aux_bytes = (size_t)4 * n * 8 + 4096;
     return p;
@@ -475,8 +506,28 @@ size_t sk_gram_ozaki_workspace(int64_t m, int64_t n, int syrk) {
            oz::align_up256(p.aux_bytes) + 1024;
 }
 
+int sk_colmax_f64(const double *x, int64_t ldx, int64_t m, int64_t n, double *colmax, sk_stream_t stream) {
+    if (!x || !colmax || m < 0 || n <= 0 || ldx < n) {
+        set_error("sk_colmax_f64: bad arguments");
+        return SK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    SK_CUDA(cudaMemsetAsync(colmax, 0, (size_t)n * sizeof(double), st));
+    if (m == 0) return SK_OK;
+    const dim3 cg((unsigned)std::min<int64_t>(m, (int64_t)sm_count() * 4), (unsigned)((n + 255) / 256));
+    oz::colmax_kernel<<<cg, 256, 0, st>>>(x, ldx, m, (int)n, reinterpret_cast<unsigned long long *>(colmax));
+    SK_LAUNCH_CHECK("oz colmax");
+    return SK_OK;
+}
+
 int sk_gram_ozaki_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n, double *g,
                       int64_t ldg, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    return sk_gram_ozaki_ex_f64(x, ldx, y, ldy, m, n, nullptr, nullptr, g, ldg, ws, ws_bytes, stream);
+}
+
+int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
+                         const double *xmax, const double *ymax, double *g, int64_t ldg, void *ws, size_t ws_bytes,
+                         sk_stream_t stream) {
     if (!x || !y || !g || m < 0 || n <= 0 || ldx < n || ldy < n || ldg < n || n > 65536) {
         set_error("sk_gram_ozaki_f64: bad arguments");
         return SK_ERR_ARG;
@@ -491,7 +542,6 @@ int sk_gram_ozaki_f64(const double *x, int64_t ldx, const double *y, int64_t ldy
     uint8_t *w = static_cast<uint8_t *>(ws);
     int8_t *res = reinterpret_cast<int8_t *>(w);
     w += oz::align_up256(p.res_bytes);
-    int32_t *part = reinterpret_cast<int32_t *>(w);
     w += oz::align_up256(p.part_bytes);
     int32_t *acc = reinterpret_cast<int32_t *>(w);
     w += oz::align_up256(p.acc_bytes);
@@ -504,11 +554,20 @@ int sk_gram_ozaki_f64(const double *x, int64_t ldx, const double *y, int64_t ldy
     const int sms = sm_count();
     const dim3 cg((unsigned)std::min<int64_t>(std::max<int64_t>(m, 1), (int64_t)sms * 4), (unsigned)((n + 255) / 256));
     if (m > 0) {
-        oz::colmax_kernel<<<cg, 256, 0, st>>>(x, ldx, m, (int)n, bits);
-        SK_LAUNCH_CHECK("oz colmax");
-        if (!syrk) {
-            oz::colmax_kernel<<<cg, 256, 0, st>>>(y, ldy, m, (int)n, bits + n);
+        // column maxima: given by the caller (sk_colmax_f64 of the same matrix) or a pass here
+        if (xmax) {
+            SK_CUDA(cudaMemcpyAsync(bits, xmax, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        } else {
+            oz::colmax_kernel<<<cg, 256, 0, st>>>(x, ldx, m, (int)n, bits);
             SK_LAUNCH_CHECK("oz colmax");
+        }
+        if (!syrk) {
+            if (ymax) {
+                SK_CUDA(cudaMemcpyAsync(bits + n, ymax, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            } else {
+                oz::colmax_kernel<<<cg, 256, 0, st>>>(y, ldy, m, (int)n, bits + n);
+                SK_LAUNCH_CHECK("oz colmax");
+            }
         }
     }
     const unsigned sgrid = (unsigned)((n + 255) / 256);
@@ -566,14 +625,11 @@ int sk_gram_ozaki_f64(const double *x, int64_t ldx, const double *y, int64_t ldy
         gp.syrk = syrk;
         gp.rows = rows;
         gp.kchunk = p.kchunk;
-        gp.part = part;
+        gp.acc = acc;
+        gp.n = (int)n;
         oz::gemm_kernel<<<std::min(gp.units, sms), oz::THREADS, oz::SMEM, st>>>(tx, ty, gp);
         SK_LAUNCH_CHECK("oz gemm");
         SK_CUDA(cudaEventRecord(sp.gemm_done[buf], st));
-        const int64_t tot = (int64_t)oz::NMOD * n * n;
-        oz::reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(part, gp.splits, p.ntiles, p.ntn, syrk,
-                                                                         (int)n, acc);
-        SK_LAUNCH_CHECK("oz reduce");
     }
     const int64_t nn = n * n;
     oz::crt_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(acc, (int)n, syrk, expo, expo + n, p.t, g, ldg);

@@ -82,6 +82,7 @@ class DMat:
     t: torch.Tensor
     frob2: float | None = None
     kind: str = "numpy"
+    colmax: torch.Tensor | None = None   # max_k |A[k, j]|, set by the pipeline (INT8 Gram scales)
 
     @property
     def shape(self):

@@ -520,18 +520,21 @@ def algorithm1_pipeline(a, b, method="pne", precision="auto", d_factor=3.0, tran
           and a.dtype == torch.float64 and a.stride(-1) == 1 and a.shape[0] >= a.shape[1] > 0):
         # device-resident A under "auto": the kappa0 Gram reads A anyway, so it doubles
         # as the validation pass (non-finite A => non-finite G; ||A||_F^2 = trace G)
-        from .dense import _rm
+        from .dense import _colmax, _gram_engine, _rm
         at = _rm(a)
         m, n = at.shape
         bd = as_dvec(b, m)
-        gram_auto = _gram(at)
+        # the INT8 Gram engine scales columns by max|A[:, j]|: scan A once for both of
+        # its Grams (kappa0 SYRK here, A_p^T A in HPNE)
+        cm = _colmax(at) if _gram_engine(m, n, False, None) == "ozaki" else None
+        gram_auto = _gram(DMat(at, None, "torch", cm))
         chk = (C.c_double * 2)()
         wp, wn = WORKSPACE.get(256)
         call("sk_gram_check", gram_auto.data_ptr(), n, chk, wp, wn, stream_handle())
         if chk[0] > 0:
             ad = as_dmat(at)          # raises ValueError on non-finite A, like _as_matrix
         else:
-            ad = DMat(at, float(chk[1]), "torch")
+            ad = DMat(at, float(chk[1]), "torch", cm)
     else:
         ad, bd = _check_system(a, b)
     t0 = time.perf_counter()
