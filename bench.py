@@ -135,6 +135,49 @@ def hbm_peak():
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
+def _peak_file(name, key, fallback, why):
+    try:
+        with open(os.path.join(HERE, "profiles", name)) as fh:
+            d = json.load(fh)
+        return float(d[key]), d.get("source", name)
+    except Exception:  # noqa: BLE001
+        return fallback, why
+
+
+def int8_peak():
+    return _peak_file("int8_peak.json", "int8_tops", 3100.0, "fallback: cuBLASLt INT8 on B200 (not measured)")
+
+
+def fp16_peak():
+    return _peak_file("fp64_peak.json", "fp16_tflops_burst", 1546.0, "fallback: cuBLAS fp16 on B200 (not measured)")
+
+
+OZ_MODULI = 16          # csrc/ozaki.cu NMOD
+OZ_RESIDUE_BYTES = 24   # per element and operand: 8 read + 16 written
+
+
+def engine_roofline(m, n, d, method, auto, ozaki):
+    """Roofline of the implemented solve, engine by engine (ms):
+    TRSM on FP64 DMMA; the kappa0 SYRK and the PNE/HPNE Gram on the INT8 tensor
+    cores (16 exact modular products, symmetric half for SYRKs) plus their residue
+    and column-scan HBM passes; the binary16 sketch on the fp16 tensor cores (or one
+    read of A if that is slower); the residual pass on HBM."""
+    p64, p8, p16, hbm = fp64_peak()[0] * 1e12, int8_peak()[0] * 1e12, fp16_peak()[0] * 1e12, hbm_peak()[0] * 1e9
+    el = float(m) * n
+    t = {"trsm": el * n / p64, "report": 8 * el / hbm,
+         "sketch": max(2.0 * d * el / p16, 10 * el / hbm)}
+
+    def gram(syrk):
+        if not ozaki:
+            return (1.0 if syrk else 2.0) * el * n / p64
+        ops = 2.0 * OZ_MODULI * el * n * (0.5 if syrk else 1.0)
+        return ops / p8 + (1 if syrk else 2) * (OZ_RESIDUE_BYTES + 8) * el / hbm
+    if auto:
+        t["kappa0"] = gram(True)
+    t["gram"] = gram(method != "hpne")
+    return t
+
+
 def ncu_traffic(kernel_key):
     try:
         with open(os.path.join(HERE, "profiles", "ncu_traffic.json")) as fh:
@@ -294,9 +337,20 @@ def run_ours(args, rank, world):
                "rel_error": rep.relative_error, "relative_residual": rep.relative_residual}
 
     # roofline of the dominant stage (CUDA events around the stage, same stream)
+    from paper_2603_16644_b200.dense import _gram_engine
+    ozaki = _gram_engine(m, n, False, None) == "ozaki"
+    if ozaki and "check" in stages and args.precision == "auto":
+        stages["kappa0"] = stages.get("kappa0", 0.0) + stages.pop("check")   # the kappa0 SYRK runs in "check"
     dom = max((k for k in stages if stage_work(k, m, n, d, args.method, level)), key=lambda k: stages[k])
     flops, bytes_, bound = stage_work(dom, m, n, d, args.method, level)
-    if bound == "tensor":
+    if bound == "tensor" and ozaki and dom in ("gram", "kappa0"):
+        peak, src = int8_peak()
+        ops = OZ_MODULI * flops        # 16 exact INT8 products of the FP64 SYRK / GEMM
+        achieved = ops / (stages[dom] * 1e-3) / 1e12
+        roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOP/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(dom), "peak_source": src,
+                "algorithmic_ops": ops, "pipe": "INT8 tcgen05 kind::i8 (16-modulus Ozaki-II FP64 emulation)"}
+    elif bound == "tensor":
         peak, src = fp64_peak()
         achieved = flops / (stages[dom] * 1e-3) / 1e12
         roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -319,7 +373,9 @@ def run_ours(args, rank, world):
             per_stage[k] = {"ms": v}
     fp64_total = (m * n * n if args.precision == "auto" else 0) + m * n * n + \
         (2.0 if args.method == "hpne" else 1.0) * m * n * n
-    t_roof = fp64_total / (fp64_peak()[0] * 1e12) + 2 * 8.0 * m * n / (hbm_peak()[0] * 1e9)
+    t_roof_fp64 = fp64_total / (fp64_peak()[0] * 1e12) + 2 * 8.0 * m * n / (hbm_peak()[0] * 1e9)
+    eng = engine_roofline(m, n, d, args.method, args.precision == "auto", ozaki)
+    t_roof = sum(eng.values())
 
     # ---- e2e: host buffers, H2D + D2H inside the timed region ----
     e2e = None
@@ -365,8 +421,15 @@ def run_ours(args, rank, world):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (GPU Algorithm-2 generator, probgen.py)",
             "config": workload_config(args), **summary,
-            "roofline": roof, "roofline_solve": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
-                                                 "model": "FP64 flops / measured DGEMM peak + 2 reads of A / HBM"},
+            "roofline": roof,
+            "roofline_solve": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
+                               "stages_roof_ms": {k: v * 1e3 for k, v in eng.items()},
+                               "model": ("per engine: TRSM m n^2 / FP64 DMMA peak; kappa0 SYRK + Gram as 16 INT8 "
+                                         "products / measured INT8 peak + residue/column passes / HBM"
+                                         if ozaki else "FP64 flops / measured DGEMM peak") +
+                                        "; sketch 2dmn / fp16 peak; residual 8mn / HBM",
+                               "t_roof_fp64_only_ms": t_roof_fp64 * 1e3,
+                               "frac_vs_fp64_only": t_roof_fp64 * 1e3 / ms},
             "stages_ms": per_stage, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
             "gpu_launches_per_step": launches / args.steps, "clocks": clk}
     print(json.dumps(line), flush=True)
