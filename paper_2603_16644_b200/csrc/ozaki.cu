@@ -22,6 +22,8 @@
 // 2^-t (2^e_i sum_k |Y_kj| + 2^f_j sum_k |X_ki|) / 2 (+ the final rounding), with t
 // = 51 at m = 4M rows: the FP64 GEMM bound is gamma_K sum_k |X_ki||Y_kj|.  The
 // SYRK path computes lower tiles only; C' is exactly symmetric, so G is too.
+#include <vector>
+
 #include "tc.cuh"
 
 namespace sk {
@@ -118,7 +120,10 @@ __device__ __forceinline__ uint32_t residue_byte(float h0, float h1, float h2, f
 // walked grid-stride; a block covers 256 column groups (one row of n = 2048, or
 // several rows of narrower matrices), so no 64-bit division per item.
 constexpr int RV = 8;
-__global__ void __launch_bounds__(256, 4)
+#ifndef SK_OZ_RES_MINB
+#define SK_OZ_RES_MINB 4   // <= 64 registers, no spills
+#endif
+__global__ void __launch_bounds__(256, SK_OZ_RES_MINB)
 residues_kernel(const double *__restrict__ x, int64_t ldx, int64_t rows, int n, const double *__restrict__ scale,
                 int8_t *__restrict__ out, int64_t ldr, int64_t plane, int vec) {
     const int cpr = (n + RV - 1) / RV;
@@ -472,8 +477,8 @@ size_t align_up256(size_t b) { return (b + 255) & ~size_t(255); }
 // per (host thread, device) side stream + events of the residue/GEMM pipeline
 struct SidePipe {
     bool ok = false;
-    cudaStream_t side = nullptr;
-    cudaEvent_t start = nullptr, res_done[2] = {nullptr, nullptr}, gemm_done[2] = {nullptr, nullptr};
+    cudaStream_t side = nullptr, hi = nullptr;   // residues (lowest priority), GEMMs (highest)
+    cudaEvent_t start = nullptr, end = nullptr, res_done[2] = {nullptr, nullptr}, gemm_done[2] = {nullptr, nullptr};
 };
 
 SidePipe &side_pipe() {
@@ -482,8 +487,12 @@ SidePipe &side_pipe() {
     cudaGetDevice(&dev);
     SidePipe &sp = pipes[dev & 63];
     if (!sp.ok) {
-        bool ok = cudaStreamCreateWithFlags(&sp.side, cudaStreamNonBlocking) == cudaSuccess;
+        int least = 0, greatest = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        bool ok = cudaStreamCreateWithPriority(&sp.side, cudaStreamNonBlocking, least) == cudaSuccess;
+        ok = ok && cudaStreamCreateWithPriority(&sp.hi, cudaStreamNonBlocking, greatest) == cudaSuccess;
         ok = ok && cudaEventCreateWithFlags(&sp.start, cudaEventDisableTiming) == cudaSuccess;
+        ok = ok && cudaEventCreateWithFlags(&sp.end, cudaEventDisableTiming) == cudaSuccess;
         for (int i = 0; i < 2; ++i) {
             ok = ok && cudaEventCreateWithFlags(&sp.res_done[i], cudaEventDisableTiming) == cudaSuccess;
             ok = ok && cudaEventCreateWithFlags(&sp.gemm_done[i], cudaEventDisableTiming) == cudaSuccess;
@@ -588,8 +597,25 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
         set_error("sk_gram_ozaki_f64: side stream unavailable");
         return SK_ERR_CUDA;
     }
-    SK_CUDA(cudaEventRecord(sp.start, st));
-    SK_CUDA(cudaStreamWaitEvent(sp.side, sp.start, 0));
+    // Default: one stream.  SK_OZ_PIPELINE=1 runs residues (lowest priority) beside the
+    // GEMMs (highest priority); measured no faster at config 3 (a GEMM CTA leaves room
+    // for one or two residue blocks per SM, and both then compete for HBM and power).
+    static const bool serial = getenv("SK_OZ_PIPELINE") == nullptr || getenv("SK_OZ_PROFILE") != nullptr;
+    static const bool prof = getenv("SK_OZ_PROFILE") != nullptr;   // phase timing to stderr (serial mode)
+    cudaStream_t rs = serial ? st : sp.side;   // residues: lowest priority
+    cudaStream_t gs = serial ? st : sp.hi;     // GEMMs + reconstruction: highest priority
+    std::vector<cudaEvent_t> pe;
+    int npe = 0;
+    if (prof) {
+        pe.resize(2 * (size_t)((m + p.chunk - 1) / p.chunk) + 4);
+        for (auto &e : pe) cudaEventCreate(&e);
+        SK_CUDA(cudaEventRecord(pe[npe++], st));   // NB: recorded after colmax (launched above)
+    }
+    if (!serial) {
+        SK_CUDA(cudaEventRecord(sp.start, st));
+        SK_CUDA(cudaStreamWaitEvent(sp.side, sp.start, 0));
+        SK_CUDA(cudaStreamWaitEvent(sp.hi, sp.start, 0));
+    }
     int chunk_idx = 0;
     for (int64_t r0 = 0; r0 < m; r0 += p.chunk, ++chunk_idx) {
         const int buf = chunk_idx & 1;
@@ -599,17 +625,20 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
         const int cpr = (int)((n + oz::RV - 1) / oz::RV);
         const int rpi = cpr >= 256 ? 1 : 256 / cpr;
         const unsigned rgrid = (unsigned)std::min<int64_t>((rows + rpi - 1) / rpi, (int64_t)sms * 16);
-        if (chunk_idx >= 2) SK_CUDA(cudaStreamWaitEvent(sp.side, sp.gemm_done[buf], 0));
-        oz::residues_kernel<<<rgrid, 256, 0, sp.side>>>(x + r0 * ldx, ldx, rows, (int)n, scale, res_x, p.ldr, plane,
-                                                        vx);
+        if (prof) SK_CUDA(cudaEventRecord(pe[npe++], st));
+        if (!serial && chunk_idx >= 2) SK_CUDA(cudaStreamWaitEvent(sp.side, sp.gemm_done[buf], 0));
+        oz::residues_kernel<<<rgrid, 256, 0, rs>>>(x + r0 * ldx, ldx, rows, (int)n, scale, res_x, p.ldr, plane, vx);
         SK_LAUNCH_CHECK("oz residues");
         if (!syrk) {
-            oz::residues_kernel<<<rgrid, 256, 0, sp.side>>>(y + r0 * ldy, ldy, rows, (int)n, scale + n, res_y,
-                                                            p.ldr, plane, vy);
+            oz::residues_kernel<<<rgrid, 256, 0, rs>>>(y + r0 * ldy, ldy, rows, (int)n, scale + n, res_y, p.ldr,
+                                                       plane, vy);
             SK_LAUNCH_CHECK("oz residues");
         }
-        SK_CUDA(cudaEventRecord(sp.res_done[buf], sp.side));
-        SK_CUDA(cudaStreamWaitEvent(st, sp.res_done[buf], 0));
+        if (!serial) {
+            SK_CUDA(cudaEventRecord(sp.res_done[buf], sp.side));
+            SK_CUDA(cudaStreamWaitEvent(sp.hi, sp.res_done[buf], 0));
+        }
+        if (prof) SK_CUDA(cudaEventRecord(pe[npe++], st));
         CUtensorMap tx, ty;
         int rc = make_tmap_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, res_x, (uint64_t)n, (uint64_t)rows, oz::NMOD,
                               (uint64_t)p.ldr, (uint64_t)plane, 128, oz::BK, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -627,13 +656,34 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
         gp.kchunk = p.kchunk;
         gp.acc = acc;
         gp.n = (int)n;
-        oz::gemm_kernel<<<std::min(gp.units, sms), oz::THREADS, oz::SMEM, st>>>(tx, ty, gp);
+        oz::gemm_kernel<<<std::min(gp.units, sms), oz::THREADS, oz::SMEM, gs>>>(tx, ty, gp);
         SK_LAUNCH_CHECK("oz gemm");
-        SK_CUDA(cudaEventRecord(sp.gemm_done[buf], st));
+        if (!serial) SK_CUDA(cudaEventRecord(sp.gemm_done[buf], gs));
     }
     const int64_t nn = n * n;
-    oz::crt_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(acc, (int)n, syrk, expo, expo + n, p.t, g, ldg);
+    if (prof) SK_CUDA(cudaEventRecord(pe[npe++], st));
+    oz::crt_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, gs>>>(acc, (int)n, syrk, expo, expo + n, p.t, g, ldg);
     SK_LAUNCH_CHECK("oz crt");
+    if (!serial) {   // the caller's stream resumes after the reconstruction
+        SK_CUDA(cudaEventRecord(sp.end, sp.hi));
+        SK_CUDA(cudaStreamWaitEvent(st, sp.end, 0));
+    }
+    if (prof) {
+        SK_CUDA(cudaEventRecord(pe[npe++], st));
+        SK_CUDA(cudaEventSynchronize(pe[npe - 1]));
+        float tot = 0, res_ms = 0, gemm_ms = 0, pre_ms = 0, t;
+        cudaEventElapsedTime(&pre_ms, pe[0], pe[1]);
+        for (int i = 1; i + 2 < npe; i += 2) {
+            cudaEventElapsedTime(&t, pe[i], pe[i + 1]);
+            res_ms += t;
+            cudaEventElapsedTime(&t, pe[i + 1], pe[i + 2]);
+            gemm_ms += t;
+        }
+        cudaEventElapsedTime(&tot, pe[0], pe[npe - 1]);
+        fprintf(stderr, "ozaki %s m=%lld: total %.2f ms, colmax+scales %.2f, residues %.2f, gemm %.2f, other %.2f\n",
+                syrk ? "syrk" : "gemm", (long long)m, tot, pre_ms, res_ms, gemm_ms, tot - pre_ms - res_ms - gemm_ms);
+        for (int i = 0; i < npe; ++i) cudaEventDestroy(pe[i]);
+    }
     return SK_OK;
 }
 
