@@ -116,6 +116,30 @@ __device__ __forceinline__ uint32_t residue_byte(float h0, float h1, float h2, f
     return __float_as_uint(r + FMAGIC);     // low byte = r as a two's-complement int8
 }
 
+// The same for two elements at once on the packed FP32x2 pipe (FFMA2 / FADD2, sm_100).
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+    return (uint64_t)__float_as_uint(a) | ((uint64_t)__float_as_uint(b) << 32);
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// returns the two residue bytes in bits 0-7 and 32-39
+__device__ __forceinline__ uint64_t residue_pair(uint64_t h0, uint64_t h1, uint64_t h2, uint64_t h3, int k) {
+    const float c1 = (float)centred_pow2_mod(13, k), c2 = (float)centred_pow2_mod(26, k),
+                c3 = (float)centred_pow2_mod(39, k), p = (float)pm(k), ip = 1.0f / (float)pm(k);
+    const uint64_t v = ffma2(h3, f2pack(c3, c3), ffma2(h2, f2pack(c2, c2), ffma2(h1, f2pack(c1, c1), h0)));
+    const uint64_t q = fadd2(ffma2(v, f2pack(ip, ip), f2pack(FMAGIC, FMAGIC)), f2pack(-FMAGIC, -FMAGIC));
+    const uint64_t r = ffma2(q, f2pack(-p, -p), v);
+    return fadd2(r, f2pack(FMAGIC, FMAGIC));
+}
+
 // 8 consecutive columns of one row per thread -> 16 planes of 8 bytes.  Rows are
 // walked grid-stride; a block covers 256 column groups (one row of n = 2048, or
 // several rows of narrower matrices), so no 64-bit division per item.
@@ -165,6 +189,14 @@ residues_kernel(const double *__restrict__ x, int64_t ldx, int64_t rows, int n, 
                 h0[q] = (float)fma(-a1, 0x1p13, r2);
             }
             int8_t *dst = out + r * ldr + c0;
+            uint64_t p0[RV / 2], p1[RV / 2], p2[RV / 2], p3[RV / 2];
+#pragma unroll
+            for (int q = 0; q < RV / 2; ++q) {
+                p0[q] = f2pack(h0[2 * q], h0[2 * q + 1]);
+                p1[q] = f2pack(h1[2 * q], h1[2 * q + 1]);
+                p2[q] = f2pack(h2[2 * q], h2[2 * q + 1]);
+                p3[q] = f2pack(h3[2 * q], h3[2 * q + 1]);
+            }
 #pragma unroll
             for (int k = 0; k < NMOD; ++k) {
                 uint32_t w[2];
@@ -172,9 +204,11 @@ residues_kernel(const double *__restrict__ x, int64_t ldx, int64_t rows, int n, 
                 for (int q4 = 0; q4 < 2; ++q4) {
                     uint32_t b[4];
 #pragma unroll
-                    for (int bb = 0; bb < 4; ++bb) {
-                        const int q = 4 * q4 + bb;
-                        b[bb] = residue_byte(h0[q], h1[q], h2[q], h3[q], k);
+                    for (int bb = 0; bb < 2; ++bb) {
+                        const int q2 = 2 * q4 + bb;
+                        const uint64_t rr = residue_pair(p0[q2], p1[q2], p2[q2], p3[q2], k);
+                        b[2 * bb] = (uint32_t)rr;
+                        b[2 * bb + 1] = (uint32_t)(rr >> 32);
                     }
                     w[q4] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
                 }
