@@ -116,14 +116,22 @@ int sk_gram_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int6
 size_t sk_gram_ozaki_workspace(int64_t m, int64_t n, int syrk);
 int sk_gram_ozaki_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
                       double *g, int64_t ldg, void *ws, size_t ws_bytes, sk_stream_t stream);
-/* Same with the column maxima max_k |X[k,i]| / |Y[k,j]| supplied (device, n doubles,
- * from sk_colmax_f64 of the same matrix; NULL = computed here), so a matrix used by
- * two Grams (A in the kappa0 SYRK and the HPNE product) is scanned once. */
+/* Same with the column statistics supplied (device, 2n doubles each, from
+ * sk_colstats_f64 of the same matrix; NULL = computed here), so a matrix used by two
+ * Grams (A in the kappa0 SYRK and the HPNE product) is scanned once.
+ * Guard: if any column has max|x| sqrt(m) > 64 ||x||_2 (a spiky column, where the
+ * scaled-integer error bound would exceed an FP64 GEMM's) or a non-finite entry, the
+ * product runs on the FP64 DMMA path instead (sk_gram_ozaki_fell_back() == 1). */
 int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
-                         const double *xmax, const double *ymax, double *g, int64_t ldg, void *ws,
+                         const double *xstats, const double *ystats, double *g, int64_t ldg, void *ws,
                          size_t ws_bytes, sk_stream_t stream);
-/* colmax[j] = max_k |X[k,j]| (device, n doubles). */
-int sk_colmax_f64(const double *x, int64_t ldx, int64_t m, int64_t n, double *colmax, sk_stream_t stream);
+/* 1 if the last sk_gram_ozaki_* call on this host thread took the FP64 fallback. */
+int sk_gram_ozaki_fell_back(void);
+/* stats[j] = max_k |X[k,j]|, stats[n + j] = sum_k X[k,j]^2 (device, fixed-order and
+ * deterministic; a non-finite column gives max = +inf). */
+size_t sk_colstats_workspace(int64_t n);
+int sk_colstats_f64(const double *x, int64_t ldx, int64_t m, int64_t n, double *stats, void *ws, size_t ws_bytes,
+                    sk_stream_t stream);
 
 /* out (n) = X^T v (X m x n row-major): `a_p.T @ b` src/solvers.py:231/251. */
 size_t sk_gemv_t_workspace(int64_t m, int64_t n);

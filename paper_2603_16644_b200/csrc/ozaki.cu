@@ -22,6 +22,8 @@
 // 2^-t (2^e_i sum_k |Y_kj| + 2^f_j sum_k |X_ki|) / 2 (+ the final rounding), with t
 // = 51 at m = 4M rows: the FP64 GEMM bound is gamma_K sum_k |X_ki||Y_kj|.  The
 // SYRK path computes lower tiles only; C' is exactly symmetric, so G is too.
+#include <math_constants.h>
+
 #include <vector>
 
 #include "tc.cuh"
@@ -65,21 +67,76 @@ constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
 constexpr int64_t KSPLIT_MAX = 131072;                       // int32-exact accumulation length
 
 // ---------------------------------------------------------- column scales ---
-// colmax bits (non-negative doubles order like their bit patterns) -> atomicMax
-__global__ void __launch_bounds__(256) colmax_kernel(const double *__restrict__ x, int64_t ldx, int64_t m, int n,
-                                                     unsigned long long *__restrict__ out) {
+// Column statistics in one pass, deterministic: a fixed grid of STAT_BLOCKS row
+// blocks writes per-block (max |x|, sum x^2) partials, reduced in block order.
+// max feeds the scales; max^2 m / sum x^2 is the guard (below).  fmax propagates a NaN
+// only from its second operand, so non-finite entries are kept sticky explicitly.
+constexpr int STAT_BLOCKS = 512;
+__global__ void __launch_bounds__(256) colstats_kernel(const double *__restrict__ x, int64_t ldx, int64_t m, int n,
+                                                       double *__restrict__ part) {
     const int c = blockIdx.y * 256 + threadIdx.x;
     if (c >= n) return;
-    double mx = 0.0;
+    double mx = 0.0, ss = 0.0;
     const int64_t g = gridDim.x;
     int64_t r = blockIdx.x;
     for (; r + 3 * g < m; r += 4 * g) {   // four independent loads in flight
         const double a0 = x[r * ldx + c], a1 = x[(r + g) * ldx + c], a2 = x[(r + 2 * g) * ldx + c],
                      a3 = x[(r + 3 * g) * ldx + c];
         mx = fmax(fmax(mx, fmax(fabs(a0), fabs(a1))), fmax(fabs(a2), fabs(a3)));
+        ss += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+        if (!isfinite(a0) || !isfinite(a1) || !isfinite(a2) || !isfinite(a3)) mx = CUDART_INF;
     }
-    for (; r < m; r += g) mx = fmax(mx, fabs(x[r * ldx + c]));
-    atomicMax(out + c, (unsigned long long)__double_as_longlong(mx));
+    for (; r < m; r += g) {
+        const double a = x[r * ldx + c];
+        mx = isfinite(a) ? fmax(mx, fabs(a)) : CUDART_INF;
+        ss += a * a;
+    }
+    part[(size_t)blockIdx.x * n + c] = mx;
+    part[((size_t)STAT_BLOCKS + blockIdx.x) * n + c] = ss;
+}
+
+__global__ void colstats_finalize(const double *__restrict__ part, int nblk, int n, double *__restrict__ stats) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    double mx = 0.0, ss = 0.0;
+    for (int b = 0; b < nblk; ++b) {
+        const double v = part[(size_t)b * n + c];
+        mx = (isfinite(v) && isfinite(mx)) ? fmax(mx, v) : CUDART_INF;
+        ss += part[((size_t)STAT_BLOCKS + b) * n + c];
+    }
+    stats[c] = mx;
+    stats[n + c] = ss;
+}
+
+// max bits of the scales input (non-negative doubles order like their bit patterns)
+__global__ void stats_to_bits(const double *__restrict__ stats, int n, unsigned long long *__restrict__ bits) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < n) bits[c] = (unsigned long long)__double_as_longlong(stats[c]);
+}
+
+// Guard: the INT8 product's error bound 2^(1-t) (2^e_i sum|Y_j| + 2^f_j sum|X_i|) is
+// within a factor 2 F of 2^-t ||X_i|| ||Y_j|| when max|X_i| sqrt(m) <= F ||X_i|| (sum|x|
+// <= sqrt(m) ||x||, 2^e <= 2 max).  F = 64: at t = 51 the bound is 2^-43 ||X_i|| ||Y_j||,
+// the size of an FP64 GEMM's typical error.  Columns spikier than that, or non-finite
+// input, take the FP64 DMMA path.
+constexpr double GUARD_F2 = 64.0 * 64.0;
+__global__ void guard_kernel(const double *__restrict__ sx, const double *__restrict__ sy, int n, int64_t m,
+                             int *flag) {
+    __shared__ int bad;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    int b = 0;
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        const double *s[2] = {sx, sy};
+        for (int o = 0; o < 2; ++o) {
+            const double mx = s[o][c], ss = s[o][n + c];
+            if (!isfinite(mx) || !isfinite(ss)) b = 1;
+            else if (mx > 0.0 && mx * mx * (double)m > GUARD_F2 * ss) b = 1;
+        }
+    }
+    if (b) atomicOr(&bad, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) *reinterpret_cast<volatile int *>(flag) = bad;
 }
 
 // e = exponent with max < 2^e; scale = 2^(t - e) (inputs), out_exp for the product
@@ -502,7 +559,8 @@ Plan make_plan(int64_t m, int64_t n, bool syrk) {
     p.res_bytes = (size_t)2 * ops * NMOD * p.chunk * p.ldr;   // double-buffered chunks
     p.part_bytes = 0;   // the GEMM epilogue accumulates modulo p straight into acc
     p.acc_bytes = (size_t)NMOD * n * n * sizeof(int32_t);
-    p.aux_bytes = (size_t)4 * n * 8 + 4096;
+    // bits / scales / exponents (6n words), column stats of X and Y (4n), stats partials
+    p.aux_bytes = (size_t)(10 * n + 2 * STAT_BLOCKS * n) * 8 + 8192;
     return p;
 }
 
@@ -549,19 +607,42 @@ size_t sk_gram_ozaki_workspace(int64_t m, int64_t n, int syrk) {
            oz::align_up256(p.aux_bytes) + 1024;
 }
 
-int sk_colmax_f64(const double *x, int64_t ldx, int64_t m, int64_t n, double *colmax, sk_stream_t stream) {
-    if (!x || !colmax || m < 0 || n <= 0 || ldx < n) {
-        set_error("sk_colmax_f64: bad arguments");
+size_t sk_colstats_workspace(int64_t n) { return (size_t)2 * oz::STAT_BLOCKS * n * sizeof(double) + 256; }
+
+int sk_colstats_f64(const double *x, int64_t ldx, int64_t m, int64_t n, double *stats, void *ws, size_t ws_bytes,
+                    sk_stream_t stream) {
+    if (!x || !stats || m < 0 || n <= 0 || ldx < n || !ws || ws_bytes < sk_colstats_workspace(n)) {
+        set_error("sk_colstats_f64: bad arguments or workspace");
         return SK_ERR_ARG;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    SK_CUDA(cudaMemsetAsync(colmax, 0, (size_t)n * sizeof(double), st));
-    if (m == 0) return SK_OK;
-    const dim3 cg((unsigned)std::min<int64_t>(m, (int64_t)sm_count() * 4), (unsigned)((n + 255) / 256));
-    oz::colmax_kernel<<<cg, 256, 0, st>>>(x, ldx, m, (int)n, reinterpret_cast<unsigned long long *>(colmax));
-    SK_LAUNCH_CHECK("oz colmax");
+    if (m == 0) {
+        SK_CUDA(cudaMemsetAsync(stats, 0, (size_t)2 * n * sizeof(double), st));
+        return SK_OK;
+    }
+    const int nblk = (int)std::min<int64_t>(m, oz::STAT_BLOCKS);
+    double *part = static_cast<double *>(ws);
+    oz::colstats_kernel<<<dim3((unsigned)nblk, (unsigned)((n + 255) / 256)), 256, 0, st>>>(x, ldx, m, (int)n, part);
+    SK_LAUNCH_CHECK("oz colstats");
+    oz::colstats_finalize<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nblk, (int)n, stats);
+    SK_LAUNCH_CHECK("oz colstats finalize");
     return SK_OK;
 }
+
+namespace {
+thread_local int g_oz_fell_back = 0;
+int *guard_slot() {
+    thread_local int *slot = nullptr;
+    if (!slot) {
+        void *p = nullptr;
+        if (cudaHostAlloc(&p, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return nullptr;
+        slot = static_cast<int *>(p);
+    }
+    return slot;
+}
+}  // namespace
+
+int sk_gram_ozaki_fell_back(void) { return g_oz_fell_back; }
 
 int sk_gram_ozaki_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n, double *g,
                       int64_t ldg, void *ws, size_t ws_bytes, sk_stream_t stream) {
@@ -569,8 +650,8 @@ int sk_gram_ozaki_f64(const double *x, int64_t ldx, const double *y, int64_t ldy
 }
 
 int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
-                         const double *xmax, const double *ymax, double *g, int64_t ldg, void *ws, size_t ws_bytes,
-                         sk_stream_t stream) {
+                         const double *xstats, const double *ystats, double *g, int64_t ldg, void *ws,
+                         size_t ws_bytes, sk_stream_t stream) {
     if (!x || !y || !g || m < 0 || n <= 0 || ldx < n || ldy < n || ldg < n || n > 65536) {
         set_error("sk_gram_ozaki_f64: bad arguments");
         return SK_ERR_ARG;
@@ -590,32 +671,48 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
     w += oz::align_up256(p.acc_bytes);
     unsigned long long *bits = reinterpret_cast<unsigned long long *>(w);   // 2n
     double *scale = reinterpret_cast<double *>(bits + 2 * n);                // 2n
-    int *expo = reinterpret_cast<int *>(scale + 2 * n);                      // 2n
+    int *expo = reinterpret_cast<int *>(scale + 2 * n);                      // 2n (+ pad)
+    double *stats = reinterpret_cast<double *>(w + oz::align_up256((size_t)6 * n * 8));   // 4n: x, y
+    void *stat_ws = w + oz::align_up256((size_t)10 * n * 8);
 
-    SK_CUDA(cudaMemsetAsync(bits, 0, (size_t)2 * n * sizeof(unsigned long long), st));
-    SK_CUDA(cudaMemsetAsync(acc, 0, p.acc_bytes, st));
+    g_oz_fell_back = 0;
     const int sms = sm_count();
-    const dim3 cg((unsigned)std::min<int64_t>(std::max<int64_t>(m, 1), (int64_t)sms * 4), (unsigned)((n + 255) / 256));
-    if (m > 0) {
-        // column maxima: given by the caller (sk_colmax_f64 of the same matrix) or a pass here
-        if (xmax) {
-            SK_CUDA(cudaMemcpyAsync(bits, xmax, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-        } else {
-            oz::colmax_kernel<<<cg, 256, 0, st>>>(x, ldx, m, (int)n, bits);
-            SK_LAUNCH_CHECK("oz colmax");
-        }
-        if (!syrk) {
-            if (ymax) {
-                SK_CUDA(cudaMemcpyAsync(bits + n, ymax, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-            } else {
-                oz::colmax_kernel<<<cg, 256, 0, st>>>(y, ldy, m, (int)n, bits + n);
-                SK_LAUNCH_CHECK("oz colmax");
-            }
-        }
-    }
     const unsigned sgrid = (unsigned)((n + 255) / 256);
+    // column statistics: given by the caller (sk_colstats_f64 of the same matrix) or a pass here
+    const double *sx = xstats, *sy = syrk ? xstats : ystats;
+    if (!sx) {
+        int rc = sk_colstats_f64(x, ldx, m, n, stats, stat_ws, sk_colstats_workspace(n), stream);
+        if (rc) return rc;
+        sx = stats;
+        if (syrk) sy = stats;
+    }
+    if (!sy) {
+        int rc = sk_colstats_f64(y, ldy, m, n, stats + 2 * n, stat_ws, sk_colstats_workspace(n), stream);
+        if (rc) return rc;
+        sy = stats + 2 * n;
+    }
+    int *flag = guard_slot();
+    if (!flag) {
+        set_error("sk_gram_ozaki_f64: pinned guard slot unavailable");
+        return SK_ERR_CUDA;
+    }
+    oz::guard_kernel<<<1, 1024, 0, st>>>(sx, sy, (int)n, m, flag);
+    SK_LAUNCH_CHECK("oz guard");
+    SK_CUDA(cudaStreamSynchronize(st));
+    if (*reinterpret_cast<volatile int *>(flag)) {
+        // spiky columns or non-finite input: the FP64 DMMA Gram (same workspace)
+        g_oz_fell_back = 1;
+        if (ws_bytes < sk_gram_workspace(m, n)) {
+            set_error("sk_gram_ozaki_f64: workspace too small for the DMMA fallback");
+            return SK_ERR_ARG;
+        }
+        return sk_gram_f64(x, ldx, y, ldy, m, n, g, ldg, 0, ws, ws_bytes, stream);
+    }
+    oz::stats_to_bits<<<sgrid, 256, 0, st>>>(sx, (int)n, bits);
+    oz::stats_to_bits<<<sgrid, 256, 0, st>>>(sy, (int)n, bits + n);
+    SK_CUDA(cudaMemsetAsync(acc, 0, p.acc_bytes, st));
     oz::scales_kernel<<<sgrid, 256, 0, st>>>(bits, (int)n, p.t, scale, expo);
-    oz::scales_kernel<<<sgrid, 256, 0, st>>>(syrk ? bits : bits + n, (int)n, p.t, scale + n, expo + n);
+    oz::scales_kernel<<<sgrid, 256, 0, st>>>(bits + n, (int)n, p.t, scale + n, expo + n);
     SK_LAUNCH_CHECK("oz scales");
 
     const int vx = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ldx % 2 == 0);

@@ -59,12 +59,14 @@ def _gram_engine(m: int, n: int, accumulate: bool, engine: str | None) -> str:
     return e
 
 
-def _colmax(t: torch.Tensor) -> torch.Tensor:
-    """max_k |T[k, j]| per column (device, f64)."""
+def _colstats(t: torch.Tensor) -> torch.Tensor:
+    """[max_k |T[k, j]| for j] + [sum_k T[k, j]^2 for j] (device, f64, 2n)."""
     t = _rm(t)
     m, n = t.shape
-    out = torch.empty(n, dtype=torch.float64, device=t.device)
-    call("sk_colmax_f64", t.data_ptr(), t.stride(0), m, n, out.data_ptr(), stream_handle())
+    out = torch.empty(2 * n, dtype=torch.float64, device=t.device)
+    lib = _lib.lib()
+    wp, wn = WORKSPACE.get(lib.sk_colstats_workspace(n))
+    call("sk_colstats_f64", t.data_ptr(), t.stride(0), m, n, out.data_ptr(), wp, wn, stream_handle())
     return out
 
 
@@ -72,7 +74,8 @@ def _gram(x: DMat | torch.Tensor, y: DMat | torch.Tensor | None = None, out: tor
           accumulate: bool = False, engine: str | None = None) -> torch.Tensor:
     """G = X^T Y (SYRK when y is None or y is x): FP64 DMMA, or the INT8 tensor-core
     Ozaki engine (sk_gram_ozaki_ex_f64) for large products.  A DMat operand whose
-    `colmax` is set (the pipeline scans A once) passes its column maxima along."""
+    `colstats` is set (the pipeline scans A once) passes its column statistics along.
+    The INT8 engine falls back to DMMA by itself on spiky or non-finite columns."""
     xt = _rm(x.t if isinstance(x, DMat) else x)
     yt = xt if y is None else _rm(y.t if isinstance(y, DMat) else y)
     m, n = xt.shape
@@ -83,8 +86,8 @@ def _gram(x: DMat | torch.Tensor, y: DMat | torch.Tensor | None = None, out: tor
     lib = _lib.lib()
     if _gram_engine(m, n, accumulate, engine) == "ozaki":
         syrk = xt.data_ptr() == yt.data_ptr() and xt.stride(0) == yt.stride(0)
-        xmax = x.colmax if isinstance(x, DMat) else None
-        ymax = (y.colmax if isinstance(y, DMat) else None) if y is not None else xmax
+        xmax = x.colstats if isinstance(x, DMat) else None
+        ymax = (y.colstats if isinstance(y, DMat) else None) if y is not None else xmax
         wp, wn = WORKSPACE.get(lib.sk_gram_ozaki_workspace(m, n, int(syrk)))
         call("sk_gram_ozaki_ex_f64", xt.data_ptr(), xt.stride(0), yt.data_ptr(), yt.stride(0), m, n,
              xmax.data_ptr() if xmax is not None else None, ymax.data_ptr() if ymax is not None else None,

@@ -82,7 +82,7 @@ class DMat:
     t: torch.Tensor
     frob2: float | None = None
     kind: str = "numpy"
-    colmax: torch.Tensor | None = None   # max_k |A[k, j]|, set by the pipeline (INT8 Gram scales)
+    colstats: torch.Tensor | None = None   # column max|A| and sum A^2 (2n), set by the pipeline for the INT8 Gram
 
     @property
     def shape(self):

@@ -520,13 +520,13 @@ def algorithm1_pipeline(a, b, method="pne", precision="auto", d_factor=3.0, tran
           and a.dtype == torch.float64 and a.stride(-1) == 1 and a.shape[0] >= a.shape[1] > 0):
         # device-resident A under "auto": the kappa0 Gram reads A anyway, so it doubles
         # as the validation pass (non-finite A => non-finite G; ||A||_F^2 = trace G)
-        from .dense import _colmax, _gram_engine, _rm
+        from .dense import _colstats, _gram_engine, _rm
         at = _rm(a)
         m, n = at.shape
         bd = as_dvec(b, m)
-        # the INT8 Gram engine scales columns by max|A[:, j]|: scan A once for both of
-        # its Grams (kappa0 SYRK here, A_p^T A in HPNE)
-        cm = _colmax(at) if _gram_engine(m, n, False, None) == "ozaki" else None
+        # the INT8 Gram engine scales columns by max|A[:, j]| (and checks them against
+        # ||A[:, j]||): scan A once for both of its Grams (kappa0 SYRK, A_p^T A in HPNE)
+        cm = _colstats(at) if _gram_engine(m, n, False, None) == "ozaki" else None
         gram_auto = _gram(DMat(at, None, "torch", cm))
         chk = (C.c_double * 2)()
         wp, wn = WORKSPACE.get(256)

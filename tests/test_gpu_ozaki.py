@@ -50,14 +50,44 @@ def test_ozaki_gram_random(torch, m, n, syrk):
     _check(torch, x, y, syrk)
 
 
+def _fell_back():
+    from paper_2603_16644_b200 import _lib
+    return _lib.lib().sk_gram_ozaki_fell_back() == 1
+
+
 def test_ozaki_gram_scaled_columns_and_rows(torch):
     g = R.philox(11, 3)
     m, n = 40000, 200
     x = g.standard_normal((m, n)) * (10.0 ** g.uniform(-8, 8, n))[None, :]
-    x *= (10.0 ** g.uniform(-3, 3, m))[:, None]
     y = g.standard_normal((m, n)) * (10.0 ** g.uniform(-8, 8, n))[None, :]
-    _check(torch, x, x, True)
+    _check(torch, x, x, True)          # column scales: per-column exponents absorb them
+    assert not _fell_back()
     _check(torch, x, y, False)
+    assert not _fell_back()
+    xr = x * (10.0 ** g.uniform(-3, 3, m))[:, None]
+    _check(torch, xr, xr, True)        # rows spanning 1e6: the top decade carries the norm,
+    assert not _fell_back()            # max sqrt(m) / ||x|| ~ 15 < 64: stays on INT8, accurate
+    xs = x * np.where(np.arange(m) % 1000 == 0, 1e4, 1.0)[:, None]
+    _check(torch, xs, xs, True)        # 40 rows 1e4 above the rest: spiky -> FP64 fallback
+    assert _fell_back()
+
+
+def test_ozaki_guard_spiky_and_non_finite(torch):
+    from paper_2603_16644_b200.dense import _gram
+    g = R.philox(12, 3)
+    m, n = 20000, 130
+    x = g.standard_normal((m, n))
+    xt = torch.from_numpy(x).cuda()
+    _gram(xt, engine="ozaki")
+    assert not _fell_back()
+    x[17, 3] = 1e6                      # one outlier: max sqrt(m) >> ||x||
+    xt = torch.from_numpy(x).cuda()
+    got = _gram(xt, engine="ozaki")
+    assert _fell_back()
+    assert torch.equal(got, _gram(xt, engine="dmma"))
+    x[17, 3] = np.nan
+    got = _gram(torch.from_numpy(x).cuda(), engine="ozaki").cpu().numpy()
+    assert _fell_back() and np.isnan(got[3, 3])
 
 
 @pytest.fixture
