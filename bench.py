@@ -294,12 +294,13 @@ def run_ours(args, rank, world):
         if dist is not None:
             dist.barrier()
 
-    def solve(A, B):
+    def solve(A, B, method=None):
+        method = method or args.method
         if dist is not None:
             from paper_2603_16644_b200.distributed import algorithm1_pipeline_sharded
-            return algorithm1_pipeline_sharded(A, B, method=args.method, precision=args.precision, seed=1,
+            return algorithm1_pipeline_sharded(A, B, method=method, precision=args.precision, seed=1,
                                                x_star=x_star, diagnostics=False, stage_timing=True)
-        return sq.algorithm1_pipeline(A, B, method=args.method, precision=args.precision, seed=1, x_star=x_star,
+        return sq.algorithm1_pipeline(A, B, method=method, precision=args.precision, seed=1, x_star=x_star,
                                       diagnostics=False, stage_timing=True)
 
     lib = _lib.lib()
@@ -326,6 +327,27 @@ def run_ours(args, rank, world):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    # the metric names both solvers: time the other one on the same A, b (after the
+    # headline's timed region, same protocol: warm-up, then args.steps timed solves)
+    other = "pne" if args.method == "hpne" else "hpne"
+    solve(a, b, other)
+    torch.cuda.synchronize()
+    barrier()
+    o0 = torch.cuda.Event(enable_timing=True)
+    o1 = torch.cuda.Event(enable_timing=True)
+    o0.record()
+    oreps = [solve(a, b, other) for _ in range(args.steps)]
+    o1.record()
+    torch.cuda.synchronize()
+    barrier()
+    oms = o0.elapsed_time(o1) / args.steps
+    if dist is not None:
+        t = torch.tensor([oms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        oms = float(t.item())
+    other_line = {"method": other, "ms_per_step": oms, "rel_error": oreps[-1].relative_error,
+                  "selected_level": oreps[-1].preconditioner.computed_in.name}
+    del oreps
     rep = reps[-1]
     stages = {}
     for r in reps:
@@ -430,7 +452,8 @@ def run_ours(args, rank, world):
                                         "; sketch 2dmn / fp16 peak; residual 8mn / HBM",
                                "t_roof_fp64_only_ms": t_roof_fp64 * 1e3,
                                "frac_vs_fp64_only": t_roof_fp64 * 1e3 / ms},
-            "stages_ms": per_stage, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
+            "stages_ms": per_stage, "other_method": other_line, "e2e": e2e, "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
             "gpu_launches_per_step": launches / args.steps, "clocks": clk}
     print(json.dumps(line), flush=True)
 

@@ -129,7 +129,7 @@ __device__ __forceinline__ T warp_tree_root(int count, G get) {
 
 // Reflector for column jj given the chunk nodes of x.x in sh_nodes[0..nq), x = w[jj:, jj].
 template <typename T>
-__device__ int reflect_from_nodes(const T *x, int L, Ctl<T> *ctl, int buf, T *alphas, int jj, T *sh_nodes,
+__device__ int reflect_from_nodes(const T *x, int L, T *tau_out, T *v0_out, T *alphas, int jj, T *sh_nodes,
                                   T *sh_root) {
     using O = LevelOps<T>;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -162,8 +162,8 @@ __device__ int reflect_from_nodes(const T *x, int L, Ctl<T> *ctl, int buf, T *al
     __syncthreads();
     const int rc = sh_rc;
     if (rc == SK_OK && threadIdx.x == 0) {
-        ctl->tau[buf] = sh_tau;
-        ctl->v0[buf] = sh_v0;
+        *tau_out = sh_tau;
+        *v0_out = sh_v0;
         alphas[jj] = sh_alpha;
     }
     (void)sh_root;
@@ -172,7 +172,7 @@ __device__ int reflect_from_nodes(const T *x, int L, Ctl<T> *ctl, int buf, T *al
 }
 
 template <typename T>
-__device__ int make_reflector(const T *w, int64_t ld, int d, int jj, Ctl<T> *ctl, int buf, T *alphas, T *sh_nodes,
+__device__ int make_reflector(const T *w, int64_t ld, int d, int jj, T *tau_out, T *v0_out, T *alphas, T *sh_nodes,
                               T *sh_root) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int L = d - jj;
@@ -183,7 +183,7 @@ __device__ int make_reflector(const T *w, int64_t ld, int d, int jj, Ctl<T> *ctl
         if (lane == 0) sh_nodes[q] = node;
     }
     __syncthreads();
-    return reflect_from_nodes<T>(x, L, ctl, buf, alphas, jj, sh_nodes, sh_root);
+    return reflect_from_nodes<T>(x, L, tau_out, v0_out, alphas, jj, sh_nodes, sh_root);
 }
 
 template <typename T>
@@ -198,7 +198,7 @@ householder_kernel(T *w, int64_t ld, int d, int n, T *alphas /* n */, T *part /*
     const int nwarps = gridDim.x * WARPS;
 
     if (blockIdx.x == 0) {
-        const int rc = make_reflector<T>(w, ld, d, 0, ctl, 0, alphas, sh_nodes, &sh_root);
+        const int rc = make_reflector<T>(w, ld, d, 0, &ctl->tau[0], &ctl->v0[0], alphas, sh_nodes, &sh_root);
         if (rc != SK_OK && threadIdx.x == 0) { ctl->fail_code = rc; ctl->fail_col = 0; }
     }
     grid.sync();
@@ -249,7 +249,8 @@ householder_kernel(T *w, int64_t ld, int d, int n, T *alphas /* n */, T *part /*
                 if (lane == 0) sh_nodes[q] = node;
             }
             __syncthreads();
-            const int rc = reflect_from_nodes<T>(x, Lx, ctl, buf ^ 1, alphas, j + 1, sh_nodes, &sh_root);
+            const int rc = reflect_from_nodes<T>(x, Lx, &ctl->tau[buf ^ 1], &ctl->v0[buf ^ 1], alphas, j + 1, sh_nodes,
+                                                 &sh_root);
             if (rc != SK_OK && threadIdx.x == 0) { ctl->fail_code = rc; ctl->fail_col = j + 1; }
         } else {
             // CTA-major: CTA b >= 1 owns columns j+2+k*(G-1)+(b-1); its warps compute t_c for
@@ -288,6 +289,130 @@ householder_kernel(T *w, int64_t ld, int d, int n, T *alphas /* n */, T *part /*
     }
 }
 
+// ---------------------------------------------------------------------------
+// Dataflow variant: no grid barriers.  Column c (> 0) is owned by CTA c mod G and only
+// its owner ever updates it, in reflector order.  Reflector j+1 is formed by the owner
+// of column j+1 right after applying reflector j to that column (before its other
+// columns) and published through flags[j+1]; every CTA waits on that flag alone before
+// applying reflector j+1.  The arithmetic (chunk trees, update order, scalar ops) is the
+// barrier kernel's, so R is bitwise the same.
+__device__ __forceinline__ int wait_flag(const int *flag) {
+    int v;
+    long long spins = 0;
+    while ((v = *reinterpret_cast<const volatile int *>(flag)) == 0) {
+        if (++spins > (1ll << 26)) return -1;     // ~seconds: report instead of hanging
+        __nanosleep(64);
+    }
+    __threadfence();
+    return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(THREADS)
+householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nqmax x n */, T *taus, T *v0s,
+                        int *flags, Ctl<T> *ctl) {
+    using O = LevelOps<T>;
+    __shared__ T sh_nodes[MAXCH];
+    __shared__ T sh_t[MAXCH];
+    __shared__ T sh_root;
+    __shared__ int sh_flag;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int G = gridDim.x, b = blockIdx.x;
+
+    auto publish = [&](int jj, int rc) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (rc != SK_OK) { ctl->fail_code = rc; ctl->fail_col = jj; }
+            __threadfence();
+            atomicExch(flags + jj, rc == SK_OK ? 1 : 2);
+        }
+    };
+    if (b == 0) publish(0, make_reflector<T>(w, ld, d, 0, taus, v0s, alphas, sh_nodes, &sh_root));
+    for (int j = 0; j < n - 1; ++j) {
+        if (threadIdx.x == 0) sh_flag = wait_flag(flags + j);
+        __syncthreads();
+        if (sh_flag != 1) {                        // failure upstream (or a stuck chain)
+            if (sh_flag < 0 && threadIdx.x == 0) { ctl->fail_code = SK_ERR_CUDA; ctl->fail_col = j; }
+            return;
+        }
+        const T tau = *reinterpret_cast<volatile T *>(taus + j), v0 = *reinterpret_cast<volatile T *>(v0s + j);
+        const T *v = w + (int64_t)j * ld + j;
+        const int L = d - j, nq = (L + CH - 1) / CH;
+        int c0 = j + 1 + ((b - (j + 1)) % G + G) % G;   // first owned column > j
+        if (c0 == j + 1) {
+            // ---- leader: column j+1 first, then reflector j+1
+            for (int q = warp; q < nq; q += WARPS) {
+                const T node = chunk_node<T>(v, w + (int64_t)(j + 1) * ld + j, L, q, 1, v0);
+                if (lane == 0) sh_nodes[q] = node;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                const T root = warp_tree_root<T>(nq, [&](int i) { return sh_nodes[i]; });
+                if (lane == 0) sh_root = O::mul(tau, root);
+            }
+            __syncthreads();
+            const T t = sh_root;
+            T *colj = w + (int64_t)(j + 1) * ld + j;
+            if (threadIdx.x == 0) colj[0] = O::sub(colj[0], O::mul(v0, t));   // R entry (row j)
+            T *x = colj + 1;
+            const T *vx = v + 1;
+            const int Lx = L - 1, nqx = (Lx + CH - 1) / CH;
+            for (int q = warp; q < nqx; q += WARPS) {
+                const int base = q * CH + lane * 8;
+                const int cnt = max(0, min(8, Lx - base));
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    if (e < cnt) x[base + e] = O::sub(x[base + e], O::mul(vx[base + e], t));
+                __syncwarp();
+                const T node = chunk_node<T>(x, x, Lx, q);
+                if (lane == 0) sh_nodes[q] = node;
+            }
+            __syncthreads();
+            const int rc = j + 1 < n ? reflect_from_nodes<T>(x, Lx, taus + j + 1, v0s + j + 1, alphas, j + 1,
+                                                             sh_nodes, &sh_root)
+                                     : SK_OK;
+            publish(j + 1, rc);
+            c0 += G;
+        }
+        // ---- the rest of the owned columns: t_c = tau * root(v . w[j:, c]), then the update
+        const int mine = c0 < n ? (n - 1 - c0) / G + 1 : 0;
+        if (mine == 0) continue;
+        const int units = mine * nq;
+        for (int u = warp; u < units; u += WARPS) {
+            const int k = u / nq, q = u % nq;
+            const int c = c0 + k * G;
+            const T node = chunk_node<T>(v, w + (int64_t)c * ld + j, L, q, 1, v0);
+            if (lane == 0) part[(size_t)q * n + c] = node;
+        }
+        __syncthreads();
+        for (int k = warp; k < mine; k += WARPS) {
+            const int c = c0 + k * G;
+            const T root = warp_tree_root<T>(nq, [&](int i) { return part[(size_t)i * n + c]; });
+            if (lane == 0) sh_t[k] = O::mul(tau, root);
+        }
+        __syncthreads();
+        for (int u = warp; u < units; u += 2 * WARPS) {
+            const int u2 = u + WARPS;
+            const bool has2 = u2 < units;
+            const int k1 = u / nq, q1 = u % nq, k2 = u2 / nq, q2 = u2 % nq;
+            T *col1 = w + (int64_t)(c0 + k1 * G) * ld + j + q1 * CH;
+            T *col2 = w + (int64_t)(c0 + (has2 ? k2 : k1) * G) * ld + j + (has2 ? q2 : q1) * CH;
+            const T t1 = sh_t[k1], t2 = has2 ? sh_t[k2] : O::zero();
+            const int cnt1 = min(CH, L - q1 * CH), cnt2 = has2 ? min(CH, L - q2 * CH) : 0;
+            const T *v1 = v + q1 * CH, *v2 = v + (has2 ? q2 : q1) * CH;
+#pragma unroll 4
+            for (int i = lane; i < CH; i += 32) {
+                T a1 = O::zero(), a2 = O::zero(), x1 = O::zero(), x2 = O::zero();
+                if (i < cnt1) { a1 = col1[i]; x1 = (q1 == 0 && i == 0) ? v0 : v1[i]; }
+                if (i < cnt2) { a2 = col2[i]; x2 = (q2 == 0 && i == 0) ? v0 : v2[i]; }
+                if (i < cnt1) col1[i] = O::sub(a1, O::mul(x1, t1));
+                if (i < cnt2) col2[i] = O::sub(a2, O::mul(x2, t2));
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // prescale for binary16: max |A_s| (as f64)
 __global__ void maxabs_half(const __half *a, int64_t count, unsigned long long *out_bits) {
     double mx = 0.0;
@@ -321,7 +446,8 @@ inline int64_t nq_max(int64_t d) { return (d + CH - 1) / CH; }
 template <typename T>
 size_t ws_bytes(int64_t d, int64_t n) {
     return align_up(sizeof(Ctl<T>), 256) + align_up((size_t)n * sizeof(T), 256) +
-           align_up((size_t)nq_max(d) * n * sizeof(T), 256) + 256;
+           align_up((size_t)nq_max(d) * n * sizeof(T), 256) + 256 +
+           2 * align_up((size_t)n * sizeof(T), 256) + align_up((size_t)n * sizeof(int), 256);   // flow kernel
 }
 
 template <typename T, bool HALF>
@@ -337,19 +463,35 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
     T *part = reinterpret_cast<T *>(p);
     p += align_up((size_t)nq_max(d) * n * sizeof(T), 256);
     int *nonfinite = reinterpret_cast<int *>(p);
+    p += 256;
+    T *taus = reinterpret_cast<T *>(p);
+    p += align_up((size_t)n * sizeof(T), 256);
+    T *v0s = reinterpret_cast<T *>(p);
+    p += align_up((size_t)n * sizeof(T), 256);
+    int *flags = reinterpret_cast<int *>(p);
     SK_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl<T>), st));
     SK_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), st));
+    static const bool barrier_kernel = getenv("SK_QR_BARRIER") != nullptr;   // A/B: the grid-barrier kernel
     auto kfn = householder_kernel<T>;
-    const int maxb = max_coop_blocks((const void *)kfn, THREADS, 0);
+    auto ffn = householder_flow_kernel<T>;
+    const bool flow = !barrier_kernel;
+    const int maxb = max_coop_blocks(flow ? (const void *)ffn : (const void *)kfn, THREADS, 0);
     if (maxb <= 0) { set_error("sk_qr_r: kernel cannot be co-resident"); return SK_ERR_ARG; }
     const int64_t units = nq_max(d) * n;
     int blocks = (int)std::min<int64_t>(std::min<int64_t>(maxb, sm_count()), (units + WARPS - 1) / WARPS + 1);
     if (blocks < 2) blocks = std::min(2, maxb);
     int di = (int)d, ni = (int)n;
     int64_t ldw = d;
-    void *args[] = {&w, &ldw, &di, &ni, &alphas, &part, &ctl};
-    SK_CUDA(cudaLaunchCooperativeKernel((const void *)kfn, dim3(blocks), dim3(THREADS), args, 0, st));
-    SK_LAUNCH_CHECK("householder_kernel");
+    if (flow && (n + blocks - 1) / blocks <= MAXCH) {
+        SK_CUDA(cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st));
+        void *args[] = {&w, &ldw, &di, &ni, &alphas, &part, &taus, &v0s, &flags, &ctl};
+        SK_CUDA(cudaLaunchCooperativeKernel((const void *)ffn, dim3(blocks), dim3(THREADS), args, 0, st));
+        SK_LAUNCH_CHECK("householder_flow_kernel");
+    } else {
+        void *args[] = {&w, &ldw, &di, &ni, &alphas, &part, &ctl};
+        SK_CUDA(cudaLaunchCooperativeKernel((const void *)kfn, dim3(blocks), dim3(THREADS), args, 0, st));
+        SK_LAUNCH_CHECK("householder_kernel");
+    }
     int fail[2];
     SK_CUDA(cudaMemcpyAsync(fail, &ctl->fail_code, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     SK_CUDA(cudaStreamSynchronize(st));

@@ -22,7 +22,11 @@
 namespace sk {
 namespace trsm {
 
-constexpr int BMR = 128, NB = 64, BK = 16, STAGES = 3, THREADS = 256;
+#ifndef SK_TRSM_BK
+#define SK_TRSM_BK 16
+#define SK_TRSM_STAGES 3
+#endif
+constexpr int BMR = 128, NB = 64, BK = SK_TRSM_BK, STAGES = SK_TRSM_STAGES, THREADS = 256;
 constexpr int WM = 32, WN = 32;             // 4 x 2 warps
 constexpr int APITCH = BK + 4;              // 20 = 4 (mod 16): conflict-free A fragments
 constexpr int BPITCH = NB + 4;              // 68 = 4 (mod 16): conflict-free B fragments
