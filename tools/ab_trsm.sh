@@ -5,7 +5,7 @@
 set -e
 NVCC="nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr"
 cp paper_2603_16644_b200/libsklsq.so /tmp/libsklsq.base.so
-objs=$(ls build/*.o | grep -v "/trsm" | tr '\n' ' ')
+objs=$(ls paper_2603_16644_b200/csrc/*.cu | xargs -n1 basename | sed "s/\.cu$/.o/" | grep -v "^trsm.o$" | sed "s|^|build/|" | tr '\n' ' ')
 for v in "$@"; do
   set -- $v
   $NVCC -DSK_TRSM_BK=$1 -DSK_TRSM_STAGES=$2 -c paper_2603_16644_b200/csrc/trsm.cu -o /tmp/trsm_v.o
