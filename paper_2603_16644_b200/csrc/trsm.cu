@@ -212,7 +212,11 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
                     ts[rr * TPITCH + cc + 1] -= acc[x][y][1];
                 }
         }
-        if (tid < NB && tid >= jw) rs[ridx(tid, tid)] = 1.0;
+        // reciprocals of the diagonal (padded entries -> 1): the substitution's dependency
+        // chain is then DMUL -> SHFL -> DFMA per column instead of a full division (the
+        // optimised BLAS dtrsm kernels the reference reaches also scale by 1/r_jj)
+        __shared__ double rinv[NB];
+        if (tid < NB) rinv[tid] = tid >= jw ? 1.0 : 1.0 / rs[ridx(tid, tid)];
         __syncthreads();
         // -- substitution: v holds columns hf, hf+2, ..., hf+62 of this row
         {
@@ -225,7 +229,7 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
                 const int owner = c & 1, kc = c >> 1;
                 double x = 0.0;
                 if (hf == owner) {
-                    v[kc] = v[kc] / rs[ridx(c, c)];
+                    v[kc] = v[kc] * rinv[c];
                     x = v[kc];
                 }
                 x = __shfl_sync(0xffffffffu, x, base | owner);
