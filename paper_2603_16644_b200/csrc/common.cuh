@@ -137,4 +137,17 @@ template <> struct LevelOps<double> {
     __device__ static __forceinline__ T zero() { return 0.0; }
 };
 
+// Dataflow kernels (co-resident CTAs, cooperative launch): wait until *flag != 0 and
+// return it (acquire); -1 after ~seconds instead of hanging if the chain is stuck.
+__device__ __forceinline__ int wait_flag(const int *flag) {
+    int v;
+    long long spins = 0;
+    while ((v = *reinterpret_cast<const volatile int *>(flag)) == 0) {
+        if (++spins > (1ll << 26)) return -1;
+        __nanosleep(64);
+    }
+    __threadfence();
+    return v;
+}
+
 }  // namespace sk

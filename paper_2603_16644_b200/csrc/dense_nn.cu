@@ -406,6 +406,118 @@ lu_kernel(double *w, double *lmul, int *perm, int n, double *candv, int *candi, 
     }
 }
 
+// Dataflow LU (no grid barriers), the same arithmetic as lu_kernel: column c of the
+// column-major working copy is owned by CTA c mod G and only its owner swaps/updates
+// it.  Step k's pivot and multipliers come from the owner of column k right after it
+// applied steps < k to that column (published through flags[k]: 1 = ok, 2 = singular);
+// every CTA then applies step k to its own columns (the next pivot column first when it
+// owns it) and swaps rows k, p of the multiplier columns it owns.
+__global__ void __launch_bounds__(THREADS)
+lu_flow_kernel(double *w, double *lmul, int *perm, int n, int *pivots, int *flags, LuCtl *ctl) {
+    __shared__ double sv[THREADS / 32];
+    __shared__ int si[THREADS / 32];
+    __shared__ double s_piv;
+    __shared__ int s_p, s_flag;
+    const int G = gridDim.x, b = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = THREADS / 32;
+    const double thresh = ctl->thresh;
+
+    // pivot, swap and multipliers of step k on column k (owned by this CTA, up to date)
+    auto pivot_step = [&](int k) {
+        double *col = w + (int64_t)k * n;
+        double bv = -1.0;
+        int bi = INT32_MAX;
+        for (int i = k + threadIdx.x; i < n; i += THREADS) better(bv, bi, fabs(col[i]), i);
+        block_argmax(bv, bi, sv, si, &s_piv, &s_p);
+        const double piv = s_piv;
+        const int p = s_p;
+        const bool bad = piv < thresh || piv == 0.0 || !(piv == piv);
+        if (!bad) {
+            if (threadIdx.x == 0 && p != k) {
+                const double t = col[k];
+                col[k] = col[p];
+                col[p] = t;
+            }
+            __syncthreads();
+            const double akk = col[k];
+            for (int i = k + 1 + threadIdx.x; i < n; i += THREADS) lmul[(int64_t)k * n + i] = __ddiv_rn(col[i], akk);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (bad) { ctl->fail_code = SK_NUMERICALLY_SINGULAR; ctl->fail_col = k; ctl->fail_value = piv; }
+            pivots[k] = p;
+            __threadfence();
+            atomicExch(flags + k, bad ? 2 : 1);
+        }
+    };
+    // step k on column c: swap rows k, p, then rows i > k -= l_i * row k (one warp)
+    auto apply_warp = [&](int k, int p, const double *l, int c) {
+        double *col = w + (int64_t)c * n;
+        if (lane == 0 && p != k) {
+            const double t = col[k];
+            col[k] = col[p];
+            col[p] = t;
+        }
+        __syncwarp();
+        const double ukc = col[k];
+        for (int i = k + 1 + lane; i < n; i += 32) col[i] = __dsub_rn(col[i], __dmul_rn(l[i], ukc));
+    };
+
+    (void)perm;                                   // built from pivots afterwards (perm_from_pivots)
+    if (b == 0) pivot_step(0);
+    for (int k = 0; k < n - 1; ++k) {
+        if (threadIdx.x == 0) s_flag = wait_flag(flags + k);
+        __syncthreads();
+        if (s_flag != 1) {
+            if (s_flag < 0 && threadIdx.x == 0) { ctl->fail_code = SK_ERR_CUDA; ctl->fail_col = k; }
+            return;
+        }
+        const int p = *reinterpret_cast<volatile int *>(pivots + k);
+        const double *l = lmul + (int64_t)k * n;
+        int c0 = k + 1 + ((b - (k + 1)) % G + G) % G;    // first owned column > k
+        if (c0 == k + 1) {                                 // next pivot column first
+            double *col = w + (int64_t)c0 * n;
+            if (threadIdx.x == 0 && p != k) {
+                const double t = col[k];
+                col[k] = col[p];
+                col[p] = t;
+            }
+            __syncthreads();
+            const double ukc = col[k];
+            for (int i = k + 1 + threadIdx.x; i < n; i += THREADS) col[i] = __dsub_rn(col[i], __dmul_rn(l[i], ukc));
+            __syncthreads();
+            pivot_step(k + 1);
+            c0 += G;
+        }
+        int wi = 0;
+        for (int c = c0; c < n; c += G, ++wi)
+            if (wi % nw == warp) apply_warp(k, p, l, c);
+        // multipliers of earlier steps move with their rows (owned L columns j < k)
+        if (p != k)
+            for (int j = b + threadIdx.x * G; j < k; j += THREADS * G) {
+                double *lm = lmul + (int64_t)j * n;
+                const double u = lm[k];
+                lm[k] = lm[p];
+                lm[p] = u;
+            }
+        __syncthreads();
+    }
+}
+
+// perm = the row swaps (k, pivots[k]) applied in order to the identity (one thread)
+__global__ void perm_from_pivots(const int *pivots, int n, int *perm) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    for (int i = 0; i < n; ++i) perm[i] = i;
+    for (int k = 0; k < n; ++k) {
+        const int p = pivots[k];
+        if (p != k && p >= 0 && p < n) {
+            const int t = perm[k];
+            perm[k] = perm[p];
+            perm[p] = t;
+        }
+    }
+}
+
 // ------------------------------------------------------------ substitution --
 // Single-CTA blocked triangular solve over an element accessor M(i,k) = m[i*rs + k*cs].
 // lower: x_i depends on k < i (forward); else k > i (backward).  unit: diag == 1.
@@ -546,7 +658,7 @@ __global__ void __launch_bounds__(1024) hager_kernel(const double *l, int n, dou
 // --------------------------------------------------------------- helpers ----
 struct Ws {
     double *w, *l, *stats, *vec, *candv;
-    int *perm, *candi, *flag;
+    int *perm, *candi, *flag, *lflags, *pivots;
     void *ctl;
 };
 static size_t ws_layout(int64_t n, void *base, Ws *o) {
@@ -556,7 +668,10 @@ static size_t ws_layout(int64_t n, void *base, Ws *o) {
     size_t ow = take(nn), ol = take(nn), os = take(8 * sizeof(double)), ov = take((size_t)n * sizeof(double) * 2);
     size_t op = take((size_t)n * sizeof(int)), oc = take(2 * 4096 * sizeof(double)), oci = take(2 * 4096 * sizeof(int));
     size_t of = take(sizeof(int) * 4), octl = take(256);
+    size_t olf = take((size_t)n * sizeof(int)), opv = take((size_t)n * sizeof(int));
     if (o && base) {
+        o->lflags = reinterpret_cast<int *>(static_cast<unsigned char *>(base) + olf);
+        o->pivots = reinterpret_cast<int *>(static_cast<unsigned char *>(base) + opv);
         unsigned char *b = static_cast<unsigned char *>(base);
         o->w = reinterpret_cast<double *>(b + ow);
         o->l = reinterpret_cast<double *>(b + ol);
@@ -718,15 +833,31 @@ int sk_lu_solve_f64(const double *g, int64_t n, const double *rhs, double *x, sk
     transpose_copy<<<(unsigned)std::min<int64_t>((n * n + 255) / 256, 4096), 256, 0, st>>>(g, (int)n, ws.w);
     SK_LAUNCH_CHECK("transpose_copy");
     SK_CUDA(cudaMemsetAsync(ws.l, 0, (size_t)n * n * sizeof(double), st));
-    int blocks = coop_blocks((const void *)lu_kernel, THREADS, 0,
-                             std::min<int64_t>(2 * sm_count(), (n * n + THREADS * 8 - 1) / (THREADS * 8)));
-    if (!blocks) { set_error("lu_kernel not co-resident"); return SK_ERR_CUDA; }
     double *w = ws.w, *lm = ws.l, *cv = ws.candv;
     int *perm = ws.perm, *ci = ws.candi;
     int ni = (int)n;
-    void *args[] = {&w, &lm, &perm, &ni, &cv, &ci, &ctl};
-    SK_CUDA(cudaLaunchCooperativeKernel((const void *)lu_kernel, dim3(blocks), dim3(THREADS), args, 0, st));
-    SK_LAUNCH_CHECK("lu_kernel");
+    // The dataflow LU (SK_LU_FLOW=1) is bitwise the same but slower at n = 2048 (39 vs
+    // 20 ms): its pivot-column critical path (update, argmax, swap, n divisions) is
+    // longer than two grid barriers over the fully parallel step.
+    static const bool barrier_lu = getenv("SK_LU_FLOW") == nullptr;
+    if (!barrier_lu) {
+        const int blocks = coop_blocks((const void *)lu_flow_kernel, THREADS, 0, std::min<int64_t>(sm_count(), n));
+        if (!blocks) { set_error("lu_flow_kernel not co-resident"); return SK_ERR_CUDA; }
+        int *lf = ws.lflags, *pv = ws.pivots;
+        SK_CUDA(cudaMemsetAsync(lf, 0, (size_t)n * sizeof(int), st));
+        void *args[] = {&w, &lm, &perm, &ni, &pv, &lf, &ctl};
+        SK_CUDA(cudaLaunchCooperativeKernel((const void *)lu_flow_kernel, dim3(blocks), dim3(THREADS), args, 0, st));
+        SK_LAUNCH_CHECK("lu_flow_kernel");
+        perm_from_pivots<<<1, 32, 0, st>>>(pv, ni, perm);
+        SK_LAUNCH_CHECK("perm_from_pivots");
+    } else {
+        int blocks = coop_blocks((const void *)lu_kernel, THREADS, 0,
+                                 std::min<int64_t>(2 * sm_count(), (n * n + THREADS * 8 - 1) / (THREADS * 8)));
+        if (!blocks) { set_error("lu_kernel not co-resident"); return SK_ERR_CUDA; }
+        void *args[] = {&w, &lm, &perm, &ni, &cv, &ci, &ctl};
+        SK_CUDA(cudaLaunchCooperativeKernel((const void *)lu_kernel, dim3(blocks), dim3(THREADS), args, 0, st));
+        SK_LAUNCH_CHECK("lu_kernel");
+    }
     LuCtl hc;
     SK_CUDA(cudaMemcpyAsync(&hc, ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
     SK_CUDA(cudaStreamSynchronize(st));

@@ -296,17 +296,6 @@ householder_kernel(T *w, int64_t ld, int d, int n, T *alphas /* n */, T *part /*
 // columns) and published through flags[j+1]; every CTA waits on that flag alone before
 // applying reflector j+1.  The arithmetic (chunk trees, update order, scalar ops) is the
 // barrier kernel's, so R is bitwise the same.
-__device__ __forceinline__ int wait_flag(const int *flag) {
-    int v;
-    long long spins = 0;
-    while ((v = *reinterpret_cast<const volatile int *>(flag)) == 0) {
-        if (++spins > (1ll << 26)) return -1;     // ~seconds: report instead of hanging
-        __nanosleep(64);
-    }
-    __threadfence();
-    return v;
-}
-
 template <typename T>
 __global__ void __launch_bounds__(THREADS)
 householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nqmax x n */, T *taus, T *v0s,
