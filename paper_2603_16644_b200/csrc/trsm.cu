@@ -218,33 +218,76 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
         __shared__ double rinv[NB];
         if (tid < NB) rinv[tid] = tid >= jw ? 1.0 : 1.0 / rs[ridx(tid, tid)];
         __syncthreads();
-        // -- substitution: v holds columns hf, hf+2, ..., hf+62 of this row
-        {
-            double v[NB / 2];
+        // -- the diagonal block in SB-wide sub-blocks: substitution on the sub-block's
+        //    triangle (two threads per row, columns split by parity), then the rest of
+        //    T loses X_s R[s, >s] on the DMMA pipe.  A quarter of the SIMT FP64 work of a
+        //    full 64-wide substitution; the order of the dot products per entry changes
+        //    (blocked instead of column by column), not the algorithm.
+#ifndef SK_TRSM_NOSUB   // (timing experiments only: -DSK_TRSM_NOSUB skips the solve)
+#ifndef SK_TRSM_SB
+#define SK_TRSM_SB 32   // measured at 4M x 2048: SB 8 592 ms, 16 584 ms, 32 580 ms, none (no solve) 533 ms
+#endif
+        constexpr int SB = SK_TRSM_SB;
+#pragma unroll 1
+        for (int s = 0; s < NB / SB; ++s) {
+            const int cs = s * SB;
+            {
+                double v[SB / 2];
 #pragma unroll
-            for (int k = 0; k < NB / 2; ++k) v[k] = ts[srow * TPITCH + 2 * k + hf];
-            const int base = lane & ~1;
+                for (int k = 0; k < SB / 2; ++k) v[k] = ts[srow * TPITCH + cs + 2 * k + hf];
+                const int base = lane & ~1;
 #pragma unroll
-            for (int c = 0; c < NB; ++c) {
-                const int owner = c & 1, kc = c >> 1;
-                double x = 0.0;
-                if (hf == owner) {
-                    v[kc] = v[kc] * rinv[c];
-                    x = v[kc];
+                for (int c = 0; c < SB; ++c) {
+                    const int owner = c & 1, kc = c >> 1;
+                    double x = 0.0;
+                    if (hf == owner) {
+                        v[kc] = v[kc] * rinv[cs + c];
+                        x = v[kc];
+                    }
+                    x = __shfl_sync(0xffffffffu, x, base | owner);
+                    // this thread's half of row cs+c of R_JJ, sub-block columns: contiguous
+                    const double *rrow = rs + (cs + c) * RPITCH + hf * (NB / 2) + cs / 2;
+#pragma unroll
+                    for (int kp = ((c + 1) >> 1) >> 1; kp < SB / 4; ++kp) {
+                        const double2 rv = *reinterpret_cast<const double2 *>(rrow + 2 * kp);
+                        if (4 * kp + hf > c) v[2 * kp] -= x * rv.x;
+                        if (4 * kp + 2 + hf > c) v[2 * kp + 1] -= x * rv.y;
+                    }
                 }
-                x = __shfl_sync(0xffffffffu, x, base | owner);
-                // this thread's half of row c of R_JJ is contiguous: 16-byte loads
-                const double *rrow = rs + c * RPITCH + hf * (NB / 2);
 #pragma unroll
-                for (int kp = ((c + 1) >> 1) >> 1; kp < NB / 4; ++kp) {
-                    const double2 rv = *reinterpret_cast<const double2 *>(rrow + 2 * kp);
-                    if (4 * kp + hf > c) v[2 * kp] -= x * rv.x;
-                    if (4 * kp + 2 + hf > c) v[2 * kp + 1] -= x * rv.y;
+                for (int k = 0; k < SB / 2; ++k) ts[srow * TPITCH + cs + 2 * k + hf] = v[k];
+            }
+            __syncthreads();
+            const int rest = NB - cs - SB;                  // columns right of the sub-block
+            if (rest > 0) {
+                // warp w: rows 16w..16w+15 (two 8-row m-tiles) x all `rest` columns
+                const int nt = rest / 8;
+                double am[2][SB / 4];
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                    for (int kk = 0; kk < SB / 4; ++kk)
+                        am[mt][kk] = -ts[(warp * 16 + mt * 8 + g) * TPITCH + cs + kk * 4 + t];
+#pragma unroll 1
+                for (int y = 0; y < nt; ++y) {
+                    const int c0 = cs + SB + y * 8;
+                    double bf[SB / 4];
+#pragma unroll
+                    for (int kk = 0; kk < SB / 4; ++kk) bf[kk] = rs[ridx(cs + kk * 4 + t, c0 + g)];
+#pragma unroll
+                    for (int mt = 0; mt < 2; ++mt) {
+                        double *crow = ts + (warp * 16 + mt * 8 + g) * TPITCH + c0 + 2 * t;
+                        double c0v = crow[0], c1v = crow[1];
+#pragma unroll
+                        for (int kk = 0; kk < SB / 4; ++kk) dmma884(c0v, c1v, am[mt][kk], bf[kk]);
+                        crow[0] = c0v;
+                        crow[1] = c1v;
+                    }
                 }
             }
-#pragma unroll
-            for (int k = 0; k < NB / 2; ++k) ts[srow * TPITCH + 2 * k + hf] = v[k];
+            __syncthreads();
         }
+#endif
         __syncthreads();
         // -- store A_p[rows, J]
         if (vec && jw == NB) {
