@@ -137,6 +137,23 @@ template <> struct LevelOps<double> {
     __device__ static __forceinline__ T zero() { return 0.0; }
 };
 
+// Packed FP32x2 arithmetic (sm_100 FFMA2 / FMUL2): two lanes per instruction.
+__device__ __forceinline__ uint64_t f32x2(float lo, float hi) {
+    return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float f32x2_lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f32x2_hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ uint64_t f32x2_fma(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t f32x2_mul(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
 // Dataflow kernels (co-resident CTAs, cooperative launch): wait until *flag != 0 and
 // return it (acquire); -1 after ~seconds instead of hanging if the chain is stuck.
 __device__ __forceinline__ int wait_flag(const int *flag) {

@@ -18,6 +18,9 @@ for i in range(4):
                                  stage_timing=True)
     print(json.dumps({"step": i, **{k: round(v, 1) for k, v in rep.stage_ms.items()}}))
 r_s = rep.preconditioner.r_device()
+if os.environ.get("PIPELINE_ONLY"):
+    sys.exit(0)
+sq.release_scratch()
 
 
 def timeit(fn, reps=3):
