@@ -49,9 +49,28 @@ class DeviceOps:
         from .device import as_dvec
         return as_dvec(b, m)
 
+    def _dmat(self, t):
+        """t as a DMat carrying cached column statistics (the INT8 Gram engine scans a
+        matrix used by two Grams once: A in the kappa0 SYRK and in A_p^T A)."""
+        from .dense import _colstats, _gram_engine
+        from .device import DMat
+        key = (t.data_ptr(), tuple(t.shape), t.stride(0))
+        cache = getattr(self, "_cs", None)
+        if cache is not None and cache[0] == key:
+            return DMat(t, None, "torch", cache[1])
+        m, n = t.shape
+        cs = _colstats(t) if _gram_engine(m, n, False, None) == "ozaki" else None
+        self._cs = (key, cs)
+        return DMat(t, None, "torch", cs)
+
     def gram(self, x, y=None):
         from .dense import _gram
-        return _gram(x, y)
+        return _gram(self._dmat(x), None if y is None else self._dmat(y))
+
+    def gram_and_rhs(self, x, y, b):
+        """(X^T Y or X^T X, X^T b) with the memory-bound GEMV on a side stream."""
+        from .solvers import _gram_and_rhs
+        return _gram_and_rhs(x, None if y is None else self._dmat(y), b)
 
     def gemv_t(self, x, v):
         from .dense import _gemv_t
@@ -78,8 +97,20 @@ class DeviceOps:
         return _qr_level_dev(a_s, level, op.d, total.shape[0])
 
     def trsm(self, a, r):
+        # A_p in the per-device scratch buffer of algorithm1_pipeline (no 64 GB
+        # allocation per solve); handed back by release()
         from .dense import _trsm
-        return _trsm(a, r)
+        from .solvers import _AP_SCRATCH
+        self._ap = _AP_SCRATCH.take(a.shape[0], a.shape[1], a.device)
+        return _trsm(a, r, out=self._ap[1])
+
+    def release(self):
+        from .solvers import _AP_SCRATCH
+        ap = getattr(self, "_ap", None)
+        if ap is not None:
+            _AP_SCRATCH.give(*ap)
+            self._ap = None
+        self._cs = None
 
     def chol_solve(self, g, rhs):
         from .dense import _chol_solve
@@ -181,14 +212,19 @@ def algorithm1_pipeline_sharded(a_local, b_local, method="pne", precision="auto"
             if escalated_from is not None or wider is None:
                 raise
             escalated_from, level = level, wider
-    stages.mark("trsm")
-    a_p = ops.trsm(a, r_s)
-    stages.mark("gram")
-    if method == "pne":
-        g = _allreduce(ops.gram(a_p))
-    else:
-        g = _allreduce(ops.gram(a_p, a))
-    rhs = _allreduce(ops.gemv_t(a_p, b))
+    try:
+        stages.mark("trsm")
+        a_p = ops.trsm(a, r_s)
+        stages.mark("gram")
+        if hasattr(ops, "gram_and_rhs"):
+            g, rhs = ops.gram_and_rhs(a_p, None if method == "pne" else a, b)
+        else:
+            g = ops.gram(a_p) if method == "pne" else ops.gram(a_p, a)
+            rhs = ops.gemv_t(a_p, b)
+        g, rhs = _allreduce(g), _allreduce(rhs)
+    finally:
+        if hasattr(ops, "release"):
+            ops.release()
     stages.mark("nxn")
     if method == "pne":
         try:
