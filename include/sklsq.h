@@ -127,11 +127,13 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
                          size_t ws_bytes, sk_stream_t stream);
 /* 1 if the last sk_gram_ozaki_* call on this host thread took the FP64 fallback. */
 int sk_gram_ozaki_fell_back(void);
-/* stats[j] = max_k |X[k,j]|, stats[n + j] = sum_k X[k,j]^2 (device, fixed-order and
- * deterministic; a non-finite column gives max = +inf). */
+/* stats[j] = max_k |X[k,j]|, stats[n + j] = sum_k X[k,j]^2 and, if v != NULL,
+ * stats[2n + j] = sum_k X[k,j] v[k] (the right-hand side a_p.T @ b of
+ * src/solvers.py:231/251 from the same pass); device, fixed-order, deterministic; a
+ * non-finite column gives max = +inf. */
 size_t sk_colstats_workspace(int64_t n);
-int sk_colstats_f64(const double *x, int64_t ldx, int64_t m, int64_t n, double *stats, void *ws, size_t ws_bytes,
-                    sk_stream_t stream);
+int sk_colstats_f64(const double *x, int64_t ldx, int64_t m, int64_t n, const double *v, double *stats, void *ws,
+                    size_t ws_bytes, sk_stream_t stream);
 
 /* out (n) = X^T v (X m x n row-major): `a_p.T @ b` src/solvers.py:231/251. */
 size_t sk_gemv_t_workspace(int64_t m, int64_t n);

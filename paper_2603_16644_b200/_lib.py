@@ -52,7 +52,7 @@ SIGNATURES = {
     "sk_gram_ozaki_ex_f64": (_i32, [_p, _i64, _p, _i64, _i64, _i64, _p, _p, _p, _i64, _p, _sz, _p]),
     "sk_gram_ozaki_fell_back": (_i32, []),
     "sk_colstats_workspace": (_sz, [_i64]),
-    "sk_colstats_f64": (_i32, [_p, _i64, _i64, _i64, _p, _p, _sz, _p]),
+    "sk_colstats_f64": (_i32, [_p, _i64, _i64, _i64, _p, _p, _p, _sz, _p]),
     "sk_gemv_t_workspace": (_sz, [_i64, _i64]),
     "sk_gemv_t_f64": (_i32, [_p, _i64, _i64, _i64, _p, _p, _i32, _p, _sz, _p]),
     "sk_trsm_right_upper_f64": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _p, _i64, _ps, _p]),

@@ -71,12 +71,14 @@ constexpr int64_t KSPLIT_MAX = 131072;                       // int32-exact accu
 // blocks writes per-block (max |x|, sum x^2) partials, reduced in block order.
 // max feeds the scales; max^2 m / sum x^2 is the guard (below).  fmax propagates a NaN
 // only from its second operand, so non-finite entries are kept sticky explicitly.
+// With v != NULL the same pass also forms X^T v (the PNE/HPNE right-hand side A_p^T b),
+// so the Gram's column scan doubles as its GEMV.
 constexpr int STAT_BLOCKS = 512;
 __global__ void __launch_bounds__(256) colstats_kernel(const double *__restrict__ x, int64_t ldx, int64_t m, int n,
-                                                       double *__restrict__ part) {
+                                                       const double *__restrict__ v, double *__restrict__ part) {
     const int c = blockIdx.y * 256 + threadIdx.x;
     if (c >= n) return;
-    double mx = 0.0, ss = 0.0;
+    double mx = 0.0, ss = 0.0, dt = 0.0;
     const int64_t g = gridDim.x;
     int64_t r = blockIdx.x;
     for (; r + 3 * g < m; r += 4 * g) {   // four independent loads in flight
@@ -84,28 +86,34 @@ __global__ void __launch_bounds__(256) colstats_kernel(const double *__restrict_
                      a3 = x[(r + 3 * g) * ldx + c];
         mx = fmax(fmax(mx, fmax(fabs(a0), fabs(a1))), fmax(fabs(a2), fabs(a3)));
         ss += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+        if (v) dt += (a0 * v[r] + a1 * v[r + g]) + (a2 * v[r + 2 * g] + a3 * v[r + 3 * g]);
         if (!isfinite(a0) || !isfinite(a1) || !isfinite(a2) || !isfinite(a3)) mx = CUDART_INF;
     }
     for (; r < m; r += g) {
         const double a = x[r * ldx + c];
         mx = isfinite(a) ? fmax(mx, fabs(a)) : CUDART_INF;
         ss += a * a;
+        if (v) dt += a * v[r];
     }
     part[(size_t)blockIdx.x * n + c] = mx;
     part[((size_t)STAT_BLOCKS + blockIdx.x) * n + c] = ss;
+    if (v) part[((size_t)2 * STAT_BLOCKS + blockIdx.x) * n + c] = dt;
 }
 
-__global__ void colstats_finalize(const double *__restrict__ part, int nblk, int n, double *__restrict__ stats) {
+__global__ void colstats_finalize(const double *__restrict__ part, int nblk, int n, int with_dot,
+                                  double *__restrict__ stats) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= n) return;
-    double mx = 0.0, ss = 0.0;
+    double mx = 0.0, ss = 0.0, dt = 0.0;
     for (int b = 0; b < nblk; ++b) {
         const double v = part[(size_t)b * n + c];
         mx = (isfinite(v) && isfinite(mx)) ? fmax(mx, v) : CUDART_INF;
         ss += part[((size_t)STAT_BLOCKS + b) * n + c];
+        if (with_dot) dt += part[((size_t)2 * STAT_BLOCKS + b) * n + c];
     }
     stats[c] = mx;
     stats[n + c] = ss;
+    if (with_dot) stats[2 * n + c] = dt;
 }
 
 // max bits of the scales input (non-negative doubles order like their bit patterns)
@@ -560,7 +568,7 @@ Plan make_plan(int64_t m, int64_t n, bool syrk) {
     p.part_bytes = 0;   // the GEMM epilogue accumulates modulo p straight into acc
     p.acc_bytes = (size_t)NMOD * n * n * sizeof(int32_t);
     // bits / scales / exponents (6n words), column stats of X and Y (4n), stats partials
-    p.aux_bytes = (size_t)(10 * n + 2 * STAT_BLOCKS * n) * 8 + 8192;
+    p.aux_bytes = (size_t)(10 * n + 3 * STAT_BLOCKS * n) * 8 + 8192;
     return p;
 }
 
@@ -607,24 +615,25 @@ size_t sk_gram_ozaki_workspace(int64_t m, int64_t n, int syrk) {
            oz::align_up256(p.aux_bytes) + 1024;
 }
 
-size_t sk_colstats_workspace(int64_t n) { return (size_t)2 * oz::STAT_BLOCKS * n * sizeof(double) + 256; }
+size_t sk_colstats_workspace(int64_t n) { return (size_t)3 * oz::STAT_BLOCKS * n * sizeof(double) + 256; }
 
-int sk_colstats_f64(const double *x, int64_t ldx, int64_t m, int64_t n, double *stats, void *ws, size_t ws_bytes,
-                    sk_stream_t stream) {
+int sk_colstats_f64(const double *x, int64_t ldx, int64_t m, int64_t n, const double *v, double *stats, void *ws,
+                    size_t ws_bytes, sk_stream_t stream) {
     if (!x || !stats || m < 0 || n <= 0 || ldx < n || !ws || ws_bytes < sk_colstats_workspace(n)) {
         set_error("sk_colstats_f64: bad arguments or workspace");
         return SK_ERR_ARG;
     }
     cudaStream_t st = (cudaStream_t)stream;
     if (m == 0) {
-        SK_CUDA(cudaMemsetAsync(stats, 0, (size_t)2 * n * sizeof(double), st));
+        SK_CUDA(cudaMemsetAsync(stats, 0, (size_t)(v ? 3 : 2) * n * sizeof(double), st));
         return SK_OK;
     }
     const int nblk = (int)std::min<int64_t>(m, oz::STAT_BLOCKS);
     double *part = static_cast<double *>(ws);
-    oz::colstats_kernel<<<dim3((unsigned)nblk, (unsigned)((n + 255) / 256)), 256, 0, st>>>(x, ldx, m, (int)n, part);
+    oz::colstats_kernel<<<dim3((unsigned)nblk, (unsigned)((n + 255) / 256)), 256, 0, st>>>(x, ldx, m, (int)n, v,
+                                                                                         part);
     SK_LAUNCH_CHECK("oz colstats");
-    oz::colstats_finalize<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nblk, (int)n, stats);
+    oz::colstats_finalize<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nblk, (int)n, v != nullptr, stats);
     SK_LAUNCH_CHECK("oz colstats finalize");
     return SK_OK;
 }
@@ -681,13 +690,13 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
     // column statistics: given by the caller (sk_colstats_f64 of the same matrix) or a pass here
     const double *sx = xstats, *sy = syrk ? xstats : ystats;
     if (!sx) {
-        int rc = sk_colstats_f64(x, ldx, m, n, stats, stat_ws, sk_colstats_workspace(n), stream);
+        int rc = sk_colstats_f64(x, ldx, m, n, nullptr, stats, stat_ws, sk_colstats_workspace(n), stream);
         if (rc) return rc;
         sx = stats;
         if (syrk) sy = stats;
     }
     if (!sy) {
-        int rc = sk_colstats_f64(y, ldy, m, n, stats + 2 * n, stat_ws, sk_colstats_workspace(n), stream);
+        int rc = sk_colstats_f64(y, ldy, m, n, nullptr, stats + 2 * n, stat_ws, sk_colstats_workspace(n), stream);
         if (rc) return rc;
         sy = stats + 2 * n;
     }

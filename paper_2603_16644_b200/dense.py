@@ -59,14 +59,16 @@ def _gram_engine(m: int, n: int, accumulate: bool, engine: str | None) -> str:
     return e
 
 
-def _colstats(t: torch.Tensor) -> torch.Tensor:
-    """[max_k |T[k, j]| for j] + [sum_k T[k, j]^2 for j] (device, f64, 2n)."""
+def _colstats(t: torch.Tensor, v: torch.Tensor | None = None) -> torch.Tensor:
+    """[max_k |T[k, j]| for j] + [sum_k T[k, j]^2 for j] (+ [T^T v] if v is given)
+    (device, f64, 2n or 3n)."""
     t = _rm(t)
     m, n = t.shape
-    out = torch.empty(2 * n, dtype=torch.float64, device=t.device)
+    out = torch.empty((3 if v is not None else 2) * n, dtype=torch.float64, device=t.device)
     lib = _lib.lib()
     wp, wn = WORKSPACE.get(lib.sk_colstats_workspace(n))
-    call("sk_colstats_f64", t.data_ptr(), t.stride(0), m, n, out.data_ptr(), wp, wn, stream_handle())
+    call("sk_colstats_f64", t.data_ptr(), t.stride(0), m, n, v.data_ptr() if v is not None else None,
+         out.data_ptr(), wp, wn, stream_handle())
     return out
 
 

@@ -425,8 +425,16 @@ _SIDE_STREAMS: dict = {}
 
 
 def _gram_and_rhs(x, y, bd):
-    """G = X^T Y (DMMA, compute-bound) and rhs = X^T b (HBM-bound) on two streams so
-    the streaming GEMV hides under the Gram."""
+    """G = X^T Y and rhs = X^T b.  On the INT8 engine the column scan of X that sets its
+    scales forms X^T b in the same pass; on DMMA the streaming GEMV runs on a second
+    stream under the Gram."""
+    from .dense import _colstats, _gram_engine
+    xt = x.t if isinstance(x, DMat) else x
+    m, n = xt.shape
+    if _gram_engine(m, n, False, None) == "ozaki":
+        st = _colstats(xt, bd)
+        g = _gram(DMat(xt, None, "torch", st[: 2 * n]), y)
+        return g, st[2 * n:]
     cur = torch.cuda.current_stream()
     side = _SIDE_STREAMS.get(cur.device.index)
     if side is None:
