@@ -134,7 +134,17 @@ struct PassAParams {
     double2 *y;             // [pair][k2][j1], pairs of this block
     int level;              // 32: demote A to binary32 on load (overflow -> *overflow = 1); 64: as is
     int *overflow;
+    const double2 *tw_n2;   // e^{-2 pi i t / N2}, t < N2 (precomputed once per call)
 };
+
+// e^{-2 pi i t / len}, t < len (one table per call instead of one per CTA)
+__global__ void twiddle_table(double2 *tw, int64_t len) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < len; t += (int64_t)gridDim.x * blockDim.x) {
+        double s, c;
+        sincospi(-2.0 * (double)t / (double)len, &s, &c);
+        tw[t] = make_double2(c, s);
+    }
+}
 
 // grid: (M1/2, ncols/8).  A CTA owns j1 in {2 a2, 2 a2 + 1} and 8 columns (4 complex
 // pairs): every gathered row segment is a full 64-byte line, every Y store 32 bytes.
@@ -142,12 +152,18 @@ __global__ void __launch_bounds__(A_THREADS) fft_pass_a(const PassAParams p) {
     extern __shared__ __align__(16) double2 fa_smem[];
     double2 *tw = fa_smem;                  // N2 twiddles
     double2 *x = fa_smem + N2;              // 8 FFTs: f = jj * 4 + pp
+    double2 *otw = x + 8 * N2;              // [jj][hi 32 | lo 32]: e^{-2 pi i j1 (32 h + l) / M}
     const int a2 = blockIdx.x;
     const int q = blockIdx.y;               // column octet
-    for (int t = threadIdx.x; t < N2; t += blockDim.x) {
+    for (int t = threadIdx.x; t < N2; t += blockDim.x) tw[t] = p.tw_n2[t];
+    if (threadIdx.x < 128) {
+        // output twiddles e^{-2 pi i j1 k2 / M} = hi[k2 / 32] * lo[k2 % 32] (j1 k2 < M, exact phases)
+        const int jj = threadIdx.x >> 6, h = (threadIdx.x >> 5) & 1, t = threadIdx.x & 31;
+        const int64_t j1 = 2 * (int64_t)a2 + jj;
+        const int64_t ph = j1 * (int64_t)(h ? t : 32 * t);
         double s, c;
-        sincospi(-2.0 * (double)t / (double)N2, &s, &c);
-        tw[t] = make_double2(c, s);
+        sincospi(-2.0 * (double)ph / (double)p.M, &s, &c);
+        otw[jj * 64 + (h ? 32 : 0) + t] = make_double2(c, s);
     }
     // ---- gather: v_{j1 + M1 j2} for the two j1 and eight columns
     const int cbase = p.c0 + 8 * q;
@@ -189,11 +205,8 @@ __global__ void __launch_bounds__(A_THREADS) fft_pass_a(const PassAParams p) {
         double2 out[2];
 #pragma unroll
         for (int jj = 0; jj < 2; ++jj) {
-            const int64_t j1 = 2 * (int64_t)a2 + jj;
-            const int64_t ph = j1 * (int64_t)k2;     // < M1 * N2 = M: no reduction needed
-            double s, c;
-            sincospi(-2.0 * (double)ph / (double)p.M, &s, &c);
-            out[jj] = cmul(x[(jj * 4 + pp) * N2 + k2], make_double2(c, s));
+            const double2 w = cmul(otw[jj * 64 + (k2 >> 5)], otw[jj * 64 + 32 + (k2 & 31)]);
+            out[jj] = cmul(x[(jj * 4 + pp) * N2 + k2], w);
         }
         double2 *dst = p.y + ((size_t)(pair0 + pp) * N2 + k2) * p.M1 + 2 * a2;
         *reinterpret_cast<double4 *>(dst) = make_double4(out[0].x, out[0].y, out[1].x, out[1].y);
@@ -210,6 +223,7 @@ struct PassBParams {
     int npairs;             // pairs in this block
     double2 *zbuf;          // [s][which][pair] (pairs of this block), ldz = npairs
     int d;
+    const double2 *tw_m1;   // e^{-2 pi i t / M1}, t < M1 (precomputed once per call)
 };
 
 // grid: (N2 k2 values, ceil(npairs / B_PAIRS))
@@ -222,11 +236,7 @@ __global__ void __launch_bounds__(B_THREADS) fft_pass_b(const PassBParams p) {
     double2 *tw = fb_smem;                  // e^{-2 pi i t / M1}
     const int pbase = blockIdx.y * B_PAIRS;
     const int np = min(B_PAIRS, p.npairs - pbase);
-    for (int t = threadIdx.x; t < M1; t += blockDim.x) {
-        double s, c;
-        sincospi(-2.0 * (double)t / (double)M1, &s, &c);
-        tw[t] = make_double2(c, s);
-    }
+    for (int t = threadIdx.x; t < M1; t += blockDim.x) tw[t] = p.tw_m1[t];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int tasks = (r1 - r0) * np;
@@ -293,7 +303,8 @@ size_t sketch_fft_workspace(int64_t m_pad, int64_t n, int64_t d) {
     const size_t ybytes = (size_t)(cb / 2) * m_pad * sizeof(double2);
     const size_t zbytes = (size_t)d * 2 * (cb / 2) * sizeof(double2);
     const size_t req = (size_t)(N2 + 1) * sizeof(int) + (size_t)2 * d * (2 * sizeof(int) + sizeof(int64_t));
-    return align_up(ybytes, 256) + align_up(zbytes, 256) + align_up(req, 256) + 1024;
+    const size_t tables = (size_t)(N2 + m_pad / N2) * sizeof(double2);
+    return align_up(ybytes, 256) + align_up(zbytes, 256) + align_up(req, 256) + align_up(tables, 256) + 1024;
 }
 
 int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int64_t row_offset, int64_t m_pad,
@@ -313,6 +324,12 @@ int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int
     int *d_s = d_ptr + (N2 + 1);
     int *d_w = d_s + 2 * d;
     int64_t *d_k1 = reinterpret_cast<int64_t *>(align_up(reinterpret_cast<uintptr_t>(d_w + 2 * d), 8));
+    p += align_up((size_t)(N2 + 1) * sizeof(int) + (size_t)2 * d * (2 * sizeof(int) + sizeof(int64_t)), 256);
+    double2 *tw_n2 = reinterpret_cast<double2 *>(p);
+    double2 *tw_m1 = tw_n2 + N2;
+    twiddle_table<<<4, 256, 0, st>>>(tw_n2, N2);
+    twiddle_table<<<(unsigned)std::min<int64_t>((M1 + 255) / 256, 1024), 256, 0, st>>>(tw_m1, M1);
+    SK_LAUNCH_CHECK("twiddle_table");
     // ---- request lists grouped by k2 (host; d entries)
     std::vector<int64_t> hrows((size_t)d);
     SK_CUDA(cudaMemcpyAsync(hrows.data(), rows, (size_t)d * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -338,7 +355,7 @@ int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int
     SK_CUDA(cudaMemcpyAsync(d_s, hs.data(), (size_t)2 * d * sizeof(int), cudaMemcpyHostToDevice, st));
     SK_CUDA(cudaMemcpyAsync(d_w, hw.data(), (size_t)2 * d * sizeof(int), cudaMemcpyHostToDevice, st));
     SK_CUDA(cudaMemcpyAsync(d_k1, hk1.data(), (size_t)2 * d * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    const size_t smem_a = (size_t)(N2 + 8 * N2) * sizeof(double2);
+    const size_t smem_a = (size_t)(N2 + 8 * N2 + 128) * sizeof(double2);
     const size_t smem_b = (size_t)M1 * sizeof(double2);
     if (smem_b > 200 * 1024) { set_error("sketch_fft: M too large for pass B (M1 %lld)", (long long)M1); return SK_ERR_ARG; }
     SK_CUDA(cudaFuncSetAttribute(fft_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
@@ -346,10 +363,11 @@ int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int
     for (int64_t c0 = 0; c0 < n; c0 += cb) {
         const int ncols = (int)std::min<int64_t>(cb, (n - c0 + 7) / 8 * 8);
         const int npairs = ncols / 2;
-        PassAParams pa{a, lda, m_local, row_offset, M, M1, signs, (int)c0, ncols, (int)n, y, level, overflow_flag_dev};
+        PassAParams pa{a,     lda,          m_local, row_offset, M, M1, signs, (int)c0, ncols, (int)n, y,
+                       level, overflow_flag_dev, tw_n2};
         fft_pass_a<<<dim3((unsigned)(M1 / 2), (unsigned)(ncols / 8)), A_THREADS, smem_a, st>>>(pa);
         SK_LAUNCH_CHECK("fft_pass_a");
-        PassBParams pb{y, M1, d_ptr, d_s, d_w, d_k1, npairs, zbuf, (int)d};
+        PassBParams pb{y, M1, d_ptr, d_s, d_w, d_k1, npairs, zbuf, (int)d, tw_m1};
         fft_pass_b<<<dim3((unsigned)N2, (unsigned)((npairs + B_PAIRS - 1) / B_PAIRS)), B_THREADS, smem_b, st>>>(pb);
         SK_LAUNCH_CHECK("fft_pass_b");
         const int64_t total = d * (int64_t)npairs;
