@@ -74,6 +74,23 @@ def test_config2_shared_single_preconditioner(sq):
         _gate(ours, ref, f"config2 {meth}")
 
 
+@pytest.mark.parametrize("kappa", [10.0, 1e3, 2e6])
+def test_large_auto_engine_vs_oracle(sq, kappa):
+    """262144 x 512 (m n^2 = 6.9e10 > 2^33): the kappa0 SYRK and the HPNE Gram take the
+    INT8 tensor-core engine on their own, the sketch the tcgen05 (binary16) or FFT
+    (binary32/64) path -- the config-3 code path at a size the oracle can finish."""
+    from paper_2603_16644_b200 import dense
+    m, n = 262144, 512
+    assert dense._gram_engine(m, n, False, None) == "ozaki"
+    p = planted_problem_lapack(m, n, kappa, 1e-6, R.mix64(20261018, 3, int(math.log10(kappa))))
+    ref = _outcome(lambda: R.pipeline(p.a, p.b, "hpne", "auto", 3.0, "dct2", 0, p.x_star, diagnostics=False))
+    ours = _outcome(lambda: sq.algorithm1_pipeline(p.a, p.b, "hpne", "auto", 3.0, "dct2", 0, p.x_star,
+                                                   diagnostics=False))
+    _gate(ours, ref, f"large kappa={kappa:g}")
+    assert ours[1].preconditioner.computed_in.name == ref[1].pre.level
+    assert abs(ours[1].precision_decision.kappa0 - ref[1].decision[0]) <= 1e-4
+
+
 C5_KAPPA = [1e2, 1e6, 1e10, 1e14]
 C5_RHO = [1e-14, 1e-6, 1e-1]
 
