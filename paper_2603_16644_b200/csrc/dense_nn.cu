@@ -406,6 +406,143 @@ lu_kernel(double *w, double *lmul, int *perm, int n, double *candv, int *candi, 
     }
 }
 
+// LU with one grid barrier per step: rows are never swapped.  A row keeps its physical
+// slot; pos[] (logical position of a physical row) and at[] (physical row at a logical
+// position) record the swaps, double-buffered by step parity and rebuilt by all threads
+// from (k, p, lp) so no thread races another.  Pivot ties resolve by logical position,
+// as with physical swaps; every multiplier and update is the same rounded operation as
+// lu_kernel's, so the factors agree bit for bit once gathered into logical order.
+__device__ __forceinline__ void better3(double &bv, int &bl, int &br, double v, int l, int r) {
+    if (v > bv || (v == bv && l < bl)) { bv = v; bl = l; br = r; }
+}
+
+__global__ void __launch_bounds__(THREADS)
+lu_perm_kernel(double *w, double *lmul, int n, int *pos2, int *at2, double *candv, int *candl, int *candr,
+               LuCtl *ctl) {
+    __shared__ double sv[THREADS / 32];
+    __shared__ int sl[THREADS / 32], sr[THREADS / 32];
+    __shared__ double s_piv;
+    __shared__ int s_lp, s_p;
+    cg::grid_group grid = cg::this_grid();
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const int G = gridDim.x;
+    const double thresh = ctl->thresh;
+    auto block_cand = [&](double bv, int bl, int br, int slot) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int ol = __shfl_xor_sync(0xffffffffu, bl, o), orr = __shfl_xor_sync(0xffffffffu, br, o);
+            better3(bv, bl, br, ov, ol, orr);
+        }
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (lane == 0) { sv[warp] = bv; sl[warp] = bl; sr[warp] = br; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double v = -1.0;
+            int l = INT32_MAX, r = INT32_MAX;
+            for (int q = 0; q < THREADS / 32; ++q) better3(v, l, r, sv[q], sl[q], sr[q]);
+            candv[slot * G + blockIdx.x] = v;
+            candl[slot * G + blockIdx.x] = l;
+            candr[slot * G + blockIdx.x] = r;
+        }
+        __syncthreads();
+    };
+    {
+        double bv = -1.0;
+        int bl = INT32_MAX, br = INT32_MAX;
+        for (int64_t i = tid; i < n; i += nthreads) {
+            better3(bv, bl, br, fabs(w[i]), (int)i, (int)i);
+            pos2[i] = (int)i;
+            at2[i] = (int)i;
+        }
+        block_cand(bv, bl, br, 0);
+    }
+    grid.sync();
+    for (int k = 0; k < n; ++k) {
+        const int buf = k & 1;
+        const int *pos = pos2 + buf * n, *at = at2 + buf * n;
+        int *npos = pos2 + (buf ^ 1) * n, *nat = at2 + (buf ^ 1) * n;
+        if (threadIdx.x < 32) {
+            double bv = -1.0;
+            int bl = INT32_MAX, br = INT32_MAX;
+            for (int b = threadIdx.x; b < G; b += 32)
+                better3(bv, bl, br, candv[buf * G + b], candl[buf * G + b], candr[buf * G + b]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int ol = __shfl_xor_sync(0xffffffffu, bl, o), orr = __shfl_xor_sync(0xffffffffu, br, o);
+                better3(bv, bl, br, ov, ol, orr);
+            }
+            if (threadIdx.x == 0) { s_piv = bv; s_lp = bl; s_p = br; }
+        }
+        __syncthreads();
+        const double piv = s_piv;
+        const int lp = s_lp, p = s_p;
+        if (piv < thresh || piv == 0.0 || !(piv == piv)) {
+            if (tid == 0) { ctl->fail_code = SK_NUMERICALLY_SINGULAR; ctl->fail_col = k; ctl->fail_value = piv; }
+            return;
+        }
+        const int rk = at[k];                    // physical row at logical k before the swap
+        // next-step maps: p -> k, rk -> lp
+        for (int64_t i = tid; i < n; i += nthreads) {
+            npos[i] = (i == p) ? k : (i == rk ? lp : pos[i]);
+            nat[i] = (i == k) ? p : (i == lp ? rk : at[i]);
+        }
+        const double akk = w[(int64_t)k * n + p];
+        double cbv = -1.0;
+        int cbl = INT32_MAX, cbr = INT32_MAX;
+        const int rem = n - k - 1;               // active rows other than p
+        if (rem > 0) {
+            // thread -> (active row, column group); active rows are those with pos >= k,
+            // enumerated by logical position lpos in (k, n): physical row at[lpos], except
+            // that logical k's row rk moved to lp (and p left the active set)
+            const int64_t groups = nthreads / rem > 0 ? nthreads / rem : 1;
+            for (int64_t t = tid; t < groups * rem; t += nthreads) {
+                const int lpos = k + 1 + (int)(t % rem);
+                const int i = (lpos == lp) ? rk : at[lpos];   // the row that ends up at lpos
+                const int g0 = (int)(t / rem);
+                const double li = __ddiv_rn(w[(int64_t)k * n + i], akk);
+                if (g0 == 0) lmul[(int64_t)k * n + i] = li;
+                constexpr int U = 8;
+                const int GG = (int)groups;
+                for (int jb = k + 1 + g0; jb < n; jb += U * GG) {
+                    double wv[U], uk[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int j = jb + u * GG;
+                        if (j < n) { wv[u] = w[(int64_t)j * n + i]; uk[u] = w[(int64_t)j * n + p]; }
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int j = jb + u * GG;
+                        if (j < n) {
+                            const double nv = __dsub_rn(wv[u], __dmul_rn(li, uk[u]));
+                            w[(int64_t)j * n + i] = nv;
+                            if (j == k + 1) better3(cbv, cbl, cbr, fabs(nv), lpos, i);
+                        }
+                    }
+                }
+            }
+        }
+        block_cand(cbv, cbl, cbr, buf ^ 1);
+        grid.sync();
+    }
+}
+
+// gather the physically stored factors into logical row order (at = final at[] map)
+__global__ void lu_gather(const double *w, const double *lmul, const int *at, int n, double *wl, double *ll,
+                          int *perm) {
+    const int64_t total = (int64_t)n * n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(e / n), i = (int)(e % n);    // column-major: column j, logical row i
+        const int r = at[i];
+        wl[e] = w[(int64_t)j * n + r];
+        ll[e] = (i > j) ? lmul[(int64_t)j * n + r] : 0.0;
+        if (j == 0) perm[i] = r;
+    }
+}
+
 // Dataflow LU (no grid barriers), the same arithmetic as lu_kernel: column c of the
 // column-major working copy is owned by CTA c mod G and only its owner swaps/updates
 // it.  Step k's pivot and multipliers come from the owner of column k right after it
@@ -660,6 +797,8 @@ struct Ws {
     double *w, *l, *stats, *vec, *candv;
     int *perm, *candi, *flag, *lflags, *pivots;
     void *ctl;
+    double *wphys, *lphys;   // lu_perm_kernel: factors in physical row slots
+    int *pos2, *at2, *candr;
 };
 static size_t ws_layout(int64_t n, void *base, Ws *o) {
     size_t off = 0;
@@ -669,7 +808,15 @@ static size_t ws_layout(int64_t n, void *base, Ws *o) {
     size_t op = take((size_t)n * sizeof(int)), oc = take(2 * 4096 * sizeof(double)), oci = take(2 * 4096 * sizeof(int));
     size_t of = take(sizeof(int) * 4), octl = take(256);
     size_t olf = take((size_t)n * sizeof(int)), opv = take((size_t)n * sizeof(int));
+    size_t owp = take(nn), olp = take(nn), op2 = take((size_t)2 * n * sizeof(int)),
+           oa2 = take((size_t)2 * n * sizeof(int)), ocr = take(2 * 4096 * sizeof(int));
     if (o && base) {
+        unsigned char *bb = static_cast<unsigned char *>(base);
+        o->wphys = reinterpret_cast<double *>(bb + owp);
+        o->lphys = reinterpret_cast<double *>(bb + olp);
+        o->pos2 = reinterpret_cast<int *>(bb + op2);
+        o->at2 = reinterpret_cast<int *>(bb + oa2);
+        o->candr = reinterpret_cast<int *>(bb + ocr);
         o->lflags = reinterpret_cast<int *>(static_cast<unsigned char *>(base) + olf);
         o->pivots = reinterpret_cast<int *>(static_cast<unsigned char *>(base) + opv);
         unsigned char *b = static_cast<unsigned char *>(base);
@@ -839,8 +986,28 @@ int sk_lu_solve_f64(const double *g, int64_t n, const double *rhs, double *x, sk
     // The dataflow LU (SK_LU_FLOW=1) is bitwise the same but slower at n = 2048 (39 vs
     // 20 ms): its pivot-column critical path (update, argmax, swap, n divisions) is
     // longer than two grid barriers over the fully parallel step.
+    // default: one grid barrier per step (lu_perm_kernel); SK_LU_KERNEL=barrier selects
+    // the two-barrier swap kernel, SK_LU_FLOW=1 the dataflow one (all bitwise the same)
+    static const char *lu_choice = getenv("SK_LU_KERNEL");
     static const bool barrier_lu = getenv("SK_LU_FLOW") == nullptr;
-    if (!barrier_lu) {
+    static const bool perm_lu = barrier_lu && !(lu_choice && strcmp(lu_choice, "barrier") == 0);
+    if (perm_lu) {
+        int blocks = coop_blocks((const void *)lu_perm_kernel, THREADS, 0,
+                                 std::min<int64_t>(std::min<int64_t>(2 * sm_count(), 4096),
+                                                   (n * n + THREADS * 8 - 1) / (THREADS * 8)));
+        if (!blocks) { set_error("lu_perm_kernel not co-resident"); return SK_ERR_CUDA; }
+        // the working copy moves to the physical-slot buffers; ws.w / ws.l get the gather
+        SK_CUDA(cudaMemcpyAsync(ws.wphys, ws.w, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        SK_CUDA(cudaMemsetAsync(ws.lphys, 0, (size_t)n * n * sizeof(double), st));
+        double *wp = ws.wphys, *lp = ws.lphys;
+        int *p2 = ws.pos2, *a2 = ws.at2, *cl = ws.candi, *cr = ws.candr;
+        void *args[] = {&wp, &lp, &ni, &p2, &a2, &cv, &cl, &cr, &ctl};
+        SK_CUDA(cudaLaunchCooperativeKernel((const void *)lu_perm_kernel, dim3(blocks), dim3(THREADS), args, 0, st));
+        SK_LAUNCH_CHECK("lu_perm_kernel");
+        lu_gather<<<(unsigned)std::min<int64_t>((n * n + 255) / 256, 4096), 256, 0, st>>>(
+            ws.wphys, ws.lphys, ws.at2 + (n & 1) * n, ni, ws.w, ws.l, perm);
+        SK_LAUNCH_CHECK("lu_gather");
+    } else if (!barrier_lu) {
         const int blocks = coop_blocks((const void *)lu_flow_kernel, THREADS, 0, std::min<int64_t>(sm_count(), n));
         if (!blocks) { set_error("lu_flow_kernel not co-resident"); return SK_ERR_CUDA; }
         int *lf = ws.lflags, *pv = ws.pivots;
