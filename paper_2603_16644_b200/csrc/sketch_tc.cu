@@ -173,6 +173,7 @@ __device__ __forceinline__ void group_coords(const Params &p, int g, int &tn, in
     nkb = (int)((k1 - k0 + BK - 1) / BK);
 }
 
+template <bool WHT>
 __global__ void __launch_bounds__(THREADS, 1)
 sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
     extern __shared__ uint8_t smem_raw[];
@@ -268,14 +269,26 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
         // per-row offset table e^{i pi r (2t) / 2M}, t = 0..31 (exact integer phases)
         // 16-entry table (registers): columns 16..31 use the base rotated by e^{i 16 delta}
         float wc[16], ws[16], wc16 = 1.f, ws16 = 0.f;
-        if (!p.wht) {
+        // DCT rows with r = 0 (all entries 1/sqrt2) or past d (zeros) use the same
+        // branch-free formula with a constant table: z = 1, wc = that constant, ws = 0
+        const bool flat = !WHT && (r == 0 || !valid);
+        if (!WHT) {
+            if (flat) {
+                const float cflat = valid ? 0.70710678118654752f : 0.f;
 #pragma unroll
-            for (int t = 0; t < 16; ++t) {
-                const uint64_t q = (f1 * (uint64_t)(2 * t)) % fourM;
-                sincospif((float)q * inv2M, &ws[t], &wc[t]);
+                for (int t = 0; t < 16; ++t) {
+                    wc[t] = cflat;
+                    ws[t] = 0.f;
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                    const uint64_t q = (f1 * (uint64_t)(2 * t)) % fourM;
+                    sincospif((float)q * inv2M, &ws[t], &wc[t]);
+                }
+                const uint64_t q16 = (f1 * (uint64_t)32) % fourM;
+                sincospif((float)q16 * inv2M, &ws16, &wc16);
             }
-            const uint64_t q16 = (f1 * (uint64_t)32) % fourM;
-            sincospif((float)q16 * inv2M, &ws16, &wc16);
         }
         for (int g = slot; g < p.groups; g += p.nslots) {
             int tn, split, nkb;
@@ -290,15 +303,13 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
                 uint8_t *tile = sa + stage * A_BYTES;
                 // 32 operator values of this (row, half) -> four 16-byte swizzled chunks,
                 // each stored as soon as its 8 values are rounded (few live registers)
-                float zs = 0.f, zc = 0.f;
-                if (!p.wht) {
+                float zs = 0.f, zc = 1.f;
+                if (!WHT && !flat) {
                     sincospif((float)ph * inv2M, &zs, &zc);
                     ph += dph;
                     if (ph >= fourM) ph -= fourM;
                 }
                 const float zc2 = zc * wc16 - zs * ws16, zs2 = zs * wc16 + zc * ws16;
-                const bool flat = !p.wht && (r == 0 || !valid);
-                const float cflat = valid ? 0.70710678118654752f : 0.f;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     uint32_t pk[4];
@@ -306,12 +317,10 @@ sketch_tc_kernel(const __grid_constant__ CUtensorMap tmap_b, const Params p) {
                     for (int e = 0; e < 4; ++e) {
                         const int t = q * 8 + 2 * e;
                         float a0, a1;
-                        if (p.wht) {
+                        if constexpr (WHT) {
                             const uint64_t j0 = (uint64_t)(jg0 + t), j1 = j0 + 1;
                             a0 = valid ? ((__popcll(r & j0) & 1) ? -1.f : 1.f) : 0.f;
                             a1 = valid ? ((__popcll(r & j1) & 1) ? -1.f : 1.f) : 0.f;
-                        } else if (flat) {
-                            a0 = a1 = cflat;
                         } else if (t < 16) {
                             a0 = zc * wc[t] - zs * ws[t];
                             a1 = zc * wc[t + 1] - zs * ws[t + 1];
@@ -458,8 +467,9 @@ int sketch_tc_run(int transform, const double *a, int64_t lda, int64_t m_local, 
     prm.wht = transform == SK_WHT;
     prm.epi_scale = transform == SK_WHT ? (float)(1.0 / sqrt((double)m_pad)) : (float)sqrt(2.0 / (double)m_pad);
     prm.part = part;
-    SK_CUDA(cudaFuncSetAttribute(sketch_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-    sketch_tc_kernel<<<p.grid, THREADS, SMEM, st>>>(tmap, prm);
+    auto kfn = prm.wht ? sketch_tc_kernel<true> : sketch_tc_kernel<false>;
+    SK_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    kfn<<<p.grid, THREADS, SMEM, st>>>(tmap, prm);
     SK_LAUNCH_CHECK("sketch_tc_kernel");
     const int64_t total = d * n;
     reduce_part<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(part, p.splits, p.ntiles, p.ntn, (int)d, (int)n, out,
