@@ -669,19 +669,26 @@ __device__ void block_trsv(const TriView M, int n, bool lower, bool unit, double
     const int tid = threadIdx.x, nt = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
     const int nb = (n + 31) / 32;
+    __shared__ double dblk[32][33];   // the diagonal block, staged so the sequential
+                                      // 32-step solve reads shared memory, not L2
     for (int bb = 0; bb < nb; ++bb) {
         const int b = lower ? bb : nb - 1 - bb;
         const int r0 = b * 32, r1 = min(n, r0 + 32);
         const int w = r1 - r0;
+        for (int e = tid; e < 32 * 32; e += nt) {
+            const int i = e >> 5, k = e & 31;
+            dblk[i][k] = (i < w && k < w) ? M(r0 + i, r0 + k) : 0.0;
+        }
+        __syncthreads();
         if (warp == 0) {
             double v = (lane < w) ? x[r0 + lane] : 0.0;
             for (int s = 0; s < w; ++s) {
                 const int r = lower ? s : w - 1 - s;
                 double xr = 0.0;
-                if (lane == r) { xr = unit ? v : v / M(r0 + r, r0 + r); v = xr; }
+                if (lane == r) { xr = unit ? v : v / dblk[r][r]; v = xr; }
                 xr = __shfl_sync(0xffffffffu, xr, r);
                 const bool dep = lower ? (lane > r) : (lane < r);
-                if (dep && lane < w) v -= M(r0 + lane, r0 + r) * xr;
+                if (dep && lane < w) v -= dblk[lane][r] * xr;
             }
             if (lane < w) x[r0 + lane] = v;
         }
@@ -694,11 +701,26 @@ __device__ void block_trsv(const TriView M, int n, bool lower, bool unit, double
                 for (int k = r0; k < r1; ++k) s += M(i, k) * x[k];
                 x[i] -= s;
             }
-        } else {           // row-major: warp per row, lanes over the block
-            for (int i = lo + warp; i < hi; i += nw) {
-                double s = (lane < w) ? M(i, r0 + lane) * x[r0 + lane] : 0.0;
-                s = warp_sum(s);
-                if (lane == 0) x[i] -= s;
+        } else {           // row-major: a warp takes 32 rows x the block's 32 columns
+            // lanes read rows coalesced (lane = column); the 32 row sums come out of a
+            // reduce-scatter butterfly (31 shuffles for 32 rows; lane r ends with row r)
+            const double xl = (lane < w) ? x[r0 + lane] : 0.0;
+            for (int i0 = lo + warp * 32; i0 < hi; i0 += nw * 32) {
+                const int rows = min(32, hi - i0);
+                double v[32];
+#pragma unroll
+                for (int rr = 0; rr < 32; ++rr) v[rr] = (rr < rows && lane < w) ? M(i0 + rr, r0 + lane) * xl : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const bool upper = (lane & o) != 0;
+#pragma unroll
+                    for (int j = 0; j < o; ++j) {
+                        const double send = upper ? v[j] : v[j + o];
+                        const double keep = upper ? v[j + o] : v[j];
+                        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                    }
+                }
+                if (lane < rows) x[i0 + lane] -= v[0];
             }
         }
         __syncthreads();
