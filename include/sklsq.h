@@ -147,6 +147,19 @@ int sk_gemv_t_f64(const double *x, int64_t ldx, int64_t m, int64_t n, const doub
 int sk_trsm_right_upper_f64(const double *a, int64_t lda, int64_t m, int64_t n, const double *r,
                             int64_t ldr, double *ap, int64_t ldap, sk_status *status,
                             sk_stream_t stream);
+/* Same solve, blocked: columns are halved recursively (h = n/2 rounded to 256) down to
+ * leaves of <= 1024 columns solved by the kernel above; each off-diagonal update
+ * A_p[:, h:] = A[:, h:] - A_p[:, :h] R[:h, h:] runs on the INT8 tensor cores (Ozaki
+ * scheme II as in sk_gram_ozaki_f64, row scales for A_p, column scales for R), error
+ * 2^-t (2^e_r sum|R_j| + 2^f_j sum|A_p,r|) / 2 per entry, an FP64 GEMM's size.  Spiky
+ * rows / columns or non-finite values re-run the whole solve on the DMMA kernel
+ * (sk_trsm_ozaki_fell_back() == 1).  ap must not alias a.  Workspace from
+ * sk_trsm_ozaki_workspace(m, n). */
+size_t sk_trsm_ozaki_workspace(int64_t m, int64_t n);
+int sk_trsm_ozaki_f64(const double *a, int64_t lda, int64_t m, int64_t n, const double *r, int64_t ldr,
+                      double *ap, int64_t ldap, sk_status *status, void *ws, size_t ws_bytes,
+                      sk_stream_t stream);
+int sk_trsm_ozaki_fell_back(void);
 
 /* ---- sketch --------------------------------------------------------------- */
 /* Partial SRTT sketch of a row block: out (d x n, COLUMN-major, ldo >= d, f64)

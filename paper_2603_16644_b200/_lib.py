@@ -56,6 +56,9 @@ SIGNATURES = {
     "sk_gemv_t_workspace": (_sz, [_i64, _i64]),
     "sk_gemv_t_f64": (_i32, [_p, _i64, _i64, _i64, _p, _p, _i32, _p, _sz, _p]),
     "sk_trsm_right_upper_f64": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _p, _i64, _ps, _p]),
+    "sk_trsm_ozaki_workspace": (_sz, [_i64, _i64]),
+    "sk_trsm_ozaki_f64": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _p, _i64, _ps, _p, _sz, _p]),
+    "sk_trsm_ozaki_fell_back": (_i32, []),
     "sk_sketch_workspace": (_sz, [_i32, _i64, _i64, _i64]),
     "sk_sketch_workspace_ex": (_sz, [_i32, _i32, _i64, _i64, _i64, _i64]),
     "sk_sketch_partial": (_i32, [_i32, _i32, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _i64,

@@ -288,6 +288,11 @@ struct GemmParams {
     int ntn, ntiles, splits, units, syrk, n;
     int64_t rows, kchunk;
     int32_t *acc;               // [mod][n][n] residues in [0, p)
+    // product mode (blocked TRSM update): C = P Q, P K-major [mod][mrows][K], Q MN-major
+    // [mod][K][nout]; residues of C stored as int8 planes out[mod][mrows][ldo]
+    int64_t mrows, ldo, oplane;
+    int nout;
+    int8_t *out;
 };
 
 // lower-triangular tile list for SYRK: tile index -> (tm, tn) with tm >= tn
@@ -313,9 +318,21 @@ __device__ __forceinline__ void tma_load_3d(void *smem_dst, const CUtensorMap *m
         : "memory");
 }
 
-__global__ void __launch_bounds__(THREADS, 1)
+// int32 product value -> a residue modulo p in [-127, 127] (as a byte in bits 0-7).
+// v = a 2^13 + b, t = a c13 + b with c13 = centred 2^13 mod p: |t| < 2^21 for |v| < 2^27
+// (K <= 8192), so round(t / p) in FP32 is off by at most 2^-9.6 < 1 / (2p), r = t - q p.
+__device__ __forceinline__ uint32_t i32_residue(int v, float fp, float fip, int c13) {
+    const int t = (v >> 13) * c13 + (v & 8191);
+    const float tf = (float)t;
+    const float q = fmaf(tf, fip, FMAGIC) - FMAGIC;
+    return __float_as_uint(fmaf(-q, fp, tf) + FMAGIC);
+}
+
+template <bool PROD>
+__global__ void __launch_bounds__(PROD ? 640 : THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
             const GemmParams p) {
+    constexpr int NTHR = PROD ? 640 : THREADS;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sa = smem;
@@ -327,7 +344,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ 
     uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int NEPI = (THREADS / 32) - EPI_WARP0;
+    constexpr int NEPI = (NTHR / 32) - EPI_WARP0;
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             tc::mbar_init(&full[s], 1);
@@ -369,8 +386,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ 
                     tc::mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
                     const int krow = (int)(k0 + (int64_t)kb * BK);
                     uint8_t *a_dst = sa + stage * A_BYTES, *b_dst = sb + stage * B_BYTES;
-                    tma_load_3d(a_dst, &tmap_x, &full[stage], tm * BM, krow, mod);
-                    tma_load_3d(a_dst + BOX_BYTES, &tmap_x, &full[stage], tm * BM + 128, krow, mod);
+                    if constexpr (PROD) {   // K-major P: box = 128 K bytes x 128 rows
+                        tma_load_3d(a_dst, &tmap_x, &full[stage], krow, tm * BM, mod);
+                        tma_load_3d(a_dst + BOX_BYTES, &tmap_x, &full[stage], krow, tm * BM + 128, mod);
+                    } else {
+                        tma_load_3d(a_dst, &tmap_x, &full[stage], tm * BM, krow, mod);
+                        tma_load_3d(a_dst + BOX_BYTES, &tmap_x, &full[stage], tm * BM + 128, krow, mod);
+                    }
                     tma_load_3d(b_dst, &tmap_y, &full[stage], tn * BN, krow, mod);
                     tma_load_3d(b_dst + BOX_BYTES, &tmap_y, &full[stage], tn * BN + 128, krow, mod);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -379,7 +401,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ 
         }
     } else if (warp == 1) {
         if (lane == 0) {   // --------------------------------------------- MMA issuer
-            constexpr uint32_t idesc = tc::idesc_s32acc_s8(UMMA_M, BN, 1, 1);
+            constexpr uint32_t idesc = tc::idesc_s32acc_s8(UMMA_M, BN, PROD ? 0 : 1, 1);
             int stage = 0;
             unsigned phase = 0, tphase = 0;
             for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
@@ -393,14 +415,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ 
                     tc::tc_fence_after();
                     const uint32_t a0 = smem_u32(sa + stage * A_BYTES), b0 = smem_u32(sb + stage * B_BYTES);
                     // MN-major SW128: 128-element MN blocks BOX_BYTES apart, 8-row K groups 1 KB apart
-                    const uint64_t ad0 = tc::desc_mnmajor_sw128(a0, BOX_BYTES, 1024);
-                    const uint64_t ad1 = tc::desc_mnmajor_sw128(a0 + BOX_BYTES, BOX_BYTES, 1024);
+                    // K-major SW128 (product mode): 128-B K rows, advance 32 B per K step
+                    const uint64_t ad0 = PROD ? tc::desc_kmajor_sw128(a0) : tc::desc_mnmajor_sw128(a0, BOX_BYTES, 1024);
+                    const uint64_t ad1 = PROD ? tc::desc_kmajor_sw128(a0 + BOX_BYTES)
+                                              : tc::desc_mnmajor_sw128(a0 + BOX_BYTES, BOX_BYTES, 1024);
                     const uint64_t bd = tc::desc_mnmajor_sw128(b0, BOX_BYTES, 1024);
 #pragma unroll
                     for (int k = 0; k < BK / UMMA_K; ++k) {   // +32 K rows = 4 KB per step
                         const uint64_t adv = (uint64_t)((UMMA_K * 128) >> 4) * k;
-                        tc::mma_i8_ss(tmem, ad0 + adv, bd + adv, idesc, (kb | k) ? 1u : 0u);
-                        tc::mma_i8_ss(tmem + BN, ad1 + adv, bd + adv, idesc, (kb | k) ? 1u : 0u);
+                        const uint64_t aadv = PROD ? (uint64_t)(UMMA_K >> 4) * k : adv;
+                        tc::mma_i8_ss(tmem, ad0 + aadv, bd + adv, idesc, (kb | k) ? 1u : 0u);
+                        tc::mma_i8_ss(tmem + BN, ad1 + aadv, bd + adv, idesc, (kb | k) ? 1u : 0u);
                     }
                     tc::mma_commit(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -412,7 +437,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ 
     } else if (warp >= EPI_WARP0) {
         // ------------------------------------------------------------- epilogue
         // warp w drains TMEM lanes 32*(w%4); warps 4-7 accumulator 0, 8-11 accumulator 1
-        const int lg = warp & 3, acc = (warp - EPI_WARP0) >> 2;
+        const int lg = warp & 3, acc = ((warp - EPI_WARP0) >> 2) & 1;
         unsigned tphase = 0;
         for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
             int mod, split, tile, nkb;
@@ -421,6 +446,47 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ 
             tc::mbar_wait(tfull, tphase);
             tc::tc_fence_after();
             tphase ^= 1;
+            if constexpr (PROD) {
+                // 16 warps: (accumulator, 128-column half, lane quadrant); each thread
+                // turns 128 int32 values of one row into residue bytes
+                int tm, tn;
+                tile_coords(p, tile, tm, tn);
+                const int half = (warp - EPI_WARP0) >> 3;
+                const int pmod = pm(mod);
+                const float fp = (float)pmod, fip = 1.0f / fp;
+                const int c13 = (int)((8192 % pmod) > (pmod - 1) / 2 ? (8192 % pmod) - pmod : 8192 % pmod);
+                const int64_t row = (int64_t)tm * BM + acc * UMMA_M + lg * 32 + lane;
+                int8_t *dst_row = p.out + (size_t)mod * p.oplane + (size_t)row * p.ldo;
+#pragma unroll 1
+                for (int cb = half * 4; cb < half * 4 + 4; ++cb) {
+                    uint32_t v[32];
+                    tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
+                    tc::tmem_ld_wait();
+                    const int col0 = tn * BN + cb * 32;
+                    if (row < p.mrows && col0 < p.nout) {
+                        uint32_t w[8];
+#pragma unroll
+                        for (int q4 = 0; q4 < 8; ++q4) {
+                            const uint32_t b0 = i32_residue((int)v[4 * q4], fp, fip, c13),
+                                           b1 = i32_residue((int)v[4 * q4 + 1], fp, fip, c13),
+                                           b2 = i32_residue((int)v[4 * q4 + 2], fp, fip, c13),
+                                           b3 = i32_residue((int)v[4 * q4 + 3], fp, fip, c13);
+                            w[q4] = __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
+                        }
+                        int8_t *dst = dst_row + col0;
+                        if (col0 + 32 <= p.nout) {
+                            reinterpret_cast<uint4 *>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                            reinterpret_cast<uint4 *>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+                        } else {
+                            for (int q = 0; q < p.nout - col0; ++q) dst[q] = (int8_t)(w[q >> 2] >> (8 * (q & 3)));
+                        }
+                    }
+                }
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(tempty);
+                continue;
+            }
             // acc[mod][row][col] = (acc + C_partial) mod p, in [0, p): one unit per
             // (modulus, tile) per launch, so no two CTAs touch the same entries
             int tm, tn;
@@ -537,6 +603,219 @@ __global__ void crt_kernel(const int32_t *__restrict__ acc, int n, int syrk, con
     g[(int64_t)i * ldg + j] = ldexp(val, ex[i] + ey[j] - 2 * t);
 }
 
+// ================================================ blocked TRSM update (product) ==
+// A_p[:, h:] = (A[:, h:] - A_p[:, :h] R[:h, h:]) R[h:, h:]^-1: the off-diagonal update
+// C = P Q (P = A_p[:, :h] rows, Q = R[:h, h:]) on the INT8 engine.  Row scales for P
+// (its rows are the output rows), column scales for Q, so the error is again
+// 2^-t (2^e_r sum_k |Q_kj| + 2^f_j sum_k |P_rk|) / 2 per entry.
+
+// P' = rint(P 2^(t - e_r)) with max_k |P[r, k]| < 2^e_r found in the same pass: 16
+// K-major planes [mod][rows][ldk].  k % 256 == 0, so each row is whole warps.  Rows
+// whose max^2 k > F^2 sum^2 (spiky) or with non-finite entries raise *flag.
+__global__ void __launch_bounds__(256, SK_OZ_RES_MINB)
+rowres_kernel(const double *__restrict__ x, int64_t ldx, int64_t rows, int k, int t, int8_t *__restrict__ out,
+              int64_t ldk, int64_t plane, int *__restrict__ expo, int *flag) {
+    __shared__ double smx[8], sss[8];
+    const int cpr = k / RV, rpi = 256 / cpr, wpr = cpr / 32;
+    const int sub = threadIdx.x / cpr, c0 = (threadIdx.x % cpr) * RV;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t r0 = (int64_t)blockIdx.x * rpi; r0 < rows; r0 += (int64_t)gridDim.x * rpi) {
+        const int64_t r = r0 + sub;
+        const bool live = sub < rpi && r < rows;   // cpr need not divide 256 (h = 768)
+        double v[RV];
+        if (live) {
+            const double *src = x + r * ldx + c0;
+#pragma unroll
+            for (int q = 0; q < RV / 2; ++q) {
+                const double2 d = __ldcs(reinterpret_cast<const double2 *>(src) + q);
+                v[2 * q] = d.x;
+                v[2 * q + 1] = d.y;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < RV; ++q) v[q] = 0.0;
+        }
+        double mx = 0.0, ss = 0.0;
+        bool bad = false;
+#pragma unroll
+        for (int q = 0; q < RV; ++q) {
+            bad |= !isfinite(v[q]);
+            mx = fmax(mx, fabs(v[q]));
+            ss = fma(v[q], v[q], ss);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        }
+        bad = __any_sync(0xffffffffu, bad);
+        if (lane == 0) {
+            smx[warp] = bad ? CUDART_INF : mx;
+            sss[warp] = ss;
+        }
+        __syncthreads();
+        double rmx = 0.0, rss = 0.0;
+        for (int w2 = sub * wpr; live && w2 < (sub + 1) * wpr; ++w2) {
+            const double a = smx[w2];
+            rmx = (isfinite(a) && isfinite(rmx)) ? fmax(rmx, a) : CUDART_INF;
+            rss += sss[w2];
+        }
+        __syncthreads();
+        if (!live) continue;
+        int e = 0;
+        const bool ok = isfinite(rmx) && isfinite(rss);
+        if (ok && rmx > 0.0) frexp(rmx, &e);
+        if (threadIdx.x % cpr == 0) {
+            expo[r] = e;
+            if (!ok || (rmx > 0.0 && rmx * rmx * (double)k > GUARD_F2 * rss)) atomicOr(flag, 1);
+        }
+        const double s = ldexp(1.0, t - e);
+        float h0[RV], h1[RV], h2[RV], h3[RV];
+#pragma unroll
+        for (int q = 0; q < RV; ++q) {
+            const double xs = ok ? rint(v[q] * s) : 0.0;
+            const double a3 = rint(xs * 0x1p-39);
+            const double r3 = fma(-a3, 0x1p39, xs);
+            const double a2 = rint(r3 * 0x1p-26);
+            const double r2 = fma(-a2, 0x1p26, r3);
+            const double a1 = rint(r2 * 0x1p-13);
+            h3[q] = (float)a3;
+            h2[q] = (float)a2;
+            h1[q] = (float)a1;
+            h0[q] = (float)fma(-a1, 0x1p13, r2);
+        }
+        int8_t *dst = out + r * ldk + c0;
+        uint64_t p0[RV / 2], p1[RV / 2], p2[RV / 2], p3[RV / 2];
+#pragma unroll
+        for (int q = 0; q < RV / 2; ++q) {
+            p0[q] = f2pack(h0[2 * q], h0[2 * q + 1]);
+            p1[q] = f2pack(h1[2 * q], h1[2 * q + 1]);
+            p2[q] = f2pack(h2[2 * q], h2[2 * q + 1]);
+            p3[q] = f2pack(h3[2 * q], h3[2 * q + 1]);
+        }
+#pragma unroll
+        for (int kk = 0; kk < NMOD; ++kk) {
+            uint32_t w[2];
+#pragma unroll
+            for (int q4 = 0; q4 < 2; ++q4) {
+                uint32_t b[4];
+#pragma unroll
+                for (int bb = 0; bb < 2; ++bb) {
+                    const int q2 = 2 * q4 + bb;
+                    const uint64_t rr = residue_pair(p0[q2], p1[q2], p2[q2], p3[q2], kk);
+                    b[2 * bb] = (uint32_t)rr;
+                    b[2 * bb + 1] = (uint32_t)(rr >> 32);
+                }
+                w[q4] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+            }
+            *reinterpret_cast<uint2 *>(dst + kk * plane) = make_uint2(w[0], w[1]);
+        }
+    }
+}
+
+// column guard of Q (same test as guard_kernel), OR-ed into *flag
+__global__ void colguard_or_kernel(const double *__restrict__ s, int n, int64_t m, int *flag) {
+    int b = 0;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+        const double mx = s[c], ss = s[n + c];
+        if (!isfinite(mx) || !isfinite(ss)) b = 1;
+        else if (mx > 0.0 && mx * mx * (double)m > GUARD_F2 * ss) b = 1;
+    }
+    if (b) atomicOr(flag, 1);
+}
+
+// (M / p_k)^-1 mod p_k: literals (folded to immediates), checked against the definition
+__host__ __device__ constexpr int crt_q(int k) {
+    return k == 0 ? 124 : k == 1 ? 215 : k == 2 ? 217 : k == 3 ? 18 : k == 4 ? 119 : k == 5 ? 134 : k == 6 ? 223
+         : k == 7 ? 51 : k == 8 ? 120 : k == 9 ? 174 : k == 10 ? 5 : k == 11 ? 6 : k == 12 ? 152 : k == 13 ? 117
+         : k == 14 ? 13 : 135;
+}
+constexpr int crt_q_def(int k) {
+    int prod = 1;
+    for (int j = 0; j < NMOD; ++j)
+        if (j != k) prod = (int)(((int64_t)prod * pm(j)) % pm(k));
+    return inv_mod(prod, pm(k));
+}
+constexpr bool crt_q_ok() {
+    for (int k = 0; k < NMOD; ++k)
+        if (crt_q(k) != crt_q_def(k)) return false;
+    return true;
+}
+static_assert(crt_q_ok(), "CRT inverse table");
+
+// Reconstruction by the CRT sum: C' = sum_k y_k W_k - q M with W_k = M / p_k and
+// y_k = r_k crt_q(k) - p_k round(r_k crt_q(k) / p_k) (any integer quotient gives a
+// residue; |y_k| <= p_k / 2 + 1).  W_k = wa 2^76 + wr: sum y wa is exact in FP64
+// (|sum| <= 16 M / 2^77 < 2^53), sum y wr (< 2^87) carries < 2^35 of rounding, far
+// below the 2^(t+5) truncation error of C' itself; q = round(sum / M) is exact since
+// |C'| < M / 2^12.  The residue arithmetic runs two columns at a time on FFMA2.
+struct CrtSub {
+    double wa[NMOD], wr[NMOD];
+    double ma, mr, rm;
+};
+
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+__global__ void __launch_bounds__(256)
+crt_sub_kernel(const int8_t *__restrict__ planes, int64_t plane, int64_t ldo, int64_t rows, int w,
+               const int *__restrict__ er, const int *__restrict__ fq, int t, const double *__restrict__ a,
+               int64_t lda, double *__restrict__ out, int64_t ldout, const CrtSub c) {
+    constexpr float BIAS = 8388736.0f;   // 2^23 + 128: byte (r + 128) in a float's mantissa
+    const int gpr = (w + 3) / 4;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int erow = er[r] - 2 * t;
+        for (int g = threadIdx.x; g < gpr; g += blockDim.x) {
+            const int j0 = g * 4;
+            const int nc = min(4, w - j0);
+            uint32_t pk[NMOD];
+            const int8_t *src = planes + r * ldo + j0;
+            if (nc == 4) {
+#pragma unroll
+                for (int k = 0; k < NMOD; ++k) pk[k] = __ldcs(reinterpret_cast<const uint32_t *>(src + k * plane));
+            } else {
+#pragma unroll
+                for (int k = 0; k < NMOD; ++k) {
+                    uint32_t x = 0;
+                    for (int q = 0; q < nc; ++q) x |= (uint32_t)(uint8_t)src[k * plane + q] << (8 * q);
+                    pk[k] = x;
+                }
+            }
+            double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int k = 0; k < NMOD; ++k) {
+                const uint32_t u = pk[k] ^ 0x80808080u;   // signed byte r -> r + 128
+                const float p = (float)pm(k), q = (float)crt_q(k), qip = (float)crt_q(k) / (float)pm(k);
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    const uint64_t rr = fadd2(f2pack(__uint_as_float(__byte_perm(u, 0x4B000000u, 0x7540 + 2 * h2)),
+                                                     __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7541 + 2 * h2))),
+                                              f2pack(-BIAS, -BIAS));
+                    const uint64_t qq = fadd2(ffma2(rr, f2pack(qip, qip), f2pack(FMAGIC, FMAGIC)),
+                                              f2pack(-FMAGIC, -FMAGIC));
+                    const uint64_t y = ffma2(qq, f2pack(-p, -p), fmul2(rr, f2pack(q, q)));
+                    const double y0 = (double)__uint_as_float((uint32_t)y), y1 = (double)__uint_as_float((uint32_t)(y >> 32));
+                    s1[2 * h2] = fma(y0, c.wa[k], s1[2 * h2]);
+                    s2[2 * h2] = fma(y0, c.wr[k], s2[2 * h2]);
+                    s1[2 * h2 + 1] = fma(y1, c.wa[k], s1[2 * h2 + 1]);
+                    s2[2 * h2 + 1] = fma(y1, c.wr[k], s2[2 * h2 + 1]);
+                }
+            }
+            const double *ar = a + r * lda + j0;
+            double *orow = out + r * ldout + j0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double qq = rint(fma(s1[q], 0x1p76, s2[q]) * c.rm);
+                const double v = fma(fma(-qq, c.ma, s1[q]), 0x1p76, fma(-qq, c.mr, s2[q]));
+                if (q < nc) orow[q] = ar[q] - ldexp(v, erow + fq[j0 + q]);
+            }
+        }
+    }
+}
+
 // -------------------------------------------------------------- planning ----
 struct Plan {
     int ntm, ntn, ntiles, t;
@@ -602,12 +881,277 @@ SidePipe &side_pipe() {
     return sp;
 }
 
+// ----------------------------------------------------- blocked TRSM plan -----
+constexpr int64_t TRSM_KMAX = 8192;   // update depth h: |int32 partials| < 2^27 (i32_residue)
+constexpr int64_t TRSM_CHUNK = 65536;
+
+int64_t trsm_split(int64_t n) { return std::min<int64_t>((n / 2 + 255) / 256 * 256, TRSM_KMAX); }
+
+struct TrsmPlan {
+    int64_t chunk, hmax, wmax, ldw;
+    size_t pres, ores, qres, aux;
+};
+
+TrsmPlan trsm_plan(int64_t m, int64_t n) {
+    TrsmPlan p;
+    p.hmax = trsm_split(n);            // the top level has the largest h and w
+    p.wmax = n - p.hmax;
+    p.ldw = (p.wmax + 15) / 16 * 16;
+    p.chunk = std::min<int64_t>((std::max<int64_t>(m, 1) + 255) / 256 * 256, TRSM_CHUNK);
+    p.pres = (size_t)NMOD * p.chunk * p.hmax;
+    p.ores = (size_t)NMOD * p.chunk * p.ldw;
+    p.qres = (size_t)NMOD * p.hmax * p.ldw;
+    // Q stats (2w) + bits (w) + scales (w) + exps (w ints) + P row exps (chunk ints) + partials
+    p.aux = (size_t)(5 * p.wmax + p.chunk) * 8 + 3 * STAT_BLOCKS * (size_t)p.wmax * 8 + 8192;
+    return p;
+}
+
+CrtSub make_crt_sub() {
+    CrtSub c;
+    unsigned __int128 M = 1;
+    for (int k = 0; k < NMOD; ++k) M *= (unsigned)pm(k);
+    const unsigned __int128 low = (((unsigned __int128)1) << 76) - 1;
+    auto dbl = [](unsigned __int128 v) {
+        return (double)(uint64_t)(v >> 64) * 18446744073709551616.0 + (double)(uint64_t)v;
+    };
+    for (int k = 0; k < NMOD; ++k) {
+        const unsigned __int128 W = M / (unsigned)pm(k);
+        c.wa[k] = dbl(W >> 76);
+        c.wr[k] = dbl(W & low);
+    }
+    c.ma = dbl(M >> 76);
+    c.mr = dbl(M & low);
+    c.rm = 1.0 / dbl(M);
+    return c;
+}
+
+struct TrsmWs {
+    int8_t *pres, *ores, *qres;
+    double *qstats, *qscale;
+    unsigned long long *bits;
+    int *qexp, *pexp, *flag;
+    void *statws;
+    size_t statws_bytes;
+    TrsmPlan plan;
+    CrtSub crt;
+    int64_t base;
+};
+
+}  // namespace oz
+
+namespace trsm {
+int launch(const double *a, int64_t lda, int64_t m, int n, const double *r, int64_t ldr, double *ap, int64_t ldap,
+           cudaStream_t st);
+int first_zero_diagonal(const double *r, int64_t ldr, int n, cudaStream_t st, int *out);
+}  // namespace trsm
+
+namespace oz {
+// A_p[:, :n] = A R^-1 by recursive column halving: solve the left part, subtract its
+// INT8 product with R[:h, h:] from the right part, solve the right part in place.
+// Leaves of width <= base are the FP64 DMMA kernel.
+// SK_TRSM_OZ_PROFILE=1: per-phase CUDA-event times to stderr (leaf solves, Q prep,
+// row residues, INT8 products, reconstruction)
+struct TrsmProf {
+    std::vector<std::pair<int, cudaEvent_t>> ev;
+    void mark(int phase, cudaStream_t st) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        ev.emplace_back(phase, e);
+    }
+    void report() {
+        if (ev.empty()) return;
+        cudaEventSynchronize(ev.back().second);
+        static const char *names[] = {"leaf", "qprep", "rowres", "product", "crt"};
+        float acc[5] = {0, 0, 0, 0, 0}, tot = 0, t;
+        for (size_t i = 1; i < ev.size(); ++i) {
+            cudaEventElapsedTime(&t, ev[i - 1].second, ev[i].second);
+            if (ev[i].first >= 0) acc[ev[i].first] += t;
+            tot += t;
+        }
+        fprintf(stderr, "trsm_ozaki: total %.2f ms", tot);
+        for (int k = 0; k < 5; ++k) fprintf(stderr, ", %s %.2f", names[k], acc[k]);
+        fprintf(stderr, "\n");
+        for (auto &p : ev) cudaEventDestroy(p.second);
+        ev.clear();
+    }
+};
+TrsmProf *trsm_prof() {
+    static const bool on = getenv("SK_TRSM_OZ_PROFILE") != nullptr;
+    thread_local TrsmProf p;
+    return on ? &p : nullptr;
+}
+
+int trsm_rec(const double *a, int64_t lda, double *ap, int64_t ldap, int64_t m, int64_t n, const double *r,
+             int64_t ldr, const TrsmWs &W, cudaStream_t st) {
+    TrsmProf *prof = trsm_prof();
+    if (n <= W.base) {
+        const int rc0 = trsm::launch(a, lda, m, (int)n, r, ldr, ap, ldap, st);
+        if (prof) prof->mark(0, st);
+        return rc0;
+    }
+    const int64_t h = trsm_split(n), w = n - h;
+    int rc = trsm_rec(a, lda, ap, ldap, m, h, r, ldr, W, st);
+    if (rc) return rc;
+    const int sms = sm_count();
+    const int t = choose_t(h);
+    // Q = R[:h, h:]: column scales, guard, residues (MN-major B planes [mod][h][ldw])
+    const double *q = r + h;
+    rc = sk_colstats_f64(q, ldr, h, w, nullptr, W.qstats, W.statws, W.statws_bytes, st);
+    if (rc) return rc;
+    const unsigned wg = (unsigned)((w + 255) / 256);
+    colguard_or_kernel<<<wg, 256, 0, st>>>(W.qstats, (int)w, h, W.flag);
+    stats_to_bits<<<wg, 256, 0, st>>>(W.qstats, (int)w, W.bits);
+    scales_kernel<<<wg, 256, 0, st>>>(W.bits, (int)w, t, W.qscale, W.qexp);
+    const int64_t ldw = W.plan.ldw, qplane = h * ldw;
+    {
+        const int cpr = (int)((w + RV - 1) / RV);
+        const int rpi = cpr >= 256 ? 1 : 256 / cpr;
+        const int vq = ((reinterpret_cast<uintptr_t>(q) & 15) == 0) && (ldr % 2 == 0);
+        residues_kernel<<<(unsigned)((h + rpi - 1) / rpi), 256, 0, st>>>(q, ldr, h, (int)w, W.qscale, W.qres, ldw,
+                                                                          qplane, vq);
+        SK_LAUNCH_CHECK("oz trsm q residues");
+    }
+    if (prof) prof->mark(1, st);
+    CUtensorMap tq;
+    rc = make_tmap_3d(&tq, CU_TENSOR_MAP_DATA_TYPE_UINT8, W.qres, (uint64_t)w, (uint64_t)h, NMOD, (uint64_t)ldw,
+                      (uint64_t)qplane, 128, BK, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    const int64_t chunk = W.plan.chunk, pplane = chunk * h, oplane = chunk * ldw;
+    SK_CUDA(cudaFuncSetAttribute(gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    for (int64_t r0 = 0; r0 < m; r0 += chunk) {
+        const int64_t rows = std::min(chunk, m - r0);
+        const int rpi = (int)(256 / (h / RV));
+        rowres_kernel<<<(unsigned)std::min<int64_t>((rows + rpi - 1) / rpi, (int64_t)sms * 16), 256, 0, st>>>(
+            ap + r0 * ldap, ldap, rows, (int)h, t, W.pres, h, pplane, W.pexp, W.flag);
+        SK_LAUNCH_CHECK("oz trsm row residues");
+        if (prof) prof->mark(2, st);
+        CUtensorMap tp;
+        rc = make_tmap_3d(&tp, CU_TENSOR_MAP_DATA_TYPE_UINT8, W.pres, (uint64_t)h, (uint64_t)rows, NMOD, (uint64_t)h,
+                          (uint64_t)pplane, BK, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+        if (rc) return rc;
+        GemmParams gp{};
+        gp.ntn = (int)((w + BN - 1) / BN);
+        gp.ntiles = (int)((rows + BM - 1) / BM) * gp.ntn;
+        gp.splits = 1;
+        gp.units = NMOD * gp.ntiles;
+        gp.syrk = 0;
+        gp.rows = h;
+        gp.kchunk = h;
+        gp.mrows = rows;
+        gp.ldo = ldw;
+        gp.oplane = oplane;
+        gp.nout = (int)w;
+        gp.out = W.ores;
+        gemm_kernel<true><<<std::min(gp.units, sms), 640, SMEM, st>>>(tp, tq, gp);
+        SK_LAUNCH_CHECK("oz trsm product");
+        if (prof) prof->mark(3, st);
+        crt_sub_kernel<<<(unsigned)std::min<int64_t>(rows, (int64_t)sms * 8), 256, 0, st>>>(
+            W.ores, oplane, ldw, rows, (int)w, W.pexp, W.qexp, t, a + r0 * lda + h, lda, ap + r0 * ldap + h, ldap,
+            W.crt);
+        SK_LAUNCH_CHECK("oz trsm reconstruction");
+        if (prof) prof->mark(4, st);
+    }
+    return trsm_rec(ap + h, ldap, ap + h, ldap, m, w, r + h * ldr + h, ldr, W, st);
+}
+
 }  // namespace oz
 }  // namespace sk
 
 using namespace sk;
 
+namespace {
+thread_local int g_trsm_oz_fell_back = 0;
+int *trsm_guard_slot() {   // mapped pinned flag: read on the host after one synchronize
+    thread_local int *slot = nullptr;
+    if (!slot) {
+        void *p = nullptr;
+        if (cudaHostAlloc(&p, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return nullptr;
+        slot = static_cast<int *>(p);
+    }
+    return slot;
+}
+}  // namespace
+
 extern "C" {
+
+size_t sk_trsm_ozaki_workspace(int64_t m, int64_t n) {
+    if (n < 2) return 256;
+    oz::TrsmPlan p = oz::trsm_plan(m, n);
+    return oz::align_up256(p.pres) + oz::align_up256(p.ores) + oz::align_up256(p.qres) + oz::align_up256(p.aux) +
+           1024;
+}
+
+int sk_trsm_ozaki_fell_back(void) { return g_trsm_oz_fell_back; }
+
+int sk_trsm_ozaki_f64(const double *a, int64_t lda, int64_t m, int64_t n, const double *r, int64_t ldr, double *ap,
+                      int64_t ldap, sk_status *status, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    if (!a || !r || !ap || m < 0 || n <= 0 || lda < n || ldr < n || ldap < n || n > (1 << 20) || a == ap) {
+        set_error("sk_trsm_ozaki_f64: bad arguments (a and a_p must be distinct)");
+        return SK_ERR_ARG;
+    }
+    if (!ws || ws_bytes < sk_trsm_ozaki_workspace(m, n)) {
+        set_error("sk_trsm_ozaki_f64: workspace %zu < %zu", ws_bytes, sk_trsm_ozaki_workspace(m, n));
+        return SK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    int first_zero = 0;
+    int rc = trsm::first_zero_diagonal(r, ldr, (int)n, st, &first_zero);
+    if (rc) return rc;
+    if (first_zero != INT32_MAX) {
+        set_error("zero diagonal entry at index %d", first_zero);
+        return fill_status(status, SK_SINGULAR_TRIANGULAR, first_zero, 0.0, 0.0);
+    }
+    g_trsm_oz_fell_back = 0;
+    static const int64_t base = getenv("SK_TRSM_OZ_BASE") ? atoll(getenv("SK_TRSM_OZ_BASE")) : 1024;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(ap) | reinterpret_cast<uintptr_t>(r) |
+                           reinterpret_cast<uintptr_t>(a)) % 16 == 0) &&
+                         (ldap % 2 == 0) && (ldr % 2 == 0) && (lda % 2 == 0);
+    if (m == 0 || n <= std::max<int64_t>(base, 256) || !aligned) {
+        rc = trsm::launch(a, lda, m, (int)n, r, ldr, ap, ldap, st);
+        if (rc) return rc;
+        return fill_status(status, SK_OK, -1, 0, 0);
+    }
+    int *flag = trsm_guard_slot();
+    if (!flag) {
+        set_error("sk_trsm_ozaki_f64: pinned guard slot unavailable");
+        return SK_ERR_CUDA;
+    }
+    *reinterpret_cast<volatile int *>(flag) = 0;   // the stream is idle (synchronized above)
+    oz::TrsmWs W;
+    W.plan = oz::trsm_plan(m, n);
+    uint8_t *w = static_cast<uint8_t *>(ws);
+    W.pres = reinterpret_cast<int8_t *>(w);
+    w += oz::align_up256(W.plan.pres);
+    W.ores = reinterpret_cast<int8_t *>(w);
+    w += oz::align_up256(W.plan.ores);
+    W.qres = reinterpret_cast<int8_t *>(w);
+    w += oz::align_up256(W.plan.qres);
+    const int64_t wm = W.plan.wmax;
+    W.qstats = reinterpret_cast<double *>(w);                  // 2 wmax
+    W.qscale = W.qstats + 2 * wm;                              // wmax
+    W.bits = reinterpret_cast<unsigned long long *>(W.qscale + wm);   // wmax
+    W.qexp = reinterpret_cast<int *>(W.bits + wm);             // wmax ints (in a wmax-double slot)
+    W.pexp = W.qexp + 2 * wm;                                  // chunk ints
+    W.statws = reinterpret_cast<uint8_t *>(W.pexp + 2 * W.plan.chunk);
+    W.statws = reinterpret_cast<void *>((reinterpret_cast<uintptr_t>(W.statws) + 255) & ~uintptr_t(255));
+    W.statws_bytes = sk_colstats_workspace(wm);
+    W.flag = flag;
+    W.crt = oz::make_crt_sub();
+    W.base = std::max<int64_t>(base, 256);
+    if (oz::TrsmProf *prof = oz::trsm_prof()) prof->mark(-1, st);
+    rc = oz::trsm_rec(a, lda, ap, ldap, m, n, r, ldr, W, st);
+    if (rc) return rc;
+    if (oz::TrsmProf *prof = oz::trsm_prof()) prof->report();
+    SK_CUDA(cudaStreamSynchronize(st));
+    if (*reinterpret_cast<volatile int *>(flag)) {
+        // spiky rows of A_p / columns of R, or non-finite values: redo on the DMMA path
+        g_trsm_oz_fell_back = 1;
+        rc = trsm::launch(a, lda, m, (int)n, r, ldr, ap, ldap, st);
+        if (rc) return rc;
+    }
+    return fill_status(status, SK_OK, -1, 0, 0);
+}
 
 size_t sk_gram_ozaki_workspace(int64_t m, int64_t n, int syrk) {
     oz::Plan p = oz::make_plan(m, n, syrk != 0);
@@ -728,7 +1272,7 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
     const int vy = ((reinterpret_cast<uintptr_t>(y) & 15) == 0) && (ldy % 2 == 0);
     const int64_t plane = p.chunk * p.ldr;
     const size_t buf_bytes = (size_t)(syrk ? 1 : 2) * oz::NMOD * plane;
-    SK_CUDA(cudaFuncSetAttribute(oz::gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz::SMEM));
+    SK_CUDA(cudaFuncSetAttribute(oz::gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz::SMEM));
     // Two-stream pipeline: the residues of chunk c+1 (ALU-bound, side stream) run
     // while the INT8 GEMM of chunk c (tensor-bound, caller's stream) runs; chunks
     // alternate between two residue buffers.
@@ -796,7 +1340,7 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
         gp.kchunk = p.kchunk;
         gp.acc = acc;
         gp.n = (int)n;
-        oz::gemm_kernel<<<std::min(gp.units, sms), oz::THREADS, oz::SMEM, gs>>>(tx, ty, gp);
+        oz::gemm_kernel<false><<<std::min(gp.units, sms), oz::THREADS, oz::SMEM, gs>>>(tx, ty, gp);
         SK_LAUNCH_CHECK("oz gemm");
         if (!serial) SK_CUDA(cudaEventRecord(sp.gemm_done[buf], gs));
     }

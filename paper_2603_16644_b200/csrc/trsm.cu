@@ -338,6 +338,34 @@ int *zero_diag_slot() {
     return slot;
 }
 
+// the kernel alone (no argument or diagonal checks); used by the blocked INT8 TRSM too
+int launch(const double *a, int64_t lda, int64_t m, int n, const double *r, int64_t ldr, double *ap, int64_t ldap,
+           cudaStream_t st) {
+    if (m == 0) return SK_OK;
+    const bool vec = ((reinterpret_cast<uintptr_t>(ap) | reinterpret_cast<uintptr_t>(r) |
+                       reinterpret_cast<uintptr_t>(a)) % 16 == 0) &&
+                     (ldap % 2 == 0) && (ldr % 2 == 0) && (lda % 2 == 0);
+    SK_CUDA(cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    const unsigned grid = (unsigned)((m + BMR - 1) / BMR);
+    trsm_kernel<<<grid, THREADS, SMEM, st>>>(a, lda, m, n, r, ldr, ap, ldap, vec);
+    SK_LAUNCH_CHECK("trsm_kernel");
+    return SK_OK;
+}
+
+// first exactly-zero diagonal entry of R (INT32_MAX if none); synchronizes the stream
+int first_zero_diagonal(const double *r, int64_t ldr, int n, cudaStream_t st, int *out) {
+    int *first = zero_diag_slot();
+    if (!first) {
+        set_error("trsm: pinned status slot unavailable");
+        return SK_ERR_CUDA;
+    }
+    first_zero_diag<<<1, 1024, 0, st>>>(r, ldr, n, first);
+    SK_LAUNCH_CHECK("first_zero_diag");
+    SK_CUDA(cudaStreamSynchronize(st));
+    *out = *reinterpret_cast<volatile int *>(first);
+    return SK_OK;
+}
+
 }  // namespace trsm
 }  // namespace sk
 
@@ -355,26 +383,14 @@ extern "C" int sk_trsm_right_upper_f64(const double *a, int64_t lda, int64_t m, 
     // exactly-zero diagonal -> SingularTriangular (src/dense.py:231-233).  No stream-
     // ordered allocation here: a cudaMallocAsync / cudaFreeAsync pair per call made the
     // following synchronize wait on pool trimming (measured 0.2-900 ms per call).
-    int *first = trsm::zero_diag_slot();
-    if (!first) {
-        set_error("sk_trsm_right_upper_f64: pinned status slot unavailable");
-        return SK_ERR_CUDA;
-    }
-    trsm::first_zero_diag<<<1, 1024, 0, st>>>(r, ldr, (int)n, first);
-    SK_LAUNCH_CHECK("first_zero_diag");
-    SK_CUDA(cudaStreamSynchronize(st));
-    const int first_zero = *reinterpret_cast<volatile int *>(first);
+    int first_zero = 0;
+    int rc = trsm::first_zero_diagonal(r, ldr, (int)n, st, &first_zero);
+    if (rc) return rc;
     if (first_zero != INT32_MAX) {
         set_error("zero diagonal entry at index %d", first_zero);
         return fill_status(status, SK_SINGULAR_TRIANGULAR, first_zero, 0.0, 0.0);
     }
-    if (m == 0) return fill_status(status, SK_OK, -1, 0, 0);
-    const bool vec = ((reinterpret_cast<uintptr_t>(ap) | reinterpret_cast<uintptr_t>(r) |
-                       reinterpret_cast<uintptr_t>(a)) % 16 == 0) &&
-                     (ldap % 2 == 0) && (ldr % 2 == 0) && (lda % 2 == 0);
-    SK_CUDA(cudaFuncSetAttribute(trsm::trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm::SMEM));
-    const unsigned grid = (unsigned)((m + trsm::BMR - 1) / trsm::BMR);
-    trsm::trsm_kernel<<<grid, trsm::THREADS, trsm::SMEM, st>>>(a, lda, m, (int)n, r, ldr, ap, ldap, vec);
-    SK_LAUNCH_CHECK("trsm_kernel");
+    rc = trsm::launch(a, lda, m, (int)n, r, ldr, ap, ldap, st);
+    if (rc) return rc;
     return fill_status(status, SK_OK, -1, 0, 0);
 }

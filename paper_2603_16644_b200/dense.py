@@ -59,6 +59,17 @@ def _gram_engine(m: int, n: int, accumulate: bool, engine: str | None) -> str:
     return e
 
 
+TRSM_ENGINE = "auto"       # "dmma" (one left-looking DMMA kernel), "ozaki" (blocked, INT8 updates)
+TRSM_OZAKI_MIN_N = 1025    # the blocked solve splits only above its 1024-column leaves
+
+
+def _trsm_engine(m: int, n: int, inplace: bool, engine: str | None) -> str:
+    e = engine or TRSM_ENGINE
+    if e == "auto":
+        e = "ozaki" if (n >= TRSM_OZAKI_MIN_N and m * n * n >= OZAKI_MIN_WORK) else "dmma"
+    return "dmma" if inplace else e
+
+
 def _colstats(t: torch.Tensor, v: torch.Tensor | None = None) -> torch.Tensor:
     """[max_k |T[k, j]| for j] + [sum_k T[k, j]^2 for j] (+ [T^T v] if v is given)
     (device, f64, 2n or 3n)."""
@@ -127,16 +138,23 @@ def _new_ap(m: int, n: int, device) -> torch.Tensor:
     return torch.empty((m, n + pad), dtype=torch.float64, device=device)[:, :n]
 
 
-def _trsm(a: DMat | torch.Tensor, r: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-    """A_p = A R^{-1} (R upper, device f64)."""
+def _trsm(a: DMat | torch.Tensor, r: torch.Tensor, out: torch.Tensor | None = None,
+          engine: str | None = None) -> torch.Tensor:
+    """A_p = A R^{-1} (R upper, device f64).  Large solves take the blocked path whose
+    off-diagonal updates run on the INT8 tensor cores (sk_trsm_ozaki_f64)."""
     at = _rm(a.t if isinstance(a, DMat) else a)
     r = _rm(r)
     m, n = at.shape
     if out is None:
         out = _new_ap(m, n, at.device)
     st = _lib.SkStatus()
-    call("sk_trsm_right_upper_f64", at.data_ptr(), at.stride(0), m, n, r.data_ptr(), r.stride(0),
-         out.data_ptr(), out.stride(0), C.byref(st), stream_handle())
+    if _trsm_engine(m, n, out.data_ptr() == at.data_ptr(), engine) == "ozaki":
+        wp, wn = WORKSPACE.get(_lib.lib().sk_trsm_ozaki_workspace(m, n))
+        call("sk_trsm_ozaki_f64", at.data_ptr(), at.stride(0), m, n, r.data_ptr(), r.stride(0),
+             out.data_ptr(), out.stride(0), C.byref(st), wp, wn, stream_handle())
+    else:
+        call("sk_trsm_right_upper_f64", at.data_ptr(), at.stride(0), m, n, r.data_ptr(), r.stride(0),
+             out.data_ptr(), out.stride(0), C.byref(st), stream_handle())
     return out
 
 
