@@ -156,15 +156,45 @@ OZ_MODULI = 16          # csrc/ozaki.cu NMOD
 OZ_RESIDUE_BYTES = 24   # per element and operand: 8 read + 16 written
 
 
-def engine_roofline(m, n, d, method, auto, ozaki):
+TRSM_LEAF = 1024        # csrc/ozaki.cu: blocked TRSM leaves (SK_TRSM_OZ_BASE default)
+
+
+def trsm_blocks(n, base=TRSM_LEAF):
+    """The blocked TRSM's recursion (csrc/ozaki.cu trsm_split / trsm_rec): leaf widths
+    and (h, w) of every INT8 update."""
+    if n <= base:
+        return [n], []
+    h = min((n // 2 + 255) // 256 * 256, 8192)
+    l1, u1 = trsm_blocks(h, base)
+    l2, u2 = trsm_blocks(n - h, base)
+    return l1 + l2, u1 + [(h, n - h)] + u2
+
+
+def trsm_roofline(m, n, blocked):
+    """TRSM stage roofline (s): FP64 DMMA leaves m nl^2 / DMMA peak; each update as 16
+    INT8 products 2 m h w / INT8 peak plus its HBM passes (A_p[:, :h] read + 16 residue
+    planes written: 24 B per element; 16 product planes written and read, A read, A_p
+    written: 48 B per element of m x w)."""
+    p64, p8, hbm = fp64_peak()[0] * 1e12, int8_peak()[0] * 1e12, hbm_peak()[0] * 1e9
+    if not blocked:
+        return float(m) * n * n / p64
+    leaves, ups = trsm_blocks(n)
+    t = sum(float(m) * nl * nl for nl in leaves) / p64
+    for h, w in ups:
+        t += 2.0 * OZ_MODULI * m * h * w / p8 + (24.0 * m * h + 48.0 * m * w) / hbm
+    return t
+
+
+def engine_roofline(m, n, d, method, auto, ozaki, trsm_blocked=False):
     """Roofline of the implemented solve, engine by engine (ms):
-    TRSM on FP64 DMMA; the kappa0 SYRK and the PNE/HPNE Gram on the INT8 tensor
-    cores (16 exact modular products, symmetric half for SYRKs) plus their residue
-    and column-scan HBM passes; the binary16 sketch on the fp16 tensor cores (or one
-    read of A if that is slower); the residual pass on HBM."""
+    TRSM on FP64 DMMA (blocked: DMMA leaves + INT8 updates, trsm_roofline); the kappa0
+    SYRK and the PNE/HPNE Gram on the INT8 tensor cores (16 exact modular products,
+    symmetric half for SYRKs) plus their residue and column-scan HBM passes; the
+    binary16 sketch on the fp16 tensor cores (or one read of A if that is slower); the
+    residual pass on HBM."""
     p64, p8, p16, hbm = fp64_peak()[0] * 1e12, int8_peak()[0] * 1e12, fp16_peak()[0] * 1e12, hbm_peak()[0] * 1e9
     el = float(m) * n
-    t = {"trsm": el * n / p64, "report": 8 * el / hbm,
+    t = {"trsm": trsm_roofline(m, n, trsm_blocked), "report": 8 * el / hbm,
          "sketch": max(2.0 * d * el / p16, 10 * el / hbm)}
 
     def gram(syrk):
@@ -176,6 +206,37 @@ def engine_roofline(m, n, d, method, auto, ozaki):
         t["kappa0"] = gram(True)
     t["gram"] = gram(method != "hpne")
     return t
+
+
+def time_trsm_leaf(a, m, n, nl, reps=3):
+    """One DMMA leaf launch of the blocked TRSM (A[:, :nl] at pitch n -> A_p scratch at
+    pitch n, as the solve issues it), CUDA events on the current stream, ms per launch."""
+    import ctypes as C
+    import torch
+    from paper_2603_16644_b200 import _lib, release_scratch
+    from paper_2603_16644_b200.device import call, stream_handle
+    release_scratch()
+    out = torch.empty_like(a)
+    g = torch.Generator(device=a.device)
+    g.manual_seed(3)
+    r = torch.triu(torch.randn(n, n, dtype=torch.float64, device=a.device, generator=g)) + \
+        8 * torch.eye(n, dtype=torch.float64, device=a.device)
+    st = _lib.SkStatus()
+
+    def leaf():
+        call("sk_trsm_right_upper_f64", a.data_ptr(), n, m, nl, r.data_ptr(), n, out.data_ptr(), n,
+             C.byref(st), stream_handle())
+    leaf()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        leaf()
+    e1.record()
+    torch.cuda.synchronize()
+    del out
+    torch.cuda.empty_cache()
+    return e0.elapsed_time(e1) / reps
 
 
 def ncu_traffic(kernel_key):
@@ -359,13 +420,28 @@ def run_ours(args, rank, world):
                "rel_error": rep.relative_error, "relative_residual": rep.relative_residual}
 
     # roofline of the dominant stage (CUDA events around the stage, same stream)
-    from paper_2603_16644_b200.dense import _gram_engine
+    from paper_2603_16644_b200.dense import _gram_engine, _trsm_engine
     ozaki = _gram_engine(m, n, False, None) == "ozaki"
     if ozaki and "check" in stages and args.precision == "auto":
         stages["kappa0"] = stages.get("kappa0", 0.0) + stages.pop("check")   # the kappa0 SYRK runs in "check"
+    trsm_blocked = _trsm_engine(m, n, False, None) == "ozaki"
     dom = max((k for k in stages if stage_work(k, m, n, d, args.method, level)), key=lambda k: stages[k])
     flops, bytes_, bound = stage_work(dom, m, n, d, args.method, level)
-    if bound == "tensor" and ozaki and dom in ("gram", "kappa0"):
+    if dom == "trsm" and trsm_blocked:
+        # the dominant kernel is the DMMA leaf solve (2 launches per solve at n = 2048):
+        # one leaf launch of the solve's shape, timed live with CUDA events
+        leaves, _ = trsm_blocks(n)
+        leaf_ms = time_trsm_leaf(a, m, n, leaves[0])
+        peak, src = fp64_peak()
+        lf = float(m) * leaves[0] ** 2
+        achieved = lf / (leaf_ms * 1e-3) / 1e12
+        roof = {"kernel": "trsm leaf (trsm_kernel, m x %d of the blocked TRSM)" % leaves[0], "bound": "tensor",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": ncu_traffic("trsm_leaf"), "peak_source": src, "algorithmic_flops": lf,
+                "launch_ms": leaf_ms, "launches_per_solve": len(leaves),
+                "stage_frac": trsm_roofline(m, n, True) * 1e3 / stages["trsm"],
+                "pipe": "FP64 DMMA (mma.sync m8n8k4); updates on INT8 tcgen05 (Ozaki-II)"}
+    elif bound == "tensor" and ozaki and dom in ("gram", "kappa0"):
         peak, src = int8_peak()
         ops = OZ_MODULI * flops        # 16 exact INT8 products of the FP64 SYRK / GEMM
         achieved = ops / (stages[dom] * 1e-3) / 1e12
@@ -396,7 +472,7 @@ def run_ours(args, rank, world):
     fp64_total = (m * n * n if args.precision == "auto" else 0) + m * n * n + \
         (2.0 if args.method == "hpne" else 1.0) * m * n * n
     t_roof_fp64 = fp64_total / (fp64_peak()[0] * 1e12) + 2 * 8.0 * m * n / (hbm_peak()[0] * 1e9)
-    eng = engine_roofline(m, n, d, args.method, args.precision == "auto", ozaki)
+    eng = engine_roofline(m, n, d, args.method, args.precision == "auto", ozaki, trsm_blocked)
     t_roof = sum(eng.values())
 
     # ---- e2e: host buffers, H2D + D2H inside the timed region ----
@@ -446,7 +522,10 @@ def run_ours(args, rank, world):
             "roofline": roof,
             "roofline_solve": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
                                "stages_roof_ms": {k: v * 1e3 for k, v in eng.items()},
-                               "model": ("per engine: TRSM m n^2 / FP64 DMMA peak; kappa0 SYRK + Gram as 16 INT8 "
+                               "model": (("blocked TRSM: DMMA leaves m nl^2 / FP64 DMMA peak + INT8 updates "
+                                          "(16 products / INT8 peak + residue and reconstruction passes / HBM)"
+                                          if trsm_blocked else "TRSM m n^2 / FP64 DMMA peak") +
+                                         "; kappa0 SYRK + Gram as 16 INT8 "
                                          "products / measured INT8 peak + residue/column passes / HBM"
                                          if ozaki else "FP64 flops / measured DGEMM peak") +
                                         "; sketch 2dmn / fp16 peak; residual 8mn / HBM",

@@ -465,13 +465,37 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ 
                     const int col0 = tn * BN + cb * 32;
                     if (row < p.mrows && col0 < p.nout) {
                         uint32_t w[8];
+                        if (p.rows <= 1024) {
+                            // |v| <= 1024 * 127^2 < 2^24: exact in FP32; two rounding steps on
+                            // FFMA2 (the first quotient may be off by one) leave |r| <= p/2
+                            const uint64_t ip2 = f2pack(fip, fip), mp2 = f2pack(-fp, -fp),
+                                           mg = f2pack(FMAGIC, FMAGIC), nmg = f2pack(-FMAGIC, -FMAGIC);
 #pragma unroll
-                        for (int q4 = 0; q4 < 8; ++q4) {
-                            const uint32_t b0 = i32_residue((int)v[4 * q4], fp, fip, c13),
-                                           b1 = i32_residue((int)v[4 * q4 + 1], fp, fip, c13),
-                                           b2 = i32_residue((int)v[4 * q4 + 2], fp, fip, c13),
-                                           b3 = i32_residue((int)v[4 * q4 + 3], fp, fip, c13);
-                            w[q4] = __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
+                            for (int q4 = 0; q4 < 8; ++q4) {
+                                uint32_t b[4];
+#pragma unroll
+                                for (int hh = 0; hh < 2; ++hh) {
+                                    const uint64_t f = f2pack((float)(int)v[4 * q4 + 2 * hh],
+                                                              (float)(int)v[4 * q4 + 2 * hh + 1]);
+                                    const uint64_t r1 = ffma2(fadd2(ffma2(f, ip2, mg), nmg), mp2, f);
+                                    const uint64_t r2 = ffma2(fadd2(ffma2(r1, ip2, mg), nmg), mp2, r1);
+                                    const uint64_t rb = fadd2(r2, mg);
+                                    b[2 * hh] = (uint32_t)rb;
+                                    b[2 * hh + 1] = (uint32_t)(rb >> 32);
+                                }
+                                w[q4] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040),
+                                                    0x5410);
+                            }
+                        } else {
+#pragma unroll
+                            for (int q4 = 0; q4 < 8; ++q4) {
+                                const uint32_t b0 = i32_residue((int)v[4 * q4], fp, fip, c13),
+                                               b1 = i32_residue((int)v[4 * q4 + 1], fp, fip, c13),
+                                               b2 = i32_residue((int)v[4 * q4 + 2], fp, fip, c13),
+                                               b3 = i32_residue((int)v[4 * q4 + 3], fp, fip, c13);
+                                w[q4] = __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040),
+                                                    0x5410);
+                            }
                         }
                         int8_t *dst = dst_row + col0;
                         if (col0 + 32 <= p.nout) {
@@ -810,7 +834,12 @@ crt_sub_kernel(const int8_t *__restrict__ planes, int64_t plane, int64_t ldo, in
             for (int q = 0; q < 4; ++q) {
                 const double qq = rint(fma(s1[q], 0x1p76, s2[q]) * c.rm);
                 const double v = fma(fma(-qq, c.ma, s1[q]), 0x1p76, fma(-qq, c.mr, s2[q]));
-                if (q < nc) orow[q] = ar[q] - ldexp(v, erow + fq[j0 + q]);
+                if (q < nc) {
+                    const int e = erow + fq[j0 + q];
+                    // 2^e from its bits (|e| < 1000 always in practice; ldexp otherwise)
+                    const double sc = __longlong_as_double((long long)(e + 1023) << 52);
+                    orow[q] = ar[q] - ((e > -1000 && e < 1000) ? v * sc : ldexp(v, e));
+                }
             }
         }
     }
