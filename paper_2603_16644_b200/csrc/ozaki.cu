@@ -797,15 +797,29 @@ crt_sub_kernel(const int8_t *__restrict__ planes, int64_t plane, int64_t ldo, in
             const int nc = min(4, w - j0);
             uint32_t pk[NMOD];
             const int8_t *src = planes + r * ldo + j0;
+            const double *ar = a + r * lda + j0;
+            double av[4];
+            int ev[4];
             if (nc == 4) {
 #pragma unroll
                 for (int k = 0; k < NMOD; ++k) pk[k] = __ldcs(reinterpret_cast<const uint32_t *>(src + k * plane));
+                // A and the exponents in flight during the reconstruction (rows 32-byte aligned)
+                const double2 a01 = __ldcs(reinterpret_cast<const double2 *>(ar)),
+                              a23 = __ldcs(reinterpret_cast<const double2 *>(ar) + 1);
+                av[0] = a01.x; av[1] = a01.y; av[2] = a23.x; av[3] = a23.y;
+                const int4 f4 = __ldg(reinterpret_cast<const int4 *>(fq + j0));
+                ev[0] = f4.x; ev[1] = f4.y; ev[2] = f4.z; ev[3] = f4.w;
             } else {
 #pragma unroll
                 for (int k = 0; k < NMOD; ++k) {
                     uint32_t x = 0;
                     for (int q = 0; q < nc; ++q) x |= (uint32_t)(uint8_t)src[k * plane + q] << (8 * q);
                     pk[k] = x;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    av[q] = q < nc ? ar[q] : 0.0;
+                    ev[q] = q < nc ? fq[j0 + q] : 0;
                 }
             }
             double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
@@ -828,18 +842,22 @@ crt_sub_kernel(const int8_t *__restrict__ planes, int64_t plane, int64_t ldo, in
                     s2[2 * h2 + 1] = fma(y1, c.wr[k], s2[2 * h2 + 1]);
                 }
             }
-            const double *ar = a + r * lda + j0;
-            double *orow = out + r * ldout + j0;
+            double res[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const double qq = rint(fma(s1[q], 0x1p76, s2[q]) * c.rm);
                 const double v = fma(fma(-qq, c.ma, s1[q]), 0x1p76, fma(-qq, c.mr, s2[q]));
-                if (q < nc) {
-                    const int e = erow + fq[j0 + q];
-                    // 2^e from its bits (|e| < 1000 always in practice; ldexp otherwise)
-                    const double sc = __longlong_as_double((long long)(e + 1023) << 52);
-                    orow[q] = ar[q] - ((e > -1000 && e < 1000) ? v * sc : ldexp(v, e));
-                }
+                const int e = erow + ev[q];
+                // 2^e from its bits (|e| < 1000 always in practice; ldexp otherwise)
+                const double sc = __longlong_as_double((long long)(e + 1023) << 52);
+                res[q] = av[q] - ((e > -1000 && e < 1000) ? v * sc : ldexp(v, e));
+            }
+            double *orow = out + r * ldout + j0;
+            if (nc == 4) {
+                reinterpret_cast<double2 *>(orow)[0] = make_double2(res[0], res[1]);
+                reinterpret_cast<double2 *>(orow)[1] = make_double2(res[2], res[3]);
+            } else {
+                for (int q = 0; q < nc; ++q) orow[q] = res[q];
             }
         }
     }
