@@ -638,7 +638,7 @@ __global__ void crt_kernel(const int32_t *__restrict__ acc, int n, int syrk, con
 // whose max^2 k > F^2 sum^2 (spiky) or with non-finite entries raise *flag.
 __global__ void __launch_bounds__(256, SK_OZ_RES_MINB)
 rowres_kernel(const double *__restrict__ x, int64_t ldx, int64_t rows, int k, int t, int8_t *__restrict__ out,
-              int64_t ldk, int64_t plane, int *__restrict__ expo, int *flag) {
+              int64_t ldk, int64_t plane, int *__restrict__ expo, int *flag, int nm) {
     __shared__ double smx[8], sss[8];
     const int cpr = k / RV, rpi = 256 / cpr, wpr = cpr / 32;
     const int sub = threadIdx.x / cpr, c0 = (threadIdx.x % cpr) * RV;
@@ -719,6 +719,7 @@ rowres_kernel(const double *__restrict__ x, int64_t ldx, int64_t rows, int k, in
         }
 #pragma unroll
         for (int kk = 0; kk < NMOD; ++kk) {
+            if (kk >= nm) break;   // the first nm moduli (uniform)
             uint32_t w[2];
 #pragma unroll
             for (int q4 = 0; q4 < 2; ++q4) {
@@ -775,7 +776,9 @@ static_assert(crt_q_ok(), "CRT inverse table");
 // |C'| < M / 2^12.  The residue arithmetic runs two columns at a time on FFMA2.
 struct CrtSub {
     double wa[NMOD], wr[NMOD];
+    float qf[NMOD], qip[NMOD];   // (M / p_k)^-1 mod p_k and that / p_k
     double ma, mr, rm;
+    int nm;                      // moduli in use (the first nm): M = p_0 ... p_{nm-1}
 };
 
 __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
@@ -784,6 +787,7 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
     return d;
 }
 
+template <int NM>
 __global__ void __launch_bounds__(256)
 crt_sub_kernel(const int8_t *__restrict__ planes, int64_t plane, int64_t ldo, int64_t rows, int w,
                const int *__restrict__ er, const int *__restrict__ fq, int t, const double *__restrict__ a,
@@ -802,7 +806,8 @@ crt_sub_kernel(const int8_t *__restrict__ planes, int64_t plane, int64_t ldo, in
             int ev[4];
             if (nc == 4) {
 #pragma unroll
-                for (int k = 0; k < NMOD; ++k) pk[k] = __ldcs(reinterpret_cast<const uint32_t *>(src + k * plane));
+                for (int k = 0; k < NMOD; ++k)
+                    pk[k] = k < NM ? __ldcs(reinterpret_cast<const uint32_t *>(src + k * plane)) : 0x80808080u;
                 // A and the exponents in flight during the reconstruction (rows 32-byte aligned)
                 const double2 a01 = __ldcs(reinterpret_cast<const double2 *>(ar)),
                               a23 = __ldcs(reinterpret_cast<const double2 *>(ar) + 1);
@@ -813,7 +818,7 @@ crt_sub_kernel(const int8_t *__restrict__ planes, int64_t plane, int64_t ldo, in
 #pragma unroll
                 for (int k = 0; k < NMOD; ++k) {
                     uint32_t x = 0;
-                    for (int q = 0; q < nc; ++q) x |= (uint32_t)(uint8_t)src[k * plane + q] << (8 * q);
+                    for (int q = 0; q < nc && k < NM; ++q) x |= (uint32_t)(uint8_t)src[k * plane + q] << (8 * q);
                     pk[k] = x;
                 }
 #pragma unroll
@@ -825,8 +830,9 @@ crt_sub_kernel(const int8_t *__restrict__ planes, int64_t plane, int64_t ldo, in
             double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int k = 0; k < NMOD; ++k) {
+                if (k >= NM) break;
                 const uint32_t u = pk[k] ^ 0x80808080u;   // signed byte r -> r + 128
-                const float p = (float)pm(k), q = (float)crt_q(k), qip = (float)crt_q(k) / (float)pm(k);
+                const float p = (float)pm(k), q = c.qf[k], qip = c.qip[k];
 #pragma unroll
                 for (int h2 = 0; h2 < 2; ++h2) {
                     const uint64_t rr = fadd2(f2pack(__uint_as_float(__byte_perm(u, 0x4B000000u, 0x7540 + 2 * h2)),
@@ -953,23 +959,37 @@ TrsmPlan trsm_plan(int64_t m, int64_t n) {
     return p;
 }
 
-CrtSub make_crt_sub() {
-    CrtSub c;
+CrtSub make_crt_sub(int nm) {
+    CrtSub c{};
+    c.nm = nm;
     unsigned __int128 M = 1;
-    for (int k = 0; k < NMOD; ++k) M *= (unsigned)pm(k);
+    for (int k = 0; k < nm; ++k) M *= (unsigned)pm(k);
     const unsigned __int128 low = (((unsigned __int128)1) << 76) - 1;
     auto dbl = [](unsigned __int128 v) {
         return (double)(uint64_t)(v >> 64) * 18446744073709551616.0 + (double)(uint64_t)v;
     };
-    for (int k = 0; k < NMOD; ++k) {
+    for (int k = 0; k < nm; ++k) {
         const unsigned __int128 W = M / (unsigned)pm(k);
         c.wa[k] = dbl(W >> 76);
         c.wr[k] = dbl(W & low);
+        const int q = inv_mod((int)(W % (unsigned)pm(k)), pm(k));
+        c.qf[k] = (float)q;
+        c.qip[k] = (float)q / (float)pm(k);
     }
     c.ma = dbl(M >> 76);
     c.mr = dbl(M & low);
     c.rm = 1.0 / dbl(M);
     return c;
+}
+
+// fewest leading moduli whose product exceeds 2 K 2^(2t) (|C'| < M / 2 with margin)
+int moduli_needed(int64_t K, int t) {
+    double lg = 0.0;
+    for (int k = 0; k < NMOD; ++k) {
+        lg += log2((double)pm(k));
+        if (lg - 1.0 - 0.01 >= 2.0 * t + log2((double)std::max<int64_t>(K, 1))) return k + 1;
+    }
+    return NMOD;
 }
 
 struct TrsmWs {
@@ -980,7 +1000,6 @@ struct TrsmWs {
     void *statws;
     size_t statws_bytes;
     TrsmPlan plan;
-    CrtSub crt;
     int64_t base;
 };
 
@@ -1042,6 +1061,8 @@ int trsm_rec(const double *a, int64_t lda, double *ap, int64_t ldap, int64_t m, 
     if (rc) return rc;
     const int sms = sm_count();
     const int t = choose_t(h);
+    const int nm = std::max(15, moduli_needed(h, t));   // 15 at h = 1024, t = 51
+    const CrtSub crt = make_crt_sub(nm);
     // Q = R[:h, h:]: column scales, guard, residues (MN-major B planes [mod][h][ldw])
     const double *q = r + h;
     rc = sk_colstats_f64(q, ldr, h, w, nullptr, W.qstats, W.statws, W.statws_bytes, st);
@@ -1070,7 +1091,7 @@ int trsm_rec(const double *a, int64_t lda, double *ap, int64_t ldap, int64_t m, 
         const int64_t rows = std::min(chunk, m - r0);
         const int rpi = (int)(256 / (h / RV));
         rowres_kernel<<<(unsigned)std::min<int64_t>((rows + rpi - 1) / rpi, (int64_t)sms * 16), 256, 0, st>>>(
-            ap + r0 * ldap, ldap, rows, (int)h, t, W.pres, h, pplane, W.pexp, W.flag);
+            ap + r0 * ldap, ldap, rows, (int)h, t, W.pres, h, pplane, W.pexp, W.flag, nm);
         SK_LAUNCH_CHECK("oz trsm row residues");
         if (prof) prof->mark(2, st);
         CUtensorMap tp;
@@ -1081,7 +1102,7 @@ int trsm_rec(const double *a, int64_t lda, double *ap, int64_t ldap, int64_t m, 
         gp.ntn = (int)((w + BN - 1) / BN);
         gp.ntiles = (int)((rows + BM - 1) / BM) * gp.ntn;
         gp.splits = 1;
-        gp.units = NMOD * gp.ntiles;
+        gp.units = nm * gp.ntiles;
         gp.syrk = 0;
         gp.rows = h;
         gp.kchunk = h;
@@ -1093,9 +1114,10 @@ int trsm_rec(const double *a, int64_t lda, double *ap, int64_t ldap, int64_t m, 
         gemm_kernel<true><<<std::min(gp.units, sms), 640, SMEM, st>>>(tp, tq, gp);
         SK_LAUNCH_CHECK("oz trsm product");
         if (prof) prof->mark(3, st);
-        crt_sub_kernel<<<(unsigned)std::min<int64_t>(rows, (int64_t)sms * 8), 256, 0, st>>>(
+        auto crt_fn = nm == 15 ? crt_sub_kernel<15> : crt_sub_kernel<16>;
+        crt_fn<<<(unsigned)std::min<int64_t>(rows, (int64_t)sms * 8), 256, 0, st>>>(
             W.ores, oplane, ldw, rows, (int)w, W.pexp, W.qexp, t, a + r0 * lda + h, lda, ap + r0 * ldap + h, ldap,
-            W.crt);
+            crt);
         SK_LAUNCH_CHECK("oz trsm reconstruction");
         if (prof) prof->mark(4, st);
     }
@@ -1184,7 +1206,6 @@ int sk_trsm_ozaki_f64(const double *a, int64_t lda, int64_t m, int64_t n, const 
     W.statws = reinterpret_cast<void *>((reinterpret_cast<uintptr_t>(W.statws) + 255) & ~uintptr_t(255));
     W.statws_bytes = sk_colstats_workspace(wm);
     W.flag = flag;
-    W.crt = oz::make_crt_sub();
     W.base = std::max<int64_t>(base, 256);
     if (oz::TrsmProf *prof = oz::trsm_prof()) prof->mark(-1, st);
     rc = oz::trsm_rec(a, lda, ap, ldap, m, n, r, ldr, W, st);
