@@ -340,8 +340,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ 
     uint64_t *full = reinterpret_cast<uint64_t *>(sb + STAGES * B_BYTES);
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;
-    uint64_t *tempty = tfull + 1;
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 1);
+    uint64_t *tempty = tfull + 1;                                   // [2] in product mode
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int NEPI = (NTHR / 32) - EPI_WARP0;
@@ -352,6 +352,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ 
         }
         tc::mbar_init(tfull, 1);
         tc::mbar_init(tempty, NEPI);
+        tc::mbar_init(tempty + 1, NEPI);
         tc::mbar_fence_init();
         tc::tma_prefetch_desc(&tmap_x);
         tc::tma_prefetch_desc(&tmap_y);
@@ -408,9 +409,46 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ 
                 int mod, split, tile, nkb;
                 int64_t k0;
                 unit_coords(u, mod, split, tile, k0, nkb);
-                tc::mbar_wait(tempty, tphase ^ 1);
-                tc::tc_fence_after();
-                for (int kb = 0; kb < nkb; ++kb) {
+                if constexpr (PROD) {
+                    // Accumulator 0 is released by the epilogue before accumulator 1: issue
+                    // accumulator 0's MMAs for the first (resident) stages as soon as it is
+                    // free, then accumulator 1's for the same stages once that is free too,
+                    // so the tile's main loop starts under the previous tile's epilogue.
+                    const int pre = nkb < STAGES ? nkb : STAGES;
+                    const int st0 = stage;
+                    const unsigned ph0 = phase;
+                    tc::mbar_wait(tempty, tphase ^ 1);
+                    tc::tc_fence_after();
+                    for (int kb = 0; kb < pre; ++kb) {
+                        tc::mbar_wait(&full[stage], phase);
+                        tc::tc_fence_after();
+                        const uint64_t ad0 = tc::desc_kmajor_sw128(smem_u32(sa + stage * A_BYTES));
+                        const uint64_t bd = tc::desc_mnmajor_sw128(smem_u32(sb + stage * B_BYTES), BOX_BYTES, 1024);
+#pragma unroll
+                        for (int k = 0; k < BK / UMMA_K; ++k)
+                            tc::mma_i8_ss(tmem, ad0 + (uint64_t)(UMMA_K >> 4) * k,
+                                          bd + (uint64_t)((UMMA_K * 128) >> 4) * k, idesc, (kb | k) ? 1u : 0u);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    tc::mbar_wait(tempty + 1, tphase ^ 1);
+                    tc::tc_fence_after();
+                    stage = st0;
+                    phase = ph0;
+                    for (int kb = 0; kb < pre; ++kb) {
+                        const uint64_t ad1 = tc::desc_kmajor_sw128(smem_u32(sa + stage * A_BYTES) + BOX_BYTES);
+                        const uint64_t bd = tc::desc_mnmajor_sw128(smem_u32(sb + stage * B_BYTES), BOX_BYTES, 1024);
+#pragma unroll
+                        for (int k = 0; k < BK / UMMA_K; ++k)
+                            tc::mma_i8_ss(tmem + BN, ad1 + (uint64_t)(UMMA_K >> 4) * k,
+                                          bd + (uint64_t)((UMMA_K * 128) >> 4) * k, idesc, (kb | k) ? 1u : 0u);
+                        tc::mma_commit(&empty[stage]);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                } else {
+                    tc::mbar_wait(tempty, tphase ^ 1);
+                    tc::tc_fence_after();
+                }
+                for (int kb = PROD ? (nkb < STAGES ? nkb : STAGES) : 0; kb < nkb; ++kb) {
                     tc::mbar_wait(&full[stage], phase);
                     tc::tc_fence_after();
                     const uint32_t a0 = smem_u32(sa + stage * A_BYTES), b0 = smem_u32(sb + stage * B_BYTES);
@@ -447,20 +485,23 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ 
             tc::tc_fence_after();
             tphase ^= 1;
             if constexpr (PROD) {
-                // 16 warps: (accumulator, 128-column half, lane quadrant); each thread
-                // turns 128 int32 values of one row into residue bytes
+                // 16 warps = (lane quadrant, 64-column quarter); all of them drain
+                // accumulator 0 first and release it (tempty[0]), then accumulator 1
+                // (tempty[1]), so the next tile's MMAs start under this epilogue
                 int tm, tn;
                 tile_coords(p, tile, tm, tn);
-                const int half = (warp - EPI_WARP0) >> 3;
+                const int cq = (warp - EPI_WARP0) >> 2;
                 const int pmod = pm(mod);
                 const float fp = (float)pmod, fip = 1.0f / fp;
                 const int c13 = (int)((8192 % pmod) > (pmod - 1) / 2 ? (8192 % pmod) - pmod : 8192 % pmod);
-                const int64_t row = (int64_t)tm * BM + acc * UMMA_M + lg * 32 + lane;
+#pragma unroll 1
+              for (int acc2 = 0; acc2 < 2; ++acc2) {
+                const int64_t row = (int64_t)tm * BM + acc2 * UMMA_M + lg * 32 + lane;
                 int8_t *dst_row = p.out + (size_t)mod * p.oplane + (size_t)row * p.ldo;
 #pragma unroll 1
-                for (int cb = half * 4; cb < half * 4 + 4; ++cb) {
+                for (int cb = cq * 2; cb < cq * 2 + 2; ++cb) {
                     uint32_t v[32];
-                    tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
+                    tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc2 * BN + cb * 32), v);
                     tc::tmem_ld_wait();
                     const int col0 = tn * BN + cb * 32;
                     if (row < p.mrows && col0 < p.nout) {
@@ -508,7 +549,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ 
                 }
                 tc::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(tempty);
+                if (lane == 0) tc::mbar_arrive(tempty + acc2);
+              }
                 continue;
             }
             // acc[mod][row][col] = (acc + C_partial) mod p, in [0, p): one unit per
