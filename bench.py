@@ -152,8 +152,26 @@ def fp16_peak():
     return _peak_file("fp64_peak.json", "fp16_tflops_burst", 1546.0, "fallback: cuBLAS fp16 on B200 (not measured)")
 
 
-OZ_MODULI = 16          # csrc/ozaki.cu NMOD
-OZ_RESIDUE_BYTES = 24   # per element and operand: 8 read + 16 written
+OZ_P = (255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193, 191)   # csrc/ozaki.cu pm()
+OZ_TRSM_MODULI = 15     # csrc/ozaki.cu trsm_rec: |C'| < 2^113 at h = 1024, t = 51
+
+
+def gram_moduli(m):
+    """csrc/ozaki.cu gram_moduli: fewest leading moduli with t >= 68 - log2 m (cap 51)."""
+    import math
+    L = math.log2(max(m, 1))
+    tmin = min(51, math.ceil(68.0 - L))
+    lg = 0.0
+    for k, p in enumerate(OZ_P):
+        lg += math.log2(p)
+        t = min(51, math.floor((lg - 1.0 - L - 0.01) / 2.0))
+        if t >= tmin:
+            return k + 1
+    return len(OZ_P)
+
+
+def oz_residue_bytes(nm):
+    return 8 + nm          # per element and operand: 8 read + nm residue bytes written
 
 
 TRSM_LEAF = 1024        # csrc/ozaki.cu: blocked TRSM leaves (SK_TRSM_OZ_BASE default)
@@ -181,7 +199,8 @@ def trsm_roofline(m, n, blocked):
     leaves, ups = trsm_blocks(n)
     t = sum(float(m) * nl * nl for nl in leaves) / p64
     for h, w in ups:
-        t += 2.0 * OZ_MODULI * m * h * w / p8 + (24.0 * m * h + 48.0 * m * w) / hbm
+        t += 2.0 * OZ_TRSM_MODULI * m * h * w / p8 + ((8.0 + OZ_TRSM_MODULI) * m * h +
+                                                             (2 * OZ_TRSM_MODULI + 16.0) * m * w) / hbm
     return t
 
 
@@ -200,8 +219,9 @@ def engine_roofline(m, n, d, method, auto, ozaki, trsm_blocked=False):
     def gram(syrk):
         if not ozaki:
             return (1.0 if syrk else 2.0) * el * n / p64
-        ops = 2.0 * OZ_MODULI * el * n * (0.5 if syrk else 1.0)
-        return ops / p8 + (1 if syrk else 2) * (OZ_RESIDUE_BYTES + 8) * el / hbm
+        nm = gram_moduli(m)
+        ops = 2.0 * nm * el * n * (0.5 if syrk else 1.0)
+        return ops / p8 + (1 if syrk else 2) * (oz_residue_bytes(nm) + 8) * el / hbm
     if auto:
         t["kappa0"] = gram(True)
     t["gram"] = gram(method != "hpne")
@@ -443,7 +463,7 @@ def run_ours(args, rank, world):
                 "pipe": "FP64 DMMA (mma.sync m8n8k4); updates on INT8 tcgen05 (Ozaki-II)"}
     elif bound == "tensor" and ozaki and dom in ("gram", "kappa0"):
         peak, src = int8_peak()
-        ops = OZ_MODULI * flops        # 16 exact INT8 products of the FP64 SYRK / GEMM
+        ops = gram_moduli(m) * flops   # exact INT8 products (15 moduli at 4M rows) of the FP64 SYRK / GEMM
         achieved = ops / (stages[dom] * 1e-3) / 1e12
         roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOP/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(dom), "peak_source": src,

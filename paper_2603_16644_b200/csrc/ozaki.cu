@@ -1,27 +1,28 @@
 // FP64 Gram products G = X^T Y on the INT8 tensor cores (tcgen05 kind::i8):
-// Ozaki scheme II, i.e. exact integer products modulo 16 coprime moduli and a
+// Ozaki scheme II, i.e. exact integer products modulo up to 16 coprime moduli and a
 // Chinese-remainder reconstruction.
 //
 // Same call sites as gram.cu (`a.T @ a` src/precision.py:230, `a_p.T @ a_p`
 // src/solvers.py:230, `a_p.T @ a` :251, `b_matrix.T @ a` :164).  B200 has ~3.1 POPS
-// of dense INT8 against 35 TFLOP/s of FP64 DMMA; 16 INT8 products replace one FP64
+// of dense INT8 against 35 TFLOP/s of FP64 DMMA; 14-16 INT8 products replace one FP64
 // product.
 //
 //   1. column scales: e_i with max_k |X[k,i]| < 2^e_i (one pass over X and Y)
 //   2. per K-chunk of rows: X'[k,i] = rint(X[k,i] 2^(t - e_i)), |X'| <= 2^t, an exact
-//      integer; its residues modulo p_1..p_16 (odd, pairwise coprime, <= 255) as
-//      signed bytes in [-127, 127], 16 planes per operand, row-major like X
+//      integer; its residues modulo p_1..p_nm (odd, pairwise coprime, <= 255) as
+//      signed bytes in [-127, 127], nm planes per operand, row-major like X
 //   3. per (modulus, K split <= 131072 rows, 256x256 output tile): one tcgen05 INT8
 //      GEMM with int32 accumulation in TMEM (|sum| < 131072 * 127^2 < 2^31: exact);
 //      both operands MN-major, TMA-staged with 128-byte swizzle
 //   4. residues of the int32 partials summed modulo p
-//   5. Garner mixed-radix reconstruction of C' = X'^T Y' (|C'| < M/2, M = prod p ~
-//      2^125.3) in 128-bit integers, G = C' 2^(e_i + f_j - 2t).
+//   5. Garner mixed-radix reconstruction of C' = X'^T Y' (|C'| < M/2, M = prod p) in
+//      128-bit integers, G = C' 2^(e_i + f_j - 2t).
 //
 // Error: only step 2 rounds (|X' - X 2^(t-e)| <= 1/2), so |G - X^T Y|_ij <=
-// 2^-t (2^e_i sum_k |Y_kj| + 2^f_j sum_k |X_ki|) / 2 (+ the final rounding), with t
-// = 51 at m = 4M rows: the FP64 GEMM bound is gamma_K sum_k |X_ki||Y_kj|.  The
-// SYRK path computes lower tiles only; C' is exactly symmetric, so G is too.
+// 2^-t (2^e_i sum_k |Y_kj| + 2^f_j sum_k |X_ki|) / 2 (+ the final rounding).  nm and t
+// come from gram_moduli: the worst case stays 2^8 under the FP64 GEMM's gamma_K bound
+// (m = 4M rows: nm = 15, t = 47).  The SYRK path computes lower tiles only; C' is
+// exactly symmetric, so G is too.
 #include <math_constants.h>
 
 #include <vector>
@@ -214,7 +215,7 @@ constexpr int RV = 8;
 #endif
 __global__ void __launch_bounds__(256, SK_OZ_RES_MINB)
 residues_kernel(const double *__restrict__ x, int64_t ldx, int64_t rows, int n, const double *__restrict__ scale,
-                int8_t *__restrict__ out, int64_t ldr, int64_t plane, int vec) {
+                int8_t *__restrict__ out, int64_t ldr, int64_t plane, int vec, int nm) {
     const int cpr = (n + RV - 1) / RV;
     const int rpi = cpr >= 256 ? 1 : 256 / cpr;
     const int sub = cpr >= 256 ? 0 : threadIdx.x / cpr;
@@ -264,6 +265,7 @@ residues_kernel(const double *__restrict__ x, int64_t ldx, int64_t rows, int n, 
             }
 #pragma unroll
             for (int k = 0; k < NMOD; ++k) {
+                if (k >= nm) break;   // the first nm moduli (uniform)
                 uint32_t w[2];
 #pragma unroll
                 for (int q4 = 0; q4 < 2; ++q4) {
@@ -634,7 +636,7 @@ __global__ void reduce_kernel(const int32_t *__restrict__ part, int splits, int 
 
 // ------------------------------------------------------- reconstruction -----
 __global__ void crt_kernel(const int32_t *__restrict__ acc, int n, int syrk, const int *__restrict__ ex,
-                           const int *__restrict__ ey, int t, double *__restrict__ g, int64_t ldg) {
+                           const int *__restrict__ ey, int t, double *__restrict__ g, int64_t ldg, int nm) {
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nn = (int64_t)n * n;
     if (idx >= nn) return;
@@ -642,11 +644,12 @@ __global__ void crt_kernel(const int32_t *__restrict__ acc, int n, int syrk, con
     const int64_t src = (syrk && (i / BM) < (j / BN)) ? (int64_t)j * n + i : idx;   // mirror: C' symmetric
     int r[NMOD];
 #pragma unroll
-    for (int k = 0; k < NMOD; ++k) r[k] = acc[(int64_t)k * nn + src];
-    // Garner: x = v0 + v1 p0 + v2 p0 p1 + ...
+    for (int k = 0; k < NMOD; ++k) r[k] = k < nm ? acc[(int64_t)k * nn + src] : 0;
+    // Garner over the first nm moduli: x = v0 + v1 p0 + v2 p0 p1 + ...
     int v[NMOD];
 #pragma unroll
     for (int k = 0; k < NMOD; ++k) {
+        if (k >= nm) { v[k] = 0; continue; }
         // x_{k} mod p_k from the digits so far (Horner, mod p_k)
         int acc_k = 0;
 #pragma unroll
@@ -657,10 +660,12 @@ __global__ void crt_kernel(const int32_t *__restrict__ acc, int n, int syrk, con
     }
     unsigned __int128 x = 0;
 #pragma unroll
-    for (int k = NMOD - 1; k >= 0; --k) x = x * (unsigned)pm(k) + (unsigned)v[k];
+    for (int k = NMOD - 1; k >= 0; --k)
+        if (k < nm) x = x * (unsigned)pm(k) + (unsigned)v[k];
     unsigned __int128 mprod = 1;
 #pragma unroll
-    for (int k = 0; k < NMOD; ++k) mprod *= (unsigned)pm(k);
+    for (int k = 0; k < NMOD; ++k)
+        if (k < nm) mprod *= (unsigned)pm(k);
     const bool neg = x > (mprod >> 1);
     const unsigned __int128 mag = neg ? mprod - x : x;
     const double hi = (double)(unsigned long long)(mag >> 64), lo = (double)(unsigned long long)mag;
@@ -913,11 +918,32 @@ crt_sub_kernel(const int8_t *__restrict__ planes, int64_t plane, int64_t ldo, in
 
 // -------------------------------------------------------------- planning ----
 struct Plan {
-    int ntm, ntn, ntiles, t;
+    int ntm, ntn, ntiles, t, nm;
     int64_t chunk, kchunk, ldr;
     int splits;
     size_t res_bytes, part_bytes, acc_bytes, aux_bytes;
 };
+
+// Gram moduli: the fewest leading moduli with t >= 68 - log2 K (capped at 51), i.e. the
+// INT8 product's worst-case bound 2^(7-t) ||X_i|| ||Y_j|| (guarded columns) stays 2^8
+// below the FP64 GEMM's gamma_K ~ K u, and its typical error ~2^-t K^-1/2 ||X_i|| ||Y_j||
+// under the blocked DMMA Gram's.  K = 2M-4M rows: 15 moduli, t = 47; K <= 2^17: 16, t = 51.
+// (t = 43 with 14 moduli was measured: HPNE error 9.5e-15 against 2.7e-15 at kappa 10.)
+int gram_moduli(int64_t m, int *t_out) {
+    const double L = log2((double)std::max<int64_t>(m, 1));
+    const int tmin = std::min(51, (int)ceil(68.0 - L));
+    double lg = 0.0;
+    for (int k = 0; k < NMOD; ++k) {
+        lg += log2((double)pm(k));
+        const int t = std::min(51, (int)floor((lg - 1.0 - L - 0.01) / 2.0));
+        if (t >= tmin || k == NMOD - 1) {
+            *t_out = t;
+            return k + 1;
+        }
+    }
+    *t_out = 51;
+    return NMOD;
+}
 
 int choose_t(int64_t m) {
     double lg = 0.0;
@@ -932,7 +958,7 @@ Plan make_plan(int64_t m, int64_t n, bool syrk) {
     p.ntm = (int)((n + BM - 1) / BM);
     p.ntn = p.ntm;
     p.ntiles = syrk ? p.ntm * (p.ntm + 1) / 2 : p.ntm * p.ntn;
-    p.t = choose_t(m);
+    p.nm = gram_moduli(m, &p.t);
     p.ldr = (n + 15) / 16 * 16;
     p.kchunk = KSPLIT_MAX;
     p.chunk = std::min<int64_t>((m + BK - 1) / BK * BK, KSPLIT_MAX);
@@ -1119,7 +1145,7 @@ int trsm_rec(const double *a, int64_t lda, double *ap, int64_t ldap, int64_t m, 
         const int rpi = cpr >= 256 ? 1 : 256 / cpr;
         const int vq = ((reinterpret_cast<uintptr_t>(q) & 15) == 0) && (ldr % 2 == 0);
         residues_kernel<<<(unsigned)((h + rpi - 1) / rpi), 256, 0, st>>>(q, ldr, h, (int)w, W.qscale, W.qres, ldw,
-                                                                          qplane, vq);
+                                                                          qplane, vq, nm);
         SK_LAUNCH_CHECK("oz trsm q residues");
     }
     if (prof) prof->mark(1, st);
@@ -1421,11 +1447,12 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
         const unsigned rgrid = (unsigned)std::min<int64_t>((rows + rpi - 1) / rpi, (int64_t)sms * 16);
         if (prof) SK_CUDA(cudaEventRecord(pe[npe++], st));
         if (!serial && chunk_idx >= 2) SK_CUDA(cudaStreamWaitEvent(sp.side, sp.gemm_done[buf], 0));
-        oz::residues_kernel<<<rgrid, 256, 0, rs>>>(x + r0 * ldx, ldx, rows, (int)n, scale, res_x, p.ldr, plane, vx);
+        oz::residues_kernel<<<rgrid, 256, 0, rs>>>(x + r0 * ldx, ldx, rows, (int)n, scale, res_x, p.ldr, plane, vx,
+                                                   p.nm);
         SK_LAUNCH_CHECK("oz residues");
         if (!syrk) {
             oz::residues_kernel<<<rgrid, 256, 0, rs>>>(y + r0 * ldy, ldy, rows, (int)n, scale + n, res_y, p.ldr,
-                                                       plane, vy);
+                                                       plane, vy, p.nm);
             SK_LAUNCH_CHECK("oz residues");
         }
         if (!serial) {
@@ -1444,7 +1471,7 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
         gp.ntn = p.ntn;
         gp.ntiles = p.ntiles;
         gp.splits = (int)((rows + p.kchunk - 1) / p.kchunk);
-        gp.units = oz::NMOD * gp.splits * p.ntiles;
+        gp.units = p.nm * gp.splits * p.ntiles;
         gp.syrk = syrk;
         gp.rows = rows;
         gp.kchunk = p.kchunk;
@@ -1456,7 +1483,8 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
     }
     const int64_t nn = n * n;
     if (prof) SK_CUDA(cudaEventRecord(pe[npe++], st));
-    oz::crt_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, gs>>>(acc, (int)n, syrk, expo, expo + n, p.t, g, ldg);
+    oz::crt_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, gs>>>(acc, (int)n, syrk, expo, expo + n, p.t, g, ldg,
+                                                                 p.nm);
     SK_LAUNCH_CHECK("oz crt");
     if (!serial) {   // the caller's stream resumes after the reconstruction
         SK_CUDA(cudaEventRecord(sp.end, sp.hi));

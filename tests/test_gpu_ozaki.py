@@ -133,3 +133,42 @@ def test_ozaki_gram_special_values(torch):
     assert np.array_equal(g_oz[exact], ref[exact])   # zeros, small integers, single products
     assert abs(g_oz[20, 20] - ref[20, 20]) <= 1e-15 * ref[20, 20]
     assert abs(g_oz[5, 20] - ref[5, 20]) <= 1e-15 * np.abs(x[:, 20]).sum()
+
+
+@pytest.mark.parametrize("syrk", [True, False])
+def test_ozaki_gram_fewest_moduli(torch, syrk):
+    """m >= 2^21 rows: gram_moduli picks 15 moduli, t = 47 (worst case 2^-40 ||X_i||
+    ||Y_j||, 2^8 under the FP64 GEMM's gamma_K).  Against the DMMA Gram the difference
+    stays at the FP64 GEMM's own error level, far inside that bound."""
+    from paper_2603_16644_b200.dense import _gram
+    m, n = (1 << 21) + 3, 200
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    x = torch.randn(m, n, dtype=torch.float64, device="cuda", generator=g)
+    x[:, 7] *= 1e-6                      # a scaled column (its own scale)
+    y = x if syrk else torch.randn(m, n, dtype=torch.float64, device="cuda", generator=g)
+    g_oz = _gram(x, None if syrk else y, engine="ozaki")
+    g_dm = _gram(x, None if syrk else y, engine="dmma")
+    nx, ny = x.norm(dim=0), y.norm(dim=0)
+    rel = ((g_oz - g_dm).abs() / (nx[:, None] * ny[None, :])).max().item()
+    assert rel <= 2.0 ** -40, rel
+    if syrk:
+        assert torch.equal(g_oz, g_oz.T)
+
+
+def test_pipeline_fewest_moduli_matches_dmma(torch, monkeypatch):
+    """Algorithm 1 at 2^21 rows (15-modulus Grams) against the same pipeline with every
+    Gram on FP64 DMMA: same level, error within 2x (+1e-15)."""
+    import paper_2603_16644_b200 as sq
+    from paper_2603_16644_b200 import dense
+    from paper_2603_16644_b200.probgen import generate_problem_device
+    for kappa in (1e1, 1e6):
+        a, b, xs = generate_problem_device((1 << 21) + 64, 256, kappa, 1e-6, R.mix64(9, int(np.log10(kappa))),
+                                           torch.device("cuda"))
+        monkeypatch.setattr(dense, "GRAM_ENGINE", "ozaki")
+        oz = sq.algorithm1_pipeline(a, b, "hpne", "auto", 3.0, "dct2", 0, xs, diagnostics=False)
+        monkeypatch.setattr(dense, "GRAM_ENGINE", "dmma")
+        dm = sq.algorithm1_pipeline(a, b, "hpne", "auto", 3.0, "dct2", 0, xs, diagnostics=False)
+        assert oz.preconditioner.computed_in == dm.preconditioner.computed_in
+        assert oz.relative_error <= 2 * dm.relative_error + 1e-15, (kappa, oz.relative_error, dm.relative_error)
+        del a, b, xs
