@@ -104,10 +104,36 @@ residual_kernel(const double *__restrict__ a, int64_t rows, int64_t cols, int64_
     const int64_t gw = blockIdx.x * (int64_t)(THREADS / 32) + warp;
     const int64_t nw = (int64_t)gridDim.x * (THREADS / 32);
     double ss = 0.0;
+    const bool vec = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(x)) % 16 == 0) && (lda % 2 == 0);
     for (int64_t i = gw; i < rows; i += nw) {
         const double *row = a + i * lda;
         double s = 0.0;
-        for (int64_t c = lane; c < cols; c += 32) s += row[c] * x[c];
+        if (vec) {
+            // 16-byte loads, four independent chains: 2 KB of the row in flight per warp
+            const double2 *r2 = reinterpret_cast<const double2 *>(row);
+            const double2 *x2 = reinterpret_cast<const double2 *>(x);
+            const int64_t n2 = cols / 2;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int64_t c = lane;
+            for (; c + 96 < n2; c += 128) {
+                const double2 a0 = __ldcs(r2 + c), a1 = __ldcs(r2 + c + 32), a2 = __ldcs(r2 + c + 64),
+                              a3 = __ldcs(r2 + c + 96);
+                const double2 y0 = __ldg(x2 + c), y1 = __ldg(x2 + c + 32), y2 = __ldg(x2 + c + 64),
+                              y3 = __ldg(x2 + c + 96);
+                s0 = fma(a0.y, y0.y, fma(a0.x, y0.x, s0));
+                s1 = fma(a1.y, y1.y, fma(a1.x, y1.x, s1));
+                s2 = fma(a2.y, y2.y, fma(a2.x, y2.x, s2));
+                s3 = fma(a3.y, y3.y, fma(a3.x, y3.x, s3));
+            }
+            for (; c < n2; c += 32) {
+                const double2 a0 = __ldcs(r2 + c), y0 = __ldg(x2 + c);
+                s0 = fma(a0.y, y0.y, fma(a0.x, y0.x, s0));
+            }
+            if ((cols & 1) && lane == 0) s1 = fma(row[cols - 1], x[cols - 1], s1);
+            s = (s0 + s1) + (s2 + s3);
+        } else {
+            for (int64_t c = lane; c < cols; c += 32) s += row[c] * x[c];
+        }
         s = warp_sum(s);
         const double ri = s - b[i];
         if (lane == 0) {
