@@ -108,8 +108,10 @@ int sk_gram_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int6
                 sk_stream_t stream);
 
 /* Same product on the INT8 tensor cores (tcgen05 kind::i8, Ozaki scheme II): X and Y
- * scaled per column to t-bit integers (t = 51 at m = 4M rows), 16 exact modular
- * INT8 GEMMs, Chinese-remainder reconstruction in 128-bit integers.  The only
+ * scaled per column to t-bit integers, nm exact modular INT8 GEMMs (nm and t chosen so
+ * the worst case stays 2^8 under the FP64 GEMM's gamma_m bound: 15 moduli, t = 47 at
+ * m = 4M rows; 16, t = 51 below 2^17 rows), Chinese-remainder reconstruction in
+ * 128-bit integers.  The only
  * rounding is the t-bit scaling: |G - X^T Y|_ij <= 2^-t (2^e_i sum|Y_j| + 2^f_j
  * sum|X_i|) / 2, with 2^e_i > max|X_i|.  SYRK when Y == X (exactly symmetric).
  * Workspace from sk_gram_ozaki_workspace(m, n, syrk). */

@@ -4,11 +4,14 @@ Same entry points, signatures, dataclasses and error behaviour as the reference
 (src/solvers.py).  Every m x n pass runs in libsklsq on the device:
 
   check      sk_cast_stats                (validation + f64 + ||A||_F^2, one pass)
-  kappa0     sk_gram_f64 (SYRK) + sk_kappa0_from_gram
+  kappa0     sk_gram_ozaki_ex_f64 (INT8 SYRK; sk_gram_f64 DMMA below 2^33 m n^2)
+             + sk_kappa0_from_gram
   sketch     sk_sketch_partial/finalize   (on-the-fly SRTT operator, level demotion fused)
   level QR   sk_qr_r                      (binary16 op-for-op emulation)
-  A_p        sk_trsm_right_upper_f64      (DMMA)
-  Gram       sk_gram_f64 (SYRK for PNE, GEMM-TN for HPNE/NNE) + sk_gemv_t_f64
+  A_p        sk_trsm_ozaki_f64            (DMMA leaves + INT8 updates; sk_trsm_right_upper_f64
+                                           DMMA for small solves)
+  Gram       sk_gram_ozaki_ex_f64 / sk_gram_f64 (SYRK for PNE, GEMM-TN for HPNE/NNE),
+             A_p^T b from sk_colstats_f64's column scan (or sk_gemv_t_f64)
   n x n      sk_chol_solve_f64 / sk_lu_solve_f64 / sk_trsv_f64
   report     sk_residual
 
