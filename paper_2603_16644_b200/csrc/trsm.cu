@@ -31,7 +31,12 @@ constexpr int WM = 32, WN = 32;             // 4 x 2 warps
 constexpr int APITCH = BK + 4;              // 20 = 4 (mod 16): conflict-free A fragments
 constexpr int BPITCH = NB + 4;              // 68 = 4 (mod 16): conflict-free B fragments
 constexpr int TPITCH = NB + 4;              // T tile rows, 16-byte aligned (544 B)
-constexpr int RPITCH = NB;
+// R_JJ rows 68 doubles apart, odd columns 34 after the even ones: the DMMA B-fragment
+// loads of the sub-block update (k = lane % 4 rows, n = lane / 4 columns) then touch each
+// bank pair at most twice (2 wavefronts, the minimum for 256 B); with 64 / 32 they were
+// 8-way conflicted (ncu: 15 excess wavefronts per load).
+constexpr int RPITCH = NB + 4;
+constexpr int RHALF = NB / 2 + 2;
 // The T tile and R_JJ alias the GEMM staging ring (they are loaded after the GEMM),
 // which keeps a CTA at ~102 KB so two CTAs share an SM: one CTA's substitution and
 // staging latency hides behind the other's DMMA work.
@@ -40,8 +45,8 @@ constexpr size_t TILE = sizeof(double) * (size_t(BMR) * TPITCH + size_t(NB) * RP
 constexpr size_t SMEM = RING > TILE ? RING : TILE;
 
 // R_JJ in shared memory with each row split by column parity: element (i, j) at
-// i*RPITCH + (j&1)*NB/2 + j/2, so a substitution thread's half-row is contiguous.
-__device__ __forceinline__ int ridx(int i, int j) { return i * RPITCH + (j & 1) * (NB / 2) + (j >> 1); }
+// i*RPITCH + (j&1)*RHALF + j/2, so a substitution thread's half-row is contiguous.
+__device__ __forceinline__ int ridx(int i, int j) { return i * RPITCH + (j & 1) * RHALF + (j >> 1); }
 
 __device__ __forceinline__ void load_stage(double *as, double *bs, const double *ap, int64_t ldap,
                                            const double *__restrict__ r, int64_t ldr, int64_t row0, int64_t m, int k0,
@@ -246,7 +251,7 @@ trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__rest
                     }
                     x = __shfl_sync(0xffffffffu, x, base | owner);
                     // this thread's half of row cs+c of R_JJ, sub-block columns: contiguous
-                    const double *rrow = rs + (cs + c) * RPITCH + hf * (NB / 2) + cs / 2;
+                    const double *rrow = rs + (cs + c) * RPITCH + hf * RHALF + cs / 2;
 #pragma unroll
                     for (int kp = ((c + 1) >> 1) >> 1; kp < SB / 4; ++kp) {
                         const double2 rv = *reinterpret_cast<const double2 *>(rrow + 2 * kp);
