@@ -30,7 +30,12 @@ constexpr int BMR = 128, NB = 64, BK = SK_TRSM_BK, STAGES = SK_TRSM_STAGES, THRE
 constexpr int WM = 32, WN = 32;             // 4 x 2 warps
 constexpr int APITCH = BK + 4;              // 20 = 4 (mod 16): conflict-free A fragments
 constexpr int BPITCH = NB + 4;              // 68 = 4 (mod 16): conflict-free B fragments
-constexpr int TPITCH = NB + 4;              // T tile rows, 16-byte aligned (544 B)
+#ifndef SK_TRSM_TPAD
+#define SK_TRSM_TPAD 2
+#endif
+// T tile rows, 16-byte aligned: 66 doubles (528 B) puts the 16 rows a warp's
+// substitution threads walk on distinct bank pairs (68 made them 4-way)
+constexpr int TPITCH = NB + SK_TRSM_TPAD;
 // R_JJ rows 68 doubles apart, odd columns 34 after the even ones: the DMMA B-fragment
 // loads of the sub-block update (k = lane % 4 rows, n = lane / 4 columns) then touch each
 // bank pair at most twice (2 wavefronts, the minimum for 256 B); with 64 / 32 they were
