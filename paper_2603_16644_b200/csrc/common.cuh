@@ -100,11 +100,15 @@ __device__ __forceinline__ double warp_max(double v) {
 // _rn intrinsics forbid FMA contraction, which numpy never does.
 template <typename T> struct LevelOps;
 
+// binary16 arithmetic.  numpy's float16 ufuncs compute in binary32 and round to
+// binary16; for +, -, x that double rounding is innocuous (24 >= 2 * 11 + 2 bits), so the
+// native round-to-nearest fp16 instructions give the same bits in one instruction
+// instead of two conversions, the op and a pack (_rn: never contracted into an FMA).
 template <> struct LevelOps<__half> {
     using T = __half;
-    __device__ static __forceinline__ T add(T a, T b) { return __float2half_rn(__fadd_rn(__half2float(a), __half2float(b))); }
-    __device__ static __forceinline__ T sub(T a, T b) { return __float2half_rn(__fsub_rn(__half2float(a), __half2float(b))); }
-    __device__ static __forceinline__ T mul(T a, T b) { return __float2half_rn(__fmul_rn(__half2float(a), __half2float(b))); }
+    __device__ static __forceinline__ T add(T a, T b) { return __hadd_rn(a, b); }
+    __device__ static __forceinline__ T sub(T a, T b) { return __hsub_rn(a, b); }
+    __device__ static __forceinline__ T mul(T a, T b) { return __hmul_rn(a, b); }
     __device__ static __forceinline__ T div(T a, T b) { return __float2half_rn(__fdiv_rn(__half2float(a), __half2float(b))); }
     __device__ static __forceinline__ T sqrt(T a) { return __float2half_rn(__fsqrt_rn(__half2float(a))); }
     __device__ static __forceinline__ double to_f64(T a) { return (double)__half2float(a); }
