@@ -641,6 +641,158 @@ lu_flow_kernel(double *w, double *lmul, int *perm, int n, int *pivots, int *flag
     }
 }
 
+// Shared-memory-resident dataflow LU (n <= ~2070 on 148 SMs): CTA b keeps its columns
+// c = b + q G (q < nloc) in shared memory for the whole factorisation, so a step touches
+// no global memory but the published multiplier column.  Rows are swapped physically
+// inside every CTA's own columns (finished L columns included, as src/dense.py:264-281
+// swaps whole rows), so the logical order is the physical one and the pivot tie rule
+// (first maximum, np.argmax) needs no position map.  The owner of column s publishes
+// step s (pivot row, multipliers l = w[s+1:, s] / w[s, s]) through flags[s]; the owner
+// of column k+1 applies step k to that column first, then publishes step k+1 before it
+// updates its other columns (lookahead 1).  Every multiplier and update is the
+// reference's separately rounded division, product and difference, as in lu_kernel.
+constexpr int LUS_THREADS = 1024, LUS_ROWS = 2;   // rows per thread: n <= LUS_THREADS * LUS_ROWS
+
+__device__ __forceinline__ int spin_flag(const int *flag) {
+    int v;
+    long long spins = 0;
+    while ((v = *reinterpret_cast<const volatile int *>(flag)) == 0)
+        if (++spins > (1ll << 27)) return -1;     // stuck chain: fail instead of hanging the GPU
+    __threadfence();
+    return v;
+}
+
+__global__ void __launch_bounds__(LUS_THREADS, 1)
+lu_smem_kernel(double *w, int n, double *gl, int *piv, int *flags, double *lout, LuCtl *ctl) {
+    extern __shared__ double W[];                 // nloc x n, column q = global column b + q G
+    __shared__ double sv[LUS_THREADS / 32];
+    __shared__ int si[LUS_THREADS / 32];
+    __shared__ double s_piv;
+    __shared__ int s_p, s_flag;
+    const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int nloc = b < n ? (n - b + G - 1) / G : 0;
+    const double thresh = ctl->thresh;
+    for (int q = 0; q < nloc; ++q) {
+        const double *src = w + (int64_t)(b + q * G) * n;
+        for (int i = tid; i < n; i += T) W[q * n + i] = src[i];
+    }
+    __syncthreads();
+
+    // pivot search, swap and multipliers of column s (owned; steps < s applied); false on failure
+    auto lead = [&](int s) -> bool {
+        double *col = W + (s / G) * n;
+        double bv = -1.0;
+        int bi = INT32_MAX;
+        for (int i = s + tid; i < n; i += T) better(bv, bi, fabs(col[i]), i);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            better(bv, bi, ov, oi);
+        }
+        if (lane == 0) { sv[warp] = bv; si[warp] = bi; }
+        __syncthreads();
+        if (warp == 0) {
+            bv = lane < T / 32 ? sv[lane] : -1.0;
+            bi = lane < T / 32 ? si[lane] : INT32_MAX;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                better(bv, bi, ov, oi);
+            }
+            if (lane == 0) {
+                s_piv = bv;
+                s_p = bi;
+                if (bi != s && bi < n) { const double t = col[s]; col[s] = col[bi]; col[bi] = t; }
+            }
+        }
+        __syncthreads();
+        const double pv = s_piv;
+        if (pv < thresh || pv == 0.0 || !(pv == pv)) {
+            if (tid == 0) {
+                ctl->fail_code = SK_NUMERICALLY_SINGULAR;
+                ctl->fail_col = s;
+                ctl->fail_value = pv;
+                __threadfence();
+                atomicExch(flags + s, 2);
+            }
+            return false;
+        }
+        const double akk = col[s];
+        double *g = gl + (int64_t)s * n;
+        for (int i = s + 1 + tid; i < n; i += T) {
+            const double li = __ddiv_rn(col[i], akk);
+            col[i] = li;
+            g[i] = li;
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            piv[s] = s_p;
+            __threadfence();
+            atomicExch(flags + s, 1);
+        }
+        return true;
+    };
+
+    if (b == 0 && n > 0 && !lead(0)) return;
+    for (int k = 0; k < n; ++k) {
+        if (tid == 0) s_flag = spin_flag(flags + k);
+        __syncthreads();
+        if (s_flag != 1) {
+            if (s_flag < 0 && tid == 0) { ctl->fail_code = SK_ERR_CUDA; ctl->fail_col = k; }
+            return;
+        }
+        const int p = __ldcg(piv + k);
+        if (p != k)
+            for (int q = tid; q < nloc; q += T)
+                if (b + q * G != k) {
+                    double *col = W + q * n;
+                    const double t = col[k];
+                    col[k] = col[p];
+                    col[p] = t;
+                }
+        __syncthreads();
+        if (k == n - 1) break;
+        const double *g = gl + (int64_t)k * n;
+        double l[LUS_ROWS];
+#pragma unroll
+        for (int r = 0; r < LUS_ROWS; ++r) {
+            const int i = k + 1 + tid + r * T;
+            l[r] = i < n ? __ldcg(g + i) : 0.0;
+        }
+        auto update = [&](int q) {
+            double *col = W + q * n;
+            const double u = col[k];
+#pragma unroll
+            for (int r = 0; r < LUS_ROWS; ++r) {
+                const int i = k + 1 + tid + r * T;
+                if (i < n) col[i] = __dsub_rn(col[i], __dmul_rn(l[r], u));
+            }
+        };
+        int q0 = k >= b ? (k - b) / G + 1 : 0;       // first owned column > k
+        if (q0 < nloc && b + q0 * G == k + 1) {
+            update(q0);
+            __syncthreads();
+            if (!lead(k + 1)) return;
+            ++q0;
+        }
+        for (int q = q0; q < nloc; ++q) update(q);
+    }
+    __syncthreads();
+    for (int q = 0; q < nloc; ++q) {
+        const int c = b + q * G;
+        double *dw = w + (int64_t)c * n, *dl = lout + (int64_t)c * n;
+        for (int i = tid; i < n; i += T) {
+            const double v = W[q * n + i];
+            dw[i] = v;
+            dl[i] = i > c ? v : 0.0;
+        }
+    }
+}
+
 // perm = the row swaps (k, pivots[k]) applied in order to the identity (one thread)
 __global__ void perm_from_pivots(const int *pivots, int n, int *perm) {
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
@@ -1012,12 +1164,41 @@ int sk_lu_solve_f64(const double *g, int64_t n, const double *rhs, double *x, sk
     // longer than two grid barriers over the fully parallel step.
     // default: one grid barrier per step (lu_perm_kernel); SK_LU_KERNEL=barrier selects
     // the two-barrier swap kernel, SK_LU_FLOW=1 the dataflow one (all bitwise the same)
+    // default for n <= 2048: the shared-memory-resident dataflow LU (lu_smem_kernel);
+    // SK_LU_KERNEL=perm forces lu_perm_kernel (also the fallback when the columns do not
+    // fit in shared memory)
     static const char *lu_choice = getenv("SK_LU_KERNEL");
     static const bool barrier_lu = getenv("SK_LU_FLOW") == nullptr;
     static const bool perm_lu = barrier_lu && !(lu_choice && strcmp(lu_choice, "barrier") == 0);
-    if (perm_lu) {
+    static const bool smem_lu = perm_lu && !(lu_choice && strcmp(lu_choice, "perm") == 0);
+    bool done = false;
+    if (smem_lu && n <= (int64_t)LUS_THREADS * LUS_ROWS) {
+        const int gs = (int)std::min<int64_t>(sm_count(), n);
+        const size_t smem = (size_t)((n + gs - 1) / gs) * (size_t)n * sizeof(double);
+        int optin = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (smem + 1024 <= (size_t)optin &&
+            cudaFuncSetAttribute(lu_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+            coop_blocks((const void *)lu_smem_kernel, LUS_THREADS, smem, gs) == gs) {
+            int *lf = ws.lflags, *pv = ws.pivots;
+            double *gl = ws.lphys;
+            SK_CUDA(cudaMemsetAsync(lf, 0, (size_t)n * sizeof(int), st));
+            void *args[] = {&w, &ni, &gl, &pv, &lf, &lm, &ctl};
+            SK_CUDA(cudaLaunchCooperativeKernel((const void *)lu_smem_kernel, dim3(gs), dim3(LUS_THREADS), args, smem, st));
+            SK_LAUNCH_CHECK("lu_smem_kernel");
+            perm_from_pivots<<<1, 32, 0, st>>>(pv, ni, perm);
+            SK_LAUNCH_CHECK("perm_from_pivots");
+            done = true;
+        }
+        cudaGetLastError();   // a refused attribute / occupancy query falls back below
+    }
+    if (done) {
+    } else if (perm_lu) {
+        static const char *lu_blocks_env = getenv("SK_LU_BLOCKS");   // grid-size sweeps (tools/lu_probe.py)
+        const int64_t lu_want = lu_blocks_env ? atoll(lu_blocks_env) : 2 * (int64_t)sm_count();
         int blocks = coop_blocks((const void *)lu_perm_kernel, THREADS, 0,
-                                 std::min<int64_t>(std::min<int64_t>(2 * sm_count(), 4096),
+                                 std::min<int64_t>(std::min<int64_t>(lu_want, 4096),
                                                    (n * n + THREADS * 8 - 1) / (THREADS * 8)));
         if (!blocks) { set_error("lu_perm_kernel not co-resident"); return SK_ERR_CUDA; }
         // the working copy moves to the physical-slot buffers; ws.w / ws.l get the gather
