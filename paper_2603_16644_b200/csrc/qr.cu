@@ -296,7 +296,11 @@ householder_kernel(T *w, int64_t ld, int d, int n, T *alphas /* n */, T *part /*
 // columns) and published through flags[j+1]; every CTA waits on that flag alone before
 // applying reflector j+1.  The arithmetic (chunk trees, update order, scalar ops) is the
 // barrier kernel's, so R is bitwise the same.
-template <typename T>
+// SMEM = true: CTA b keeps its columns c = b + q G in shared memory for the whole
+// factorisation (binary16 at d x n = 6144 x 2048 on 148 SMs: 14 x 12 KB); the leader
+// stores the finished reflector column to global memory before publishing it, and every
+// CTA writes its columns back at the end.  Same arithmetic, so R is bitwise the same.
+template <typename T, bool SMEM>
 __global__ void __launch_bounds__(THREADS)
 householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nqmax x n */, T *taus, T *v0s,
                         int *flags, Ctl<T> *ctl) {
@@ -305,8 +309,24 @@ householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nq
     __shared__ T sh_t[MAXCH];
     __shared__ T sh_root;
     __shared__ int sh_flag;
+    extern __shared__ __align__(16) unsigned char qr_dyn[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int G = gridDim.x, b = blockIdx.x;
+    const int nloc = b < n ? (n - b + G - 1) / G : 0;
+    const int nqd = (d + CH - 1) / CH;
+    T *sm_cols = reinterpret_cast<T *>(qr_dyn);                         // nloc x d
+    T *sm_part = sm_cols + (SMEM ? (size_t)nloc * d : 0);              // nloc x nqd chunk nodes
+    // owned column c (c mod G == b)
+    auto col = [&](int c) -> T * { return SMEM ? sm_cols + (size_t)(c / G) * d : w + (int64_t)c * ld; };
+    auto part_at = [&](int k, int q, int c) -> T & { return SMEM ? sm_part[k * nqd + q] : part[(size_t)q * n + c]; };
+    if (SMEM) {
+        for (int q = 0; q < nloc; ++q) {
+            const T *src = w + (int64_t)(b + q * G) * ld;
+            T *dst = sm_cols + (size_t)q * d;
+            for (int i = threadIdx.x; i < d; i += THREADS) dst[i] = src[i];
+        }
+        __syncthreads();
+    }
 
     auto publish = [&](int jj, int rc) {
         __syncthreads();
@@ -331,7 +351,7 @@ householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nq
         if (c0 == j + 1) {
             // ---- leader: column j+1 first, then reflector j+1
             for (int q = warp; q < nq; q += WARPS) {
-                const T node = chunk_node<T>(v, w + (int64_t)(j + 1) * ld + j, L, q, 1, v0);
+                const T node = chunk_node<T>(v, col(j + 1) + j, L, q, 1, v0);
                 if (lane == 0) sh_nodes[q] = node;
             }
             __syncthreads();
@@ -341,7 +361,7 @@ householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nq
             }
             __syncthreads();
             const T t = sh_root;
-            T *colj = w + (int64_t)(j + 1) * ld + j;
+            T *colj = col(j + 1) + j;
             if (threadIdx.x == 0) colj[0] = O::sub(colj[0], O::mul(v0, t));   // R entry (row j)
             T *x = colj + 1;
             const T *vx = v + 1;
@@ -360,6 +380,11 @@ householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nq
             const int rc = j + 1 < n ? reflect_from_nodes<T>(x, Lx, taus + j + 1, v0s + j + 1, alphas, j + 1,
                                                              sh_nodes, &sh_root)
                                      : SK_OK;
+            if (SMEM) {   // the reflector column (rows j+1..) goes to global memory for the other CTAs
+                T *dst = w + (int64_t)(j + 1) * ld;
+                for (int i = j + 1 + threadIdx.x; i < d; i += THREADS) dst[i] = colj[i - j];
+                __threadfence();
+            }
             publish(j + 1, rc);
             c0 += G;
         }
@@ -370,13 +395,13 @@ householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nq
         for (int u = warp; u < units; u += WARPS) {
             const int k = u / nq, q = u % nq;
             const int c = c0 + k * G;
-            const T node = chunk_node<T>(v, w + (int64_t)c * ld + j, L, q, 1, v0);
-            if (lane == 0) part[(size_t)q * n + c] = node;
+            const T node = chunk_node<T>(v, col(c) + j, L, q, 1, v0);
+            if (lane == 0) part_at(k, q, c) = node;
         }
         __syncthreads();
         for (int k = warp; k < mine; k += WARPS) {
             const int c = c0 + k * G;
-            const T root = warp_tree_root<T>(nq, [&](int i) { return part[(size_t)i * n + c]; });
+            const T root = warp_tree_root<T>(nq, [&](int i) { return part_at(k, i, c); });
             if (lane == 0) sh_t[k] = O::mul(tau, root);
         }
         __syncthreads();
@@ -384,8 +409,8 @@ householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nq
             const int u2 = u + WARPS;
             const bool has2 = u2 < units;
             const int k1 = u / nq, q1 = u % nq, k2 = u2 / nq, q2 = u2 % nq;
-            T *col1 = w + (int64_t)(c0 + k1 * G) * ld + j + q1 * CH;
-            T *col2 = w + (int64_t)(c0 + (has2 ? k2 : k1) * G) * ld + j + (has2 ? q2 : q1) * CH;
+            T *col1 = col(c0 + k1 * G) + j + q1 * CH;
+            T *col2 = col(c0 + (has2 ? k2 : k1) * G) + j + (has2 ? q2 : q1) * CH;
             const T t1 = sh_t[k1], t2 = has2 ? sh_t[k2] : O::zero();
             const int cnt1 = min(CH, L - q1 * CH), cnt2 = has2 ? min(CH, L - q2 * CH) : 0;
             const T *v1 = v + q1 * CH, *v2 = v + (has2 ? q2 : q1) * CH;
@@ -399,6 +424,14 @@ householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nq
             }
         }
         __syncthreads();
+    }
+    if (SMEM) {
+        __syncthreads();
+        for (int q = 0; q < nloc; ++q) {
+            T *dst = w + (int64_t)(b + q * G) * ld;
+            const T *src = sm_cols + (size_t)q * d;
+            for (int i = threadIdx.x; i < d; i += THREADS) dst[i] = src[i];
+        }
     }
 }
 
@@ -462,7 +495,7 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
     SK_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), st));
     static const bool barrier_kernel = getenv("SK_QR_BARRIER") != nullptr;   // A/B: the grid-barrier kernel
     auto kfn = householder_kernel<T>;
-    auto ffn = householder_flow_kernel<T>;
+    auto ffn = householder_flow_kernel<T, false>;
     const bool flow = !barrier_kernel;
     const int maxb = max_coop_blocks(flow ? (const void *)ffn : (const void *)kfn, THREADS, 0);
     if (maxb <= 0) { set_error("sk_qr_r: kernel cannot be co-resident"); return SK_ERR_ARG; }
@@ -471,7 +504,33 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
     if (blocks < 2) blocks = std::min(2, maxb);
     int di = (int)d, ni = (int)n;
     int64_t ldw = d;
-    if (flow && (n + blocks - 1) / blocks <= MAXCH) {
+    // shared-memory-resident columns whenever they fit (SK_QR_SMEM=0 forces the global one)
+    static const char *qr_smem_env = getenv("SK_QR_SMEM");
+    const bool try_smem = flow && !(qr_smem_env && strcmp(qr_smem_env, "0") == 0);
+    bool launched = false;
+    if (try_smem) {
+        auto sfn = householder_flow_kernel<T, true>;
+        const int gs = (int)std::min<int64_t>(sm_count(), n);
+        const int64_t nloc = (n + gs - 1) / gs;
+        const size_t smem = (size_t)(nloc * d + nloc * nq_max(d)) * sizeof(T);
+        int optin = 0, dev = 0;
+        cudaFuncAttributes fa{};
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (gs >= 2 && cudaFuncGetAttributes(&fa, (const void *)sfn) == cudaSuccess &&
+            smem + fa.sharedSizeBytes + 1024 <= (size_t)optin &&
+            cudaFuncSetAttribute((const void *)sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+            max_coop_blocks((const void *)sfn, THREADS, smem) >= gs) {
+            SK_CUDA(cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st));
+            void *args[] = {&w, &ldw, &di, &ni, &alphas, &part, &taus, &v0s, &flags, &ctl};
+            SK_CUDA(cudaLaunchCooperativeKernel((const void *)sfn, dim3(gs), dim3(THREADS), args, smem, st));
+            SK_LAUNCH_CHECK("householder_flow_kernel (smem)");
+            launched = true;
+        }
+        cudaGetLastError();   // a refused attribute / occupancy query falls back below
+    }
+    if (launched) {
+    } else if (flow && (n + blocks - 1) / blocks <= MAXCH) {
         SK_CUDA(cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st));
         void *args[] = {&w, &ldw, &di, &ni, &alphas, &part, &taus, &v0s, &flags, &ctl};
         SK_CUDA(cudaLaunchCooperativeKernel((const void *)ffn, dim3(blocks), dim3(THREADS), args, 0, st));
