@@ -60,26 +60,33 @@ __device__ __forceinline__ T chunk_node(const T *u, const T *v, int L, int q, in
     const int base = q * CH + lane * 8;
     const int cnt = max(0, min(8, L - base));
     T x[8];
+    T node;
+    if (cnt == 8 && (ov == 0 || base != 0)) {   // full leaves, no compact-reflector element: no guards
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        if (e < cnt) {
-            const bool first = (base + e) == 0;
-            const T a = (first && (ov & 1)) ? v0 : u[base + e];
-            const T b = (first && (ov & 2)) ? v0 : v[base + e];
-            x[e] = O::mul(a, b);
-        } else {
-            x[e] = O::zero();
+        for (int e = 0; e < 8; ++e) x[e] = O::mul(u[base + e], v[base + e]);
+        node = O::add(O::add(O::add(x[0], x[1]), O::add(x[2], x[3])), O::add(O::add(x[4], x[5]), O::add(x[6], x[7])));
+    } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            if (e < cnt) {
+                const bool first = (base + e) == 0;
+                const T a = (first && (ov & 1)) ? v0 : u[base + e];
+                const T b = (first && (ov & 2)) ? v0 : v[base + e];
+                x[e] = O::mul(a, b);
+            } else {
+                x[e] = O::zero();
+            }
         }
+        const T y0 = (1 < cnt) ? O::add(x[0], x[1]) : x[0];
+        const T y1 = (3 < cnt) ? O::add(x[2], x[3]) : x[2];
+        const T y2 = (5 < cnt) ? O::add(x[4], x[5]) : x[4];
+        const T y3 = (7 < cnt) ? O::add(x[6], x[7]) : x[6];
+        const int c1 = (cnt + 1) >> 1;
+        const T z0 = (1 < c1) ? O::add(y0, y1) : y0;
+        const T z1 = (3 < c1) ? O::add(y2, y3) : y2;
+        const int c2 = (c1 + 1) >> 1;
+        node = (1 < c2) ? O::add(z0, z1) : z0;
     }
-    const T y0 = (1 < cnt) ? O::add(x[0], x[1]) : x[0];
-    const T y1 = (3 < cnt) ? O::add(x[2], x[3]) : x[2];
-    const T y2 = (5 < cnt) ? O::add(x[4], x[5]) : x[4];
-    const T y3 = (7 < cnt) ? O::add(x[6], x[7]) : x[6];
-    const int c1 = (cnt + 1) >> 1;
-    const T z0 = (1 < c1) ? O::add(y0, y1) : y0;
-    const T z1 = (3 < c1) ? O::add(y2, y3) : y2;
-    const int c2 = (c1 + 1) >> 1;
-    T node = (1 < c2) ? O::add(z0, z1) : z0;
 #pragma unroll
     for (int s = 1; s < 32; s <<= 1) {
         const T other = __shfl_xor_sync(0xffffffffu, node, s);
@@ -392,11 +399,11 @@ householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nq
         const int mine = c0 < n ? (n - 1 - c0) / G + 1 : 0;
         if (mine == 0) continue;
         const int units = mine * nq;
-        for (int u = warp; u < units; u += WARPS) {
-            const int k = u / nq, q = u % nq;
+        for (int u = warp, k = warp / nq, q = warp % nq; u < units; u += WARPS) {   // (k, q) = (u / nq, u % nq)
             const int c = c0 + k * G;
             const T node = chunk_node<T>(v, col(c) + j, L, q, 1, v0);
             if (lane == 0) part_at(k, q, c) = node;
+            for (q += WARPS; q >= nq; q -= nq) ++k;
         }
         __syncthreads();
         for (int k = warp; k < mine; k += WARPS) {
@@ -405,15 +412,28 @@ householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nq
             if (lane == 0) sh_t[k] = O::mul(tau, root);
         }
         __syncthreads();
-        for (int u = warp; u < units; u += 2 * WARPS) {
+        for (int u = warp, kn = warp / nq, qn = warp % nq; u < units; u += 2 * WARPS) {
             const int u2 = u + WARPS;
             const bool has2 = u2 < units;
-            const int k1 = u / nq, q1 = u % nq, k2 = u2 / nq, q2 = u2 % nq;
+            const int k1 = kn, q1 = qn;                 // (u / nq, u % nq)
+            int k2 = k1, q2 = q1;                       // (u2 / nq, u2 % nq)
+            for (q2 += WARPS; q2 >= nq; q2 -= nq) ++k2;
+            kn = k2;                                    // next u = u2 + WARPS
+            for (qn = q2 + WARPS; qn >= nq; qn -= nq) ++kn;
             T *col1 = col(c0 + k1 * G) + j + q1 * CH;
             T *col2 = col(c0 + (has2 ? k2 : k1) * G) + j + (has2 ? q2 : q1) * CH;
             const T t1 = sh_t[k1], t2 = has2 ? sh_t[k2] : O::zero();
             const int cnt1 = min(CH, L - q1 * CH), cnt2 = has2 ? min(CH, L - q2 * CH) : 0;
             const T *v1 = v + q1 * CH, *v2 = v + (has2 ? q2 : q1) * CH;
+            if (cnt1 == CH && cnt2 == CH && q1 != 0 && q2 != 0) {   // two full chunks without v_0: no guards
+#pragma unroll
+                for (int i = lane; i < CH; i += 32) {
+                    const T a1 = col1[i], a2 = col2[i], x1 = v1[i], x2 = v2[i];
+                    col1[i] = O::sub(a1, O::mul(x1, t1));
+                    col2[i] = O::sub(a2, O::mul(x2, t2));
+                }
+                continue;
+            }
 #pragma unroll 4
             for (int i = lane; i < CH; i += 32) {
                 T a1 = O::zero(), a2 = O::zero(), x1 = O::zero(), x2 = O::zero();
