@@ -32,6 +32,8 @@
 // extract_r.  v.v differs from x.x only in element 0, so only chunk 0 is redone.
 // The Q factor is not formed (build_preconditioner only uses R,
 // src/solvers.py:196-197); see DESIGN.md for the reference's non-finite-Q check.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -426,11 +428,35 @@ householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nq
             const int cnt1 = min(CH, L - q1 * CH), cnt2 = has2 ? min(CH, L - q2 * CH) : 0;
             const T *v1 = v + q1 * CH, *v2 = v + (has2 ? q2 : q1) * CH;
             if (cnt1 == CH && cnt2 == CH && q1 != 0 && q2 != 0) {   // two full chunks without v_0: no guards
+                if (std::is_same<T, __half>::value && (ld & 1) == 0 && (d & 1) == 0) {
+                    // element pairs on 4-byte boundaries (column and reflector share the parity
+                    // of j): HMUL2 / HSUB2 round each half exactly like the scalar ops
+                    const int off = j & 1;
+                    const __half2 tt1 = __half2half2(t1), tt2 = __half2half2(t2);
 #pragma unroll
-                for (int i = lane; i < CH; i += 32) {
-                    const T a1 = col1[i], a2 = col2[i], x1 = v1[i], x2 = v2[i];
-                    col1[i] = O::sub(a1, O::mul(x1, t1));
-                    col2[i] = O::sub(a2, O::mul(x2, t2));
+                    for (int r = 0; r < CH / 64; ++r) {
+                        const int i = off + 2 * (lane + 32 * r);
+                        if (i + 1 < CH) {
+                            __half2 *p1 = reinterpret_cast<__half2 *>(col1 + i), *p2 = reinterpret_cast<__half2 *>(col2 + i);
+                            const __half2 a1 = *p1, a2 = *p2;
+                            const __half2 x1 = *reinterpret_cast<const __half2 *>(v1 + i);
+                            const __half2 x2 = *reinterpret_cast<const __half2 *>(v2 + i);
+                            *p1 = __hsub2_rn(a1, __hmul2_rn(x1, tt1));
+                            *p2 = __hsub2_rn(a2, __hmul2_rn(x2, tt2));
+                        }
+                    }
+                    if (off && lane < 2) {     // odd j: elements 0 and CH - 1 stay single
+                        const int i = lane ? CH - 1 : 0;
+                        col1[i] = O::sub(col1[i], O::mul(v1[i], t1));
+                        col2[i] = O::sub(col2[i], O::mul(v2[i], t2));
+                    }
+                } else {
+#pragma unroll
+                    for (int i = lane; i < CH; i += 32) {
+                        const T a1 = col1[i], a2 = col2[i], x1 = v1[i], x2 = v2[i];
+                        col1[i] = O::sub(a1, O::mul(x1, t1));
+                        col2[i] = O::sub(a2, O::mul(x2, t2));
+                    }
                 }
                 continue;
             }

@@ -20,7 +20,7 @@ import paper_2603_16644_b200 as sq
 from oracle import restatement as R
 out = {}
 cases = [(6144, 2048, "binary16", 1.0), (3000, 1000, "binary32", 1.0), (1200, 400, "binary64", 1.0),
-         (700, 300, "binary16", 1.0), (600, 40, "binary16", 1e-6)]
+         (700, 300, "binary16", 1.0), (600, 40, "binary16", 1e-6), (1001, 333, "binary16", 1.0)]   # odd d: no half2 pairs
 for d, n, lev, spread in cases:
     g = R.philox(d + n, 5)
     a = g.standard_normal((d, n)) * np.logspace(0, np.log10(spread), n)   # spread < 1: graded columns
