@@ -64,9 +64,27 @@ __device__ __forceinline__ T chunk_node(const T *u, const T *v, int L, int q, in
     T x[8];
     T node;
     if (cnt == 8 && (ov == 0 || base != 0)) {   // full leaves, no compact-reflector element: no guards
+        bool paired = false;
+        if constexpr (std::is_same<T, __half>::value) {
+            // 4-byte aligned operands: the products and the first two tree levels as half2
+            // ops (each half rounded like the scalar op, so the node is bitwise the same)
+            if (((reinterpret_cast<uintptr_t>(u + base) | reinterpret_cast<uintptr_t>(v + base)) & 3) == 0) {
+                const __half2 *u2 = reinterpret_cast<const __half2 *>(u + base);
+                const __half2 *v2 = reinterpret_cast<const __half2 *>(v + base);
+                const __half2 p0 = __hmul2_rn(u2[0], v2[0]), p1 = __hmul2_rn(u2[1], v2[1]);
+                const __half2 p2 = __hmul2_rn(u2[2], v2[2]), p3 = __hmul2_rn(u2[3], v2[3]);
+                const __half2 y01 = __hadd2_rn(__lows2half2(p0, p1), __highs2half2(p0, p1));   // (x0+x1, x2+x3)
+                const __half2 y23 = __hadd2_rn(__lows2half2(p2, p3), __highs2half2(p2, p3));   // (x4+x5, x6+x7)
+                const __half2 z = __hadd2_rn(__lows2half2(y01, y23), __highs2half2(y01, y23)); // (z0, z1)
+                node = O::add(__low2half(z), __high2half(z));
+                paired = true;
+            }
+        }
+        if (!paired) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) x[e] = O::mul(u[base + e], v[base + e]);
-        node = O::add(O::add(O::add(x[0], x[1]), O::add(x[2], x[3])), O::add(O::add(x[4], x[5]), O::add(x[6], x[7])));
+            for (int e = 0; e < 8; ++e) x[e] = O::mul(u[base + e], v[base + e]);
+            node = O::add(O::add(O::add(x[0], x[1]), O::add(x[2], x[3])), O::add(O::add(x[4], x[5]), O::add(x[6], x[7])));
+        }
     } else {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
