@@ -7,7 +7,16 @@ SRCS := $(wildcard $(SRC_DIR)/*.cu)
 OBJS := $(patsubst $(SRC_DIR)/%.cu,build/%.o,$(SRCS))
 LIB := paper_2603_16644_b200/libsklsq.so
 
-all: $(LIB)
+ORACLE_LIB := oracle/_build/liboracle.so
+
+all: $(LIB) $(ORACLE_LIB)
+
+oracle: $(ORACLE_LIB)
+
+# the CPU oracle's compiled restatement (test infrastructure, never linked into the product)
+$(ORACLE_LIB): oracle/csrc/*.c
+	@mkdir -p oracle/_build
+	gcc -O3 -fopenmp -ffp-contract=off -mavx2 -mf16c -fPIC -shared -o $@ oracle/csrc/*.c
 
 build/%.o: $(SRC_DIR)/%.cu $(SRC_DIR)/*.cuh include/sklsq.h
 	@mkdir -p build
@@ -17,6 +26,6 @@ $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) oracle/_build
 
-.PHONY: all clean
+.PHONY: all clean oracle

@@ -48,7 +48,8 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--m", type=int, default=4 * 1024 * 1024, help="rows per GPU")
+    p.add_argument("--m", type=int, default=None,
+                   help="total rows (default: config 3, 4M, at N = 1; config 4, 16M row-sharded, at N > 1)")
     p.add_argument("--n", type=int, default=2048)
     p.add_argument("--kappa", type=float, default=10.0)
     p.add_argument("--rho", type=float, default=1e-6)
@@ -182,7 +183,7 @@ def trsm_blocks(n, base=TRSM_LEAF):
     and (h, w) of every INT8 update."""
     if n <= base:
         return [n], []
-    h = min((n // 2 + 255) // 256 * 256, 8192)
+    h = min((n // 2 + 255) // 256 * 256, 2048)
     l1, u1 = trsm_blocks(h, base)
     l2, u2 = trsm_blocks(n - h, base)
     return l1 + l2, u1 + [(h, n - h)] + u2
@@ -297,7 +298,7 @@ def cpu_sample_run(args, sample):
     rep = R.pipeline(p.a, p.b, method=args.method, precision=args.precision, seed=1, x_star=p.x_star,
                      diagnostics=False, timings=tm)
     wall = time.perf_counter() - t0
-    M, N = args.m * args.gpus, args.n
+    M, N = total_rows(args), args.n
     fm, fn = M / ms, N / ns
     scale = {"kappa0": fm * fn * fn, "sketch": fm * fn * math.log2(M) / math.log2(ms),
              "level_qr": fn ** 3, "trsm": fm * fn * fn, "solve": fm * fn * fn}
@@ -331,7 +332,7 @@ def run_reference(args, rank, world):
               f"{args.cpu_sample} planted problem (kappa={args.kappa:g}, {args.method}, precision={args.precision}); "
               f"measured {statistics.median([r['sample_s'] for r in reps]):.2f} s per sample, extrapolated per stage "
               f"(m n^2 stages x (M/m_s)(N/n_s)^2, level QR x (N/n_s)^3, sketch x m log m n) to "
-              f"{args.m * args.gpus}x{args.n}")
+              f"{total_rows(args)}x{args.n}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "ms", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -342,14 +343,25 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+CONFIG3_M = 4 * 1024 * 1024
+CONFIG4_M = 16 * 1024 * 1024
+
+
+def total_rows(args):
+    return args.m if args.m else (CONFIG3_M if args.gpus == 1 else CONFIG4_M)
+
+
 def workload_config(args):
-    return {"workload": (f"config 3: A {args.m * args.gpus:,} x {args.n} fp64 (rows/GPU {args.m:,}), "
-                         f"kappa(A)={args.kappa:g}, residual rho={args.rho:g}, {args.method.upper()}, "
-                         f"precision={args.precision}, d=3n DCT-II sketch"),
-            "m_total": args.m * args.gpus, "m_per_gpu": args.m, "n": args.n, "kappa": args.kappa, "rho": args.rho,
+    m = total_rows(args)
+    name = "config 3" if (args.gpus == 1 and m == CONFIG3_M) else ("config 4" if m == CONFIG4_M else "custom")
+    return {"workload": (f"{name}: A {m:,} x {args.n} fp64, {args.gpus} GPU(s) x {m // args.gpus:,} rows "
+                         f"(one global planted problem, contiguous row shards), kappa(A)={args.kappa:g}, "
+                         f"residual rho={args.rho:g}, {args.method.upper()}, precision={args.precision}, "
+                         f"d=3n DCT-II sketch"),
+            "m_total": m, "m_per_gpu": m // args.gpus, "n": args.n, "kappa": args.kappa, "rho": args.rho,
             "method": args.method, "precision": args.precision, "d_factor": 3.0, "transform": "dct2",
             "l2": "inputs larger than L2 (A is 8 m n bytes >> 126 MB): no flush needed",
-            "parallelism": f"row-shard x{args.gpus}"}
+            "parallelism": f"row-shard x{args.gpus} (NCCL all-reduce of the kappa0 Gram, sketch, Gram + rhs)"}
 
 
 # --------------------------------------------------------------- our arm ----
@@ -366,9 +378,13 @@ def run_ours(args, rank, world):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    m, n = args.m, args.n
+    m_total, n = total_rows(args), args.n
+    if m_total % world:
+        raise SystemExit(f"rows {m_total} not divisible by {world} ranks")
+    m = m_total // world
     d = int(math.ceil(3.0 * n))
-    a, b, x_star = generate_problem_device(m, n, args.kappa, args.rho, args.seed + 7919 * rank, dev)
+    # one global planted problem: the same R and x* on every rank, Q1_g and e_g per rank
+    a, b, x_star = generate_problem_device(m, n, args.kappa, args.rho, args.seed, dev, rank=rank, world=world)
     torch.cuda.synchronize()
 
     def barrier():
@@ -497,7 +513,16 @@ def run_ours(args, rank, world):
 
     # ---- e2e: host buffers, H2D + D2H inside the timed region ----
     e2e = None
-    if not args.no_e2e and args.e2e_steps > 0:
+    host_need = 8.0 * m * n * world * 1.15
+    host_ok = True
+    try:
+        import psutil
+        host_ok = psutil.virtual_memory().available > host_need
+    except Exception:  # noqa: BLE001
+        pass
+    if not host_ok:
+        e2e = {"value": None, "unit": "ms", "skipped": f"host RAM: {world} pinned shards need {host_need / 1e9:.0f} GB"}
+    elif not args.no_e2e and args.e2e_steps > 0:
         a_host = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
         a_host.copy_(a)
         b_host = b.to("cpu").pin_memory()
@@ -535,8 +560,14 @@ def run_ours(args, rank, world):
                               f"{m * world}x{n}; sample level {s['level']}")}
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "ms", "cores": cpu_cores(), "kind": "port", "sample": f"failed: {ex!r}"}
+    extra = {}
+    if world == 1 and m == CONFIG3_M:
+        extra["config4_t1_extrapolated_ms"] = {
+            "value": 4 * ms, "basis": "linear-in-m extrapolation 4 x T(1 GPU, 4M x 2048): config 4 "
+                                      "(16M x 2048, 275 GB) does not fit one GPU (SURVEY §8(d))"}
     line = {"metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "strong" if world > 1 else "weak", **extra,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (GPU Algorithm-2 generator, probgen.py)",
             "config": workload_config(args), **summary,
             "roofline": roof,
@@ -568,9 +599,24 @@ def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
-    if world != args.gpus and world == 1 and args.gpus > 1:
-        print(json.dumps({"error": "launch with torchrun for --gpus > 1"}))
-        return 2
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "reference":      # the CPU arm runs on rank 0 only anyway
+            run_reference(args, 0, 1)
+            return 0
+        # plain `python bench.py --gpus N`: spawn one rank per GPU ourselves
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"metric": METRIC, "n_gpus": args.gpus,
+                              "error": f"--gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}"}))
+            return 1
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return 0

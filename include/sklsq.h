@@ -127,6 +127,11 @@ int sk_gram_ozaki_f64(const double *x, int64_t ldx, const double *y, int64_t ldy
 int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
                          const double *xstats, const double *ystats, double *g, int64_t ldg, void *ws,
                          size_t ws_bytes, sk_stream_t stream);
+/* Same, G += X^T Y when accumulate != 0 (the per-call FP64 result is added to G, so
+ * row-chunked products, e.g. A_p produced chunk by chunk, sum their Grams in FP64). */
+int sk_gram_ozaki_acc_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
+                          const double *xstats, const double *ystats, double *g, int64_t ldg, int accumulate,
+                          void *ws, size_t ws_bytes, sk_stream_t stream);
 /* 1 if the last sk_gram_ozaki_* call on this host thread took the FP64 fallback. */
 int sk_gram_ozaki_fell_back(void);
 /* stats[j] = max_k |X[k,j]|, stats[n + j] = sum_k X[k,j]^2 and, if v != NULL,
@@ -212,6 +217,30 @@ size_t sk_qr_workspace(int level, int64_t d, int64_t n);
 int sk_qr_r(int level, void *a_s, int64_t d, int64_t n, double *r, int64_t ldr,
             sk_status *status, void *ws, size_t ws_bytes, sk_stream_t stream);
 
+/* qr_in_precision(a, level) in full: src/precision.py:153-202.  a is the f64 input
+ * (d x n row-major, lda; not modified).  The demotion follows the reference: binary16
+ * takes max|a| and the power-of-two scale on the f64 values and rounds a * scale once
+ * (src/precision.py:188-194), binary32 raises SK_OVERFLOW when the demotion overflows
+ * (:181-184), binary64 is householder_qr (:179-180).  R as sk_qr_r; if q != NULL the thin
+ * Q (d x n row-major f64, ldq) is accumulated backward from the reflectors in the level
+ * arithmetic (accumulate_thin_q src/dense.py:164-172; binary16 op for op with HALF_OPS) and
+ * a non-finite binary16 Q or R gives SK_OVERFLOW (src/precision.py:200-201).
+ * d <= 262144.  Workspace from sk_qr_factors_workspace(level, d, n). */
+size_t sk_qr_factors_workspace(int level, int64_t d, int64_t n);
+int sk_qr_in_precision_f64(int level, const double *a, int64_t lda, int64_t d, int64_t n, double *r, int64_t ldr,
+                           double *q, int64_t ldq, sk_status *status, void *ws, size_t ws_bytes, sk_stream_t stream);
+/* householder_reduce(a) src/dense.py:108-161 in binary64: R (n x n), the reflectors
+ * (v, m x n row-major ldv: reflector j = v[j:, j] with its unnormalised first entry
+ * x_0 - alpha on the diagonal, zeros above; NULL to skip) and taus (n, tau_j = 2 / v_j.v_j;
+ * NULL to skip).  m <= 262144.  Workspace from sk_qr_factors_workspace(64, m, n). */
+int sk_householder_f64(const double *a, int64_t lda, int64_t m, int64_t n, double *r, int64_t ldr, double *v,
+                       int64_t ldv, double *taus, sk_status *status, void *ws, size_t ws_bytes, sk_stream_t stream);
+/* accumulate_thin_q(reflectors, taus, m, n, ops, dtype) src/dense.py:164-172 in the level
+ * dtype (16: HALF_OPS semantics; 32 / 64 native): v COLUMN-major m x n (ldv >= m),
+ * reflector j in v[j:, j]; taus (n); q COLUMN-major m x n (ldq >= m), overwritten. */
+int sk_accumulate_q(int level, const void *v, int64_t ldv, const void *taus, int64_t m, int64_t n, void *q,
+                    int64_t ldq, sk_stream_t stream);
+
 /* ---- n x n FP64 kernels (replicated, latency-bound) ---------------------- */
 /* x = S^{-1} rhs by Cholesky: cholesky_solve src/dense.py:314-342 (symmetry gate
  * 10 eps max|S| -> SK_NOT_SYMMETRIC, pivot <= 0 or non-finite ->
@@ -257,10 +286,14 @@ int sk_jacobi_sv_f64(const double *a, int64_t rows, int64_t n, int64_t lda, int 
                      double tol, double *sv_host, void *ws, size_t ws_bytes, sk_stream_t stream);
 
 /* ---- the SURVEY §8(b) contract names ------------------------------------- */
-/* Gram plus rhs in one call: G = X^T Y (SYRK when Y == X) and, if v != NULL,
+/* These run on the production Gram engine, the one algorithm1_pipeline uses: the INT8
+ * tensor-core Ozaki-II product (sk_gram_ozaki_ex_f64, its column scan forming X^T v in
+ * the same pass) when m n^2 >= 2^33 and n >= 128, FP64 DMMA (sk_gram_f64 +
+ * sk_gemv_t_f64) below; the environment variable SK_GRAM_ENGINE=dmma|ozaki overrides.
+ * Gram plus rhs in one call: G = X^T Y (SYRK when Y == X) and, if v != NULL,
  * rhs = X^T v.  solve_pne / solve_hpne / solve_notnormal: `g, rhs = a_p.T @ a_p,
  * a_p.T @ b` src/solvers.py:230-231, `a_p.T @ a, a_p.T @ b` :251, `b_matrix.T @ a`
- * :164. */
+ * :164.  sk_gemm_tn_workspace(m, n) also sizes sk_syrk_f64. */
 size_t sk_gemm_tn_workspace(int64_t m, int64_t n);
 int sk_gemm_tn_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
                    const double *v, double *g, int64_t ldg, double *rhs, void *ws, size_t ws_bytes,

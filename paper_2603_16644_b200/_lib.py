@@ -50,6 +50,7 @@ SIGNATURES = {
     "sk_gram_ozaki_workspace": (_sz, [_i64, _i64, _i32]),
     "sk_gram_ozaki_f64": (_i32, [_p, _i64, _p, _i64, _i64, _i64, _p, _i64, _p, _sz, _p]),
     "sk_gram_ozaki_ex_f64": (_i32, [_p, _i64, _p, _i64, _i64, _i64, _p, _p, _p, _i64, _p, _sz, _p]),
+    "sk_gram_ozaki_acc_f64": (_i32, [_p, _i64, _p, _i64, _i64, _i64, _p, _p, _p, _i64, _i32, _p, _sz, _p]),
     "sk_gram_ozaki_fell_back": (_i32, []),
     "sk_colstats_workspace": (_sz, [_i64]),
     "sk_colstats_f64": (_i32, [_p, _i64, _i64, _i64, _p, _p, _p, _sz, _p]),
@@ -69,6 +70,10 @@ SIGNATURES = {
     "sk_sketch_finalize": (_i32, [_i32, _p, _i64, _i64, _i64, _i64, _p, _p, _p]),
     "sk_qr_workspace": (_sz, [_i32, _i64, _i64]),
     "sk_qr_r": (_i32, [_i32, _p, _i64, _i64, _p, _i64, _ps, _p, _sz, _p]),
+    "sk_qr_factors_workspace": (_sz, [_i32, _i64, _i64]),
+    "sk_qr_in_precision_f64": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _i64, _p, _i64, _ps, _p, _sz, _p]),
+    "sk_householder_f64": (_i32, [_p, _i64, _i64, _i64, _p, _i64, _p, _i64, _p, _ps, _p, _sz, _p]),
+    "sk_accumulate_q": (_i32, [_i32, _p, _i64, _p, _i64, _i64, _p, _i64, _p]),
     "sk_nxn_workspace": (_sz, [_i64]),
     "sk_chol_solve_f64": (_i32, [_p, _i64, _p, _p, _ps, _p, _sz, _p]),
     "sk_gram_check": (_i32, [_p, _i64, _pd, _p, _sz, _p]),

@@ -636,7 +636,8 @@ __global__ void reduce_kernel(const int32_t *__restrict__ part, int splits, int 
 
 // ------------------------------------------------------- reconstruction -----
 __global__ void crt_kernel(const int32_t *__restrict__ acc, int n, int syrk, const int *__restrict__ ex,
-                           const int *__restrict__ ey, int t, double *__restrict__ g, int64_t ldg, int nm) {
+                           const int *__restrict__ ey, int t, double *__restrict__ g, int64_t ldg, int nm,
+                           int accumulate) {
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nn = (int64_t)n * n;
     if (idx >= nn) return;
@@ -671,7 +672,9 @@ __global__ void crt_kernel(const int32_t *__restrict__ acc, int n, int syrk, con
     const double hi = (double)(unsigned long long)(mag >> 64), lo = (double)(unsigned long long)mag;
     double val = fma(hi, 18446744073709551616.0, lo);
     val = neg ? -val : val;
-    g[(int64_t)i * ldg + j] = ldexp(val, ex[i] + ey[j] - 2 * t);
+    const double out = ldexp(val, ex[i] + ey[j] - 2 * t);
+    double *dst = g + (int64_t)i * ldg + j;
+    *dst = accumulate ? *dst + out : out;   // row-chunked callers sum per-chunk Grams in FP64
 }
 
 // ================================================ blocked TRSM update (product) ==
@@ -1003,7 +1006,10 @@ SidePipe &side_pipe() {
 }
 
 // ----------------------------------------------------- blocked TRSM plan -----
-constexpr int64_t TRSM_KMAX = 8192;   // update depth h: |int32 partials| < 2^27 (i32_residue)
+// update depth h: rowres_kernel spreads one row of P over its 256 threads x RV = 2048
+// columns (and |int32 partials| < 2^27 needs h <= 8192), so h is capped at 2048; wider
+// solves recurse on the right part with more updates
+constexpr int64_t TRSM_KMAX = 2048;
 constexpr int64_t TRSM_CHUNK = 65536;
 
 int64_t trsm_split(int64_t n) { return std::min<int64_t>((n / 2 + 255) / 256 * 256, TRSM_KMAX); }
@@ -1341,6 +1347,12 @@ int sk_gram_ozaki_f64(const double *x, int64_t ldx, const double *y, int64_t ldy
 int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
                          const double *xstats, const double *ystats, double *g, int64_t ldg, void *ws,
                          size_t ws_bytes, sk_stream_t stream) {
+    return sk_gram_ozaki_acc_f64(x, ldx, y, ldy, m, n, xstats, ystats, g, ldg, 0, ws, ws_bytes, stream);
+}
+
+int sk_gram_ozaki_acc_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
+                          const double *xstats, const double *ystats, double *g, int64_t ldg, int accumulate,
+                          void *ws, size_t ws_bytes, sk_stream_t stream) {
     if (!x || !y || !g || m < 0 || n <= 0 || ldx < n || ldy < n || ldg < n || n > 65536) {
         set_error("sk_gram_ozaki_f64: bad arguments");
         return SK_ERR_ARG;
@@ -1395,7 +1407,7 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
             set_error("sk_gram_ozaki_f64: workspace too small for the DMMA fallback");
             return SK_ERR_ARG;
         }
-        return sk_gram_f64(x, ldx, y, ldy, m, n, g, ldg, 0, ws, ws_bytes, stream);
+        return sk_gram_f64(x, ldx, y, ldy, m, n, g, ldg, accumulate, ws, ws_bytes, stream);
     }
     oz::stats_to_bits<<<sgrid, 256, 0, st>>>(sx, (int)n, bits);
     oz::stats_to_bits<<<sgrid, 256, 0, st>>>(sy, (int)n, bits + n);
@@ -1484,7 +1496,7 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
     const int64_t nn = n * n;
     if (prof) SK_CUDA(cudaEventRecord(pe[npe++], st));
     oz::crt_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, gs>>>(acc, (int)n, syrk, expo, expo + n, p.t, g, ldg,
-                                                                 p.nm);
+                                                                 p.nm, accumulate);
     SK_LAUNCH_CHECK("oz crt");
     if (!serial) {   // the caller's stream resumes after the reconstruction
         SK_CUDA(cudaEventRecord(sp.end, sp.hi));

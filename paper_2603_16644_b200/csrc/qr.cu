@@ -536,9 +536,16 @@ size_t ws_bytes(int64_t d, int64_t n) {
            2 * align_up((size_t)n * sizeof(T), 256) + align_up((size_t)n * sizeof(int), 256);   // flow kernel
 }
 
+// Compact reflectors left behind by the dataflow kernels (taus[j], v0s[j] = v_j[0]),
+// for forming Q afterwards.
+template <typename T>
+struct Reflectors {
+    T *taus = nullptr, *v0s = nullptr;
+};
+
 template <typename T, bool HALF>
 int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_status *status, void *ws, size_t wsb,
-        cudaStream_t st) {
+        cudaStream_t st, Reflectors<T> *refl = nullptr) {
     if (wsb < ws_bytes<T>(d, n)) { set_error("sk_qr_r: workspace too small"); return SK_ERR_ARG; }
     if (nq_max(d) > MAXCH) { set_error("sk_qr_r: d too large"); return SK_ERR_ARG; }
     unsigned char *p = static_cast<unsigned char *>(ws);
@@ -557,7 +564,10 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
     int *flags = reinterpret_cast<int *>(p);
     SK_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl<T>), st));
     SK_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), st));
-    static const bool barrier_kernel = getenv("SK_QR_BARRIER") != nullptr;   // A/B: the grid-barrier kernel
+    // A/B: the grid-barrier kernel (keeps only the current reflector, so never when Q is wanted)
+    static const bool barrier_env = getenv("SK_QR_BARRIER") != nullptr;
+    const bool barrier_kernel = barrier_env && refl == nullptr;
+    if (refl) { refl->taus = taus; refl->v0s = v0s; }
     auto kfn = householder_kernel<T>;
     auto ffn = householder_flow_kernel<T, false>;
     const bool flow = !barrier_kernel;
@@ -600,6 +610,7 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
         SK_CUDA(cudaLaunchCooperativeKernel((const void *)ffn, dim3(blocks), dim3(THREADS), args, 0, st));
         SK_LAUNCH_CHECK("householder_flow_kernel");
     } else {
+        if (refl) { set_error("sk_qr: Q needs the dataflow kernel (n too large)"); return SK_ERR_ARG; }
         void *args[] = {&w, &ldw, &di, &ni, &alphas, &part, &ctl};
         SK_CUDA(cudaLaunchCooperativeKernel((const void *)kfn, dim3(blocks), dim3(THREADS), args, 0, st));
         SK_LAUNCH_CHECK("householder_kernel");
@@ -622,6 +633,208 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
         return fill_status(status, SK_OVERFLOW, -1, 0.0, 0.0);
     }
     return fill_status(status, SK_OK, -1, 0.0, 0.0);
+}
+
+
+// ------------------------------------------------ full factors (public API) --
+// qr_in_precision / householder_reduce / accumulate_thin_q of the reference
+// (src/precision.py:153-202, src/dense.py:108-172): the level QR from an f64 input
+// (demotion and the binary16 power-of-two prescale on the f64 values, exactly as
+// the reference orders them) plus, on request, the thin Q accumulated backward from
+// the compact reflectors in the level arithmetic.
+
+__global__ void maxabs_f64(const double *a, int64_t lda, int64_t rows, int64_t cols, unsigned long long *out_bits) {
+    double mx = 0.0;
+    const int64_t count = rows * cols;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        mx = fmax(mx, fabs(a[(i / cols) * lda + i % cols]));
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) atomicMax(out_bits, (unsigned long long)__double_as_longlong(mx));
+}
+
+// w (column-major, ld = d) = level(a * scale): round_to_precision src/precision.py:90-103
+// (one correctly rounded conversion from f64; `scale` is a power of two, so a * scale is
+// exact); *overflow counts entries that became infinite from finite input
+template <typename T>
+__global__ void demote_colmajor(const double *a, int64_t lda, int64_t d, int64_t n, double scale, T *w,
+                                int *overflow) {
+    __shared__ double tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8 threads
+    for (int k = ty; k < 32; k += 8) {
+        const int64_t r = r0 + k, c = c0 + tx;
+        tile[k][tx] = (r < d && c < n) ? a[r * lda + c] : 0.0;
+    }
+    __syncthreads();
+    int bad = 0;
+    for (int k = ty; k < 32; k += 8) {
+        const int64_t c = c0 + k, r = r0 + tx;
+        if (r < d && c < n) {
+            const double x = tile[tx][k];
+            const T y = LevelOps<T>::from_f64(x * scale);
+            bad |= (!LevelOps<T>::finite(y) && isfinite(x));
+            w[c * d + r] = y;
+        }
+    }
+    if (bad) atomicAdd(overflow, 1);
+}
+
+// compact reflector v_j = [v0_j, w[j+1:, j]]: put v0_j on the diagonal so every column
+// holds its whole reflector
+template <typename T>
+__global__ void put_v0(T *w, int64_t ld, const T *v0s, int n) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) w[(int64_t)j * ld + j] = v0s[j];
+}
+
+// accumulate_thin_q src/dense.py:164-172: Q = H_0 ... H_{n-1} eye(m, n), reflectors applied
+// backward, each as t = tau_j * tree(v_j o Q[j:, c]) and Q[j:, c] -= v_j t (every product,
+// sum and difference rounded in T; the tree is the pairwise one of src/precision.py:106-115).
+// Columns are independent: one CTA per column.  Reflectors j > c leave column c exactly
+// zero below row c (0 - v 0 = +0 for either sign of the product), so they are skipped.
+template <typename T>
+__global__ void __launch_bounds__(512)
+accum_q_kernel(const T *v, int64_t ldv, const T *taus, int m, int n, T *q, int64_t ldq) {
+    using O = LevelOps<T>;
+    __shared__ T sh_nodes[MAXCH];
+    __shared__ T sh_t;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int c = blockIdx.x; c < n; c += gridDim.x) {
+        T *qc = q + (int64_t)c * ldq;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) qc[i] = (i == c) ? O::from_f64(1.0) : O::zero();
+        __syncthreads();
+        for (int j = c; j >= 0; --j) {
+            const int L = m - j;
+            const T *vj = v + (int64_t)j * ldv + j;
+            T *x = qc + j;
+            const int nq = (L + CH - 1) / CH;
+            for (int qq = warp; qq < nq; qq += nw) {
+                const T node = chunk_node<T>(vj, x, L, qq);
+                if (lane == 0) sh_nodes[qq] = node;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                const T root = warp_tree_root<T>(nq, [&](int i) { return sh_nodes[i]; });
+                if (lane == 0) sh_t = O::mul(taus[j], root);
+            }
+            __syncthreads();
+            const T t = sh_t;
+            for (int i = threadIdx.x; i < L; i += blockDim.x) x[i] = O::sub(x[i], O::mul(vj[i], t));
+            __syncthreads();
+        }
+    }
+}
+
+// column-major level-dtype d x n -> row-major f64 (exact promotion); counts non-finite
+template <typename T>
+__global__ void colmajor_to_f64(const T *src, int64_t lds, int64_t d, int64_t n, double *dst, int64_t ldd,
+                                int lower_only, int *nonfinite) {
+    __shared__ double tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    int bad = 0;
+    for (int k = ty; k < 32; k += 8) {
+        const int64_t c = c0 + k, r = r0 + tx;
+        double x = 0.0;
+        if (r < d && c < n && (!lower_only || r >= c)) {
+            x = LevelOps<T>::to_f64(src[c * lds + r]);
+            bad |= !isfinite(x);
+        }
+        tile[tx][k] = x;
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+        const int64_t r = r0 + k, c = c0 + tx;
+        if (r < d && c < n) dst[r * ldd + c] = tile[k][tx];
+    }
+    if (bad && nonfinite) atomicAdd(nonfinite, 1);
+}
+
+template <typename T>
+__global__ void vec_to_f64(const T *src, int n, double *dst) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) dst[j] = LevelOps<T>::to_f64(src[j]);
+}
+
+template <typename T>
+size_t factor_ws(int64_t d, int64_t n) {
+    const size_t mat = align_up((size_t)d * n * sizeof(T), 256);
+    return mat + ws_bytes<T>(d, n) + mat + 1024;
+}
+
+template <typename T, bool HALF>
+int factor(const double *a, int64_t lda, int64_t d, int64_t n, double *r, int64_t ldr, double *q, int64_t ldq,
+           double *v, int64_t ldv, double *taus_out, sk_status *status, void *ws, size_t wsb, cudaStream_t st) {
+    if (wsb < factor_ws<T>(d, n)) { set_error("sk_qr: workspace too small"); return SK_ERR_ARG; }
+    unsigned char *p = static_cast<unsigned char *>(ws);
+    const size_t mat = align_up((size_t)d * n * sizeof(T), 256);
+    T *w = reinterpret_cast<T *>(p);
+    void *qws = p + mat;
+    T *qb = reinterpret_cast<T *>(p + mat + ws_bytes<T>(d, n));
+    int *flags = reinterpret_cast<int *>(p + 2 * mat + ws_bytes<T>(d, n));   // [0] overflow/non-finite [1..2] max bits
+    SK_CUDA(cudaMemsetAsync(flags, 0, 64, st));
+    double scale = 1.0;
+    if (HALF) {   // src/precision.py:188-194: maxabs and the power-of-two scale on the f64 input
+        unsigned long long *bits = reinterpret_cast<unsigned long long *>(flags + 2);
+        const unsigned g = (unsigned)std::min<int64_t>((d * n + 255) / 256, 4 * sm_count());
+        maxabs_f64<<<g, 256, 0, st>>>(a, lda, d, n, bits);
+        SK_LAUNCH_CHECK("maxabs_f64");
+        unsigned long long hb = 0;
+        SK_CUDA(cudaMemcpyAsync(&hb, bits, sizeof(hb), cudaMemcpyDeviceToHost, st));
+        SK_CUDA(cudaStreamSynchronize(st));
+        double maxabs;
+        memcpy(&maxabs, &hb, sizeof(double));
+        if (maxabs == 0.0) {
+            set_error("zero matrix");
+            return fill_status(status, SK_RANK_DEFICIENT, -1, 0.0, 0.0);
+        }
+        int e = 0;
+        frexp(maxabs, &e);
+        scale = ldexp(1.0, -e);
+    }
+    const dim3 tg((unsigned)((n + 31) / 32), (unsigned)((d + 31) / 32));
+    demote_colmajor<T><<<tg, 256, 0, st>>>(a, lda, d, n, scale, w, flags);
+    SK_LAUNCH_CHECK("demote_colmajor");
+    if (std::is_same<T, float>::value) {   // src/precision.py:181-184
+        int ov = 0;
+        SK_CUDA(cudaMemcpyAsync(&ov, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+        SK_CUDA(cudaStreamSynchronize(st));
+        if (ov) {
+            set_error("input exceeds the binary32 range");
+            return fill_status(status, SK_OVERFLOW, -1, 0.0, 0.0);
+        }
+    }
+    Reflectors<T> refl;
+    const bool need_refl = q || v || taus_out;
+    const int rc = run<T, HALF>(w, d, n, scale, r, ldr, status, qws, ws_bytes<T>(d, n), st, need_refl ? &refl : nullptr);
+    if (rc != SK_OK || !need_refl) return rc;
+    put_v0<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w, d, refl.v0s, (int)n);
+    SK_LAUNCH_CHECK("put_v0");
+    if (v) {
+        colmajor_to_f64<T><<<tg, 256, 0, st>>>(w, d, d, n, v, ldv, 1, nullptr);
+        SK_LAUNCH_CHECK("reflectors_to_f64");
+    }
+    if (taus_out) {
+        vec_to_f64<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(refl.taus, (int)n, taus_out);
+        SK_LAUNCH_CHECK("taus_to_f64");
+    }
+    if (!q) return SK_OK;
+    const unsigned qg = (unsigned)std::min<int64_t>(n, 8 * (int64_t)sm_count());
+    accum_q_kernel<T><<<qg, 512, 0, st>>>(w, d, refl.taus, (int)d, (int)n, qb, d);
+    SK_LAUNCH_CHECK("accum_q_kernel");
+    SK_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), st));
+    colmajor_to_f64<T><<<tg, 256, 0, st>>>(qb, d, d, n, q, ldq, 0, flags);
+    SK_LAUNCH_CHECK("q_to_f64");
+    if (HALF) {   // src/precision.py:200-201
+        int nf = 0;
+        SK_CUDA(cudaMemcpyAsync(&nf, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+        SK_CUDA(cudaStreamSynchronize(st));
+        if (nf) {
+            set_error("binary16 computation produced non-finite values");
+            return fill_status(status, SK_OVERFLOW, -1, 0.0, 0.0);
+        }
+    }
+    return SK_OK;
 }
 
 }  // namespace qr
@@ -677,4 +890,74 @@ int sk_qr_r(int level, void *a_s, int64_t d, int64_t n, double *r, int64_t ldr, 
     return qr::run<__half, true>(a, d, n, scale, r, ldr, status, ws, ws_bytes, st);
 }
 
+size_t sk_qr_factors_workspace(int level, int64_t d, int64_t n) {
+    if (level == 16) return qr::factor_ws<__half>(d, n) + 256;
+    if (level == 32) return qr::factor_ws<float>(d, n);
+    return qr::factor_ws<double>(d, n);
+}
+
+static int qr_factor_args(const double *a, int64_t lda, int64_t d, int64_t n, const double *r, int64_t ldr,
+                          sk_status *status, void *ws) {
+    if (n > 0 && d < n) {
+        set_error("need rows >= cols, got %lld x %lld", (long long)d, (long long)n);
+        return fill_status(status, SK_DIMENSION_MISMATCH, -1, 0, 0);
+    }
+    if (!a || !r || !ws || n <= 0 || lda < n || ldr < n || qr::nq_max(d) > qr::MAXCH || d > INT32_MAX) {
+        set_error("sk_qr: bad arguments (d must be <= %d)", qr::MAXCH * qr::CH);
+        return SK_ERR_ARG;
+    }
+    return SK_OK;
+}
+
+int sk_qr_in_precision_f64(int level, const double *a, int64_t lda, int64_t d, int64_t n, double *r, int64_t ldr,
+                           double *q, int64_t ldq, sk_status *status, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    const int rc = qr_factor_args(a, lda, d, n, r, ldr, status, ws);
+    if (rc) return rc;
+    if (q && ldq < n) { set_error("sk_qr_in_precision_f64: ldq < n"); return SK_ERR_ARG; }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (level == 16)
+        return qr::factor<__half, true>(a, lda, d, n, r, ldr, q, ldq, nullptr, 0, nullptr, status, ws, ws_bytes, st);
+    if (level == 32)
+        return qr::factor<float, false>(a, lda, d, n, r, ldr, q, ldq, nullptr, 0, nullptr, status, ws, ws_bytes, st);
+    if (level == 64)
+        return qr::factor<double, false>(a, lda, d, n, r, ldr, q, ldq, nullptr, 0, nullptr, status, ws, ws_bytes, st);
+    set_error("bad level");
+    return SK_ERR_ARG;
+}
+
+int sk_householder_f64(const double *a, int64_t lda, int64_t m, int64_t n, double *r, int64_t ldr, double *v,
+                       int64_t ldv, double *taus, sk_status *status, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    const int rc = qr_factor_args(a, lda, m, n, r, ldr, status, ws);
+    if (rc) return rc;
+    if (v && ldv < n) { set_error("sk_householder_f64: ldv < n"); return SK_ERR_ARG; }
+    return qr::factor<double, false>(a, lda, m, n, r, ldr, nullptr, 0, v, ldv, taus, status, ws, ws_bytes,
+                                     (cudaStream_t)stream);
+}
+
+int sk_accumulate_q(int level, const void *v, int64_t ldv, const void *taus, int64_t m, int64_t n, void *q,
+                    int64_t ldq, sk_stream_t stream) {
+    if (!v || !taus || !q || n <= 0 || m < n || ldv < m || ldq < m || qr::nq_max(m) > qr::MAXCH) {
+        set_error("sk_accumulate_q: bad arguments");
+        return SK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned qg = (unsigned)std::min<int64_t>(n, 8 * (int64_t)sm_count());
+    if (level == 16)
+        qr::accum_q_kernel<__half><<<qg, 512, 0, st>>>(static_cast<const __half *>(v), ldv,
+                                                       static_cast<const __half *>(taus), (int)m, (int)n,
+                                                       static_cast<__half *>(q), ldq);
+    else if (level == 32)
+        qr::accum_q_kernel<float><<<qg, 512, 0, st>>>(static_cast<const float *>(v), ldv,
+                                                      static_cast<const float *>(taus), (int)m, (int)n,
+                                                      static_cast<float *>(q), ldq);
+    else if (level == 64)
+        qr::accum_q_kernel<double><<<qg, 512, 0, st>>>(static_cast<const double *>(v), ldv,
+                                                       static_cast<const double *>(taus), (int)m, (int)n,
+                                                       static_cast<double *>(q), ldq);
+    else { set_error("bad level"); return SK_ERR_ARG; }
+    SK_LAUNCH_CHECK("accum_q_kernel");
+    return SK_OK;
+}
+
 }  // extern "C"
+

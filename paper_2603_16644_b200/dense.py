@@ -24,8 +24,7 @@ from .errors import DimensionMismatch, RankDeficient
 
 @dataclass(frozen=True)
 class QRFactors:
-    """Thin QR factors (src/dense.py:29-34).  The device QR forms R only (the
-    solve path never needs Q); q is None unless explicitly requested."""
+    """Thin QR factors (src/dense.py:29-34)."""
 
     q: np.ndarray | None
     r: np.ndarray
@@ -53,9 +52,11 @@ OZAKI_MIN_WORK = 1 << 33   # m * n^2 above which "auto" takes the INT8 engine
 
 
 def _gram_engine(m: int, n: int, accumulate: bool, engine: str | None) -> str:
+    """Engine for an m x n Gram (accumulating calls sum per-call FP64 results on either
+    engine, so row chunks of A_p / A take the same engine as the whole would)."""
     e = engine or GRAM_ENGINE
     if e == "auto":
-        e = "ozaki" if (not accumulate and n >= 128 and m * n * n >= OZAKI_MIN_WORK) else "dmma"
+        e = "ozaki" if (n >= 128 and m * n * n >= OZAKI_MIN_WORK) else "dmma"
     return e
 
 
@@ -101,10 +102,10 @@ def _gram(x: DMat | torch.Tensor, y: DMat | torch.Tensor | None = None, out: tor
         syrk = xt.data_ptr() == yt.data_ptr() and xt.stride(0) == yt.stride(0)
         xmax = x.colstats if isinstance(x, DMat) else None
         ymax = (y.colstats if isinstance(y, DMat) else None) if y is not None else xmax
-        wp, wn = WORKSPACE.get(lib.sk_gram_ozaki_workspace(m, n, int(syrk)))
-        call("sk_gram_ozaki_ex_f64", xt.data_ptr(), xt.stride(0), yt.data_ptr(), yt.stride(0), m, n,
+        wp, wn = WORKSPACE.get(max(lib.sk_gram_ozaki_workspace(m, n, int(syrk)), lib.sk_gram_workspace(m, n)))
+        call("sk_gram_ozaki_acc_f64", xt.data_ptr(), xt.stride(0), yt.data_ptr(), yt.stride(0), m, n,
              xmax.data_ptr() if xmax is not None else None, ymax.data_ptr() if ymax is not None else None,
-             out.data_ptr(), out.stride(0), wp, wn, stream_handle())
+             out.data_ptr(), out.stride(0), int(accumulate), wp, wn, stream_handle())
         return out
     wsb = lib.sk_gram_workspace(m, n)
     wp, wn = WORKSPACE.get(wsb)
@@ -325,22 +326,91 @@ def cholesky_solve(s, rhs):
     return outs[0] if rhs_np.ndim == 1 else np.stack(outs, axis=1)
 
 
-def householder_reduce(a):
-    """R factor of a tall matrix (src/dense.py:108-161); reflectors are not
-    materialised on the host: returns (None, None, R)."""
-    ad = as_dmat(a)
-    return None, None, to_host(_householder_r64(ad.t))
+def _qr_factors_dev(at: torch.Tensor, level_code: int, want_q: bool):
+    """(R, Q or None) of a device f64 row-major d x n matrix at the given level:
+    sk_qr_in_precision_f64 (demotion and binary16 prescale on the f64 values, Q
+    accumulated from the reflectors in the level arithmetic)."""
+    at = _rm(at)
+    d, n = at.shape
+    r = torch.empty((n, n), dtype=torch.float64, device=at.device)
+    q = torch.empty((d, n), dtype=torch.float64, device=at.device) if want_q else None
+    wp, wn = WORKSPACE.get(_lib.lib().sk_qr_factors_workspace(level_code, d, n))
+    st = _lib.SkStatus()
+    call("sk_qr_in_precision_f64", level_code, at.data_ptr(), at.stride(0), d, n, r.data_ptr(), n,
+         q.data_ptr() if q is not None else None, n, C.byref(st), wp, wn, stream_handle())
+    return r, q
 
 
-def householder_qr(a):
-    """Thin QR (src/dense.py:175-201).  R on the device; Q formed on request as
-    Q = A R^{-1} only for API completeness (the solvers never need it)."""
+def householder_reduce(a, ops=None):
+    """householder_reduce (src/dense.py:108-161) in binary64 on the device:
+    (reflectors, taus, R) with reflector j of length m - j (unnormalised, first
+    entry x_0 - alpha) and tau_j = 2 / v_j.v_j, the reference's sign convention.
+    `ops` is accepted for signature parity; only the native arithmetic exists
+    (binary16 emulation is reached through qr_in_precision).  Above
+    TALL_QR_MAX_ROWS rows R comes from TSQR and the reflectors are not formed
+    (returns (None, None, R))."""
+    if ops is not None and getattr(ops, "name", "native") != "native":
+        raise ValueError("householder_reduce: only the native arithmetic is available; use qr_in_precision")
     ad = as_dmat(a)
     m, n = ad.shape
     if m < n:
         raise DimensionMismatch(f"need rows >= cols, got {m} x {n}")
-    r = _householder_r64(ad.t)
-    q = _trsm(ad, r)
+    if m > TALL_QR_MAX_ROWS:
+        return None, None, to_host(_householder_r64(ad.t))
+    r = torch.empty((n, n), dtype=torch.float64, device=ad.t.device)
+    v = torch.empty((m, n), dtype=torch.float64, device=ad.t.device)
+    taus = torch.empty(n, dtype=torch.float64, device=ad.t.device)
+    wp, wn = WORKSPACE.get(_lib.lib().sk_qr_factors_workspace(64, m, n))
+    st = _lib.SkStatus()
+    call("sk_householder_f64", ad.ptr, ad.ld, m, n, r.data_ptr(), n, v.data_ptr(), n, taus.data_ptr(),
+         C.byref(st), wp, wn, stream_handle())
+    vh, th = to_host(v), to_host(taus)
+    reflectors = [vh[j:, j].copy() for j in range(n)]
+    return reflectors, [np.float64(t) for t in th], to_host(r)
+
+
+_LEVEL_OF_DTYPE = {np.dtype(np.float16): (16, torch.float16), np.dtype(np.float32): (32, torch.float32),
+                   np.dtype(np.float64): (64, torch.float64)}
+
+
+def accumulate_thin_q(reflectors, taus, m, n, ops=None, dtype=np.float64):
+    """accumulate_thin_q (src/dense.py:164-172): the thin Q formed by applying the
+    reflectors backward to eye(m, n) in `dtype` arithmetic (float16: every scalar op
+    rounded to binary16 and pairwise-tree sums, the reference's HALF_OPS; float32 /
+    float64: native), on the device (sk_accumulate_q).  `ops` is accepted for
+    signature parity: the arithmetic follows `dtype`."""
+    dt = np.dtype(dtype)
+    if dt not in _LEVEL_OF_DTYPE:
+        raise ValueError(f"unsupported dtype {dt}")
+    if len(reflectors) != n or len(taus) != n:
+        raise DimensionMismatch(f"need {n} reflectors and taus, got {len(reflectors)} / {len(taus)}")
+    code, tdt = _LEVEL_OF_DTYPE[dt]
+    vpack = np.zeros((n, m), dtype=dt)          # row j = column j of the column-major m x n pack
+    for j, vj in enumerate(reflectors):
+        vj = np.asarray(vj)
+        if vj.shape != (m - j,):
+            raise DimensionMismatch(f"reflector {j} has shape {vj.shape}, expected {(m - j,)}")
+        vpack[j, j:] = vj.astype(dt)
+    dev = device()
+    vd = torch.from_numpy(vpack).to(dev)
+    td = torch.from_numpy(np.asarray(taus, dtype=dt)).to(dev)
+    qd = torch.empty((n, m), dtype=tdt, device=dev)
+    call("sk_accumulate_q", code, vd.data_ptr(), m, td.data_ptr(), m, n, qd.data_ptr(), m, stream_handle())
+    return np.asfortranarray(to_host(qd).T)
+
+
+def householder_qr(a):
+    """Thin QR (src/dense.py:175-201): R and Q = H_0 ... H_{n-1} eye(m, n) from the
+    device Householder factorisation (binary64, the reference's sign convention).
+    Above TALL_QR_MAX_ROWS rows R comes from TSQR and Q is formed as A R^-1."""
+    ad = as_dmat(a)
+    m, n = ad.shape
+    if m < n:
+        raise DimensionMismatch(f"need rows >= cols, got {m} x {n}")
+    if m > TALL_QR_MAX_ROWS:
+        r = _householder_r64(ad.t)
+        return QRFactors(q=to_host(_trsm(ad, r)), r=to_host(r))
+    r, q = _qr_factors_dev(ad.t, 64, True)
     return QRFactors(q=to_host(q), r=to_host(r))
 
 

@@ -96,6 +96,16 @@ class DeviceOps:
         a_s, _ = _sketch_finalize(total, op, level)
         return _qr_level_dev(a_s, level, op.d, total.shape[0])
 
+    def chunk_rows(self, m, n, device):
+        from .solvers import _ap_chunk_rows
+        return _ap_chunk_rows(m, n, device)
+
+    def trsm_gram(self, a, r, b, method, rows):
+        """TRSM -> Gram per row chunk (A_p never materialised; config 4 at P = 2)."""
+        from .solvers import _trsm_gram_chunked
+        from .device import DMat
+        return _trsm_gram_chunked(self._dmat(a) if method != "pne" else DMat(a, None, "torch"), r, b, method, rows)
+
     def trsm(self, a, r):
         # A_p in the per-device scratch buffer of algorithm1_pipeline (no 64 GB
         # allocation per solve); handed back by release()
@@ -141,10 +151,54 @@ class DeviceOps:
         return float(out[0]), float(out[1])
 
 
+def _world() -> int:
+    return dist.get_world_size() if (dist.is_available() and dist.is_initialized()) else 1
+
+
 def _allreduce(t: torch.Tensor, op=None) -> torch.Tensor:
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        dist.all_reduce(t, op=op or dist.ReduceOp.SUM)
+    """In-place all-reduce (SUM by default).  NCCL reduces device tensors over NVLink;
+    under gloo (CPU tests, or ranks sharing one GPU in the device tests) a CUDA tensor
+    is staged through host memory."""
+    if _world() > 1:
+        op = op or dist.ReduceOp.SUM
+        if t.is_cuda and dist.get_backend() == "gloo":
+            h = t.cpu()
+            dist.all_reduce(h, op=op)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=op)
     return t
+
+
+_ERR_CLASSES = None
+
+
+def _agree(fn, *args, **kw):
+    """Run a rank-local step and agree on its outcome before anyone enters the next
+    collective: if any rank raised, every rank raises (the failing rank its own
+    exception, the others the same class naming the failing rank), so one bad shard
+    cannot leave the other ranks waiting in an all-reduce."""
+    global _ERR_CLASSES
+    from . import errors as E
+    if _ERR_CLASSES is None:
+        _ERR_CLASSES = [ValueError, E.DimensionMismatch, E.Overflow, E.RankDeficient, E.SingularTriangular,
+                        E.NumericallySingular, E.NotPositiveDefinite, E.NoConvergence, E.SketchLsqError, RuntimeError]
+    exc, code = None, 0
+    try:
+        out = fn(*args, **kw)
+    except Exception as ex:  # noqa: BLE001
+        exc, out = ex, None
+        code = next((i + 1 for i, c in enumerate(_ERR_CLASSES) if isinstance(ex, c)), len(_ERR_CLASSES))
+    if _world() > 1:
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else "cpu"
+        flag = torch.tensor([code, dist.get_rank() if code else -1], dtype=torch.int64, device=dev)
+        _allreduce(flag, dist.ReduceOp.MAX)
+        code, who = int(flag[0]), int(flag[1])
+        if code and exc is None:
+            raise _ERR_CLASSES[min(code, len(_ERR_CLASSES)) - 1](f"rank {who} failed this step")
+    if exc is not None:
+        raise exc
+    return out
 
 
 def _row_layout(m_local: int, device) -> tuple[int, int]:
@@ -167,11 +221,17 @@ def algorithm1_pipeline_sharded(a_local, b_local, method="pne", precision="auto"
     ops = ops or DeviceOps()
     stages = _Stages(stage_timing and torch.cuda.is_available())
     stages.mark("check")
-    a, frob2_local = ops.validate(a_local)
+
+    def check():
+        if method not in ("pne", "hpne"):
+            raise ValueError(f"pipeline method must be pne or hpne, got {method!r}")
+        if not isinstance(precision, PrecisionLevel) and precision != "auto":
+            level_from_name(precision)
+        a_, frob2_ = ops.validate(a_local)
+        return a_, frob2_, ops.vector(b_local, a_.shape[0])
+
+    a, frob2_local, b = _agree(check)      # a bad shard raises on every rank
     m_local, n = a.shape
-    b = ops.vector(b_local, m_local)
-    if method not in ("pne", "hpne"):
-        raise ValueError(f"pipeline method must be pne or hpne, got {method!r}")
     m, offset = _row_layout(m_local, a.device)
     if m < n:
         raise DimensionMismatch(f"need rows >= cols, got {(m, n)}")
@@ -212,15 +272,20 @@ def algorithm1_pipeline_sharded(a_local, b_local, method="pne", precision="auto"
             if escalated_from is not None or wider is None:
                 raise
             escalated_from, level = level, wider
-    try:
+    def local_gram():
+        rows = ops.chunk_rows(m_local, n, a.device) if hasattr(ops, "chunk_rows") else 0
+        if rows:
+            stages.mark("trsm_gram")
+            return ops.trsm_gram(a, r_s, b, method, rows)
         stages.mark("trsm")
         a_p = ops.trsm(a, r_s)
         stages.mark("gram")
         if hasattr(ops, "gram_and_rhs"):
-            g, rhs = ops.gram_and_rhs(a_p, None if method == "pne" else a, b)
-        else:
-            g = ops.gram(a_p) if method == "pne" else ops.gram(a_p, a)
-            rhs = ops.gemv_t(a_p, b)
+            return ops.gram_and_rhs(a_p, None if method == "pne" else a, b)
+        return (ops.gram(a_p) if method == "pne" else ops.gram(a_p, a)), ops.gemv_t(a_p, b)
+
+    try:
+        g, rhs = _agree(local_gram)
         g, rhs = _allreduce(g), _allreduce(rhs)
     finally:
         if hasattr(ops, "release"):

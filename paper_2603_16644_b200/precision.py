@@ -150,19 +150,17 @@ def _qr_level_dev(a_s_colmajor: torch.Tensor, level: PrecisionLevel, d: int, n: 
 
 
 def qr_in_precision(a, level):
-    """Householder QR in the given precision, R promoted to binary64
-    (src/precision.py:153-202).  Q is not formed (q=None): the reference's only
-    caller on the hot path (build_preconditioner) discards it."""
+    """Householder QR with all arithmetic in the given precision, factors promoted
+    to binary64 (src/precision.py:153-202): binary16 takes the power-of-two scale
+    from the f64 max and rounds a * scale once (:188-194), runs the op-for-op
+    binary16 emulation and un-scales R after promotion; binary32 raises Overflow
+    when the demotion overflows (:181-184); binary64 is householder_qr.  Q is
+    accumulated from the reflectors in the same arithmetic (accumulate_thin_q).
+    All on the device (sk_qr_in_precision_f64)."""
+    from .dense import _qr_factors_dev
     ad = as_dmat(a)
     m, n = ad.shape
     if m < n:
         raise DimensionMismatch(f"need rows >= cols, got {m} x {n}")
-    if level.name == "binary32":
-        over = C.c_int(0)
-        wp, wn = WORKSPACE.get(64)
-        call("sk_level_overflow", ad.ptr, m, n, ad.ld, 32, C.byref(over), wp, wn, stream_handle())
-        if over.value:
-            raise Overflow("input exceeds the binary32 range")
-    work = ad.t.t().contiguous().to(level.torch_dtype)   # column-major copy in the level dtype
-    r = _qr_level_dev(work, level, m, n)
-    return QRFactors(q=None, r=to_host(r))
+    r, q = _qr_factors_dev(ad.t, level.code, True)
+    return QRFactors(q=to_host(q), r=to_host(r))

@@ -185,6 +185,21 @@ def _report(method, ad: DMat, bd, x_dev, t0, x_star=None, preconditioner=None, s
                        stage_ms=stages.result() if stages is not None else {})
 
 
+def _kappa_from_gram(g: torch.Tensor, strict: bool) -> float:
+    """kappa(A_p) from the PNE Gram A_p^T A_p (singular values of its Cholesky factor;
+    the chunked path has no A_p to factor).  NaN when the Cholesky breaks down."""
+    from .dense import _chol_factor, _jacobi_sv
+    try:
+        sv = _jacobi_sv(_chol_factor(g))
+    except NoConvergence:
+        if strict:
+            raise
+        return math.nan
+    except NotPositiveDefinite:
+        return math.nan
+    return float(sv[0] / sv[-1]) if sv[-1] > 0 else float("inf")
+
+
 def _kappa(at: torch.Tensor, strict: bool) -> float:
     try:
         return _diagnostics_dev(at).two_norm_condition
@@ -383,6 +398,64 @@ class _ApScratch:
 
 _AP_SCRATCH = _ApScratch()
 
+AP_CHUNK_ROWS = None        # rows per A_p chunk when A_p is produced chunk by chunk (None: auto)
+AP_HEADROOM = 24 << 30      # device bytes kept free beside a full A_p (workspaces, sketch, LU)
+
+
+def _ap_chunk_rows(m: int, n: int, dev) -> int:
+    """0 when the full m x n A_p fits beside A (the default, one TRSM, one Gram), else
+    the row-chunk height of the streamed TRSM -> Gram (at config 4 on
+    two GPUs, A_p of 8M x 2048 rows does not fit next to A).  SK_AP_CHUNK_ROWS or
+    AP_CHUNK_ROWS forces a height (tests)."""
+    import os
+    forced = AP_CHUNK_ROWS or int(os.environ.get("SK_AP_CHUNK_ROWS", "0") or 0)
+    if forced:
+        return forced if forced < m else 0
+    need = 8 * m * n
+    key = (torch.device(dev).index, m, n)
+    if key in _AP_SCRATCH._bufs:          # already resident from an earlier solve
+        return 0
+    free, _ = torch.cuda.mem_get_info(dev)
+    if need + AP_HEADROOM <= free:
+        return 0
+    rows = 1 << 20
+    while rows > 65536 and 8 * rows * n * 2 + AP_HEADROOM > free:
+        rows //= 2
+    return rows
+
+
+def _trsm_gram_chunked(ad: DMat, r: torch.Tensor, bd: torch.Tensor, method: str, rows: int):
+    """A_p = A R^-1 produced `rows` rows at a time and consumed at once by the Gram:
+    G = sum_c A_p,c^T A_c (HPNE) or A_p,c^T A_p,c (PNE), rhs = sum_c A_p,c^T b_c.  A_p is
+    never materialised; each chunk's Gram is formed on the same engine as the whole
+    (INT8 Ozaki-II at scale, per-chunk FP64 results summed in FP64; A's column scales
+    from its one full scan) and its A_p^T b comes from the chunk's column scan."""
+    from .dense import _colstats, _gram_engine, _new_ap
+    at = ad.t
+    m, n = at.shape
+    dev = at.device
+    g = torch.empty((n, n), dtype=torch.float64, device=dev)
+    rhs = torch.zeros(n, dtype=torch.float64, device=dev)
+    buf = _new_ap(rows, n, dev)
+    ozaki = _gram_engine(rows, n, True, None) == "ozaki"
+    a_stats = ad.colstats if (method != "pne" and ozaki) else None
+    if method != "pne" and ozaki and a_stats is None:
+        a_stats = _colstats(at)
+    for i, r0 in enumerate(range(0, m, rows)):
+        r1 = min(m, r0 + rows)
+        a_c, ap_c, b_c = at[r0:r1], buf[: r1 - r0], bd[r0:r1]
+        _trsm(a_c, r, out=ap_c)
+        y = None if method == "pne" else (DMat(a_c, None, "torch", a_stats) if ozaki else a_c)
+        if ozaki and (r1 - r0) * n * n >= 1 << 33:
+            st = _colstats(ap_c, b_c)
+            _gram(DMat(ap_c, None, "torch", st[: 2 * n]), y, out=g, accumulate=i > 0)
+            rhs += st[2 * n:]
+        else:
+            _gram(ap_c, y if not isinstance(y, DMat) else y.t, out=g, accumulate=i > 0, engine="dmma")
+            _gemv_t(ap_c, b_c, out=rhs, accumulate=True)
+    del buf
+    return g, rhs
+
 
 def release_scratch():
     """Free the cached A_p buffer of algorithm1_pipeline."""
@@ -390,11 +463,13 @@ def release_scratch():
 
 
 def _prepare_dev(ad, d_factor, transform, level, seed, diagnostics=True, strict=False, stages=None,
-                 presketch=None, out=None):
+                 presketch=None, out=None, build_only=False):
     escalated_from = None
     while True:
         try:
             pre = _build_dev(ad, d_factor, transform, level, seed, diagnostics, strict, stages, presketch)
+            if build_only:   # A_p is produced chunk by chunk by the caller
+                return pre, None, escalated_from
             a_p = _precondition_dev(ad, pre, diagnostics, strict, stages, out=out)
             return pre, a_p, escalated_from
         except RankDeficient:
@@ -451,10 +526,10 @@ def _gram_and_rhs(x, y, bd):
     return g, rhs
 
 
-def _pne_dev(ad, bd, pre, a_p, stages=None):
-    if stages is not None:
+def _pne_dev(ad, bd, pre, a_p, stages=None, gram=None):
+    if stages is not None and gram is None:
         stages.mark("gram")
-    g, rhs = _gram_and_rhs(a_p, None, bd)
+    g, rhs = gram if gram is not None else _gram_and_rhs(a_p, None, bd)
     if stages is not None:
         stages.mark("nxn")
     try:
@@ -464,10 +539,10 @@ def _pne_dev(ad, bd, pre, a_p, stages=None):
     return _trsv(pre.r_device(), y)
 
 
-def _hpne_dev(ad, bd, pre, a_p, stages=None):
-    if stages is not None:
+def _hpne_dev(ad, bd, pre, a_p, stages=None, gram=None):
+    if stages is not None and gram is None:
         stages.mark("gram")
-    g, rhs = _gram_and_rhs(a_p, ad, bd)
+    g, rhs = gram if gram is not None else _gram_and_rhs(a_p, ad, bd)
     if stages is not None:
         stages.mark("nxn")
     return _lu_solve(g, rhs)
@@ -501,6 +576,11 @@ def algorithm1_pipeline(a, b, method="pne", precision="auto", d_factor=3.0, tran
     """
     stages = _Stages(stage_timing)
     stages.mark("check")
+    # wall_ms covers the estimate, sketch, factor, precondition and solve like the
+    # reference's (src/solvers.py:300-306).  For device-resident input under "auto" the
+    # validation pass is fused into the kappa0 Gram and for streamed host input into the
+    # H2D copy, so there the clock starts before them (it then also covers validation).
+    t0 = time.perf_counter()
     if method not in ("pne", "hpne"):
         raise ValueError(f"pipeline method must be pne or hpne, got {method!r}")
     if not isinstance(precision, PrecisionLevel) and precision != "auto":
@@ -548,7 +628,7 @@ def algorithm1_pipeline(a, b, method="pne", precision="auto", d_factor=3.0, tran
             ad = DMat(at, float(chk[1]), "torch", cm)
     else:
         ad, bd = _check_system(a, b)
-    t0 = time.perf_counter()
+        t0 = time.perf_counter()     # src/solvers.py:303: after _check_system, before the estimate
     decision = None
     if isinstance(precision, PrecisionLevel):
         level = precision
@@ -564,13 +644,24 @@ def algorithm1_pipeline(a, b, method="pne", precision="auto", d_factor=3.0, tran
     else:
         level = level_from_name(precision)
     m_rows, n_cols = ad.shape
-    ap_key, ap_buf = _AP_SCRATCH.take(m_rows, n_cols, ad.t.device)
-    try:
-        pre, a_p, escalated_from = _prepare_dev(ad, d_factor, transform, level, seed, diagnostics,
-                                                strict_diagnostics, stages, presketch, out=ap_buf)
-        x = (_pne_dev if method == "pne" else _hpne_dev)(ad, bd, pre, a_p, stages)
-    finally:
-        _AP_SCRATCH.give(ap_key, ap_buf)
+    chunk = _ap_chunk_rows(m_rows, n_cols, ad.t.device)
+    if chunk:
+        # A_p does not fit beside A: TRSM -> Gram per row chunk, A_p never materialised
+        pre, _, escalated_from = _prepare_dev(ad, d_factor, transform, level, seed, diagnostics,
+                                              strict_diagnostics, stages, presketch, build_only=True)
+        stages.mark("trsm_gram")
+        gr = _trsm_gram_chunked(ad, pre.r_device(), bd, method, chunk)
+        pre.kappa_ap = _kappa_from_gram(gr[0], strict_diagnostics) if (diagnostics and method == "pne") \
+            else math.nan
+        x = (_pne_dev if method == "pne" else _hpne_dev)(ad, bd, pre, None, stages, gram=gr)
+    else:
+        ap_key, ap_buf = _AP_SCRATCH.take(m_rows, n_cols, ad.t.device)
+        try:
+            pre, a_p, escalated_from = _prepare_dev(ad, d_factor, transform, level, seed, diagnostics,
+                                                    strict_diagnostics, stages, presketch, out=ap_buf)
+            x = (_pne_dev if method == "pne" else _hpne_dev)(ad, bd, pre, a_p, stages)
+        finally:
+            _AP_SCRATCH.give(ap_key, ap_buf)
     stages.mark("report")
     report = _report(method, ad, bd, x, t0, x_star, preconditioner=pre, stages=stages)
     report.precision_decision = decision

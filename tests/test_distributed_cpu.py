@@ -23,10 +23,16 @@ from oracle.problems import planted_problem
 class OracleOps:
     def validate(self, a):
         t = torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64))
+        if not torch.isfinite(t).all():
+            raise ValueError("a contains non-finite entries")      # src/dense.py:63-64
         return t, float((t * t).sum())
 
     def vector(self, b, m):
-        return torch.as_tensor(np.asarray(b, dtype=np.float64))
+        import paper_2603_16644_b200 as sq
+        t = torch.as_tensor(np.asarray(b, dtype=np.float64))
+        if t.shape[0] != m:
+            raise sq.DimensionMismatch(f"b length {t.shape[0]} != rows {m}")
+        return t
 
     def gram(self, x, y=None):
         y = x if y is None else y
@@ -147,3 +153,51 @@ def test_two_rank_gloo_matches_single_process_and_oracle():
         assert np.linalg.norm(r0[0] - single.x_hat) <= max(1e-6, 50 * ref.relative_error) * np.linalg.norm(single.x_hat)
         assert r0[4] == pytest.approx(ref.residual_norm, rel=1e-6)
         assert r0[5] == {"m": m, "d": int(math.ceil(3.0 * n)), "transform": "dct2", "seed": seed}
+
+
+def _fail_worker(rank, world, port, q):
+    """Rank-local validation failures must raise on EVERY rank (no rank may be left
+    waiting in the next all-reduce): NaN in rank 1's shard, a short b on rank 0, a bad
+    method name."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2603_16644_b200 as sq
+    from paper_2603_16644_b200.distributed import algorithm1_pipeline_sharded
+    p = planted_problem(300, 20, 1e2, 1e-8, 3)
+    lo, hi = (0, 150) if rank == 0 else (150, 300)
+    out = []
+    a = p.a[lo:hi].copy()
+    if rank == 1:
+        a[7, 3] = np.nan
+    for args, kw in (((a, p.b[lo:hi]), {}),
+                     ((p.a[lo:hi], p.b[lo:hi - 1] if rank == 0 else p.b[lo:hi]), {}),
+                     ((p.a[lo:hi], p.b[lo:hi]), {"method": "qr"})):
+        try:
+            algorithm1_pipeline_sharded(*args, ops=OracleOps(), **kw)
+            out.append(None)
+        except (ValueError, sq.SketchLsqError) as ex:
+            out.append(type(ex).__name__)
+    # the group still works afterwards: a good solve on both ranks
+    rep = algorithm1_pipeline_sharded(p.a[lo:hi], p.b[lo:hi], method="pne", seed=3, x_star=p.x_star, ops=OracleOps())
+    out.append(rep.relative_error < 1e-8)
+    q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_two_rank_local_errors_raise_on_every_rank():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fail_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    results = dict(q.get(timeout=150) for _ in procs)
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    assert results[0][0] == "ValueError" and results[1][0] == "ValueError"             # NaN on rank 1
+    assert results[0][1] == "DimensionMismatch" and results[1][1] == "DimensionMismatch"   # short b on rank 0
+    assert results[0][2] == results[1][2] == "ValueError"                                # bad method
+    assert results[0][3] and results[1][3]

@@ -1,10 +1,13 @@
 """Pin the oracle restatement to the real reference's outputs (CPU only)."""
+import json
 import math
+import os
 
 import numpy as np
 import pytest
 
 from oracle import restatement as R
+from oracle.problems import planted_problem
 from tests.golden_data import ARR, META, problem, sha
 
 
@@ -132,3 +135,45 @@ def test_thresholds_and_names():
     assert R.choose_level(math.nan, True) == "binary64"
     with pytest.raises(ValueError):
         R.canonical_level("quad")
+
+
+# ---- compiled oracle pieces and the row-chunked hybrid oracle (round 2) ----
+QR16 = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "qr16_golden.json")))["cases"]
+
+
+def _qr16_input(c):
+    g = np.random.default_rng(c["seed"]).standard_normal((c["d"], c["n"]))
+    return g * (10.0 ** (-c["span"] * np.arange(c["n"], dtype=np.float64) / max(c["n"] - 1, 1)))[None, :]
+
+
+@pytest.mark.parametrize("name", [k for k in sorted(QR16) if QR16[k]["d"] <= 1536])
+def test_c_oracle_binary16_qr_bitwise_reference(name):
+    """oracle/csrc/householder16.c (the emulated binary16 Householder in C) gives the
+    reference's R bit for bit, and the same collapse column (qr16_golden.json)."""
+    import hashlib
+    from oracle import fast
+    c = QR16[name]
+    a = _qr16_input(c)
+    assert hashlib.sha256(a.tobytes()).hexdigest() == c["input_sha256"]
+    if c["outcome"] != "ok":
+        with pytest.raises(R.RankDeficient, match=c["message"]):
+            fast.qr_at_level16(a)
+        return
+    r = fast.qr_at_level16(a)
+    assert hashlib.sha256(np.ascontiguousarray(r).tobytes()).hexdigest() == c["r_sha256"]
+
+
+@pytest.mark.parametrize("m,n,kappa,method,prec,seed", [(6000, 120, 1e2, "hpne", "auto", 3),
+                                                        (6000, 120, 1e6, "pne", "half", 4),
+                                                        (5000, 100, 1e10, "hpne", "auto", 5),
+                                                        (4096, 64, 1e3, "pne", "single", 6)])
+def test_hybrid_oracle_matches_restatement(m, n, kappa, method, prec, seed):
+    """The row-chunked hybrid oracle (LAPACK TRSM, chunked Grams, C binary16 QR) takes
+    the same decisions and R_s as the op-for-op restatement; errors within 10x."""
+    from oracle import hybrid
+    p = planted_problem(m, n, kappa, 1e-6, seed)
+    ref = R.pipeline(p.a, p.b, method=method, precision=prec, seed=seed, x_star=p.x_star, diagnostics=False)
+    h = hybrid.pipeline(p.a, p.b, method=method, precision=prec, seed=seed, x_star=p.x_star, chunk=1000)
+    assert h.pre.level == ref.pre.level and h.escalated_from == ref.escalated_from
+    assert np.array_equal(h.pre.r_s, ref.pre.r_s)
+    assert h.relative_error <= 10 * ref.relative_error and ref.relative_error <= 10 * h.relative_error
