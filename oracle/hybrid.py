@@ -59,19 +59,50 @@ def kappa0(a, chunk=CHUNK):
     return R.kappa0_from_gram(g)
 
 
-def sketch(a, level, d_factor=3.0, transform="dct2", seed=0, workers=-1):
-    """build_preconditioner's demotion + apply_sketch (src/solvers.py:188-195)."""
+COLBLOCK = 128
+
+
+def checked_system(a, b, chunk=CHUNK):
+    """src/solvers.py:87-96 without the full-size copies (f64 C-order input is used
+    in place; the finiteness scan runs per row chunk)."""
+    a = np.asarray(a)
+    if a.ndim != 2:
+        raise ValueError(f"a must be 2-D, got ndim={a.ndim}")
+    if a.dtype != np.float64 or not a.flags.c_contiguous:
+        return R.checked_system(a, b)
+    for r0 in range(0, a.shape[0], chunk):
+        if not np.isfinite(a[r0:r0 + chunk]).all():
+            raise ValueError("a contains non-finite entries")
+    b = np.asarray(b, dtype=np.float64)
+    if b.ndim != 1:
+        raise ValueError(f"b must be 1-D, got ndim={b.ndim}")
+    if a.shape[0] < a.shape[1]:
+        raise R.DimensionMismatch(f"need rows >= cols, got {a.shape}")
+    if b.shape[0] != a.shape[0]:
+        raise R.DimensionMismatch(f"b length {b.shape[0]} != rows {a.shape[0]}")
+    return a, b
+
+
+def sketch(a, level, d_factor=3.0, transform="dct2", seed=0, workers=-1, colblock=COLBLOCK):
+    """build_preconditioner's demotion + apply_sketch (src/solvers.py:188-195), in
+    blocks of columns: demotion, sign flip, transform, row sampling and scaling act on
+    each column independently, so the blocked result is bitwise the whole-matrix one
+    (and a 4M-row A needs no full-size temporaries)."""
     m, n = a.shape
     d = int(math.ceil(d_factor * n))
-    data, over = R.demote(a, level)
-    if over:
-        raise R.Overflow(f"input exceeds the {level} range")
     op = R.draw_sketch(m, d, transform, seed)
-    if transform == "dct2":
-        import scipy.fft
-        with scipy.fft.set_workers(workers):
-            return R.sketch_apply(op, data), op
-    return R.sketch_apply(op, data), op
+    out = None
+    import scipy.fft
+    with scipy.fft.set_workers(workers):
+        for c0 in range(0, n, colblock):
+            data, over = R.demote(np.ascontiguousarray(a[:, c0:c0 + colblock]), level)
+            if over:
+                raise R.Overflow(f"input exceeds the {level} range")
+            blk = R.sketch_apply(op, data)
+            if out is None:
+                out = np.empty((d, n), dtype=blk.dtype)
+            out[:, c0:c0 + colblock] = blk
+    return out, op
 
 
 def level_r(a_s, level):
@@ -104,7 +135,7 @@ def pipeline(a, b, method="pne", precision="auto", d_factor=3.0, transform="dct2
              chunk=CHUNK, workers=-1, timings=None):
     """algorithm1_pipeline (src/solvers.py:282-324) at scale -> restatement.Report."""
     tm = timings if timings is not None else {}
-    a, b = R.checked_system(a, b)
+    a, b = checked_system(a, b, chunk)
     if method not in ("pne", "hpne"):
         raise ValueError(f"pipeline method must be pne or hpne, got {method!r}")
     t0 = time.perf_counter()
