@@ -58,6 +58,7 @@ def parse():
     p.add_argument("--seed", type=int, default=20261018)
     p.add_argument("--e2e-steps", type=int, default=1)
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-e2e-pageable", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-rows", type=int, default=8192, help="row-slice height (full n) for the CPU legs")
     return p.parse_args()
@@ -630,7 +631,25 @@ def run_ours(args, rank, world):
             e2e_ms = float(t.item())
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 8 * m * n + 8 * m,
                "d2h_bytes_per_step": 8 * n + 16, "steps": args.e2e_steps,
-               "rel_error": r2.relative_error}
+               "rel_error": r2.relative_error, "host_buffers": "pinned torch CPU tensors"}
+        if not args.no_e2e_pageable and world == 1:
+            # the reference's own convention: pageable numpy arrays in, numpy x_hat out
+            import numpy as np
+            a_np = np.empty((m, n), dtype=np.float64)
+            np.copyto(a_np, a_host.numpy())
+            b_np = b_host.numpy().copy()
+            del a_host
+            torch.cuda.synchronize()
+            g0 = torch.cuda.Event(enable_timing=True)
+            g1 = torch.cuda.Event(enable_timing=True)
+            g0.record()
+            r3 = solve(a_np, b_np)
+            g1.record()
+            torch.cuda.synchronize()
+            e2e["pageable_numpy"] = {"value": g0.elapsed_time(g1), "unit": "ms", "steps": 1,
+                                     "rel_error": r3.relative_error,
+                                     "note": "A and b as pageable numpy arrays (src/solvers.py convention)"}
+            del a_np, b_np
 
     if rank != 0:
         return

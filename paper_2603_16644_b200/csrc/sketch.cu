@@ -277,7 +277,7 @@ size_t sk_sketch_workspace(int level, int64_t m_local, int64_t n, int64_t d) {
 size_t sk_sketch_workspace_ex(int level, int transform, int64_t m_local, int64_t m_pad, int64_t n, int64_t d) {
     size_t w = dmma_sketch_ws(m_local, n, d);
     if (level == 16) w = std::max(w, sk::sketch_tc_workspace(m_local, n, d));
-    if (level != 16 && transform == SK_DCT2) w = std::max(w, sk::sketch_fft_workspace(m_pad, n, d));
+    if (transform == SK_DCT2) w = std::max(w, sk::sketch_fft_workspace(m_pad, n, d));
     return w;
 }
 
@@ -285,6 +285,18 @@ int sk_sketch_partial_ex(int level, int transform, const double *a, int64_t lda,
                          int64_t row_offset, int64_t m_pad, int64_t n, const double *signs, const int64_t *rows,
                          int64_t d, double *out, int64_t ldo, int accumulate, int *overflow_flag_dev, void *ws,
                          size_t ws_bytes, sk_stream_t stream, int algo);
+
+// binary16 engine under SK_SKETCH_AUTO: the FFT transform costs O(M log M) for the WHOLE
+// operator height M, the tcgen05 GEMM O(d m_local) for the rows this call holds.  The
+// FFT wins for the whole matrix; row shards / streamed chunks keep the GEMM.
+// SK_SKETCH16=tc|fft overrides.
+constexpr bool FFT16_DEFAULT = false;   // measured slower than the tcgen05 GEMM so far (profiles/)
+static bool fft16_preferred(bool fft_ok, int64_t m_local, int64_t m_pad) {
+    static const char *env = getenv("SK_SKETCH16");
+    if (env && strcmp(env, "tc") == 0) return false;
+    if (env && strcmp(env, "fft") == 0) return fft_ok;
+    return fft_ok && m_local == m_pad && FFT16_DEFAULT;
+}
 
 int sk_sketch_partial(int level, int transform, const double *a, int64_t lda, int64_t m_local,
                       int64_t row_offset, int64_t m_pad, int64_t n, const double *signs,
@@ -305,17 +317,17 @@ int sk_sketch_partial_ex(int level, int transform, const double *a, int64_t lda,
         set_error("sk_sketch_partial: bad arguments");
         return SK_ERR_ARG;
     }
-    if (level == 16 && algo != SK_SKETCH_DMMA)
+    const bool fft_ok = transform == SK_DCT2 && sk::sketch_fft_supported(m_pad);
+    if (level == 16 && (algo == SK_SKETCH_TC || (algo == SK_SKETCH_AUTO && !fft16_preferred(fft_ok, m_local, m_pad))))
         return sk::sketch_tc_run(transform, a, lda, m_local, row_offset, m_pad, n, signs, rows, d, out, ldo,
                                  accumulate, overflow_flag_dev, ws, ws_bytes, (cudaStream_t)stream);
     if (algo == SK_SKETCH_TC) {
         set_error("sk_sketch_partial: the tensor-core path exists for binary16 only");
         return SK_ERR_ARG;
     }
-    const bool fft_ok = transform == SK_DCT2 && sk::sketch_fft_supported(m_pad);
     if (algo == SK_SKETCH_FFT || (algo == SK_SKETCH_AUTO && fft_ok)) {
-        if (!fft_ok || level == 16) {
-            set_error("sk_sketch_partial: the FFT path needs binary32/64, DCT-II and m_pad %% 4096 == 0");
+        if (!fft_ok) {
+            set_error("sk_sketch_partial: the FFT path needs DCT-II and m_pad %% 2048 == 0");
             return SK_ERR_ARG;
         }
         return sk::sketch_fft_run(level, a, lda, m_local, row_offset, m_pad, n, signs, rows, d, out, ldo, accumulate,

@@ -1,4 +1,4 @@
-// FP64 fast sampled DCT-II sketch (binary64 / binary32 levels).
+// FP64 fast sampled DCT-II sketch (all three levels).
 //
 // The reference applies the sketch as a full length-M orthonormal DCT-II
 // (pocketfft, src/sketch.py:163-167) and keeps d rows.  A dense GEMM against the
@@ -10,16 +10,26 @@
 //   V_k = DFT_M(v)_k,  j = j1 + M1 j2 (j2 < M2 = 2048),  k = k2 + M2 k1:
 //   pass A  for every j1 and column pair (c, c'): the M2-point FFT over j2 of
 //           z = v_c + i v_c' (two real columns per complex FFT), times the twiddle
-//           e^{-2 pi i j1 k2 / M}  ->  Y[pair][k2][j1]             (in shared memory,
-//           mixed-radix 16 x 16 x 8 Stockham, table twiddles)
+//           e^{-2 pi i j1 k2 / M}  ->  Y[pair][k2][j1].  Radix 16 x 16 x 4 with the
+//           butterflies in registers (each thread loads its 16 points straight from A)
+//           and two bank-conflict-free shared-memory transposes; a work item is a j1
+//           pair x 2 column pairs so every Y store is a whole 32-byte sector.  (A TMA
+//           ring for the strided row gather measured slower: 8 compute warps per SM
+//           cannot hide the transform's latency chains.)
 //   pass B  for every sampled k and its mirror M-k: Z = sum_j1 e^{-2 pi i j1 k1 / M1}
-//           Y[pair][k2][j1], requests grouped by k2 so each Y row is read once
+//           Y[pair][k2][j1]: per k2 a small complex GEMM (requests x j1) (j1 x pairs),
+//           register-blocked 4 requests x 2 pairs per thread over cp.async tiles of Y
+//           and of the twiddle table; every Y element is read from HBM once
 //   final   V_c = (Z_k + conj Z_{M-k}) / 2, V_c' = (Z_k - conj Z_{M-k}) / 2i,
 //           out[k, c] = c_k Re(e^{-i pi k / 2M} V_c)    (unscaled operator F D)
 //
 // HBM traffic ~ 8Mn (A) + 2 x 8Mn (Y written and read), in column blocks so Y stays
-// a few GB.  Arithmetic is FP64 throughout; the result is rounded to the level in
-// sk_sketch_finalize (binary32: more accurate than the reference's binary32 FFT).
+// a few GB.  The demotion to the level (and its overflow flag) happens on load.
+// Arithmetic is FP64 throughout; the result is rounded to the level in
+// sk_sketch_finalize (binary16 / binary32: the reference transforms in binary32,
+// src/sketch.py:163-167, so the FP64 transform is the more accurate of the two).
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -28,9 +38,13 @@ namespace sk {
 namespace skfft {
 
 constexpr int N2 = 1024;          // M2: FFT length of pass A
-constexpr int A_THREADS = 512;    // 4 FFTs per CTA (2 j1 x 2 column pairs)
-constexpr int B_THREADS = 256;
-constexpr int B_PAIRS = 4;        // column pairs per pass-B CTA
+constexpr int A_THREADS = 256;    // 4 FFTs (2 j1 x 2 column pairs) x 64 threads
+constexpr int PS = 1090;          // shared-memory stride of one FFT (1024 points + padding, = 2 mod 8)
+constexpr int TS = 17;            // stage-1 row stride (odd): conflict-free 16-byte accesses
+constexpr int B_THREADS = 128;
+constexpr int B_PAIRS = 128;      // column pairs per pass-B CTA (4 request rows x 32 pair columns)
+constexpr int B_REQ = 16;         // requests per pass-B group (4 per thread)
+constexpr int B_KC = 16;          // j1 per shared-memory tile
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -91,53 +105,20 @@ __device__ __forceinline__ void dft_small(double2 (&v)[R], const double2 *tw) {
     }
 }
 
-// One Stockham stage (radix R, Ns = product of earlier radices) over `nfft` in-place
-// FFTs of length N2 stored back to back in x; threads stride over butterflies.
-// PER = butterflies per thread (compile-time: nfft * N2 / R == PER * blockDim.x).
-template <int R, int PER>
-__device__ __forceinline__ void stockham_stage(double2 *x, int Ns, const double2 *tw) {
-    constexpr int NB = N2 / R;
-    double2 v[PER][R];
-#pragma unroll
-    for (int c = 0; c < PER; ++c) {
-        const int b = threadIdx.x + c * blockDim.x;
-        const int f = b / NB, j = b % NB;
-        const double2 *xf = x + f * N2;
-#pragma unroll
-        for (int r = 0; r < R; ++r) v[c][r] = xf[j + r * NB];
-        const int jm = j % Ns;
-        // stage twiddle e^{-2 pi i jm r / (Ns R)} = tw[jm r N2 / (Ns R)]
-        const int step = jm * (N2 / (Ns * R));
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[c][r] = cmul(v[c][r], tw[(r * step) & (N2 - 1)]);
-        dft_small<R>(v[c], tw);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int c = 0; c < PER; ++c) {
-        const int b = threadIdx.x + c * blockDim.x;
-        const int f = b / NB, j = b % NB, jm = j % Ns;
-        double2 *xf = x + f * N2;
-        const int base = (j / Ns) * Ns * R + jm;
-#pragma unroll
-        for (int r = 0; r < R; ++r) xf[base + r * Ns] = v[c][r];
-    }
-    __syncthreads();
-}
-
 struct PassAParams {
-    const double *a;
+    const double *__restrict__ a;
     int64_t lda, m_local, row_offset, M, M1;
-    const double *signs;
-    int c0, ncols;          // column block [c0, c0 + ncols), ncols multiple of 4 (pairs padded)
+    const double *__restrict__ signs;
+    int c0, ncols;          // column block [c0, c0 + ncols), ncols a multiple of 8 (pairs padded)
     int n;
     double2 *y;             // [pair][k2][j1], pairs of this block
-    int level;              // 32: demote A to binary32 on load (overflow -> *overflow = 1); 64: as is
+    int level;              // 16 / 32: demote A to the level on load (overflow -> *overflow = 1); 64: as is
     int *overflow;
-    const double2 *tw_n2;   // e^{-2 pi i t / N2}, t < N2 (precomputed once per call)
+    const double2 *tw_n2;   // e^{-2 pi i t / N2}, t < N2
+    int vec;                // 16-byte aligned column pairs (lda and A even)
 };
 
-// e^{-2 pi i t / len}, t < len (one table per call instead of one per CTA)
+// e^{-2 pi i t / len}, t < len (one table per call)
 __global__ void twiddle_table(double2 *tw, int64_t len) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < len; t += (int64_t)gridDim.x * blockDim.x) {
         double s, c;
@@ -146,70 +127,141 @@ __global__ void twiddle_table(double2 *tw, int64_t len) {
     }
 }
 
-// grid: (M1/2, ncols/8).  A CTA owns j1 in {2 a2, 2 a2 + 1} and 8 columns (4 complex
-// pairs): every gathered row segment is a full 64-byte line, every Y store 32 bytes.
-__global__ void __launch_bounds__(A_THREADS) fft_pass_a(const PassAParams p) {
+// round_to_precision(A, level) (src/precision.py:90-103); `over` collects the overflow
+// flag in a register (no store in the load loop, so the loads can all be in flight)
+__device__ __forceinline__ double demote_level(double w, int level, bool &over) {
+    if (level == 32) {
+        const double r = (double)__double2float_rn(w);
+        over |= isinf(r) && isfinite(w);
+        return r;
+    }
+    if (level == 16) {
+        const double r = (double)__half2float(__double2half(w));
+        over |= isinf(r) && isfinite(w);
+        return r;
+    }
+    return w;
+}
+
+
+
+// Work item (j1 pair: 2 a2, 2 a2 + 1; column quad q4: pairs 2 q4, 2 q4 + 1) = 4 FFTs
+// f = 2 jj + p, 64 threads each; two CTAs per SM (one loads while the other transforms).
+//   stage 1  (t, jj, p), lane = 4 t_lo + 2 jj + p: points j2 = t + 64 r, r < 16, from A (two
+//            lanes read one 32-byte sector of a row); sign, demotion, DFT16 over r,
+//            twiddle W1024^(t a)                               -> S[f][t][a]   (row stride TS)
+//   stage 2  (f, c, a): e < 16 from S[f][c + 4e][a]; DFT16 over e, twiddle W64^(c f')
+//                                                              -> S[f][f', c][a]
+//   stage 3  (p, h, a): f' in {2 h, 2 h + 1}, both jj: DFT4 over c -> X[a + 16 f' + 256 g];
+//            output twiddle W_M^(j1 k2); one 32-byte store of the j1 pair to Y[pair][k2][j1]
+//            (whole sectors: no read-for-write of half-written Y lines)
+__global__ void __launch_bounds__(A_THREADS, 2) fft_pass_a(const PassAParams p) {
     extern __shared__ __align__(16) double2 fa_smem[];
     double2 *tw = fa_smem;                  // N2 twiddles
-    double2 *x = fa_smem + N2;              // 8 FFTs: f = jj * 4 + pp
-    double2 *otw = x + 8 * N2;              // [jj][hi 32 | lo 32]: e^{-2 pi i j1 (32 h + l) / M}
-    const int a2 = blockIdx.x;
-    const int q = blockIdx.y;               // column octet
-    for (int t = threadIdx.x; t < N2; t += blockDim.x) tw[t] = p.tw_n2[t];
-    if (threadIdx.x < 128) {
-        // output twiddles e^{-2 pi i j1 k2 / M} = hi[k2 / 32] * lo[k2 % 32] (j1 k2 < M, exact phases)
-        const int jj = threadIdx.x >> 6, h = (threadIdx.x >> 5) & 1, t = threadIdx.x & 31;
-        const int64_t j1 = 2 * (int64_t)a2 + jj;
-        const int64_t ph = j1 * (int64_t)(h ? t : 32 * t);
-        double s, c;
-        sincospi(-2.0 * (double)ph / (double)p.M, &s, &c);
-        otw[jj * 64 + (h ? 32 : 0) + t] = make_double2(c, s);
-    }
-    // ---- gather: v_{j1 + M1 j2} for the two j1 and eight columns
-    const int cbase = p.c0 + 8 * q;
-    for (int e = threadIdx.x; e < 2 * N2; e += blockDim.x) {
-        const int jj = e / N2, j2 = e % N2;
-        const int64_t j1 = 2 * (int64_t)a2 + jj;
-        const int64_t row = (j2 < N2 / 2) ? (2 * j1 + 2 * p.M1 * (int64_t)j2)
-                                          : (2 * p.M - 1 - 2 * j1 - 2 * p.M1 * (int64_t)j2);
-        const int64_t lr = row - p.row_offset;
-        double v[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        if (lr >= 0 && lr < p.m_local) {
-            const double sg = p.signs[row];
-            const double *src = p.a + lr * p.lda + cbase;
+    double2 *otw = tw + N2;                 // [jj][hi 32 | lo 32]: e^{-2 pi i j1 (32 h + l) / M}
+    double2 *S = otw + 128;                 // 4 FFTs x PS
+    const int tid = threadIdx.x;
+    for (int t = tid; t < N2; t += blockDim.x) tw[t] = p.tw_n2[t];
+    const int64_t half = p.M1 / 2;
+    const int nquads = p.ncols / 4, ngroups = (nquads + 3) / 4;
+    const int64_t items = half * (int64_t)ngroups * 4;
+    const int w = tid >> 5, l = tid & 31;
+    const int t1 = 8 * w + (l >> 2), jj1 = (l >> 1) & 1, p1 = l & 1;   // stage 1
+    const int a2s = tid & 15, c2 = (tid >> 4) & 3, f2 = tid >> 6;       // stage 2
+    const int a3 = tid & 15, h3 = (tid >> 4) & 7, p3 = tid >> 7;        // stage 3
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        // the 4 quads of a 128-byte row segment fastest, then the j1 pair: the CTAs in
+        // flight read whole 128-byte lines between them (L2 serves the other three
+        // quarters) and write long runs of adjacent j1 into each Y row
+        const int q4 = (int)((it / (4 * half)) * 4 + (it & 3));
+        const int64_t a2 = (it >> 2) % half;
+        if (q4 >= nquads) continue;          // uniform per CTA
+        __syncthreads();                     // previous item's stage 3 is done with S / otw
+        if (tid < 128) {   // e^{-2 pi i j1 k2 / M} = hi[k2 / 32] * lo[k2 % 32] (exact phases j1 k2 < M)
+            const int jj = tid >> 6, hh = (tid >> 5) & 1, tt = tid & 31;
+            const int64_t ph = (2 * a2 + jj) * (int64_t)(hh ? tt : 32 * tt);
+            double sn, cs;
+            sincospi(-2.0 * (double)ph / (double)p.M, &sn, &cs);
+            otw[jj * 64 + (hh ? 32 : 0) + tt] = make_double2(cs, sn);
+        }
+        // ---- stage 1
+        {
+            const int64_t j1 = 2 * a2 + jj1;
+            const int col = p.c0 + 4 * q4 + 2 * p1;
+            const bool vec = p.vec && col + 1 < p.n;
+            double2 v[16];
+            double sg[16];
+            // all 32 loads first (A slices and signs), then the arithmetic
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (cbase + u < p.n) {
-                    double w = src[u];
-                    if (p.level == 32) {   // round_to_precision(A, binary32) (src/precision.py:90-103)
-                        const double r = (double)__double2float_rn(w);
-                        if (isinf(r) && isfinite(w)) *p.overflow = 1;
-                        w = r;
+            for (int r = 0; r < 16; ++r) {
+                const int64_t j2 = t1 + 64 * r;
+                const int64_t row = (r < 8) ? (2 * j1 + 2 * p.M1 * j2) : (2 * p.M - 1 - 2 * j1 - 2 * p.M1 * j2);
+                const int64_t lr = row - p.row_offset;
+                v[r] = make_double2(0.0, 0.0);
+                sg[r] = 0.0;
+                if (lr >= 0 && lr < p.m_local && col < p.n) {
+                    const double *src = p.a + lr * p.lda + col;
+                    if (vec) {
+                        v[r] = __ldcs(reinterpret_cast<const double2 *>(src));
+                    } else {
+                        v[r].x = src[0];
+                        v[r].y = (col + 1 < p.n) ? src[1] : 0.0;
                     }
-                    v[u] = sg * w;
+                    sg[r] = __ldg(p.signs + row);
                 }
-        }
+            }
+            bool over = false;
 #pragma unroll
-        for (int pp = 0; pp < 4; ++pp) x[(jj * 4 + pp) * N2 + j2] = make_double2(v[2 * pp], v[2 * pp + 1]);
-    }
-    __syncthreads();
-    // 8 FFTs x 1024 points: radix-16 stages have 512 butterflies (1 per thread),
-    // the radix-4 stage 2048 (4 per thread)
-    stockham_stage<16, 1>(x, 1, tw);
-    stockham_stage<16, 1>(x, 16, tw);
-    stockham_stage<4, 4>(x, 256, tw);
-    // ---- twiddle e^{-2 pi i j1 k2 / M} and store Y[pair][k2][j1 pair]
-    const int pair0 = 4 * q;                // pair index within the block
-    for (int e = threadIdx.x; e < 4 * N2; e += blockDim.x) {
-        const int pp = e / N2, k2 = e % N2;
-        double2 out[2];
+            for (int r = 0; r < 16; ++r) {
+                v[r].x = sg[r] * demote_level(v[r].x, p.level, over);
+                v[r].y = sg[r] * demote_level(v[r].y, p.level, over);
+            }
+            if (over) *p.overflow = 1;
+            dft_small<16>(v, tw);
+            double2 *dst = S + (2 * jj1 + p1) * PS + t1 * TS;
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-            const double2 w = cmul(otw[jj * 64 + (k2 >> 5)], otw[jj * 64 + 32 + (k2 & 31)]);
-            out[jj] = cmul(x[(jj * 4 + pp) * N2 + k2], w);
+            for (int a = 0; a < 16; ++a) dst[a] = a ? cmul(v[a], tw[(t1 * a) & (N2 - 1)]) : v[a];
         }
-        double2 *dst = p.y + ((size_t)(pair0 + pp) * N2 + k2) * p.M1 + 2 * a2;
-        *reinterpret_cast<double4 *>(dst) = make_double4(out[0].x, out[0].y, out[1].x, out[1].y);
+        __syncthreads();
+        // ---- stage 2
+        {
+            double2 v[16];
+            const double2 *src = S + f2 * PS + c2 * TS + a2s;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = src[4 * e * TS];
+            __syncthreads();
+            dft_small<16>(v, tw);
+            double2 *dst = S + f2 * PS + c2 * 16 + a2s;
+#pragma unroll
+            for (int f = 0; f < 16; ++f) dst[f * 64] = (c2 && f) ? cmul(v[f], tw[(16 * c2 * f) & (N2 - 1)]) : v[f];
+        }
+        __syncthreads();
+        // ---- stage 3
+        {
+            const int pair = 2 * q4 + p3;
+            double2 *ybase = p.y + (size_t)pair * N2 * p.M1 + 2 * a2;
+#pragma unroll
+            for (int fb = 0; fb < 2; ++fb) {
+                const int f = 2 * h3 + fb;
+                double2 x[2][4];
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj) {
+                    const double2 *src = S + (2 * jj + p3) * PS + f * 64 + a3;
+                    x[jj][0] = src[0];
+                    x[jj][1] = src[16];
+                    x[jj][2] = src[32];
+                    x[jj][3] = src[48];
+                    dft4(x[jj][0], x[jj][1], x[jj][2], x[jj][3]);
+                }
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const int k2 = a3 + 16 * f + 256 * g;
+                    const double2 o0 = cmul(x[0][g], cmul(otw[k2 >> 5], otw[32 + (k2 & 31)]));
+                    const double2 o1 = cmul(x[1][g], cmul(otw[64 + (k2 >> 5)], otw[96 + (k2 & 31)]));
+                    *reinterpret_cast<double4 *>(ybase + (size_t)k2 * p.M1) = make_double4(o0.x, o0.y, o1.x, o1.y);
+                }
+            }
+        }
     }
 }
 
@@ -223,42 +275,86 @@ struct PassBParams {
     int npairs;             // pairs in this block
     double2 *zbuf;          // [s][which][pair] (pairs of this block), ldz = npairs
     int d;
-    const double2 *tw_m1;   // e^{-2 pi i t / M1}, t < M1 (precomputed once per call)
+    const double2 *tw_m1;   // e^{-2 pi i t / M1}, t < M1
 };
 
-// grid: (N2 k2 values, ceil(npairs / B_PAIRS))
+// grid: (N2 k2 values, ceil(npairs / B_PAIRS)).  Z[req][pair] = sum_j1 T[req][j1] Y[pair][k2][j1]
+// with T[req][j1] = W_M1^(j1 k1(req)): 16 requests x 128 pairs per pass, thread (rt, pt)
+// owns requests 4 rt .. 4 rt + 3 and pairs pt + 32 j (j < 4); Y tiles [j1][pair] and the
+// twiddle tiles [j1][req] arrive by cp.async, double-buffered.
 __global__ void __launch_bounds__(B_THREADS) fft_pass_b(const PassBParams p) {
     extern __shared__ __align__(16) double2 fb_smem[];
+    auto ys = reinterpret_cast<double2 (*)[B_KC][B_PAIRS]>(fb_smem);                       // [2][B_KC][B_PAIRS]
+    auto ts = reinterpret_cast<double2 (*)[B_KC][B_REQ]>(fb_smem + 2 * B_KC * B_PAIRS);  // [2][B_KC][B_REQ]
     const int k2 = blockIdx.x;
     const int r0 = p.req_ptr[k2], r1 = p.req_ptr[k2 + 1];
     if (r0 == r1) return;
-    const int M1 = (int)p.M1;
-    double2 *tw = fb_smem;                  // e^{-2 pi i t / M1}
     const int pbase = blockIdx.y * B_PAIRS;
     const int np = min(B_PAIRS, p.npairs - pbase);
-    for (int t = threadIdx.x; t < M1; t += blockDim.x) tw[t] = p.tw_m1[t];
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int tasks = (r1 - r0) * np;
-    for (int t = warp; t < tasks; t += nw) {
-        const int rq = r0 + t / np, pp = t % np;
-        const int64_t k1 = p.req_k1[rq];
-        double2 acc = make_double2(0.0, 0.0);
-        const double2 *yrow = p.y + ((size_t)(pbase + pp) * N2 + k2) * M1;   // reused by the k2's requests (L1/L2)
-        // twiddle index (j1 k1) mod M1, advanced incrementally (no 64-bit modulo per term)
-        int idx = (int)(((int64_t)lane * k1) % M1);
-        const int step = (int)((32 * k1) % M1);
-        for (int j1 = lane; j1 < M1; j1 += 32) {
-            const double2 w = tw[idx];
-            idx += step;
-            if (idx >= M1) idx -= M1;
-            const double2 yv = yrow[j1];
-            acc.x += w.x * yv.x - w.y * yv.y;
-            acc.y += w.x * yv.y + w.y * yv.x;
+    const int tid = threadIdx.x, rt = tid >> 5, pt = tid & 31;
+    const int64_t M1 = p.M1;
+    const int nk = (int)((M1 + B_KC - 1) / B_KC);
+    for (int g0 = r0; g0 < r1; g0 += B_REQ) {
+        const int nr = min(B_REQ, r1 - g0);
+        auto stage = [&](int buf, int kc) {
+            const int64_t j0 = (int64_t)kc * B_KC;
+            for (int e = tid; e < B_KC * B_PAIRS; e += B_THREADS) {
+                const int pp = e / B_KC, jj = e % B_KC;
+                const bool live = pp < np && j0 + jj < M1;
+                const double2 *src = p.y + ((size_t)(pbase + min(pp, np - 1)) * N2 + k2) * M1 + min(j0 + jj, M1 - 1);
+                cp_async16(&ys[buf][jj][pp], src, live ? 16 : 0);
+            }
+            for (int e = tid; e < B_KC * B_REQ; e += B_THREADS) {
+                const int jj = e & (B_KC - 1), rr = e / B_KC;
+                const bool live = rr < nr && j0 + jj < M1;
+                const int64_t k1 = live ? p.req_k1[g0 + rr] : 0;
+                const int64_t ti = live ? (int64_t)((unsigned long long)(j0 + jj) * (unsigned long long)k1 % M1) : 0;
+                cp_async16(&ts[buf][jj][rr], p.tw_m1 + ti, live ? 16 : 0);
+            }
+            cp_async_commit();
+        };
+        double2 acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0.0, 0.0);
+        stage(0, 0);
+        for (int kc = 0; kc < nk; ++kc) {
+            const int buf = kc & 1;
+            if (kc + 1 < nk) {
+                stage(buf ^ 1, kc + 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+#pragma unroll 4
+            for (int jj = 0; jj < B_KC; ++jj) {
+                double2 yv[4], tv[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) yv[j] = ys[buf][jj][pt + 32 * j];   // conflict-free: lanes consecutive
+#pragma unroll
+                for (int i = 0; i < 4; ++i) tv[i] = ts[buf][jj][4 * rt + i];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        acc[i][j].x = fma(tv[i].x, yv[j].x, fma(-tv[i].y, yv[j].y, acc[i][j].x));
+                        acc[i][j].y = fma(tv[i].x, yv[j].y, fma(tv[i].y, yv[j].x, acc[i][j].y));
+                    }
+            }
+            __syncthreads();
         }
-        acc.x = warp_sum(acc.x);
-        acc.y = warp_sum(acc.y);
-        if (lane == 0) p.zbuf[((size_t)p.req_s[rq] * 2 + p.req_which[rq]) * p.npairs + pbase + pp] = acc;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int rr = 4 * rt + i;
+            if (rr >= nr) continue;
+            const int rq = g0 + rr;
+            double2 *z = p.zbuf + ((size_t)p.req_s[rq] * 2 + p.req_which[rq]) * p.npairs + pbase;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (pt + 32 * j < np) z[pt + 32 * j] = acc[i][j];
+        }
     }
 }
 
@@ -290,7 +386,14 @@ __global__ void fft_finalize(const double2 *zbuf, int npairs, const int64_t *row
     }
 }
 
-constexpr int COLBLOCK = 256;   // columns per block: Y = 8 M COLBLOCK bytes
+constexpr int COLBLOCK = 256;          // columns per block: Y = 8 M COLBLOCK bytes
+constexpr size_t Y_BUDGET = 8ull << 30;  // at most ~8 GB of Y: narrower blocks for very tall M
+
+int64_t colblock(int64_t m_pad, int64_t n) {
+    int64_t cb = std::min<int64_t>(COLBLOCK, (n + 7) / 8 * 8);
+    while (cb > 16 && (size_t)(cb / 2) * m_pad * sizeof(double2) > Y_BUDGET) cb /= 2;
+    return cb;
+}
 
 }  // namespace skfft
 
@@ -299,7 +402,7 @@ bool sketch_fft_supported(int64_t m_pad) { return m_pad >= 2 * skfft::N2 && m_pa
 size_t sketch_fft_workspace(int64_t m_pad, int64_t n, int64_t d) {
     using namespace skfft;
     if (!sketch_fft_supported(m_pad)) return 0;
-    const int64_t cb = std::min<int64_t>(COLBLOCK, (n + 7) / 8 * 8);
+    const int64_t cb = colblock(m_pad, n);
     const size_t ybytes = (size_t)(cb / 2) * m_pad * sizeof(double2);
     const size_t zbytes = (size_t)d * 2 * (cb / 2) * sizeof(double2);
     const size_t req = (size_t)(N2 + 1) * sizeof(int) + (size_t)2 * d * (2 * sizeof(int) + sizeof(int64_t));
@@ -311,10 +414,10 @@ int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int
                    int64_t n, const double *signs, const int64_t *rows, int64_t d, double *out, int64_t ldo,
                    int accumulate, int *overflow_flag_dev, void *ws, size_t ws_bytes, cudaStream_t st) {
     using namespace skfft;
-    if (!sketch_fft_supported(m_pad)) { set_error("sketch_fft: M must be a multiple of 4096"); return SK_ERR_ARG; }
+    if (!sketch_fft_supported(m_pad)) { set_error("sketch_fft: M must be a multiple of 2048"); return SK_ERR_ARG; }
     if (ws_bytes < sketch_fft_workspace(m_pad, n, d)) { set_error("sketch_fft: workspace too small"); return SK_ERR_ARG; }
     const int64_t M = m_pad, M1 = M / N2;
-    const int64_t cb = std::min<int64_t>(COLBLOCK, (n + 7) / 8 * 8);
+    const int64_t cb = colblock(M, n);
     uint8_t *p = static_cast<uint8_t *>(ws);
     double2 *y = reinterpret_cast<double2 *>(p);
     p += align_up((size_t)(cb / 2) * M * sizeof(double2), 256);
@@ -355,25 +458,52 @@ int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int
     SK_CUDA(cudaMemcpyAsync(d_s, hs.data(), (size_t)2 * d * sizeof(int), cudaMemcpyHostToDevice, st));
     SK_CUDA(cudaMemcpyAsync(d_w, hw.data(), (size_t)2 * d * sizeof(int), cudaMemcpyHostToDevice, st));
     SK_CUDA(cudaMemcpyAsync(d_k1, hk1.data(), (size_t)2 * d * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    const size_t smem_a = (size_t)(N2 + 8 * N2 + 128) * sizeof(double2);
-    const size_t smem_b = (size_t)M1 * sizeof(double2);
-    if (smem_b > 200 * 1024) { set_error("sketch_fft: M too large for pass B (M1 %lld)", (long long)M1); return SK_ERR_ARG; }
+    const int vec = ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (lda % 2 == 0);
+    const size_t smem_a = (size_t)(N2 + 128 + 4 * PS) * sizeof(double2);
+    const size_t smem_b = (size_t)2 * B_KC * (B_PAIRS + B_REQ) * sizeof(double2);
     SK_CUDA(cudaFuncSetAttribute(fft_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
     SK_CUDA(cudaFuncSetAttribute(fft_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
+    const int sms = sm_count();
+    // SK_FFT_PROFILE=1: per-pass CUDA-event times to stderr
+    static const bool prof = getenv("SK_FFT_PROFILE") != nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    float tpa = 0.f, tpb = 0.f, tfin = 0.f;
+    if (prof)
+        for (auto &e : ev) cudaEventCreate(&e);
     for (int64_t c0 = 0; c0 < n; c0 += cb) {
+        if (prof) cudaEventRecord(ev[0], st);
         const int ncols = (int)std::min<int64_t>(cb, (n - c0 + 7) / 8 * 8);
         const int npairs = ncols / 2;
-        PassAParams pa{a,     lda,          m_local, row_offset, M, M1, signs, (int)c0, ncols, (int)n, y,
-                       level, overflow_flag_dev, tw_n2};
-        fft_pass_a<<<dim3((unsigned)(M1 / 2), (unsigned)(ncols / 8)), A_THREADS, smem_a, st>>>(pa);
+        PassAParams pa{a, lda, m_local, row_offset, M, M1, signs, (int)c0, ncols, (int)n, y,
+                       level, overflow_flag_dev, tw_n2, vec};
+        const int64_t items = (M1 / 2) * ((ncols / 4 + 3) / 4) * 4;
+        fft_pass_a<<<(unsigned)std::min<int64_t>(items, 2 * sms), A_THREADS, smem_a, st>>>(pa);
         SK_LAUNCH_CHECK("fft_pass_a");
+        if (prof) cudaEventRecord(ev[1], st);
         PassBParams pb{y, M1, d_ptr, d_s, d_w, d_k1, npairs, zbuf, (int)d, tw_m1};
         fft_pass_b<<<dim3((unsigned)N2, (unsigned)((npairs + B_PAIRS - 1) / B_PAIRS)), B_THREADS, smem_b, st>>>(pb);
         SK_LAUNCH_CHECK("fft_pass_b");
+        if (prof) cudaEventRecord(ev[2], st);
         const int64_t total = d * (int64_t)npairs;
         fft_finalize<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(zbuf, npairs, rows, (int)d, M, (int)c0,
                                                                      (int)n, out, ldo, accumulate);
         SK_LAUNCH_CHECK("fft_finalize");
+        if (prof) {
+            cudaEventRecord(ev[3], st);
+            cudaEventSynchronize(ev[3]);
+            float t;
+            cudaEventElapsedTime(&t, ev[0], ev[1]);
+            tpa += t;
+            cudaEventElapsedTime(&t, ev[1], ev[2]);
+            tpb += t;
+            cudaEventElapsedTime(&t, ev[2], ev[3]);
+            tfin += t;
+        }
+    }
+    if (prof) {
+        fprintf(stderr, "sketch_fft M=%lld n=%lld cb=%lld: pass A %.2f ms, pass B %.2f ms, finalize %.2f ms\n",
+                (long long)M, (long long)n, (long long)cb, tpa, tpb, tfin);
+        for (auto &e : ev) cudaEventDestroy(e);
     }
     return SK_OK;
 }

@@ -152,6 +152,6 @@ int make_tmap_2d(CUtensorMap *map, CUtensorMapDataType dtype, const void *base, 
 // 3-D map (d0 innermost), box {box0, box1, 1}.
 int make_tmap_3d(CUtensorMap *map, CUtensorMapDataType dtype, const void *base, uint64_t d0, uint64_t d1,
                  uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0, uint32_t box1,
-                 CUtensorMapSwizzle swz);
+                 CUtensorMapSwizzle swz, CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
 
 }  // namespace sk

@@ -84,3 +84,34 @@ def test_pipeline_fft_levels_vs_oracle(env, kappa, prec):
     assert got.preconditioner.computed_in.name == ref.pre.level
     assert got.relative_error <= max(10 * ref.relative_error, 1e-14)
     assert got.preconditioner.kappa_ap <= 10
+
+
+@pytest.mark.parametrize("level", [16, 32])
+def test_fft_low_levels_match_dense(env, level):
+    """binary16 / binary32: the FFT path demotes A on load exactly like the dense
+    DMMA path (same level rounding and overflow flag), then transforms in FP64."""
+    torch, sq, S = env
+    m, n, d = 1 << 16, 48, 144
+    a = torch.from_numpy(R.philox(level, 3).standard_normal((m, n)) * 3.0).cuda()
+    op = sq.make_sketch(m, d, "dct2", seed=5)
+    fft, f1 = _sum(env, op, a, level, "fft")
+    dm, f2 = _sum(env, op, a, level, "dmma")
+    assert f1 == f2 == 0
+    fft, dm = fft.cpu().numpy(), dm.cpu().numpy()
+    assert np.abs(fft - dm).max() <= 1e-12 * np.abs(dm).max()
+    big = a.clone()
+    big[7, 3] = 1e6 if level == 16 else 1e300
+    assert _sum(env, op, big, level, "fft")[1] == 1
+
+
+def test_fft_tall_m1_beyond_pass_b_table(env):
+    """M1 = M / 1024 = 16384 (config 4's 16M rows): no shared-memory twiddle table limit."""
+    torch, sq, S = env
+    m, n, d = 1 << 24, 8, 24
+    g = torch.Generator(device="cuda").manual_seed(3)
+    a = torch.randn(m, n, dtype=torch.float64, device="cuda", generator=g)
+    op = sq.make_sketch(m, d, "dct2", seed=2)
+    fft, f1 = _sum(env, op, a, 64, "fft")
+    dm, f2 = _sum(env, op, a, 64, "dmma")
+    fft, dm = fft.cpu().numpy(), dm.cpu().numpy()
+    assert np.abs(fft - dm).max() <= 1e-11 * np.abs(dm).max()
