@@ -146,10 +146,12 @@ def _qr16_input(c):
     return g * (10.0 ** (-c["span"] * np.arange(c["n"], dtype=np.float64) / max(c["n"] - 1, 1)))[None, :]
 
 
-@pytest.mark.parametrize("name", [k for k in sorted(QR16) if QR16[k]["d"] <= 1536])
+@pytest.mark.parametrize("name", sorted(QR16))
 def test_c_oracle_binary16_qr_bitwise_reference(name):
     """oracle/csrc/householder16.c (the emulated binary16 Householder in C) gives the
-    reference's R bit for bit, and the same collapse column (qr16_golden.json)."""
+    reference's R bit for bit, and the same collapse column (qr16_golden.json), up to the
+    config-3 shape 6144 x 2048 (the reference's numpy emulation took 1202 s for it; the C
+    restatement ~45 s on 4 threads)."""
     import hashlib
     from oracle import fast
     c = QR16[name]
