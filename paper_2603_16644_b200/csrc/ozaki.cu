@@ -1010,7 +1010,15 @@ SidePipe &side_pipe() {
 // columns (and |int32 partials| < 2^27 needs h <= 8192), so h is capped at 2048; wider
 // solves recurse on the right part with more updates
 constexpr int64_t TRSM_KMAX = 2048;
-constexpr int64_t TRSM_CHUNK = 65536;
+// rows per update chunk (residue planes: 15 x chunk x (h + w) bytes); SK_TRSM_CHUNK overrides
+int64_t trsm_chunk() {
+    static const int64_t c = [] {
+        const char *e = getenv("SK_TRSM_CHUNK");
+        const int64_t v = e ? atoll(e) : 0;
+        return v >= 256 ? v / 256 * 256 : (int64_t)65536;
+    }();
+    return c;
+}
 
 int64_t trsm_split(int64_t n) { return std::min<int64_t>((n / 2 + 255) / 256 * 256, TRSM_KMAX); }
 
@@ -1024,7 +1032,7 @@ TrsmPlan trsm_plan(int64_t m, int64_t n) {
     p.hmax = trsm_split(n);            // the top level has the largest h and w
     p.wmax = n - p.hmax;
     p.ldw = (p.wmax + 15) / 16 * 16;
-    p.chunk = std::min<int64_t>((std::max<int64_t>(m, 1) + 255) / 256 * 256, TRSM_CHUNK);
+    p.chunk = std::min<int64_t>((std::max<int64_t>(m, 1) + 255) / 256 * 256, trsm_chunk());
     p.pres = (size_t)NMOD * p.chunk * p.hmax;
     p.ores = (size_t)NMOD * p.chunk * p.ldw;
     p.qres = (size_t)NMOD * p.hmax * p.ldw;

@@ -168,3 +168,31 @@ def test_sharded_device_generator_is_one_global_problem():
     e = b - a @ x
     assert np.linalg.norm(e) == pytest.approx(1e-3, rel=1e-10)
     assert np.linalg.norm(a.T @ e) <= 1e-12
+
+
+def test_measure_bound_inputs_matches_oracle_diagnostics():
+    """measure_bound_inputs (src/bounds.py:202-255) on the device against the same
+    quantities from the oracle's Jacobi diagnostics (restatement.condition_number)."""
+    p = planted_problem(600, 40, 1e4, 1e-6, 8)
+    rep = sq.algorithm1_pipeline(p.a, p.b, method="pne", precision="single", seed=2, x_star=p.x_star,
+                                 diagnostics=False)
+    pre = rep.preconditioner
+    bi = sq.measure_bound_inputs(p, rep, pre)
+    r_s = pre.r_s
+    a_p = np.linalg.solve(r_s.T, p.a.T).T
+    ka = R.condition_number(p.a)[1]
+    krs = R.condition_number(r_s)[1]
+    kap = R.condition_number(a_p)[1]
+    kapta = R.condition_number(a_p.T @ p.a)[1]
+    assert bi.kappa_a == pytest.approx(ka, rel=1e-8)
+    assert bi.kappa_rs == pytest.approx(krs, rel=1e-8)
+    assert bi.kappa_ap == pytest.approx(kap, rel=1e-8)
+    assert bi.kappa_apta == pytest.approx(kapta, rel=1e-6)
+    assert bi.u1 == 2.0 ** -23 and bi.u2 == 2.0 ** -52 and bi.eps_b is None
+    x = rep.x_hat
+    na = R.condition_number(p.a)[0]
+    assert bi.res_ratio_a == pytest.approx(np.linalg.norm(p.a @ x - p.b) / (na * np.linalg.norm(x)), rel=1e-6)
+    y = r_s @ x
+    assert bi.nu_pne == pytest.approx(np.linalg.norm(y) / (R.condition_number(r_s)[0] * np.linalg.norm(x)), rel=1e-8)
+    nap, napta = R.condition_number(a_p)[0], R.condition_number(a_p.T @ p.a)[0]
+    assert bi.nu_hpne == pytest.approx(nap * na / napta, rel=1e-6)
