@@ -5,8 +5,10 @@ Mirrors the measurement half of src/bounds.py (the reference's `BoundInputs`,
 :202-255): the condition numbers kappa(A), kappa(R_s), kappa(A_p), kappa(A_p^T A), the
 nu factors and the residual ratios, from the device condition diagnostics
 (`condition_diagnostics`: Householder / TSQR R factor + one-sided Jacobi) and the
-residual kernel.  The closed-form bound formulas themselves (bound_*, eta1) are scalar
-post-processing outside the hot path and are not restated here.
+residual kernel.  The closed-form bound formulas (`eta1`, `bound_ls`, `bound_ne_family`,
+`bound_pne`, `bound_hpne`, `bound_notnormal`, src/bounds.py:55-156) are scalar host
+arithmetic on those measurements; they are restated here for the sweep harness
+(harness.py) with the reference's argument checks and exceptions.
 
 Tall matrices: the reference reduces a tall matrix to its Householder R before the
 Jacobi sweep; here `tall_route="tsqr"` (the default) does the same through TSQR, which
@@ -24,7 +26,7 @@ import torch
 
 from .dense import ConditionDiagnostics, _gemv_t, _householder_r64, _jacobi_sv, _gram, _rm, TALL_QR_MAX_ROWS
 from .device import DMat, as_dmat, as_dvec, to_host
-from .errors import MissingField, NoConvergence, RankDeficient
+from .errors import MissingField, NoConvergence, PoleAtOne, RankDeficient
 
 _U2_DEFAULT = 2.0 ** -52
 
@@ -55,6 +57,68 @@ class BoundInputs:
         for name in names:
             if getattr(self, name) is None:
                 raise MissingField(f"bound needs {name!r} but it was not measured")
+
+
+def _need(inputs, *names):
+    inputs.need(*names)
+
+
+def eta1(kappa_rs, u1):
+    """src/bounds.py:55-66: |k u / (1 - k u)|; PoleAtOne within 1e-15 of the pole."""
+    x = kappa_rs * u1
+    if abs(x - 1.0) <= 1e-15:
+        raise PoleAtOne(f"kappa_rs * u1 = {x} is at the pole")
+    return abs(x / (1.0 - x))
+
+
+def bound_ls(inputs):
+    """src/bounds.py:69-76: kappa_a eps_a (1 + kappa_a res_ratio_a)."""
+    _need(inputs, "kappa_a", "eps_a", "res_ratio_a")
+    k = inputs.kappa_a
+    return k * inputs.eps_a * (1.0 + k * inputs.res_ratio_a)
+
+
+def bound_ne_family(inputs, kind="normal"):
+    """src/bounds.py:79-90: kappa_a^2 eps_a (res_ratio_a + 1 + eps_a)."""
+    if kind not in ("normal", "seminormal"):
+        raise ValueError(f"kind must be normal or seminormal, got {kind!r}")
+    _need(inputs, "kappa_a", "eps_a", "res_ratio_a")
+    k = inputs.kappa_a
+    return k * k * inputs.eps_a * (inputs.res_ratio_a + 1.0 + inputs.eps_a)
+
+
+def bound_pne(inputs, variant="new"):
+    """src/bounds.py:93-115 ("old": residual of the preconditioned system, "new": of
+    the original system)."""
+    if variant == "old":
+        _need(inputs, "kappa_rs", "kappa_ap", "nu_pne", "u1", "u2", "res_ratio_ap")
+        e1 = eta1(inputs.kappa_rs, inputs.u1)
+        return inputs.kappa_rs * inputs.kappa_ap * inputs.nu_pne * (
+            inputs.u2 + inputs.kappa_ap * e1 * (inputs.res_ratio_ap + inputs.u2))
+    if variant == "new":
+        _need(inputs, "kappa_rs", "kappa_ap", "kappa_a", "u2", "res_ratio_a")
+        return inputs.kappa_rs * inputs.kappa_ap * inputs.u2 * (
+            inputs.kappa_ap * inputs.kappa_rs * inputs.res_ratio_a + 1.0 + inputs.kappa_a * inputs.u2)
+    raise ValueError(f"variant must be old or new, got {variant!r}")
+
+
+def bound_hpne(inputs, variant="new"):
+    """src/bounds.py:118-140."""
+    if variant == "old":
+        _need(inputs, "kappa_apta", "nu_hpne", "kappa_rs", "u1", "u2", "res_ratio_a")
+        e1 = eta1(inputs.kappa_rs, inputs.u1)
+        return inputs.kappa_apta * inputs.nu_hpne * (e1 * inputs.res_ratio_a + (1.0 + e1) * inputs.u2)
+    if variant == "new":
+        _need(inputs, "kappa_apta", "nu_hpne", "kappa_rs", "kappa_a", "u2", "res_ratio_a")
+        return inputs.kappa_apta * inputs.nu_hpne * inputs.u2 * (
+            inputs.kappa_rs * inputs.res_ratio_a + 1.0 + inputs.kappa_a * inputs.u2)
+    raise ValueError(f"variant must be old or new, got {variant!r}")
+
+
+def bound_notnormal(inputs, kappa_bta, nu_b):
+    """src/bounds.py:143-156: kappa_bta nu_b (eps_b res_ratio_a + (1 + eps_b) eps_a)."""
+    _need(inputs, "eps_a", "eps_b", "res_ratio_a")
+    return kappa_bta * nu_b * (inputs.eps_b * inputs.res_ratio_a + (1.0 + inputs.eps_b) * inputs.eps_a)
 
 
 @dataclass

@@ -215,3 +215,7 @@ def generate_problem(m, n, kappa, rho, seed):
         b += e
     return LeastSquaresProblem(a=to_host(a), b=to_host(b), x_star=x_star, rho=float(rho), kappa=float(kappa),
                                seed=int(seed))
+
+
+# archive I/O (src/probgen.py:126-159) lives in mmio.py; re-exported under the reference's names
+from .mmio import FORMAT_VERSION, load_problem, save_problem  # noqa: E402,F401

@@ -169,3 +169,48 @@ def apply_sketch(op, a):
     _, f64 = _sketch_finalize(total, op, level, want_f64=True)
     out = to_host(f64).astype(level.dtype)   # exact: every value is representable in the level
     return out if not isinstance(a, torch.Tensor) else torch.from_numpy(out).to(a.device)
+
+
+# ------------------------------------------------ embedding theory helpers ---
+@dataclass(frozen=True)
+class EmbeddingParams:
+    """src/sketch.py:29-57: inputs to the subspace-embedding sample-size bound
+    (m >= n >= 1, coherence mu in (0, 1] and >= n/m, eps and delta in (0, 1))."""
+
+    m: int
+    n: int
+    mu: float
+    eps: float
+    delta: float
+
+    def __post_init__(self):
+        if self.n < 1 or self.m < self.n:
+            raise ValueError(f"need m >= n >= 1, got m={self.m}, n={self.n}")
+        if not 0 < self.mu <= 1:
+            raise ValueError(f"coherence must be in (0, 1], got {self.mu}")
+        if self.mu * self.m < self.n * (1 - 1e-12):
+            raise ValueError(f"coherence {self.mu} below the floor n/m = {self.n / self.m}")
+        if not 0 < self.eps < 1:
+            raise ValueError(f"distortion must be in (0, 1), got {self.eps}")
+        if not 0 < self.delta < 1:
+            raise ValueError(f"failure probability must be in (0, 1), got {self.delta}")
+
+
+def sample_size_lower_bound(params):
+    """src/sketch.py:172-179: ceil(2 m mu (1 + eps/3) ln(n/delta) / eps^2)."""
+    raw = 2.0 * params.m * params.mu * (1.0 + params.eps / 3.0) * math.log(params.n / params.delta) / params.eps ** 2
+    return int(math.ceil(raw))
+
+
+def coherence(q):
+    """src/sketch.py:182-195: largest squared row norm of an orthonormal-column q, on the
+    device (q^T q by the Gram kernel, ||q^T q - I|| by the Jacobi diagnostics);
+    NotOrthonormal beyond 1e-10."""
+    from .dense import _gram, condition_diagnostics
+    from .errors import NotOrthonormal
+    qd = as_dmat(q, "q")
+    n = qd.shape[1]
+    dev = _gram(qd) - torch.eye(n, dtype=torch.float64, device=qd.t.device)
+    if condition_diagnostics(dev).two_norm > 1e-10:
+        raise NotOrthonormal("columns are not orthonormal to 1e-10")
+    return float(torch.einsum("ij,ij->i", qd.t, qd.t).max())
