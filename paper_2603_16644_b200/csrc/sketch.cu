@@ -290,7 +290,9 @@ int sk_sketch_partial_ex(int level, int transform, const double *a, int64_t lda,
 // operator height M, the tcgen05 GEMM O(d m_local) for the rows this call holds.  The
 // FFT wins for the whole matrix; row shards / streamed chunks keep the GEMM.
 // SK_SKETCH16=tc|fft overrides.
-constexpr bool FFT16_DEFAULT = false;   // measured slower than the tcgen05 GEMM so far (profiles/)
+// Whole matrix at 4M x 2048: FFT (binary32 transform, whole-sector Y) 88 ms vs the
+// tcgen05 GEMM 100 ms (profiles/r2s2_sketch_engines.json).
+constexpr bool FFT16_DEFAULT = true;
 static bool fft16_preferred(bool fft_ok, int64_t m_local, int64_t m_pad) {
     static const char *env = getenv("SK_SKETCH16");
     if (env && strcmp(env, "tc") == 0) return false;

@@ -10,7 +10,7 @@
 //   V_k = DFT_M(v)_k,  j = j1 + M1 j2 (j2 < M2 = 2048),  k = k2 + M2 k1:
 //   pass A  for every j1 and column pair (c, c'): the M2-point FFT over j2 of
 //           z = v_c + i v_c' (two real columns per complex FFT), times the twiddle
-//           e^{-2 pi i j1 k2 / M}  ->  Y[pair][k2][j1].  Radix 16 x 16 x 4 with the
+//           e^{-2 pi i j1 k2 / M}  ->  Y[pair][k2][j1] (binary32: [quad][k2][j1][2]).  Radix 16 x 16 x 4 with the
 //           butterflies in registers (each thread loads its 16 points straight from A)
 //           and two bank-conflict-free shared-memory transposes; a work item is a j1
 //           pair x 2 column pairs so every Y store is a whole 32-byte sector.  (A TMA
@@ -39,7 +39,6 @@ namespace skfft {
 
 constexpr int N2 = 1024;          // M2: FFT length of pass A
 constexpr int A_THREADS = 256;    // 4 FFTs (2 j1 x 2 column pairs) x 64 threads
-constexpr int PS = 1090;          // shared-memory stride of one FFT (1024 points + padding, = 2 mod 8)
 constexpr int TS = 17;            // stage-1 row stride (odd): conflict-free 16-byte accesses
 constexpr int B_THREADS = 128;
 constexpr int B_PAIRS = 128;      // column pairs per pass-B CTA (4 request rows x 32 pair columns)
@@ -52,10 +51,31 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }   // a * (-i)
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }
+
+// complex type of the transform arithmetic: double2 (binary64 level) or float2 (binary16 /
+// binary32: the reference's own DCT runs in binary32 there, src/sketch.py:163-167)
+template <typename C> struct CxT;
+template <> struct CxT<double2> {
+    using R = double;
+    static constexpr int PS = 1090;   // FFT stride in complex entries: = 2 mod 8 (16-byte entries)
+    __device__ static __forceinline__ double2 make(double x, double y) { return make_double2(x, y); }
+};
+template <> struct CxT<float2> {
+    using R = float;
+    static constexpr int PS = 1092;   // = 4 mod 16 (8-byte entries: 16 lanes per wavefront)
+    __device__ static __forceinline__ float2 make(double x, double y) { return make_float2((float)x, (float)y); }
+};
 
 // forward 4-point DFT (W4 = -i)
-__device__ __forceinline__ void dft4(double2 &x0, double2 &x1, double2 &x2, double2 &x3) {
-    const double2 a = cadd(x0, x2), b = csub(x0, x2), c = cadd(x1, x3), d = mul_mi(csub(x1, x3));
+template <typename C>
+__device__ __forceinline__ void dft4(C &x0, C &x1, C &x2, C &x3) {
+    const C a = cadd(x0, x2), b = csub(x0, x2), c = cadd(x1, x3), d = mul_mi(csub(x1, x3));
     x0 = cadd(a, c);
     x2 = csub(a, c);
     x1 = cadd(b, d);
@@ -63,8 +83,8 @@ __device__ __forceinline__ void dft4(double2 &x0, double2 &x1, double2 &x2, doub
 }
 
 // forward R-point DFT in registers, R = 16 (4 x 4) or 8 (4 x 2); tw = e^{-2 pi i t / N2} table
-template <int R>
-__device__ __forceinline__ void dft_small(double2 (&v)[R], const double2 *tw) {
+template <int R, typename C>
+__device__ __forceinline__ void dft_small(C (&v)[R], const C *tw) {
     if constexpr (R == 4) {
         dft4(v[0], v[1], v[2], v[3]);
     } else if constexpr (R == 16) {
@@ -79,7 +99,7 @@ __device__ __forceinline__ void dft_small(double2 (&v)[R], const double2 *tw) {
 #pragma unroll
         for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
         // v[4 k1 + k2] = X[k1 + 4 k2] -> reorder
-        double2 t[16];
+        C t[16];
 #pragma unroll
         for (int k1 = 0; k1 < 4; ++k1)
 #pragma unroll
@@ -94,7 +114,7 @@ __device__ __forceinline__ void dft_small(double2 (&v)[R], const double2 *tw) {
         // v[2 k1 + n2] = A[n2][k1]
 #pragma unroll
         for (int k1 = 1; k1 < 4; ++k1) v[2 * k1 + 1] = cmul(v[2 * k1 + 1], tw[k1 * (N2 / 8)]);
-        double2 t[8];
+        C t[8];
 #pragma unroll
         for (int k1 = 0; k1 < 4; ++k1) {
             t[k1] = cadd(v[2 * k1], v[2 * k1 + 1]);
@@ -105,25 +125,28 @@ __device__ __forceinline__ void dft_small(double2 (&v)[R], const double2 *tw) {
     }
 }
 
+template <typename C>
 struct PassAParams {
     const double *__restrict__ a;
     int64_t lda, m_local, row_offset, M, M1;
-    const double *__restrict__ signs;
+    const uint16_t *__restrict__ sbits;   // [j1][t]: bit r = sign of point j2 = t + 64 r is -1
     int c0, ncols;          // column block [c0, c0 + ncols), ncols a multiple of 8 (pairs padded)
     int n;
-    double2 *y;             // [pair][k2][j1], pairs of this block
+    C *y;                   // [pair][k2][j1], pairs of this block
     int level;              // 16 / 32: demote A to the level on load (overflow -> *overflow = 1); 64: as is
     int *overflow;
-    const double2 *tw_n2;   // e^{-2 pi i t / N2}, t < N2
+    const C *tw_n2;         // e^{-2 pi i t / N2}, t < N2
     int vec;                // 16-byte aligned column pairs (lda and A even)
+    int prefetch;           // binary16 / binary32: next item's loads during stages 2-3
 };
 
-// e^{-2 pi i t / len}, t < len (one table per call)
-__global__ void twiddle_table(double2 *tw, int64_t len) {
+// e^{-2 pi i t / len}, t < len (one table per call; computed in FP64, rounded once)
+template <typename C>
+__global__ void twiddle_table(C *tw, int64_t len) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < len; t += (int64_t)gridDim.x * blockDim.x) {
         double s, c;
         sincospi(-2.0 * (double)t / (double)len, &s, &c);
-        tw[t] = make_double2(c, s);
+        tw[t] = CxT<C>::make(c, s);
     }
 }
 
@@ -145,6 +168,49 @@ __device__ __forceinline__ double demote_level(double w, int level, bool &over) 
 
 
 
+// Row of A (global index) holding point j2 of the pass-A FFT of j1 (Makhoul's reordering)
+__device__ __forceinline__ int64_t fft_row(int64_t j1, int64_t j2, int64_t M, int64_t M1) {
+    return (j2 < N2 / 2) ? (2 * j1 + 2 * M1 * j2) : (2 * M - 1 - 2 * j1 - 2 * M1 * j2);
+}
+
+// The sign flips of D in pass-A order, one bit per point: sbits[j1 * 64 + t] bit r is
+// set when signs[fft_row(j1, t + 64 r)] < 0.  A pass-A thread then reads its 16 signs
+// as one 2-byte word instead of 16 scattered doubles (M / 8 bytes per call).
+__global__ void pack_sign_bits(const double *__restrict__ signs, int64_t M, int64_t M1, uint16_t *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M1 * 64; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j1 = i >> 6, t = i & 63;
+        unsigned b = 0;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) b |= (__ldg(signs + fft_row(j1, t + 64 * r, M, M1)) < 0.0 ? 1u : 0u) << r;
+        out[i] = (uint16_t)b;
+    }
+}
+
+// One point of the transform input: round_to_precision to the level (overflow: a finite
+// value rounding to inf), sign flip, in the transform type.  The binary32 transform
+// rounds once, straight to the level (F2F.F32.F64 / F2F.F16.F64 + HADD2.F32): the
+// double round trip of demote_level would cost three F2F per element on the slow pipe.
+__device__ __forceinline__ bool finite_bits(double x) {
+    return (__double_as_longlong(x) & 0x7ff0000000000000ll) != 0x7ff0000000000000ll;
+}
+template <typename C>
+__device__ __forceinline__ typename CxT<C>::R level_point(double x, int level, bool neg, bool &over) {
+    if constexpr (sizeof(C) == 16) {
+        const double r = demote_level(x, level, over);
+        return neg ? -r : r;
+    } else {
+        float f;
+        if (level == 16) {
+            const __half h = __double2half(x);
+            f = __half2float(h);
+        } else {
+            f = __double2float_rn(x);
+        }
+        over |= isinf(f) && finite_bits(x);
+        return neg ? -f : f;
+    }
+}
+
 // Work item (j1 pair: 2 a2, 2 a2 + 1; column quad q4: pairs 2 q4, 2 q4 + 1) = 4 FFTs
 // f = 2 jj + p, 64 threads each; two CTAs per SM (one loads while the other transforms).
 //   stage 1  (t, jj, p), lane = 4 t_lo + 2 jj + p: points j2 = t + 64 r, r < 16, from A (two
@@ -155,13 +221,21 @@ __device__ __forceinline__ double demote_level(double w, int level, bool &over) 
 //   stage 3  (p, h, a): f' in {2 h, 2 h + 1}, both jj: DFT4 over c -> X[a + 16 f' + 256 g];
 //            output twiddle W_M^(j1 k2); one 32-byte store of the j1 pair to Y[pair][k2][j1]
 //            (whole sectors: no read-for-write of half-written Y lines)
-__global__ void __launch_bounds__(A_THREADS, 2) fft_pass_a(const PassAParams p) {
-    extern __shared__ __align__(16) double2 fa_smem[];
-    double2 *tw = fa_smem;                  // N2 twiddles
-    double2 *otw = tw + N2;                 // [jj][hi 32 | lo 32]: e^{-2 pi i j1 (32 h + l) / M}
-    double2 *S = otw + 128;                 // 4 FFTs x PS
+template <typename C>
+__global__ void __launch_bounds__(A_THREADS, 2) fft_pass_a(const PassAParams<C> p) {
+    constexpr int PS = CxT<C>::PS;
+    extern __shared__ __align__(16) unsigned char fa_raw[];
+    C *tw = reinterpret_cast<C *>(fa_raw);   // N2 twiddles
+    C *otw = tw + N2;                       // [jj][hi 32 | lo 32]: e^{-2 pi i j1 (32 h + l) / M}
+    C *tlo = otw + 128;                     // [32][8]: W1024^l, replicated per t_lo (conflict-free)
+    C *thi = tlo + 256;                     // [32][8]: W1024^(32 h)
+    C *S = thi + 256;                       // 4 FFTs x PS
     const int tid = threadIdx.x;
     for (int t = tid; t < N2; t += blockDim.x) tw[t] = p.tw_n2[t];
+    for (int t = tid; t < 256; t += blockDim.x) {
+        tlo[t] = p.tw_n2[t >> 3];
+        thi[t] = p.tw_n2[32 * (t >> 3)];
+    }
     const int64_t half = p.M1 / 2;
     const int nquads = p.ncols / 4, ngroups = (nquads + 3) / 4;
     const int64_t items = half * (int64_t)ngroups * 4;
@@ -169,84 +243,150 @@ __global__ void __launch_bounds__(A_THREADS, 2) fft_pass_a(const PassAParams p) 
     const int t1 = 8 * w + (l >> 2), jj1 = (l >> 1) & 1, p1 = l & 1;   // stage 1
     const int a2s = tid & 15, c2 = (tid >> 4) & 3, f2 = tid >> 6;       // stage 2
     const int a3 = tid & 15, h3 = (tid >> 4) & 7, p3 = tid >> 7;        // stage 3
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        // the 4 quads of a 128-byte row segment fastest, then the j1 pair: the CTAs in
-        // flight read whole 128-byte lines between them (L2 serves the other three
-        // quarters) and write long runs of adjacent j1 into each Y row
-        const int q4 = (int)((it / (4 * half)) * 4 + (it & 3));
+    // the 4 quads of a 128-byte row segment fastest, then the j1 pair: the CTAs in
+    // flight read whole 128-byte lines between them (L2 serves the other three quarters)
+    // and write long runs of adjacent j1 into each Y row.  Items whose quad is past the
+    // block (ragged column counts) are skipped (uniform per CTA).
+    auto item_q4 = [&](int64_t it) { return (int)((it / (4 * half)) * 4 + (it & 3)); };
+    auto next_item = [&](int64_t it) {
+        do { it += gridDim.x; } while (it < items && item_q4(it) >= nquads);
+        return it;
+    };
+    // stage-1 operands of an item: 16 A slices (two columns each) and the 16 sign bits
+    double2 v[16];
+    unsigned sgb = 0;
+    const bool full_rows = p.row_offset == 0 && p.m_local == p.M;
+    auto load_item = [&](int64_t it) {
+        const int q4 = item_q4(it);
         const int64_t a2 = (it >> 2) % half;
-        if (q4 >= nquads) continue;          // uniform per CTA
+        const int64_t j1 = 2 * a2 + jj1;
+        const int col = p.c0 + 4 * q4 + 2 * p1;
+        const bool vec = p.vec && col + 1 < p.n;
+        sgb = __ldg(p.sbits + j1 * 64 + t1);
+        if (full_rows && vec) {   // whole A on this GPU, aligned pair: two strided pointer walks
+            const int64_t step = 128 * p.M1 * p.lda;           // j2 -> j2 + 64
+            const double *pe = p.a + fft_row(j1, t1, p.M, p.M1) * p.lda + col;
+            const double *po = p.a + fft_row(j1, t1 + 512, p.M, p.M1) * p.lda + col;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                v[r] = __ldcs(reinterpret_cast<const double2 *>(pe + r * step));
+                v[r + 8] = __ldcs(reinterpret_cast<const double2 *>(po - r * step));
+            }
+            return;
+        }
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int64_t lr = fft_row(j1, t1 + 64 * r, p.M, p.M1) - p.row_offset;
+            v[r] = make_double2(0.0, 0.0);
+            if (lr >= 0 && lr < p.m_local && col < p.n) {
+                const double *src = p.a + lr * p.lda + col;
+                if (vec) {
+                    v[r] = __ldcs(reinterpret_cast<const double2 *>(src));
+                } else {
+                    v[r].x = src[0];
+                    v[r].y = (col + 1 < p.n) ? src[1] : 0.0;
+                }
+            }
+        }
+    };
+    int64_t it = blockIdx.x;
+    if (it < items && item_q4(it) >= nquads) it = next_item(it);
+    if constexpr (sizeof(C) == 8)
+        if (p.prefetch && it < items) load_item(it);
+    for (; it < items;) {
+        const int q4 = item_q4(it);
+        const int64_t a2 = (it >> 2) % half;
         __syncthreads();                     // previous item's stage 3 is done with S / otw
         if (tid < 128) {   // e^{-2 pi i j1 k2 / M} = hi[k2 / 32] * lo[k2 % 32] (exact phases j1 k2 < M)
             const int jj = tid >> 6, hh = (tid >> 5) & 1, tt = tid & 31;
             const int64_t ph = (2 * a2 + jj) * (int64_t)(hh ? tt : 32 * tt);
             double sn, cs;
             sincospi(-2.0 * (double)ph / (double)p.M, &sn, &cs);
-            otw[jj * 64 + (hh ? 32 : 0) + tt] = make_double2(cs, sn);
+            otw[jj * 64 + (hh ? 32 : 0) + tt] = CxT<C>::make(cs, sn);
         }
-        // ---- stage 1
+        // ---- stage 1 (binary16 / binary32: operands loaded by the previous iteration)
         {
-            const int64_t j1 = 2 * a2 + jj1;
-            const int col = p.c0 + 4 * q4 + 2 * p1;
-            const bool vec = p.vec && col + 1 < p.n;
-            double2 v[16];
-            double sg[16];
-            // all 32 loads first (A slices and signs), then the arithmetic
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                const int64_t j2 = t1 + 64 * r;
-                const int64_t row = (r < 8) ? (2 * j1 + 2 * p.M1 * j2) : (2 * p.M - 1 - 2 * j1 - 2 * p.M1 * j2);
-                const int64_t lr = row - p.row_offset;
-                v[r] = make_double2(0.0, 0.0);
-                sg[r] = 0.0;
-                if (lr >= 0 && lr < p.m_local && col < p.n) {
-                    const double *src = p.a + lr * p.lda + col;
-                    if (vec) {
-                        v[r] = __ldcs(reinterpret_cast<const double2 *>(src));
-                    } else {
-                        v[r].x = src[0];
-                        v[r].y = (col + 1 < p.n) ? src[1] : 0.0;
-                    }
-                    sg[r] = __ldg(p.signs + row);
-                }
-            }
+            if (sizeof(C) == 16 || !p.prefetch) load_item(it);
+            C u[16];
             bool over = false;
 #pragma unroll
             for (int r = 0; r < 16; ++r) {
-                v[r].x = sg[r] * demote_level(v[r].x, p.level, over);
-                v[r].y = sg[r] * demote_level(v[r].y, p.level, over);
+                const bool neg = (sgb >> r) & 1u;
+                u[r].x = level_point<C>(v[r].x, p.level, neg, over);
+                u[r].y = level_point<C>(v[r].y, p.level, neg, over);
             }
             if (over) *p.overflow = 1;
-            dft_small<16>(v, tw);
-            double2 *dst = S + (2 * jj1 + p1) * PS + t1 * TS;
+            // the next item's loads go out now and land while this item's stages 2 and 3
+            // run (binary16 / binary32: the FP32 stages leave room for the 64 registers)
+            if constexpr (sizeof(C) == 8) {
+                const int64_t nx = next_item(it);
+                if (p.prefetch && nx < items) load_item(nx);
+            }
+            dft_small<16>(u, tw);
+            C *dst = S + (2 * jj1 + p1) * PS + t1 * TS;
 #pragma unroll
-            for (int a = 0; a < 16; ++a) dst[a] = a ? cmul(v[a], tw[(t1 * a) & (N2 - 1)]) : v[a];
+            for (int a = 0; a < 16; ++a) {
+                // W1024^(t a) = W^(32 hi) W^lo from the replicated tables: the 8 distinct t
+                // of a warp hit 8 distinct bank groups (the flat table is 8-way conflicted
+                // for a = 8)
+                const int x = t1 * a, tl = t1 & 7;
+                dst[a] = a ? cmul(u[a], cmul(thi[(x >> 5) * 8 + tl], tlo[(x & 31) * 8 + tl])) : u[a];
+            }
         }
         __syncthreads();
         // ---- stage 2
         {
-            double2 v[16];
-            const double2 *src = S + f2 * PS + c2 * TS + a2s;
+            C v[16];
+            const C *src = S + f2 * PS + c2 * TS + a2s;
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = src[4 * e * TS];
             __syncthreads();
             dft_small<16>(v, tw);
-            double2 *dst = S + f2 * PS + c2 * 16 + a2s;
+            C *dst = S + f2 * PS + c2 * 16 + a2s;
 #pragma unroll
             for (int f = 0; f < 16; ++f) dst[f * 64] = (c2 && f) ? cmul(v[f], tw[(16 * c2 * f) & (N2 - 1)]) : v[f];
         }
         __syncthreads();
         // ---- stage 3
-        {
+        if constexpr (sizeof(C) == 8) {
+            // binary32 transform: Y[quad][k2][j1][pair in quad] so that each thread stores
+            // whole 32-byte sectors (2 j1 x 2 pairs of FP32 complex); thread (f, a3)
+            // transforms both pairs of the quad for one f
+            const int f = tid >> 4;
+            C *ybase = p.y + ((size_t)q4 * N2 * p.M1 + 2 * a2) * 2;
+            C x[2][2][4];
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+                for (int pp = 0; pp < 2; ++pp) {
+                    const C *src = S + (2 * jj + pp) * PS + f * 64 + a3;
+                    x[jj][pp][0] = src[0];
+                    x[jj][pp][1] = src[16];
+                    x[jj][pp][2] = src[32];
+                    x[jj][pp][3] = src[48];
+                    dft4(x[jj][pp][0], x[jj][pp][1], x[jj][pp][2], x[jj][pp][3]);
+                }
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                const int k2 = a3 + 16 * f + 256 * g;
+                const C w0 = cmul(otw[k2 >> 5], otw[32 + (k2 & 31)]);
+                const C w1 = cmul(otw[64 + (k2 >> 5)], otw[96 + (k2 & 31)]);
+                const C o00 = cmul(x[0][0][g], w0), o01 = cmul(x[0][1][g], w0);
+                const C o10 = cmul(x[1][0][g], w1), o11 = cmul(x[1][1][g], w1);
+                float4 *dst = reinterpret_cast<float4 *>(ybase + (size_t)k2 * p.M1 * 2);
+                dst[0] = make_float4(o00.x, o00.y, o01.x, o01.y);
+                dst[1] = make_float4(o10.x, o10.y, o11.x, o11.y);
+            }
+        } else {
             const int pair = 2 * q4 + p3;
-            double2 *ybase = p.y + (size_t)pair * N2 * p.M1 + 2 * a2;
+            C *ybase = p.y + (size_t)pair * N2 * p.M1 + 2 * a2;
 #pragma unroll
             for (int fb = 0; fb < 2; ++fb) {
                 const int f = 2 * h3 + fb;
-                double2 x[2][4];
+                C x[2][4];
 #pragma unroll
                 for (int jj = 0; jj < 2; ++jj) {
-                    const double2 *src = S + (2 * jj + p3) * PS + f * 64 + a3;
+                    const C *src = S + (2 * jj + p3) * PS + f * 64 + a3;
                     x[jj][0] = src[0];
                     x[jj][1] = src[16];
                     x[jj][2] = src[32];
@@ -256,17 +396,26 @@ __global__ void __launch_bounds__(A_THREADS, 2) fft_pass_a(const PassAParams p) 
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
                     const int k2 = a3 + 16 * f + 256 * g;
-                    const double2 o0 = cmul(x[0][g], cmul(otw[k2 >> 5], otw[32 + (k2 & 31)]));
-                    const double2 o1 = cmul(x[1][g], cmul(otw[64 + (k2 >> 5)], otw[96 + (k2 & 31)]));
+                    const C o0 = cmul(x[0][g], cmul(otw[k2 >> 5], otw[32 + (k2 & 31)]));
+                    const C o1 = cmul(x[1][g], cmul(otw[64 + (k2 >> 5)], otw[96 + (k2 & 31)]));
                     *reinterpret_cast<double4 *>(ybase + (size_t)k2 * p.M1) = make_double4(o0.x, o0.y, o1.x, o1.y);
                 }
             }
         }
+        it = next_item(it);
     }
 }
 
+// element (pair, k2, j1) of Y: FP64 [pair][k2][j1]; FP32 [quad][k2][j1][pair & 1]
+template <typename C>
+__device__ __forceinline__ size_t y_index(int64_t pair, int k2, int64_t j1, int64_t M1) {
+    if constexpr (sizeof(C) == 16) return ((size_t)pair * N2 + k2) * M1 + j1;
+    else return (((size_t)(pair >> 1) * N2 + k2) * M1 + j1) * 2 + (pair & 1);
+}
+
+template <typename C>
 struct PassBParams {
-    const double2 *y;
+    const C *y;
     int64_t M1;
     const int *req_ptr;     // CSR over k2: requests [req_ptr[k2], req_ptr[k2+1])
     const int *req_s;       // sample index
@@ -275,17 +424,20 @@ struct PassBParams {
     int npairs;             // pairs in this block
     double2 *zbuf;          // [s][which][pair] (pairs of this block), ldz = npairs
     int d;
-    const double2 *tw_m1;   // e^{-2 pi i t / M1}, t < M1
+    const C *tw_m1;         // e^{-2 pi i t / M1}, t < M1
 };
 
 // grid: (N2 k2 values, ceil(npairs / B_PAIRS)).  Z[req][pair] = sum_j1 T[req][j1] Y[pair][k2][j1]
 // with T[req][j1] = W_M1^(j1 k1(req)): 16 requests x 128 pairs per pass, thread (rt, pt)
 // owns requests 4 rt .. 4 rt + 3 and pairs pt + 32 j (j < 4); Y tiles [j1][pair] and the
 // twiddle tiles [j1][req] arrive by cp.async, double-buffered.
-__global__ void __launch_bounds__(B_THREADS) fft_pass_b(const PassBParams p) {
-    extern __shared__ __align__(16) double2 fb_smem[];
-    auto ys = reinterpret_cast<double2 (*)[B_KC][B_PAIRS]>(fb_smem);                       // [2][B_KC][B_PAIRS]
-    auto ts = reinterpret_cast<double2 (*)[B_KC][B_REQ]>(fb_smem + 2 * B_KC * B_PAIRS);  // [2][B_KC][B_REQ]
+template <typename C>
+__global__ void __launch_bounds__(B_THREADS) fft_pass_b(const PassBParams<C> p) {
+    using R = typename CxT<C>::R;
+    extern __shared__ __align__(16) unsigned char fb_raw[];
+    C *fb_smem = reinterpret_cast<C *>(fb_raw);
+    auto ys = reinterpret_cast<C (*)[B_KC][B_PAIRS]>(fb_smem);                       // [2][B_KC][B_PAIRS]
+    auto ts = reinterpret_cast<C (*)[B_KC][B_REQ]>(fb_smem + 2 * B_KC * B_PAIRS);  // [2][B_KC][B_REQ]
     const int k2 = blockIdx.x;
     const int r0 = p.req_ptr[k2], r1 = p.req_ptr[k2 + 1];
     if (r0 == r1) return;
@@ -301,15 +453,17 @@ __global__ void __launch_bounds__(B_THREADS) fft_pass_b(const PassBParams p) {
             for (int e = tid; e < B_KC * B_PAIRS; e += B_THREADS) {
                 const int pp = e / B_KC, jj = e % B_KC;
                 const bool live = pp < np && j0 + jj < M1;
-                const double2 *src = p.y + ((size_t)(pbase + min(pp, np - 1)) * N2 + k2) * M1 + min(j0 + jj, M1 - 1);
-                cp_async16(&ys[buf][jj][pp], src, live ? 16 : 0);
+                const C *src = p.y + y_index<C>(pbase + min(pp, np - 1), k2, min(j0 + jj, M1 - 1), M1);
+                if constexpr (sizeof(C) == 16) cp_async16(&ys[buf][jj][pp], src, live ? 16 : 0);
+                else cp_async8(&ys[buf][jj][pp], src, live ? 8 : 0);
             }
             for (int e = tid; e < B_KC * B_REQ; e += B_THREADS) {
                 const int jj = e & (B_KC - 1), rr = e / B_KC;
                 const bool live = rr < nr && j0 + jj < M1;
                 const int64_t k1 = live ? p.req_k1[g0 + rr] : 0;
                 const int64_t ti = live ? (int64_t)((unsigned long long)(j0 + jj) * (unsigned long long)k1 % M1) : 0;
-                cp_async16(&ts[buf][jj][rr], p.tw_m1 + ti, live ? 16 : 0);
+                if constexpr (sizeof(C) == 16) cp_async16(&ts[buf][jj][rr], p.tw_m1 + ti, live ? 16 : 0);
+                else cp_async8(&ts[buf][jj][rr], p.tw_m1 + ti, live ? 8 : 0);
             }
             cp_async_commit();
         };
@@ -328,9 +482,16 @@ __global__ void __launch_bounds__(B_THREADS) fft_pass_b(const PassBParams p) {
                 cp_async_wait<0>();
             }
             __syncthreads();
+            // per tile: B_KC products summed in the transform precision R, the tile sums
+            // accumulated in FP64 (binary32 transforms: ~B_KC u32 per tile, pocketfft-sized)
+            R px[4][4], py[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) px[i][j] = py[i][j] = R(0);
 #pragma unroll 4
             for (int jj = 0; jj < B_KC; ++jj) {
-                double2 yv[4], tv[4];
+                C yv[4], tv[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) yv[j] = ys[buf][jj][pt + 32 * j];   // conflict-free: lanes consecutive
 #pragma unroll
@@ -339,10 +500,17 @@ __global__ void __launch_bounds__(B_THREADS) fft_pass_b(const PassBParams p) {
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        acc[i][j].x = fma(tv[i].x, yv[j].x, fma(-tv[i].y, yv[j].y, acc[i][j].x));
-                        acc[i][j].y = fma(tv[i].x, yv[j].y, fma(tv[i].y, yv[j].x, acc[i][j].y));
+                        px[i][j] = fma(tv[i].x, yv[j].x, fma(-tv[i].y, yv[j].y, px[i][j]));
+                        py[i][j] = fma(tv[i].x, yv[j].y, fma(tv[i].y, yv[j].x, py[i][j]));
                     }
             }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    acc[i][j].x += (double)px[i][j];
+                    acc[i][j].y += (double)py[i][j];
+                }
             __syncthreads();
         }
 #pragma unroll
@@ -354,6 +522,102 @@ __global__ void __launch_bounds__(B_THREADS) fft_pass_b(const PassBParams p) {
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 if (pt + 32 * j < np) z[pt + 32 * j] = acc[i][j];
+        }
+    }
+}
+
+// Pass B on the FP64 tensor pipe (DMMA m8n8k4), both transform precisions: per k2 and
+// request group, the complex product Z (16 requests x 128 pairs) = T (16 x M1) Y^T as one
+// real GEMM  [Zr; Zi] (32 x 128) = [[Tr, -Ti]; [Ti, Tr]] (32 x 2 M1) [Yr; Yi] (2 M1 x 128),
+// accumulated in FP64 (binary32 transforms: FP32 data and twiddles, FP64 sums).  Warp w
+// owns pairs 32 w .. 32 w + 31 (four n-tiles) and all 32 rows (four m-tiles); a k-step
+// is a j1 pair x (re, im).  Fragment lane = 4 g + t: A[g][t], B[t][g], C[g][2t + i].
+constexpr int BM_YS = B_PAIRS + 8;   // Y tile row stride (elements): conflict-free component loads
+template <typename C>
+__global__ void __launch_bounds__(B_THREADS) fft_pass_b_mma(const PassBParams<C> p) {
+    extern __shared__ __align__(16) unsigned char fb_raw[];
+    C *fb_smem = reinterpret_cast<C *>(fb_raw);
+    auto ys = reinterpret_cast<C (*)[B_KC][BM_YS]>(fb_smem);                     // [2][B_KC][BM_YS]
+    auto ts = reinterpret_cast<C (*)[B_KC][B_REQ]>(fb_smem + 2 * B_KC * BM_YS);  // [2][B_KC][B_REQ]
+    const int k2 = blockIdx.x;
+    const int r0 = p.req_ptr[k2], r1 = p.req_ptr[k2 + 1];
+    if (r0 == r1) return;
+    const int pbase = blockIdx.y * B_PAIRS;
+    const int np = min(B_PAIRS, p.npairs - pbase);
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int64_t M1 = p.M1;
+    const int nk = (int)((M1 + B_KC - 1) / B_KC);
+    using R = typename CxT<C>::R;
+    for (int g0 = r0; g0 < r1; g0 += B_REQ) {
+        const int nr = min(B_REQ, r1 - g0);
+        auto stage = [&](int buf, int kc) {
+            const int64_t j0 = (int64_t)kc * B_KC;
+            for (int e = tid; e < B_KC * B_PAIRS; e += B_THREADS) {
+                const int pp = e / B_KC, jj = e % B_KC;
+                const bool live = pp < np && j0 + jj < M1;
+                const C *src = p.y + y_index<C>(pbase + min(pp, np - 1), k2, min(j0 + jj, M1 - 1), M1);
+                if constexpr (sizeof(C) == 16) cp_async16(&ys[buf][jj][pp], src, live ? 16 : 0);
+                else cp_async8(&ys[buf][jj][pp], src, live ? 8 : 0);
+            }
+            for (int e = tid; e < B_KC * B_REQ; e += B_THREADS) {
+                const int jj = e & (B_KC - 1), rr = e / B_KC;
+                const bool live = rr < nr && j0 + jj < M1;
+                const int64_t k1 = live ? p.req_k1[g0 + rr] : 0;
+                const int64_t ti = live ? (int64_t)((unsigned long long)(j0 + jj) * (unsigned long long)k1 % M1) : 0;
+                if constexpr (sizeof(C) == 16) cp_async16(&ts[buf][jj][rr], p.tw_m1 + ti, live ? 16 : 0);
+                else cp_async8(&ts[buf][jj][rr], p.tw_m1 + ti, live ? 8 : 0);
+            }
+            cp_async_commit();
+        };
+        double acc[4][4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        stage(0, 0);
+        for (int kc = 0; kc < nk; ++kc) {
+            const int buf = kc & 1;
+            if (kc + 1 < nk) {
+                stage(buf ^ 1, kc + 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+            const R *yb = reinterpret_cast<const R *>(&ys[buf][0][0]);
+#pragma unroll
+            for (int jj = 0; jj < B_KC; jj += 2) {
+                const int j1 = jj + (t >> 1);
+                const C t0 = ts[buf][j1][g], t1 = ts[buf][j1][g + 8];
+                double a[4], b[4];
+                if (t & 1) {   // imaginary K half: rows Zr get -Ti, rows Zi get Tr
+                    a[0] = -(double)t0.y; a[1] = -(double)t1.y; a[2] = (double)t0.x; a[3] = (double)t1.x;
+                } else {       // real K half: rows Zr get Tr, rows Zi get Ti
+                    a[0] = (double)t0.x; a[1] = (double)t1.x; a[2] = (double)t0.y; a[3] = (double)t1.y;
+                }
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+                    b[nt] = (double)yb[2 * (j1 * BM_YS + 32 * w + 8 * nt + g) + (t & 1)];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {            // requests g (m-tiles 0 / 2) and g + 8 (1 / 3)
+            const int rr = g + 8 * h;
+            if (rr >= nr) continue;
+            const int rq = g0 + rr;
+            double2 *z = p.zbuf + ((size_t)p.req_s[rq] * 2 + p.req_which[rq]) * p.npairs + pbase;
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int pp = 32 * w + 8 * nt + 2 * t + i;
+                    if (pp < np) z[pp] = make_double2(acc[h][nt][i], acc[h + 2][nt][i]);
+                }
         }
     }
 }
@@ -397,6 +661,95 @@ int64_t colblock(int64_t m_pad, int64_t n) {
 
 }  // namespace skfft
 
+namespace skfft {
+struct SketchFftCall {
+    const double *a;
+    int64_t lda, m_local, row_offset, M, M1, n, cb;
+    const double *signs;
+    uint16_t *sbits;
+    const int64_t *rows;
+    int64_t d;
+    double *out;
+    int64_t ldo;
+    int accumulate;
+    int *overflow;
+    void *y;
+    double2 *zbuf;
+    int *d_ptr, *d_s, *d_w;
+    int64_t *d_k1;
+    unsigned char *tables;
+    int level, vec;
+};
+
+template <typename C>
+int run_blocks(const SketchFftCall &c, cudaStream_t st) {
+    C *tw_n2 = reinterpret_cast<C *>(c.tables);
+    C *tw_m1 = tw_n2 + N2;
+    twiddle_table<C><<<4, 256, 0, st>>>(tw_n2, N2);
+    twiddle_table<C><<<(unsigned)std::min<int64_t>((c.M1 + 255) / 256, 1024), 256, 0, st>>>(tw_m1, c.M1);
+    pack_sign_bits<<<(unsigned)std::min<int64_t>((c.M1 * 64 + 255) / 256, 4096), 256, 0, st>>>(c.signs, c.M, c.M1,
+                                                                                              c.sbits);
+    SK_LAUNCH_CHECK("twiddle_table / pack_sign_bits");
+    const size_t smem_a = (size_t)(N2 + 128 + 512 + 4 * CxT<C>::PS) * sizeof(C);
+    const size_t smem_b = (size_t)2 * B_KC * (B_PAIRS + B_REQ) * sizeof(C);
+    SK_CUDA(cudaFuncSetAttribute(fft_pass_a<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
+    SK_CUDA(cudaFuncSetAttribute(fft_pass_b<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
+    const size_t smem_bm = (size_t)2 * B_KC * (BM_YS + B_REQ) * sizeof(C);
+    SK_CUDA(cudaFuncSetAttribute(fft_pass_b_mma<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bm));
+    // pass B engine: DMMA (default) or the FP32/FP64 SIMT kernel (SK_FFT_PASSB=simt)
+    const char *pf_env = getenv("SK_FFT_PF");
+    const int pf = pf_env && pf_env[0] == '1';   // measured slower at 4M x 2048 (108 vs 96 ms): off
+    const char *pb_env = getenv("SK_FFT_PASSB");
+    const bool passb_mma = !(pb_env && pb_env[0] == 's');
+    const int sms = sm_count();
+    // SK_FFT_PROFILE=1: per-pass CUDA-event times to stderr
+    static const bool prof = getenv("SK_FFT_PROFILE") != nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    float tpa = 0.f, tpb = 0.f, tfin = 0.f;
+    if (prof)
+        for (auto &e : ev) cudaEventCreate(&e);
+    C *y = static_cast<C *>(c.y);
+    for (int64_t c0 = 0; c0 < c.n; c0 += c.cb) {
+        if (prof) cudaEventRecord(ev[0], st);
+        const int ncols = (int)std::min<int64_t>(c.cb, (c.n - c0 + 7) / 8 * 8);
+        const int npairs = ncols / 2;
+        PassAParams<C> pa{c.a, c.lda, c.m_local, c.row_offset, c.M, c.M1, c.sbits, (int)c0, ncols, (int)c.n, y,
+                          c.level, c.overflow, tw_n2, c.vec, pf};
+        const int64_t items = (c.M1 / 2) * ((ncols / 4 + 3) / 4) * 4;
+        fft_pass_a<C><<<(unsigned)std::min<int64_t>(items, 2 * sms), A_THREADS, smem_a, st>>>(pa);
+        SK_LAUNCH_CHECK("fft_pass_a");
+        if (prof) cudaEventRecord(ev[1], st);
+        PassBParams<C> pb{y, c.M1, c.d_ptr, c.d_s, c.d_w, c.d_k1, npairs, c.zbuf, (int)c.d, tw_m1};
+        const dim3 gb((unsigned)N2, (unsigned)((npairs + B_PAIRS - 1) / B_PAIRS));
+        if (passb_mma) fft_pass_b_mma<C><<<gb, B_THREADS, smem_bm, st>>>(pb);
+        else fft_pass_b<C><<<gb, B_THREADS, smem_b, st>>>(pb);
+        SK_LAUNCH_CHECK("fft_pass_b");
+        if (prof) cudaEventRecord(ev[2], st);
+        const int64_t total = c.d * (int64_t)npairs;
+        fft_finalize<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(c.zbuf, npairs, c.rows, (int)c.d, c.M, (int)c0,
+                                                                     (int)c.n, c.out, c.ldo, c.accumulate);
+        SK_LAUNCH_CHECK("fft_finalize");
+        if (prof) {
+            cudaEventRecord(ev[3], st);
+            cudaEventSynchronize(ev[3]);
+            float t;
+            cudaEventElapsedTime(&t, ev[0], ev[1]);
+            tpa += t;
+            cudaEventElapsedTime(&t, ev[1], ev[2]);
+            tpb += t;
+            cudaEventElapsedTime(&t, ev[2], ev[3]);
+            tfin += t;
+        }
+    }
+    if (prof) {
+        fprintf(stderr, "sketch_fft M=%lld n=%lld cb=%lld %s: pass A %.2f ms, pass B %.2f ms, finalize %.2f ms\n",
+                (long long)c.M, (long long)c.n, (long long)c.cb, sizeof(C) == 16 ? "fp64" : "fp32", tpa, tpb, tfin);
+        for (auto &e : ev) cudaEventDestroy(e);
+    }
+    return SK_OK;
+}
+}  // namespace skfft
+
 bool sketch_fft_supported(int64_t m_pad) { return m_pad >= 2 * skfft::N2 && m_pad % (2 * skfft::N2) == 0; }
 
 size_t sketch_fft_workspace(int64_t m_pad, int64_t n, int64_t d) {
@@ -407,7 +760,9 @@ size_t sketch_fft_workspace(int64_t m_pad, int64_t n, int64_t d) {
     const size_t zbytes = (size_t)d * 2 * (cb / 2) * sizeof(double2);
     const size_t req = (size_t)(N2 + 1) * sizeof(int) + (size_t)2 * d * (2 * sizeof(int) + sizeof(int64_t));
     const size_t tables = (size_t)(N2 + m_pad / N2) * sizeof(double2);
-    return align_up(ybytes, 256) + align_up(zbytes, 256) + align_up(req, 256) + align_up(tables, 256) + 1024;
+    const size_t sbits = (size_t)(m_pad / N2) * 64 * sizeof(uint16_t);
+    return align_up(ybytes, 256) + align_up(zbytes, 256) + align_up(req, 256) + align_up(tables, 256) +
+           align_up(sbits, 256) + 1024;
 }
 
 int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int64_t row_offset, int64_t m_pad,
@@ -428,11 +783,9 @@ int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int
     int *d_w = d_s + 2 * d;
     int64_t *d_k1 = reinterpret_cast<int64_t *>(align_up(reinterpret_cast<uintptr_t>(d_w + 2 * d), 8));
     p += align_up((size_t)(N2 + 1) * sizeof(int) + (size_t)2 * d * (2 * sizeof(int) + sizeof(int64_t)), 256);
-    double2 *tw_n2 = reinterpret_cast<double2 *>(p);
-    double2 *tw_m1 = tw_n2 + N2;
-    twiddle_table<<<4, 256, 0, st>>>(tw_n2, N2);
-    twiddle_table<<<(unsigned)std::min<int64_t>((M1 + 255) / 256, 1024), 256, 0, st>>>(tw_m1, M1);
-    SK_LAUNCH_CHECK("twiddle_table");
+    unsigned char *tables = p;   // twiddle tables in the transform precision (filled below)
+    p += align_up((size_t)(N2 + M1) * sizeof(double2), 256);
+    uint16_t *sbits = reinterpret_cast<uint16_t *>(p);   // packed signs (filled below)
     // ---- request lists grouped by k2 (host; d entries)
     std::vector<int64_t> hrows((size_t)d);
     SK_CUDA(cudaMemcpyAsync(hrows.data(), rows, (size_t)d * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -459,53 +812,10 @@ int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int
     SK_CUDA(cudaMemcpyAsync(d_w, hw.data(), (size_t)2 * d * sizeof(int), cudaMemcpyHostToDevice, st));
     SK_CUDA(cudaMemcpyAsync(d_k1, hk1.data(), (size_t)2 * d * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     const int vec = ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (lda % 2 == 0);
-    const size_t smem_a = (size_t)(N2 + 128 + 4 * PS) * sizeof(double2);
-    const size_t smem_b = (size_t)2 * B_KC * (B_PAIRS + B_REQ) * sizeof(double2);
-    SK_CUDA(cudaFuncSetAttribute(fft_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a));
-    SK_CUDA(cudaFuncSetAttribute(fft_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
-    const int sms = sm_count();
-    // SK_FFT_PROFILE=1: per-pass CUDA-event times to stderr
-    static const bool prof = getenv("SK_FFT_PROFILE") != nullptr;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    float tpa = 0.f, tpb = 0.f, tfin = 0.f;
-    if (prof)
-        for (auto &e : ev) cudaEventCreate(&e);
-    for (int64_t c0 = 0; c0 < n; c0 += cb) {
-        if (prof) cudaEventRecord(ev[0], st);
-        const int ncols = (int)std::min<int64_t>(cb, (n - c0 + 7) / 8 * 8);
-        const int npairs = ncols / 2;
-        PassAParams pa{a, lda, m_local, row_offset, M, M1, signs, (int)c0, ncols, (int)n, y,
-                       level, overflow_flag_dev, tw_n2, vec};
-        const int64_t items = (M1 / 2) * ((ncols / 4 + 3) / 4) * 4;
-        fft_pass_a<<<(unsigned)std::min<int64_t>(items, 2 * sms), A_THREADS, smem_a, st>>>(pa);
-        SK_LAUNCH_CHECK("fft_pass_a");
-        if (prof) cudaEventRecord(ev[1], st);
-        PassBParams pb{y, M1, d_ptr, d_s, d_w, d_k1, npairs, zbuf, (int)d, tw_m1};
-        fft_pass_b<<<dim3((unsigned)N2, (unsigned)((npairs + B_PAIRS - 1) / B_PAIRS)), B_THREADS, smem_b, st>>>(pb);
-        SK_LAUNCH_CHECK("fft_pass_b");
-        if (prof) cudaEventRecord(ev[2], st);
-        const int64_t total = d * (int64_t)npairs;
-        fft_finalize<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(zbuf, npairs, rows, (int)d, M, (int)c0,
-                                                                     (int)n, out, ldo, accumulate);
-        SK_LAUNCH_CHECK("fft_finalize");
-        if (prof) {
-            cudaEventRecord(ev[3], st);
-            cudaEventSynchronize(ev[3]);
-            float t;
-            cudaEventElapsedTime(&t, ev[0], ev[1]);
-            tpa += t;
-            cudaEventElapsedTime(&t, ev[1], ev[2]);
-            tpb += t;
-            cudaEventElapsedTime(&t, ev[2], ev[3]);
-            tfin += t;
-        }
-    }
-    if (prof) {
-        fprintf(stderr, "sketch_fft M=%lld n=%lld cb=%lld: pass A %.2f ms, pass B %.2f ms, finalize %.2f ms\n",
-                (long long)M, (long long)n, (long long)cb, tpa, tpb, tfin);
-        for (auto &e : ev) cudaEventDestroy(e);
-    }
-    return SK_OK;
+    SketchFftCall c{a, lda, m_local, row_offset, M, M1, n, cb, signs, sbits, rows, d, out, ldo, accumulate, overflow_flag_dev,
+                    y, zbuf, d_ptr, d_s, d_w, d_k1, tables, level, vec};
+    // binary16 / binary32 levels transform in binary32 (as the reference does); binary64 in FP64
+    return level == 64 ? run_blocks<double2>(c, st) : run_blocks<float2>(c, st);
 }
 
 }  // namespace sk

@@ -24,8 +24,15 @@ def _sum(env, op, a, level, algo, row_offset=0, out=None, accumulate=False):
     return total, int(flag.item())
 
 
+@pytest.fixture(params=["mma", "simt"])
+def passb(request, monkeypatch):
+    """pass-B engine of the FFT sketch (libsklsq reads SK_FFT_PASSB per call)"""
+    monkeypatch.setenv("SK_FFT_PASSB", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("m,n,d", [(4096, 20, 60), (8192, 37, 111), (65536, 130, 390), (1 << 20, 64, 192)])
-def test_fft_matches_dense_fp64(env, m, n, d):
+def test_fft_matches_dense_fp64(env, passb, m, n, d):
     torch, sq, S = env
     a = torch.from_numpy(R.philox(m + n, 3).standard_normal((m, n))).cuda()
     op = sq.make_sketch(m, d, "dct2", seed=3)
@@ -87,9 +94,11 @@ def test_pipeline_fft_levels_vs_oracle(env, kappa, prec):
 
 
 @pytest.mark.parametrize("level", [16, 32])
-def test_fft_low_levels_match_dense(env, level):
+def test_fft_low_levels_match_dense(env, passb, level):
     """binary16 / binary32: the FFT path demotes A on load exactly like the dense
-    DMMA path (same level rounding and overflow flag), then transforms in FP64."""
+    DMMA path (same level rounding and overflow flag), then transforms in binary32 like
+    the reference (src/sketch.py:163-167: pocketfft on float32 data; pass B sums in
+    FP64), so it agrees with the FP64 dense sum to binary32 transform roundoff."""
     torch, sq, S = env
     m, n, d = 1 << 16, 48, 144
     a = torch.from_numpy(R.philox(level, 3).standard_normal((m, n)) * 3.0).cuda()
@@ -98,7 +107,7 @@ def test_fft_low_levels_match_dense(env, level):
     dm, f2 = _sum(env, op, a, level, "dmma")
     assert f1 == f2 == 0
     fft, dm = fft.cpu().numpy(), dm.cpu().numpy()
-    assert np.abs(fft - dm).max() <= 1e-12 * np.abs(dm).max()
+    assert np.abs(fft - dm).max() <= 4e-6 * np.abs(dm).max()
     big = a.clone()
     big[7, 3] = 1e6 if level == 16 else 1e300
     assert _sum(env, op, big, level, "fft")[1] == 1
