@@ -550,22 +550,47 @@ __global__ void __launch_bounds__(B_THREADS) fft_pass_b_mma(const PassBParams<C>
     using R = typename CxT<C>::R;
     for (int g0 = r0; g0 < r1; g0 += B_REQ) {
         const int nr = min(B_REQ, r1 - g0);
+        // staging with incremental addressing (no 64-bit index math or modulo per tile):
+        // thread tid stages j1 offset jj = tid & 15 of the tile for pairs (tid >> 4) + 8 i
+        // (i < 16) and for requests (tid >> 4) + 8 i (i < 2)
+        const int jj_s = tid & 15, row_s = tid >> 4;
+        size_t ystride, yoff;   // element offsets: pair step of 8 and the (pair, k2, j1 = jj_s) start
+        if constexpr (sizeof(C) == 16) {
+            ystride = (size_t)8 * N2 * M1;
+            yoff = ((size_t)(pbase + row_s) * N2 + k2) * M1 + jj_s;
+        } else {
+            ystride = (size_t)8 * N2 * M1;   // 8 pairs = 4 quads x 2 elements per j1 ... x M1 x N2
+            yoff = ((((size_t)(pbase + row_s) >> 1) * N2 + k2) * M1 + jj_s) * 2 + ((pbase + row_s) & 1);
+        }
+        constexpr int YJ = sizeof(C) == 16 ? 1 : 2;   // elements per j1 step
+        int64_t ti[2], tstep[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int rr = row_s + 8 * i;
+            const uint64_t k1 = rr < nr ? (uint64_t)p.req_k1[g0 + rr] : 0;
+            ti[i] = (int64_t)(((uint64_t)jj_s * k1) % (uint64_t)M1);
+            tstep[i] = (int64_t)(((uint64_t)B_KC * k1) % (uint64_t)M1);
+        }
         auto stage = [&](int buf, int kc) {
-            const int64_t j0 = (int64_t)kc * B_KC;
-            for (int e = tid; e < B_KC * B_PAIRS; e += B_THREADS) {
-                const int pp = e / B_KC, jj = e % B_KC;
-                const bool live = pp < np && j0 + jj < M1;
-                const C *src = p.y + y_index<C>(pbase + min(pp, np - 1), k2, min(j0 + jj, M1 - 1), M1);
-                if constexpr (sizeof(C) == 16) cp_async16(&ys[buf][jj][pp], src, live ? 16 : 0);
-                else cp_async8(&ys[buf][jj][pp], src, live ? 8 : 0);
+            const int64_t j = (int64_t)kc * B_KC + jj_s;
+            const bool jlive = j < M1;
+            const C *ysrc = p.y + yoff + (size_t)kc * B_KC * YJ;
+#pragma unroll 4
+            for (int i = 0; i < B_PAIRS / 8; ++i) {
+                const int pp = row_s + 8 * i;
+                const bool live = jlive && pp < np;
+                const C *src = live ? ysrc + i * ystride : p.y;
+                if constexpr (sizeof(C) == 16) cp_async16(&ys[buf][jj_s][pp], src, live ? 16 : 0);
+                else cp_async8(&ys[buf][jj_s][pp], src, live ? 8 : 0);
             }
-            for (int e = tid; e < B_KC * B_REQ; e += B_THREADS) {
-                const int jj = e & (B_KC - 1), rr = e / B_KC;
-                const bool live = rr < nr && j0 + jj < M1;
-                const int64_t k1 = live ? p.req_k1[g0 + rr] : 0;
-                const int64_t ti = live ? (int64_t)((unsigned long long)(j0 + jj) * (unsigned long long)k1 % M1) : 0;
-                if constexpr (sizeof(C) == 16) cp_async16(&ts[buf][jj][rr], p.tw_m1 + ti, live ? 16 : 0);
-                else cp_async8(&ts[buf][jj][rr], p.tw_m1 + ti, live ? 8 : 0);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int rr = row_s + 8 * i;
+                const bool live = jlive && rr < nr;
+                if constexpr (sizeof(C) == 16) cp_async16(&ts[buf][jj_s][rr], p.tw_m1 + (live ? ti[i] : 0), live ? 16 : 0);
+                else cp_async8(&ts[buf][jj_s][rr], p.tw_m1 + (live ? ti[i] : 0), live ? 8 : 0);
+                ti[i] += tstep[i];
+                if (ti[i] >= M1) ti[i] -= M1;
             }
             cp_async_commit();
         };
@@ -619,6 +644,313 @@ __global__ void __launch_bounds__(B_THREADS) fft_pass_b_mma(const PassBParams<C>
                     if (pp < np) z[pp] = make_double2(acc[h][nt][i], acc[h + 2][nt][i]);
                 }
         }
+    }
+}
+
+// Pass B for the binary32 transform on the TF32 tensor pipe, split three ways
+// (x = hi + lo, both TF32; products hi hi + hi lo + lo hi, the dropped lo lo is 2^-22
+// relative): the same real-embedded GEMM as fft_pass_b_mma with mma.sync m16n8k8 TF32
+// (rows 0-15 Zr and 16-31 Zi of 16 requests, a k-step = 4 j1 x (re, im)), FP32
+// accumulation within a 16-j1 tile, FP64 across tiles.  No FP32 -> FP64 conversions and
+// ~1/4 of the DMMA's tensor instructions.
+// x = hi + lo exactly: hi = x with the 13 low mantissa bits cleared (a TF32 value), lo the
+// FP32 remainder (|lo| < 2^-10 |x|); the tensor core reads lo's top 19 bits, so the
+// split keeps ~2^-23 |x| (the cvt.rna rounding would cost a compare-and-select sequence)
+__device__ __forceinline__ void split_tf32(float x, uint32_t &hi, uint32_t &lo) {
+    hi = __float_as_uint(x) & 0xffffe000u;
+    lo = __float_as_uint(x - __uint_as_float(hi));
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};\n"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(B_THREADS) fft_pass_b_tf32(const PassBParams<float2> p) {
+    using C = float2;
+    extern __shared__ __align__(16) unsigned char fbt_raw[];
+    C *fb_smem = reinterpret_cast<C *>(fbt_raw);
+    auto ys = reinterpret_cast<C (*)[B_KC][BM_YS]>(fb_smem);                     // [2][B_KC][BM_YS]
+    auto ts = reinterpret_cast<C (*)[B_KC][B_REQ]>(fb_smem + 2 * B_KC * BM_YS);  // [2][B_KC][B_REQ]
+    const int k2 = blockIdx.x;
+    const int r0 = p.req_ptr[k2], r1 = p.req_ptr[k2 + 1];
+    if (r0 == r1) return;
+    const int pbase = blockIdx.y * B_PAIRS;
+    const int np = min(B_PAIRS, p.npairs - pbase);
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int64_t M1 = p.M1;
+    const int nk = (int)((M1 + B_KC - 1) / B_KC);
+    const int jj_s = tid & 15, row_s = tid >> 4;
+    const size_t ystride = (size_t)8 * N2 * M1;
+    const size_t yoff = ((((size_t)(pbase + row_s) >> 1) * N2 + k2) * M1 + jj_s) * 2 + ((pbase + row_s) & 1);
+    for (int g0 = r0; g0 < r1; g0 += B_REQ) {
+        const int nr = min(B_REQ, r1 - g0);
+        int64_t ti[2], tstep[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int rr = row_s + 8 * i;
+            const uint64_t k1 = rr < nr ? (uint64_t)p.req_k1[g0 + rr] : 0;
+            ti[i] = (int64_t)(((uint64_t)jj_s * k1) % (uint64_t)M1);
+            tstep[i] = (int64_t)(((uint64_t)B_KC * k1) % (uint64_t)M1);
+        }
+        auto stage = [&](int buf, int kc) {
+            const int64_t j = (int64_t)kc * B_KC + jj_s;
+            const bool jlive = j < M1;
+            const C *ysrc = p.y + yoff + (size_t)kc * B_KC * 2;
+#pragma unroll 4
+            for (int i = 0; i < B_PAIRS / 8; ++i) {
+                const int pp = row_s + 8 * i;
+                const bool live = jlive && pp < np;
+                cp_async8(&ys[buf][jj_s][pp], live ? ysrc + i * ystride : p.y, live ? 8 : 0);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int rr = row_s + 8 * i;
+                const bool live = jlive && rr < nr;
+                cp_async8(&ts[buf][jj_s][rr], p.tw_m1 + (live ? ti[i] : 0), live ? 8 : 0);
+                ti[i] += tstep[i];
+                if (ti[i] >= M1) ti[i] -= M1;
+            }
+            cp_async_commit();
+        };
+        double accd[2][4][4];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) accd[i][j][e] = 0.0;
+        stage(0, 0);
+        for (int kc = 0; kc < nk; ++kc) {
+            const int buf = kc & 1;
+            if (kc + 1 < nk) {
+                stage(buf ^ 1, kc + 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+            float acc[2][4][4];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.f;
+            const float *yb = reinterpret_cast<const float *>(&ys[buf][0][0]);
+#pragma unroll
+            for (int jb = 0; jb < B_KC; jb += 4) {
+                // K' = t -> (j1 = jb + t/2, part t&1); K' = t + 4 -> (j1 = jb + 2 + t/2, part t&1)
+                const int ja = jb + (t >> 1), jc = ja + 2, part = t & 1;
+                const C ta0 = ts[buf][ja][g], ta1 = ts[buf][ja][g + 8], tc0 = ts[buf][jc][g], tc1 = ts[buf][jc][g + 8];
+                // A fragments (a0 = A[g][t], a1 = A[g+8][t], a2 = A[g][t+4], a3 = A[g+8][t+4]):
+                // Zr rows: re -> Tr, im -> -Ti;  Zi rows: re -> Ti, im -> Tr
+                const float zr[4] = {part ? -ta0.y : ta0.x, part ? -ta1.y : ta1.x, part ? -tc0.y : tc0.x,
+                                     part ? -tc1.y : tc1.x};
+                const float zi[4] = {part ? ta0.x : ta0.y, part ? ta1.x : ta1.y, part ? tc0.x : tc0.y,
+                                     part ? tc1.x : tc1.y};
+                uint32_t arh[4], arl[4], aih[4], ail[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    split_tf32(zr[e], arh[e], arl[e]);
+                    split_tf32(zi[e], aih[e], ail[e]);
+                }
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    const int pp = 32 * w + 8 * nt + g;
+                    uint32_t b0h, b0l, b1h, b1l;
+                    split_tf32(yb[2 * (ja * BM_YS + pp) + part], b0h, b0l);
+                    split_tf32(yb[2 * (jc * BM_YS + pp) + part], b1h, b1l);
+                    mma_tf32(acc[0][nt], arh, b0h, b1h);
+                    mma_tf32(acc[0][nt], arh, b0l, b1l);
+                    mma_tf32(acc[0][nt], arl, b0h, b1h);
+                    mma_tf32(acc[1][nt], aih, b0h, b1h);
+                    mma_tf32(acc[1][nt], aih, b0l, b1l);
+                    mma_tf32(acc[1][nt], ail, b0h, b1h);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) accd[i][j][e] += (double)acc[i][j][e];
+            __syncthreads();
+        }
+        // C fragment: c0 = C[g][2t], c1 = C[g][2t+1], c2 = C[g+8][2t], c3 = C[g+8][2t+1]
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int rr = g + 8 * h;
+            if (rr >= nr) continue;
+            const int rq = g0 + rr;
+            double2 *z = p.zbuf + ((size_t)p.req_s[rq] * 2 + p.req_which[rq]) * p.npairs + pbase;
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int pp = 32 * w + 8 * nt + 2 * t + i;
+                    if (pp < np) z[pp] = make_double2(accd[0][nt][2 * h + i], accd[1][nt][2 * h + i]);
+                }
+        }
+    }
+}
+
+// Pass B as a full length-M1 FFT over j1 (M1 a power of two, 16 <= M1 <= FFTB_MAX): for
+// every (k2, unit) with at least one request, the unit's Y rows (contiguous in j1) are
+// loaded into shared memory, transformed in place by Stockham radix-16 (+ one radix
+// 2/4/8) stages, and the requested k1 are read out.  O(M1 log M1) per row instead of
+// O(16 M1) for the direct sum, and Y is streamed once with 16-byte loads.  A unit is a
+// quad (two pairs, binary32 transform: Y[quad][k2][j1][2]) or one pair (binary64).
+constexpr int FFTB_THREADS = 256;
+constexpr int FFTB_MAX = 4096;
+
+// forward radix-R DFT (R = 2, 4, 8, 16) with compile-time W16 constants
+template <int R, typename C>
+__device__ __forceinline__ void dft_r(C (&v)[16]) {   // uses v[0 .. R)
+    using T = typename CxT<C>::R;
+    if constexpr (R == 2) {
+        const C a = v[0];
+        v[0] = cadd(a, v[1]);
+        v[1] = csub(a, v[1]);
+    } else if constexpr (R == 4) {
+        dft4(v[0], v[1], v[2], v[3]);
+    } else if constexpr (R == 8) {
+        // n = 2 n1 + n2: DFT4 over n1, twiddle W8^(n2 k1), DFT2 over n2
+        dft4(v[0], v[2], v[4], v[6]);
+        dft4(v[1], v[3], v[5], v[7]);
+        const T h = (T)0.70710678118654752440;
+        v[3] = cmul(v[3], CxT<C>::make(h, -h));
+        v[5] = mul_mi(v[5]);
+        v[7] = cmul(v[7], CxT<C>::make(-h, -h));
+        C t[8];
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) {
+            t[k1] = cadd(v[2 * k1], v[2 * k1 + 1]);
+            t[k1 + 4] = csub(v[2 * k1], v[2 * k1 + 1]);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = t[i];
+    } else {
+        static_assert(R == 16, "radix");
+        constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, h = 0.70710678118654752440;
+        // W16^e = (cos, -sin)(2 pi e / 16) for the e = n2 k1 in {1, 2, 3, 4, 6, 9}
+#pragma unroll
+        for (int n2 = 0; n2 < 4; ++n2) dft4(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);
+        v[5] = cmul(v[5], CxT<C>::make(c1, -s1));     // n2 1, k1 1: W^1
+        v[9] = cmul(v[9], CxT<C>::make(h, -h));       // n2 1, k1 2: W^2
+        v[13] = cmul(v[13], CxT<C>::make(s1, -c1));   // n2 1, k1 3: W^3
+        v[6] = cmul(v[6], CxT<C>::make(h, -h));       // n2 2, k1 1: W^2
+        v[10] = mul_mi(v[10]);                        // n2 2, k1 2: W^4
+        v[14] = cmul(v[14], CxT<C>::make(-h, -h));    // n2 2, k1 3: W^6
+        v[7] = cmul(v[7], CxT<C>::make(s1, -c1));     // n2 3, k1 1: W^3
+        v[11] = cmul(v[11], CxT<C>::make(-h, -h));    // n2 3, k1 2: W^6
+        v[15] = cmul(v[15], CxT<C>::make(-c1, s1));   // n2 3, k1 3: W^9
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+        C t[16];
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+            for (int k2 = 0; k2 < 4; ++k2) t[k1 + 4 * k2] = v[4 * k1 + k2];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = t[i];
+    }
+}
+
+// shared-memory slot of FFT point i: one padding entry after every 16 (the radix-16
+// first stage writes 16 consecutive points per item, i.e. a 16-entry stride across lanes)
+__device__ __forceinline__ int pslot(int i) { return i + (i >> 4); }
+
+// one in-place Stockham stage of radix R = 2^lr over U rows of length N = 2^ln (row
+// stride ldS slots), sub-transform length L = 2^ll: item (u, j), j < N / R, k = j mod L;
+// x_t = S[u][j + t N / R] W_{L R}^(k t), DFT_R, S[u][(j - k) R + k + t L] = X_t.  All
+// reads of the stage precede one barrier, then the writes.
+template <int R, int U, typename C>
+__device__ __forceinline__ void stockham_stage(C *S, int ldS, int ln, int ll, const C *__restrict__ tw, int tid) {
+    constexpr int LR = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
+    constexpr int IPT_MAX = (FFTB_MAX * U / R + FFTB_THREADS - 1) / FFTB_THREADS;   // items per thread
+    const int lnr = ln - LR;                       // log2(N / R)
+    const int items = U << lnr;
+    const int twsh = ln - ll - LR;                 // log2(N / (L R))
+    C v[IPT_MAX][R];
+#pragma unroll
+    for (int q = 0; q < IPT_MAX; ++q) {
+        const int it = tid + q * FFTB_THREADS;
+        if (it < items) {
+            const int u = it >> lnr, j = it & ((1 << lnr) - 1), k = j & ((1 << ll) - 1);
+            const C *src = S + u * ldS;
+#pragma unroll
+            for (int t = 0; t < R; ++t) {
+                C x = src[pslot(j + (t << lnr))];
+                if (t && k) x = cmul(x, __ldg(tw + ((k * t) << twsh)));
+                v[q][t] = x;
+            }
+            C w[16];
+#pragma unroll
+            for (int t = 0; t < R; ++t) w[t] = v[q][t];
+            dft_r<R>(w);
+#pragma unroll
+            for (int t = 0; t < R; ++t) v[q][t] = w[t];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < IPT_MAX; ++q) {
+        const int it = tid + q * FFTB_THREADS;
+        if (it < items) {
+            const int u = it >> lnr, j = it & ((1 << lnr) - 1), k = j & ((1 << ll) - 1);
+            C *dst = S + u * ldS;
+            const int base = ((j - k) << LR) + k;
+#pragma unroll
+            for (int t = 0; t < R; ++t) dst[pslot(base + (t << ll))] = v[q][t];
+        }
+    }
+    __syncthreads();
+}
+
+template <typename C>
+__global__ void __launch_bounds__(FFTB_THREADS) fft_pass_b_fft(const PassBParams<C> p) {
+    constexpr int U = sizeof(C) == 8 ? 2 : 1;     // pairs per unit
+    extern __shared__ __align__(16) unsigned char fbf_raw[];
+    C *S = reinterpret_cast<C *>(fbf_raw);        // [U][pslot(N)]
+    const int k2 = blockIdx.x;
+    const int r0 = p.req_ptr[k2], r1 = p.req_ptr[k2 + 1];
+    if (r0 == r1) return;
+    const int N = (int)p.M1;
+    const int ln = 31 - __clz(N);
+    const int ldS = pslot(N);
+    const int unit = blockIdx.y, pair0 = unit * U;
+    if (pair0 >= p.npairs) return;
+    const int tid = threadIdx.x;
+    // load the unit's rows (coalesced 16-byte loads; binary32: deinterleave the quad)
+    if constexpr (U == 2) {
+        const float4 *src = reinterpret_cast<const float4 *>(p.y + y_index<C>(pair0, k2, 0, p.M1));
+        for (int j = tid; j < N; j += FFTB_THREADS) {
+            const float4 v = __ldcs(src + j);
+            S[pslot(j)] = CxT<C>::make(v.x, v.y);
+            S[ldS + pslot(j)] = CxT<C>::make(v.z, v.w);
+        }
+    } else {
+        const C *src = p.y + y_index<C>(pair0, k2, 0, p.M1);
+        for (int j = tid; j < N; j += FFTB_THREADS) S[pslot(j)] = __ldcs(src + j);
+    }
+    __syncthreads();
+    int ll = 0;
+    while (ll + 4 <= ln) {
+        stockham_stage<16, U>(S, ldS, ln, ll, p.tw_m1, tid);
+        ll += 4;
+    }
+    const int rest = ln - ll;
+    if (rest == 3) stockham_stage<8, U>(S, ldS, ln, ll, p.tw_m1, tid);
+    else if (rest == 2) stockham_stage<4, U>(S, ldS, ln, ll, p.tw_m1, tid);
+    else if (rest == 1) stockham_stage<2, U>(S, ldS, ln, ll, p.tw_m1, tid);
+    // requested k1 (natural order after the Stockham stages)
+    for (int e = tid; e < (r1 - r0) * U; e += FFTB_THREADS) {
+        const int rq = r0 + e / U, u = e % U;
+        const C x = S[u * ldS + pslot((int)p.req_k1[rq])];
+        p.zbuf[((size_t)p.req_s[rq] * 2 + p.req_which[rq]) * p.npairs + pair0 + u] =
+            make_double2((double)x.x, (double)x.y);
     }
 }
 
@@ -701,6 +1033,16 @@ int run_blocks(const SketchFftCall &c, cudaStream_t st) {
     const int pf = pf_env && pf_env[0] == '1';   // measured slower at 4M x 2048 (108 vs 96 ms): off
     const char *pb_env = getenv("SK_FFT_PASSB");
     const bool passb_mma = !(pb_env && pb_env[0] == 's');
+    // FFT over j1 for power-of-two M1 up to FFTB_MAX (default), else the DMMA direct sum
+    const bool m1_pow2 = c.M1 >= 16 && c.M1 <= FFTB_MAX && (c.M1 & (c.M1 - 1)) == 0;
+    const bool passb_fft = m1_pow2 && pb_env && pb_env[0] == 'f';
+    // binary32 transform: 3xTF32 tensor-core pass B unless SK_FFT_PASSB names another engine
+    const bool passb_tf32 = !pb_env || pb_env[0] == 't';
+    if (sizeof(C) == 8)
+        SK_CUDA(cudaFuncSetAttribute(fft_pass_b_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bm));
+    const size_t smem_bf = (size_t)(sizeof(C) == 8 ? 2 : 1) * (c.M1 + c.M1 / 16) * sizeof(C);
+    if (passb_fft)
+        SK_CUDA(cudaFuncSetAttribute(fft_pass_b_fft<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bf));
     const int sms = sm_count();
     // SK_FFT_PROFILE=1: per-pass CUDA-event times to stderr
     static const bool prof = getenv("SK_FFT_PROFILE") != nullptr;
@@ -721,8 +1063,22 @@ int run_blocks(const SketchFftCall &c, cudaStream_t st) {
         if (prof) cudaEventRecord(ev[1], st);
         PassBParams<C> pb{y, c.M1, c.d_ptr, c.d_s, c.d_w, c.d_k1, npairs, c.zbuf, (int)c.d, tw_m1};
         const dim3 gb((unsigned)N2, (unsigned)((npairs + B_PAIRS - 1) / B_PAIRS));
-        if (passb_mma) fft_pass_b_mma<C><<<gb, B_THREADS, smem_bm, st>>>(pb);
-        else fft_pass_b<C><<<gb, B_THREADS, smem_b, st>>>(pb);
+        bool launched = false;
+        if constexpr (sizeof(C) == 8) {
+            if (passb_tf32) {
+                fft_pass_b_tf32<<<gb, B_THREADS, smem_bm, st>>>(pb);
+                launched = true;
+            }
+        }
+        if (launched) {
+        } else if (passb_fft) {
+            constexpr int U = sizeof(C) == 8 ? 2 : 1;
+            fft_pass_b_fft<C><<<dim3((unsigned)N2, (unsigned)((npairs + U - 1) / U)), FFTB_THREADS, smem_bf, st>>>(pb);
+        } else if (passb_mma) {
+            fft_pass_b_mma<C><<<gb, B_THREADS, smem_bm, st>>>(pb);
+        } else {
+            fft_pass_b<C><<<gb, B_THREADS, smem_b, st>>>(pb);
+        }
         SK_LAUNCH_CHECK("fft_pass_b");
         if (prof) cudaEventRecord(ev[2], st);
         const int64_t total = c.d * (int64_t)npairs;

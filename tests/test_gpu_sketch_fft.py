@@ -24,9 +24,12 @@ def _sum(env, op, a, level, algo, row_offset=0, out=None, accumulate=False):
     return total, int(flag.item())
 
 
-@pytest.fixture(params=["mma", "simt"])
+@pytest.fixture(params=["tf32", "fft", "mma", "simt"])
 def passb(request, monkeypatch):
-    """pass-B engine of the FFT sketch (libsklsq reads SK_FFT_PASSB per call)"""
+    """pass-B engine of the FFT sketch (libsklsq reads SK_FFT_PASSB per call): "tf32" the
+    default (3xTF32 tensor cores for the binary32 transform, DMMA for binary64), "fft" the
+    length-M1 FFT over j1 (power-of-two M1 in [16, 4096]; the DMMA sum otherwise), "mma"
+    the DMMA direct sum, "simt" the SIMT direct sum"""
     monkeypatch.setenv("SK_FFT_PASSB", request.param)
     return request.param
 
