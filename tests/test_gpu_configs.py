@@ -2,12 +2,13 @@
 
 * config 1: generate_problem(1000, 100, 1e8, rho), HPNE, precision "single",
   d = 300 (3n), DCT-II, over the rho grid (SPEC rho_grid(1e-16, 1, 33) subsampled);
-* config 2 (scaled to 20000 x 200; the full 100000 x 1000 case runs in
-  tools/config_parity.py, the oracle needs minutes there): kappa = 1e10, rho = 1e-6,
+* config 2 (scaled to 20000 x 200 against the op-for-op restatement, and at the full
+  100000 x 1000 against the row-chunked hybrid oracle): kappa = 1e10, rho = 1e-6,
   PNE and HPNE sharing ONE fixed "single" preconditioner (binary32 is outside its
   safe band here, so both errors are large: gate on <= 10x the oracle's);
-* config 5 (scaled to 8192 x 64 so the oracle finishes in seconds; full size in
-  tools/config_parity.py): the kappa x rho grid over pne / hpne (auto), nne with
+* config 5 (scaled to 8192 x 64 so the oracle finishes in seconds; the full
+  1M x 1024 grid against the hybrid oracle in tools/config5_parity.py,
+  profiles/r2_config5_parity.jsonl): the kappa x rho grid over pne / hpne (auto), nne with
   B = A_p and B = A, and sne on a sub-grid (the oracle's Householder of A is a
   Python loop).
 
@@ -72,6 +73,34 @@ def test_config2_shared_single_preconditioner(sq):
         ref = _outcome(lambda: fr(p.a, p.b, pre_ref, x_star=p.x_star, a_p=ap_ref))
         ours = _outcome(lambda: fo(p.a, p.b, pre, x_star=p.x_star, a_p=ap, diagnostics=False))
         _gate(ours, ref, f"config2 {meth}")
+
+
+def test_config2_full_size_vs_hybrid_oracle(sq):
+    """Config 2 at its full 100000 x 1000 (d = 3000) against the row-chunked hybrid
+    oracle (oracle/hybrid.py: the reference's sketch, binary32 Householder and n x n
+    solves; LAPACK for A_p per row chunk): one fixed binary32 preconditioner shared by
+    PNE and HPNE, as SURVEY §8(d) specifies."""
+    from oracle import hybrid as H
+    p = planted_problem_lapack(100000, 1000, 1e10, 1e-6, R.mix64(20261018, 2))
+    a_s, _ = H.sketch(p.a, "binary32", 3.0, "dct2", 0)
+    r_s = H.level_r(a_s, "binary32")
+    pre = sq.build_preconditioner(p.a, 3.0, "dct2", sq.BINARY32, 0, diagnostics=False)
+    ap = sq.precondition_matrix(p.a, pre, diagnostics=False)
+    for meth in ("pne", "hpne"):
+        g, rhs = H.trsm_gram(p.a, p.b, r_s, meth)
+        if meth == "pne":
+            try:
+                y = R.spd_solve(g, rhs)
+            except R.NotPositiveDefinite:
+                y = R.lu_pivoted_solve(g, rhs)
+            x_ref = R.tri_solve(r_s, y)
+        else:
+            x_ref = R.lu_pivoted_solve(g, rhs)
+        e_ref = float(np.linalg.norm(x_ref - p.x_star) / np.linalg.norm(p.x_star))
+        fo = sq.solve_pne if meth == "pne" else sq.solve_hpne
+        ours = fo(p.a, p.b, pre, x_star=p.x_star, a_p=ap, diagnostics=False)
+        assert np.isfinite(ours.relative_error)
+        assert ours.relative_error <= max(10 * e_ref, FLOOR), (meth, ours.relative_error, e_ref)
 
 
 @pytest.mark.parametrize("kappa", [10.0, 1e3, 2e6])
