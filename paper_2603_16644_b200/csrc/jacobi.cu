@@ -8,6 +8,8 @@
 // cooperative kernel; columns live column-major in the workspace so every dot
 // and rotation is a coalesced stream.  Singular values are column norms, sorted
 // descending on the device (bitonic, one CTA).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -86,6 +88,83 @@ jacobi_kernel(double *w, int64_t rows, int n, int max_sweeps, double tol, double
     if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->sweeps_done = sweep; ctl->converged = converged ? 1 : 0; }
 }
 
+// One CTA of CT threads per pair (the columns of a pair live in registers between the
+// dot products and the rotation: one L2 read and one write per element per round),
+// rows <= CT * RPT.  Same schedule, gate, tangent and stop rule as jacobi_kernel; the
+// three dot products are summed per thread, per warp, then over the CTA's warps in a
+// fixed order.  For the n x n diagnostics (R_s, the R factor of A_p) at n = 2048 this
+// is 1024 CTAs, all resident, one grid barrier per round.
+constexpr int CT = 128, CT_WARPS = CT / 32;
+template <int RPT>
+__global__ void __launch_bounds__(CT)
+jacobi_cta_kernel(double *w, int64_t rows, int n, int max_sweeps, double tol, double gate, Ctl *ctl) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[CT_WARPS][3];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int k = n + (n & 1);
+    const int npairs = k / 2;
+    bool converged = n < 2;
+    int sweep = 0;
+    for (; sweep < max_sweeps && !converged; ++sweep) {
+        const int sb = sweep & 1;
+        for (int r = 0; r < k - 1; ++r) {
+            for (int pi = blockIdx.x; pi < npairs; pi += gridDim.x) {
+                int p = player(pi, r, k), q = player(k - 1 - pi, r, k);
+                if (p > q) { const int t = p; p = q; q = t; }
+                if (q >= n) continue;   // bye (uniform per CTA)
+                double *cp = w + (int64_t)p * rows, *cq = w + (int64_t)q * rows;
+                double x[RPT], y[RPT];
+                double app = 0, aqq = 0, apq = 0;
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    const int64_t row = tid + (int64_t)i * CT;
+                    x[i] = row < rows ? cp[row] : 0.0;
+                    y[i] = row < rows ? cq[row] : 0.0;
+                }
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    app += x[i] * x[i];
+                    aqq += y[i] * y[i];
+                    apq += x[i] * y[i];
+                }
+                app = warp_sum(app);
+                aqq = warp_sum(aqq);
+                apq = warp_sum(apq);
+                if (lane == 0) { red[warp][0] = app; red[warp][1] = aqq; red[warp][2] = apq; }
+                __syncthreads();
+                app = red[0][0]; aqq = red[0][1]; apq = red[0][2];
+#pragma unroll
+                for (int v = 1; v < CT_WARPS; ++v) { app += red[v][0]; aqq += red[v][1]; apq += red[v][2]; }
+                __syncthreads();   // red is reused by the next pair of this CTA
+                const bool rotate = fabs(apq) > gate * sqrt(app) * sqrt(aqq);
+                double t = 0.0;
+                if (rotate) {
+                    const double tau = (aqq - app) / (2.0 * apq);
+                    const double sgn = tau >= 0 ? 1.0 : -1.0;
+                    t = sgn / (fabs(tau) + hypot(1.0, tau));
+                    const double c = 1.0 / sqrt(1.0 + t * t), s = t * c;
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) {
+                        const int64_t row = tid + (int64_t)i * CT;
+                        if (row < rows) {
+                            cp[row] = c * x[i] - s * y[i];
+                            cq[row] = s * x[i] + c * y[i];
+                        }
+                    }
+                }
+                if (tid == 0 && t != 0.0)
+                    atomicMax(&ctl->maxt_bits[sb], (unsigned long long)__double_as_longlong(fabs(t)));
+            }
+            grid.sync();
+        }
+        const double mt = __longlong_as_double((long long)ctl->maxt_bits[sb]);
+        converged = mt < tol;
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->maxt_bits[sb ^ 1] = 0ull;
+        grid.sync();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->sweeps_done = sweep; ctl->converged = converged ? 1 : 0; }
+}
+
 __global__ void to_colmajor(const double *a, int64_t rows, int n, int64_t lda, double *w) {
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < rows * n;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -150,14 +229,29 @@ int sk_jacobi_sv_f64(const double *a, int64_t rows, int64_t n, int64_t lda, int 
     jac::to_colmajor<<<(unsigned)std::min<int64_t>((rows * n + 255) / 256, 8192), 256, 0, st>>>(a, rows, (int)n, lda, w);
     SK_LAUNCH_CHECK("to_colmajor");
     const double gate = sqrt((double)rows) * ldexp(1.0, -52);
-    int maxb = max_coop_blocks((const void *)jac::jacobi_kernel, jac::THREADS, 0);
-    int blocks = (int)std::min<int64_t>((n / 2 + jac::WARPS - 1) / jac::WARPS + 1, maxb);
-    if (blocks < 1) blocks = 1;
     int ni = (int)n;
     int64_t r64 = rows;
     void *args[] = {&w, &r64, &ni, &max_sweeps, &tol, (void *)&gate, &ctl};
-    SK_CUDA(cudaLaunchCooperativeKernel((const void *)jac::jacobi_kernel, dim3(blocks), dim3(jac::THREADS), args, 0, st));
-    SK_LAUNCH_CHECK("jacobi_kernel");
+    // pair-per-CTA kernel when a column fits the CTA's registers (SK_JACOBI=warp: the
+    // warp-per-pair kernel); the CTA count is capped by co-residency (cooperative launch)
+    const char *je = getenv("SK_JACOBI");
+    const bool cta = !(je && je[0] == 'w') && rows <= (int64_t)jac::CT * 16;
+    if (cta) {
+        const void *fn = rows <= jac::CT * 4 ? (const void *)jac::jacobi_cta_kernel<4>
+                                            : rows <= jac::CT * 8 ? (const void *)jac::jacobi_cta_kernel<8>
+                                                                  : (const void *)jac::jacobi_cta_kernel<16>;
+        const int maxb = max_coop_blocks(fn, jac::CT, 0);
+        const int blocks = std::max(1, (int)std::min<int64_t>((n + 1) / 2, maxb));
+        SK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(jac::CT), args, 0, st));
+        SK_LAUNCH_CHECK("jacobi_cta_kernel");
+    } else {
+        int maxb = max_coop_blocks((const void *)jac::jacobi_kernel, jac::THREADS, 0);
+        int blocks = (int)std::min<int64_t>((n / 2 + jac::WARPS - 1) / jac::WARPS + 1, maxb);
+        if (blocks < 1) blocks = 1;
+        SK_CUDA(cudaLaunchCooperativeKernel((const void *)jac::jacobi_kernel, dim3(blocks), dim3(jac::THREADS), args, 0,
+                                            st));
+        SK_LAUNCH_CHECK("jacobi_kernel");
+    }
     int npow2 = 1;
     while (npow2 < n) npow2 <<= 1;
     const size_t smem = (size_t)npow2 * sizeof(double);
