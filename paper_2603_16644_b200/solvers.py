@@ -261,11 +261,43 @@ STREAM_MIN_BYTES = 1 << 30      # host matrices at least this large are streamed
 STREAM_CHUNKS = 16
 
 
+class _PinnedRing:
+    """K page-locked staging buffers for pageable host input (numpy arrays, the
+    reference's convention): the driver would otherwise stage a pageable copy through
+    its own small bounce buffers at ~10 GB/s.  Host threads copy a row chunk into a free
+    slot (torch's multi-threaded CPU copy, GIL released) while the copy engine moves
+    the previous slot over PCIe; a slot is reused once its H2D event has completed."""
+
+    SLOTS = 4
+    PIECE_BYTES = 256 << 20
+
+    def __init__(self):
+        self._bufs: list[torch.Tensor] = []
+        self._events: list = []
+        self._lock = threading.Lock()
+
+    def slots(self, nbytes: int):
+        with self._lock:
+            if not self._bufs or self._bufs[0].numel() < nbytes:
+                self._bufs = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(self.SLOTS)]
+                self._events = [None] * self.SLOTS
+            return self._bufs, self._events
+
+    def release(self):
+        with self._lock:
+            self._bufs, self._events = [], []
+
+
+_PINNED = _PinnedRing()
+
+
 def _ingest_streamed(a_cpu: torch.Tensor, want_gram: bool, sketch_plan=None):
     """Host -> device copy of A in row chunks on a side stream, overlapped with the
     per-chunk work that does not need all of A: validation + ||A||_F^2, the kappa0
     SYRK (accumulated chunk by chunk) and the (speculative) sketch partial sums
-    with global row offsets.  Returns (DMat, G or None, sketch (total, flag) or None)."""
+    with global row offsets.  Pageable input is staged through a pinned ring
+    (`_PinnedRing`), chunk by chunk, interleaved with the enqueueing of that chunk's
+    device work.  Returns (DMat, G or None, sketch (total, flag) or None)."""
     from .device import device as _device
     from .sketch import _sketch_sum
     dev = _device()
@@ -277,13 +309,11 @@ def _ingest_streamed(a_cpu: torch.Tensor, want_gram: bool, sketch_plan=None):
     rows = max(64, -(-m // STREAM_CHUNKS))
     rows = -(-rows // 64) * 64
     chunks = [(r0, min(m, r0 + rows)) for r0 in range(0, m, rows)]
-    events = []
-    with torch.cuda.stream(copier):
-        for r0, r1 in chunks:
-            out[r0:r1].copy_(a_cpu[r0:r1], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(copier)
-            events.append(ev)
+    pinned = a_cpu.is_pinned()
+    if not pinned:
+        piece = max(1, min(rows, _PINNED.PIECE_BYTES // (n * 8)))   # rows per staged piece
+        bufs, slot_events = _PINNED.slots(piece * n * 8)
+        nslot = [0]
     stats = torch.zeros(2, dtype=torch.float64, device=dev)
     g = torch.zeros((n, n), dtype=torch.float64, device=dev) if want_gram else None
     sk_total = sk_flag = None
@@ -292,8 +322,34 @@ def _ingest_streamed(a_cpu: torch.Tensor, want_gram: bool, sketch_plan=None):
         sk_total = torch.zeros((n, dsk.op.d), dtype=torch.float64, device=dev)
         sk_flag = torch.zeros(1, dtype=torch.int32, device=dev)
     lib = _lib.lib()
+
+    def enqueue_copy(i, r0, r1):
+        with torch.cuda.stream(copier):
+            if pinned:
+                out[r0:r1].copy_(a_cpu[r0:r1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copier)
+                return ev
+            for p0 in range(r0, r1, piece):
+                p1 = min(r1, p0 + piece)
+                slot = nslot[0] % len(bufs)
+                nslot[0] += 1
+                if slot_events[slot] is not None:
+                    slot_events[slot].synchronize()     # the H2D that last used this slot is done
+                stage = bufs[slot][: (p1 - p0) * n * 8].view(torch.float64).view(p1 - p0, n)
+                stage.copy_(a_cpu[p0:p1])                # host threads, pageable -> pinned
+                out[p0:p1].copy_(stage, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copier)
+                slot_events[slot] = ev
+        return ev
+
+    # pinned input: every copy is enqueued up front; pageable input: the host stages
+    # chunk i + 1 while the GPU copies and processes chunk i
+    events = [enqueue_copy(i, r0, r1) for i, (r0, r1) in enumerate(chunks)] if pinned else []
     for i, (r0, r1) in enumerate(chunks):
-        compute.wait_event(events[i])
+        ev = events[i] if pinned else enqueue_copy(i, r0, r1)
+        compute.wait_event(ev)
         part = out[r0:r1]
         wp, wn = WORKSPACE.get(lib.sk_matrix_stats_workspace(r1 - r0, n))
         call("sk_cast_stats_async", part.data_ptr(), 8, r1 - r0, n, n, None, n, stats.data_ptr(), wp, wn,
@@ -458,8 +514,9 @@ def _trsm_gram_chunked(ad: DMat, r: torch.Tensor, bd: torch.Tensor, method: str,
 
 
 def release_scratch():
-    """Free the cached A_p buffer of algorithm1_pipeline."""
+    """Free the cached A_p buffer of algorithm1_pipeline and the pinned staging ring."""
     _AP_SCRATCH.release()
+    _PINNED.release()
 
 
 def _prepare_dev(ad, d_factor, transform, level, seed, diagnostics=True, strict=False, stages=None,

@@ -196,3 +196,22 @@ def test_measure_bound_inputs_matches_oracle_diagnostics():
     assert bi.nu_pne == pytest.approx(np.linalg.norm(y) / (R.condition_number(r_s)[0] * np.linalg.norm(x)), rel=1e-8)
     nap, napta = R.condition_number(a_p)[0], R.condition_number(a_p.T @ p.a)[0]
     assert bi.nu_hpne == pytest.approx(nap * na / napta, rel=1e-6)
+
+
+def test_pageable_host_input_staged_bitwise(monkeypatch):
+    """Pageable numpy input above STREAM_MIN_BYTES goes through the pinned staging ring
+    (several pieces per chunk, slots reused); the result is bitwise that of pinned
+    input, which the copy engine reads directly."""
+    from paper_2603_16644_b200 import solvers as S
+    monkeypatch.setattr(S, "STREAM_MIN_BYTES", 0)
+    monkeypatch.setattr(S._PinnedRing, "PIECE_BYTES", 96 * 1024)       # many pieces, slot reuse
+    S._PINNED.release()
+    p = planted_problem(20000, 48, 1e3, 1e-6, 3)
+    a_np = np.ascontiguousarray(p.a)
+    pageable = sq.algorithm1_pipeline(a_np, p.b, method="hpne", precision="auto", seed=3, x_star=p.x_star,
+                                      diagnostics=False)
+    pinned = sq.algorithm1_pipeline(torch.from_numpy(a_np).pin_memory(), p.b, method="hpne", precision="auto",
+                                    seed=3, x_star=p.x_star, diagnostics=False)
+    assert np.array_equal(pageable.x_hat, pinned.x_hat)
+    assert pageable.precision_decision.selected == pinned.precision_decision.selected
+    S._PINNED.release()
