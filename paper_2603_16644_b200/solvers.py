@@ -137,6 +137,11 @@ def _host_f64_matrix(a):
     if isinstance(a, torch.Tensor):
         return a if (not a.is_cuda and a.dim() == 2 and a.dtype == torch.float64 and a.is_contiguous()) else None
     if isinstance(a, np.ndarray) and a.ndim == 2 and a.dtype == np.float64 and a.flags.c_contiguous:
+        if not a.flags.writeable:   # e.g. a memory-mapped .npy archive: only ever read here
+            import warnings
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", UserWarning)
+                return torch.from_numpy(a)
         return torch.from_numpy(a)
     return None
 
