@@ -330,7 +330,7 @@ householder_kernel(T *w, int64_t ld, int d, int n, T *alphas /* n */, T *part /*
 template <typename T, bool SMEM>
 __global__ void __launch_bounds__(THREADS)
 householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nqmax x n */, T *taus, T *v0s,
-                        int *flags, Ctl<T> *ctl) {
+                        int *flags, Ctl<T> *ctl, int qs) {
     using O = LevelOps<T>;
     __shared__ T sh_nodes[MAXCH];
     __shared__ T sh_t[MAXCH];
@@ -341,15 +341,21 @@ householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nq
     const int G = gridDim.x, b = blockIdx.x;
     const int nloc = b < n ? (n - b + G - 1) / G : 0;
     const int nqd = (d + CH - 1) / CH;
-    T *sm_cols = reinterpret_cast<T *>(qr_dyn);                         // nloc x d
-    T *sm_part = sm_cols + (SMEM ? (size_t)nloc * d : 0);              // nloc x nqd chunk nodes
+    // SMEM with qs > 0 (binary32 / binary64 at 6144 x 2048 do not fit whole): the CTA's
+    // first qs local columns stay in global memory, the later ones (which take the most
+    // reflector updates) in shared memory; all accesses go through generic pointers
+    T *sm_cols = reinterpret_cast<T *>(qr_dyn);                         // (nloc - qs) x d
+    T *sm_part = sm_cols + (SMEM ? (size_t)max(nloc - qs, 0) * d : 0); // nloc x nqd chunk nodes
     // owned column c (c mod G == b)
-    auto col = [&](int c) -> T * { return SMEM ? sm_cols + (size_t)(c / G) * d : w + (int64_t)c * ld; };
+    auto in_smem = [&](int c) { return SMEM && c / G >= qs; };
+    auto col = [&](int c) -> T * {
+        return in_smem(c) ? sm_cols + (size_t)(c / G - qs) * d : w + (int64_t)c * ld;
+    };
     auto part_at = [&](int k, int q, int c) -> T & { return SMEM ? sm_part[k * nqd + q] : part[(size_t)q * n + c]; };
     if (SMEM) {
-        for (int q = 0; q < nloc; ++q) {
+        for (int q = qs; q < nloc; ++q) {
             const T *src = w + (int64_t)(b + q * G) * ld;
-            T *dst = sm_cols + (size_t)q * d;
+            T *dst = sm_cols + (size_t)(q - qs) * d;
             for (int i = threadIdx.x; i < d; i += THREADS) dst[i] = src[i];
         }
         __syncthreads();
@@ -407,7 +413,7 @@ householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nq
             const int rc = j + 1 < n ? reflect_from_nodes<T>(x, Lx, taus + j + 1, v0s + j + 1, alphas, j + 1,
                                                              sh_nodes, &sh_root)
                                      : SK_OK;
-            if (SMEM) {   // the reflector column (rows j+1..) goes to global memory for the other CTAs
+            if (in_smem(j + 1)) {   // the reflector column (rows j+1..) goes to global memory for the other CTAs
                 T *dst = w + (int64_t)(j + 1) * ld;
                 for (int i = j + 1 + threadIdx.x; i < d; i += THREADS) dst[i] = colj[i - j];
                 __threadfence();
@@ -491,9 +497,9 @@ householder_flow_kernel(T *w, int64_t ld, int d, int n, T *alphas, T *part /* nq
     }
     if (SMEM) {
         __syncthreads();
-        for (int q = 0; q < nloc; ++q) {
+        for (int q = qs; q < nloc; ++q) {
             T *dst = w + (int64_t)(b + q * G) * ld;
-            const T *src = sm_cols + (size_t)q * d;
+            const T *src = sm_cols + (size_t)(q - qs) * d;
             for (int i = threadIdx.x; i < d; i += THREADS) dst[i] = src[i];
         }
     }
@@ -586,17 +592,27 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
         auto sfn = householder_flow_kernel<T, true>;
         const int gs = (int)std::min<int64_t>(sm_count(), n);
         const int64_t nloc = (n + gs - 1) / gs;
-        const size_t smem = (size_t)(nloc * d + nloc * nq_max(d)) * sizeof(T);
         int optin = 0, dev = 0;
         cudaFuncAttributes fa{};
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        if (gs >= 2 && cudaFuncGetAttributes(&fa, (const void *)sfn) == cudaSuccess &&
+        const bool fa_ok = cudaFuncGetAttributes(&fa, (const void *)sfn) == cudaSuccess;
+        // as many of each CTA's columns as fit (the later ones); SK_QR_SMEM=full: all or none
+        const int64_t room = (int64_t)optin - (int64_t)fa.sharedSizeBytes - 1024 -
+                             (int64_t)(nloc * nq_max(d) * sizeof(T));
+        const int64_t fit = room > 0 ? room / (int64_t)(d * sizeof(T)) : 0;
+        const bool whole_only = qr_smem_env && strcmp(qr_smem_env, "full") == 0;
+        // partly resident only when at least half of a CTA's columns fit: binary32 at
+        // 6144 x 2048 (9 of 14) 46.6 -> 42.3 ms; binary64 (4 of 14) measured slower
+        int qs = (int)std::max<int64_t>(0, nloc - fit);
+        if ((whole_only && qs > 0) || 2 * qs > nloc) qs = (int)nloc;
+        const size_t smem = (size_t)((nloc - qs) * d + nloc * nq_max(d)) * sizeof(T);
+        if (gs >= 2 && fa_ok && qs < nloc &&
             smem + fa.sharedSizeBytes + 1024 <= (size_t)optin &&
             cudaFuncSetAttribute((const void *)sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
             max_coop_blocks((const void *)sfn, THREADS, smem) >= gs) {
             SK_CUDA(cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st));
-            void *args[] = {&w, &ldw, &di, &ni, &alphas, &part, &taus, &v0s, &flags, &ctl};
+            void *args[] = {&w, &ldw, &di, &ni, &alphas, &part, &taus, &v0s, &flags, &ctl, &qs};
             SK_CUDA(cudaLaunchCooperativeKernel((const void *)sfn, dim3(gs), dim3(THREADS), args, smem, st));
             SK_LAUNCH_CHECK("householder_flow_kernel (smem)");
             launched = true;
@@ -606,7 +622,8 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
     if (launched) {
     } else if (flow && (n + blocks - 1) / blocks <= MAXCH) {
         SK_CUDA(cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st));
-        void *args[] = {&w, &ldw, &di, &ni, &alphas, &part, &taus, &v0s, &flags, &ctl};
+        int qs0 = 0;
+        void *args[] = {&w, &ldw, &di, &ni, &alphas, &part, &taus, &v0s, &flags, &ctl, &qs0};
         SK_CUDA(cudaLaunchCooperativeKernel((const void *)ffn, dim3(blocks), dim3(THREADS), args, 0, st));
         SK_LAUNCH_CHECK("householder_flow_kernel");
     } else {

@@ -1,6 +1,8 @@
 """The level QR with shared-memory-resident columns (householder_flow_kernel<T, true>,
 the default whenever a CTA's columns fit) against the global-memory flow kernel
 (SK_QR_SMEM=0): the same chunk trees and rounding points, so R agrees bit for bit at
+every level -- also when only a CTA's later columns fit shared memory (binary32 / binary64
+at 6144 x 2048) --
 every level, including the binary16 collapse that drives the escalation
 (src/precision.py:153-202, src/solvers.py:255-279).  The choice is read once per
 process, so each arm runs in its own process."""
@@ -20,6 +22,7 @@ import paper_2603_16644_b200 as sq
 from oracle import restatement as R
 out = {}
 cases = [(6144, 2048, "binary16", 1.0), (3000, 1000, "binary32", 1.0), (1200, 400, "binary64", 1.0),
+         (6144, 2048, "binary32", 1.0), (6144, 2048, "binary64", 1.0),   # partly shared-memory resident
          (700, 300, "binary16", 1.0), (600, 40, "binary16", 1e-6), (1001, 333, "binary16", 1.0)]   # odd d: no half2 pairs
 for d, n, lev, spread in cases:
     g = R.philox(d + n, 5)
