@@ -1113,7 +1113,7 @@ size_t sketch_fft_workspace(int64_t m_pad, int64_t n, int64_t d) {
     if (!sketch_fft_supported(m_pad)) return 0;
     const int64_t cb = colblock(m_pad, n);
     const size_t ybytes = (size_t)(cb / 2) * m_pad * sizeof(double2);
-    const size_t zbytes = (size_t)d * 2 * (cb / 2) * sizeof(double2);
+    const size_t zbytes = (size_t)d * 2 * cb * sizeof(double2);   // up to 2 cb columns (binary32 transform)
     const size_t req = (size_t)(N2 + 1) * sizeof(int) + (size_t)2 * d * (2 * sizeof(int) + sizeof(int64_t));
     const size_t tables = (size_t)(N2 + m_pad / N2) * sizeof(double2);
     const size_t sbits = (size_t)(m_pad / N2) * 64 * sizeof(uint16_t);
@@ -1128,12 +1128,16 @@ int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int
     if (!sketch_fft_supported(m_pad)) { set_error("sketch_fft: M must be a multiple of 2048"); return SK_ERR_ARG; }
     if (ws_bytes < sketch_fft_workspace(m_pad, n, d)) { set_error("sketch_fft: workspace too small"); return SK_ERR_ARG; }
     const int64_t M = m_pad, M1 = M / N2;
-    const int64_t cb = colblock(M, n);
+    const int64_t cb64 = colblock(M, n);
+    // the binary32 transform's Y (8-byte entries) fits twice the columns in the same bytes
+    const char *cb_env = getenv("SK_FFT_CB32");
+    const bool wide32 = !(cb_env && cb_env[0] == '0');
+    const int64_t cb = (level == 64 || !wide32) ? cb64 : std::min<int64_t>(2 * cb64, (n + 7) / 8 * 8);
     uint8_t *p = static_cast<uint8_t *>(ws);
     double2 *y = reinterpret_cast<double2 *>(p);
-    p += align_up((size_t)(cb / 2) * M * sizeof(double2), 256);
+    p += align_up((size_t)(cb64 / 2) * M * sizeof(double2), 256);
     double2 *zbuf = reinterpret_cast<double2 *>(p);
-    p += align_up((size_t)d * 2 * (cb / 2) * sizeof(double2), 256);
+    p += align_up((size_t)d * 2 * cb64 * sizeof(double2), 256);
     int *d_ptr = reinterpret_cast<int *>(p);
     int *d_s = d_ptr + (N2 + 1);
     int *d_w = d_s + 2 * d;
