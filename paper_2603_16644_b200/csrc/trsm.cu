@@ -26,7 +26,11 @@ namespace trsm {
 #define SK_TRSM_BK 16
 #define SK_TRSM_STAGES 3
 #endif
-constexpr int BMR = 128, NB = 64, BK = SK_TRSM_BK, STAGES = SK_TRSM_STAGES, THREADS = 256;
+#ifndef SK_TRSM_BMR
+#define SK_TRSM_BMR 128   // rows per CTA; 2 threads per row in the substitution
+#endif
+constexpr int BMR = SK_TRSM_BMR, NB = 64, BK = SK_TRSM_BK, STAGES = SK_TRSM_STAGES, THREADS = 2 * BMR;
+constexpr int MINB = BMR >= 128 ? 2 : 3;   // CTAs per SM (shared memory: 102 KB at 128 rows, 69 KB at 64)
 constexpr int WM = 32, WN = 32;             // 4 x 2 warps
 constexpr int APITCH = BK + 4;              // 20 = 4 (mod 16): conflict-free A fragments
 constexpr int BPITCH = NB + 4;              // 68 = 4 (mod 16): conflict-free B fragments
@@ -139,7 +143,7 @@ __device__ __forceinline__ void load_block(double *ts, double *rs, const double 
     }
 }
 
-__global__ void __launch_bounds__(THREADS, 2)
+__global__ void __launch_bounds__(THREADS, MINB)
 trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__restrict__ r, int64_t ldr, double *ap,
             int64_t ldap, bool vec) {
     extern __shared__ __align__(16) double smem[];
