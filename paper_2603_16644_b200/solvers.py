@@ -271,26 +271,24 @@ class _PinnedRing:
     reference's convention): the driver would otherwise stage a pageable copy through
     its own small bounce buffers at ~10 GB/s.  Host threads copy a row chunk into a free
     slot (torch's multi-threaded CPU copy, GIL released) while the copy engine moves
-    the previous slot over PCIe; a slot is reused once its H2D event has completed."""
+    the previous slot over PCIe; a slot is reused once its H2D event has completed.
+    Rings are per host thread (the reference's API is safe for concurrent calls)."""
 
     SLOTS = 4
     PIECE_BYTES = 256 << 20
 
     def __init__(self):
-        self._bufs: list[torch.Tensor] = []
-        self._events: list = []
-        self._lock = threading.Lock()
+        self._local = threading.local()    # one ring per host thread: concurrent calls stay safe
 
     def slots(self, nbytes: int):
-        with self._lock:
-            if not self._bufs or self._bufs[0].numel() < nbytes:
-                self._bufs = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(self.SLOTS)]
-                self._events = [None] * self.SLOTS
-            return self._bufs, self._events
+        loc = self._local
+        if not getattr(loc, "bufs", None) or loc.bufs[0].numel() < nbytes:
+            loc.bufs = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(self.SLOTS)]
+            loc.events = [None] * self.SLOTS
+        return loc.bufs, loc.events
 
     def release(self):
-        with self._lock:
-            self._bufs, self._events = [], []
+        self._local.bufs, self._local.events = [], []
 
 
 _PINNED = _PinnedRing()
