@@ -535,12 +535,146 @@ __global__ void extract_r(const T *w, int64_t ld, const T *alphas, int n, double
 
 inline int64_t nq_max(int64_t d) { return (d + CH - 1) / CH; }
 
+constexpr int NBQ = 64;          // panel width of the blocked (WY) binary32 / binary64 QR
+constexpr int64_t BLOCKED_MAX_D = 32768;   // sketch heights; taller (TSQR blocks) keep the dataflow kernel
+
+template <typename T>
+size_t blocked_ws_bytes(int64_t d, int64_t n) {
+    if (std::is_same<T, __half>::value || d > BLOCKED_MAX_D || n <= NBQ) return 0;
+    return align_up((size_t)d * NBQ * sizeof(T), 256) + 2 * align_up((size_t)NBQ * NBQ * sizeof(T), 256) +
+           2 * align_up((size_t)NBQ * n * sizeof(T), 256);   // V, V^T V, T, G, W
+}
+
 template <typename T>
 size_t ws_bytes(int64_t d, int64_t n) {
     return align_up(sizeof(Ctl<T>), 256) + align_up((size_t)n * sizeof(T), 256) +
            align_up((size_t)nq_max(d) * n * sizeof(T), 256) + 256 +
-           2 * align_up((size_t)n * sizeof(T), 256) + align_up((size_t)n * sizeof(int), 256);   // flow kernel
+           2 * align_up((size_t)n * sizeof(T), 256) + align_up((size_t)n * sizeof(int), 256) +   // flow kernel
+           blocked_ws_bytes<T>(d, n);
 }
+
+// ---------------------------------------------------- blocked (WY) QR pieces --
+// binary32 / binary64: panels of NBQ columns are factored by the dataflow kernel (one
+// column per CTA, so a reflector step is one column's work, not a CTA's 14), and the
+// trailing columns take the panel's reflectors at once in compact WY form,
+// A_trail <- (I - V T^T V^T) A_trail = A_trail - V (T^T (V^T A_trail)), with T from
+// LAPACK's forward columnwise recurrence (xLARFT).  All arithmetic in the level type
+// (true FP32 for binary32); the reference's own order here is BLAS-defined
+// (src/precision.py:181-187), so R agrees to level roundoff, with the reference's
+// sign convention (the panel reflectors are the same Householder steps).
+
+// V (dv x nbp, column-major, ld dv): zeros above the diagonal, v0 on it, the compact
+// reflector storage of the panel below it
+template <typename T>
+__global__ void qrb_make_v(const T *wp, int64_t ld, int dv, int nbp, const T *v0s, T *v) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)dv * nbp;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(idx / dv), r = (int)(idx % dv);
+        v[idx] = r < k ? LevelOps<T>::zero() : (r == k ? v0s[k] : wp[(int64_t)k * ld + r]);
+    }
+}
+
+// C (nbp x nc, ld nbp) = X^T Y over dv rows; X: dv x nbp (ld ldx), Y: dv x nc (ld ldy).
+// CTA: all nbp (<= 64) rows of C x 32 columns; thread (c = tid % 32, kq = tid / 32): 8 k.
+template <typename T>
+__global__ void __launch_bounds__(256) qrb_gemm_tn(const T *x, int64_t ldx, const T *y, int64_t ldy, int dv, int nbp,
+                                                   int nc, T *c, int64_t ldc) {
+    __shared__ T xs[32][NBQ + 1];
+    __shared__ T ys[32][33];
+    const int tid = threadIdx.x, cc = tid & 31, kq = tid >> 5;
+    const int c0 = blockIdx.x * 32;
+    T acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = LevelOps<T>::zero();
+    for (int r0 = 0; r0 < dv; r0 += 32) {
+        for (int e = tid; e < 32 * NBQ; e += 256) {
+            const int rr = e & 31, k = e >> 5;
+            xs[rr][k] = (r0 + rr < dv && k < nbp) ? x[(int64_t)k * ldx + r0 + rr] : LevelOps<T>::zero();
+        }
+        for (int e = tid; e < 32 * 32; e += 256) {
+            const int rr = e & 31, j = e >> 5;
+            ys[rr][j] = (r0 + rr < dv && c0 + j < nc) ? y[(int64_t)(c0 + j) * ldy + r0 + rr] : LevelOps<T>::zero();
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int rr = 0; rr < 32; ++rr) {
+            const T yv = ys[rr][cc];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = acc[i] + xs[rr][kq * 8 + i] * yv;
+        }
+        __syncthreads();
+    }
+    if (c0 + cc < nc)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (kq * 8 + i < nbp) c[(int64_t)(c0 + cc) * ldc + kq * 8 + i] = acc[i];
+}
+
+// xLARFT (forward, columnwise): T upper nbp x nbp (column-major, ld NBQ) from V^T V and tau
+template <typename T>
+__global__ void qrb_larft(const T *vtv, const T *tau, int nbp, T *tm) {
+    __shared__ T t[NBQ];
+    const int i = threadIdx.x;
+    for (int e = i; e < NBQ * NBQ; e += blockDim.x) tm[e] = LevelOps<T>::zero();
+    __syncthreads();
+    for (int j = 0; j < nbp; ++j) {
+        if (i < j) t[i] = -tau[j] * vtv[(int64_t)j * nbp + i];    // -tau_j v_i . v_j
+        __syncthreads();
+        if (i < j) {
+            T s = LevelOps<T>::zero();
+            for (int k = i; k < j; ++k) s = s + tm[(int64_t)k * NBQ + i] * t[k];
+            tm[(int64_t)j * NBQ + i] = s;
+        }
+        if (i == j) tm[(int64_t)j * NBQ + j] = tau[j];
+        __syncthreads();
+    }
+}
+
+// W (nbp x nc, ld nbp) = T^T G
+template <typename T>
+__global__ void qrb_tmul(const T *tm, const T *g, int nbp, int nc, T *wt) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)nbp * nc;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx % nbp), c = (int)(idx / nbp);
+        T s = LevelOps<T>::zero();
+        for (int k = 0; k <= i; ++k) s = s + tm[(int64_t)i * NBQ + k] * g[(int64_t)c * nbp + k];
+        wt[idx] = s;
+    }
+}
+
+// A_trail (dv x nc, ld) -= V (dv x nbp) W (nbp x nc); CTA: 32 rows x 32 columns,
+// thread (row tid % 32, column group tid / 32 of 4)
+template <typename T>
+__global__ void __launch_bounds__(256) qrb_update(T *a, int64_t ld, const T *v, int dv, int nbp, const T *wt, int nc) {
+    __shared__ T vs[NBQ][33];
+    __shared__ T ws_[NBQ][33];
+    const int tid = threadIdx.x, rr = tid & 31, cq = tid >> 5;
+    const int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    for (int e = tid; e < 32 * NBQ; e += 256) {
+        const int r = e & 31, k = e >> 5;
+        vs[k][r] = (r0 + r < dv && k < nbp) ? v[(int64_t)k * dv + r0 + r] : LevelOps<T>::zero();
+    }
+    for (int e = tid; e < NBQ * 32; e += 256) {
+        const int k = e & (NBQ - 1), j = e / NBQ;
+        ws_[k][j] = (k < nbp && c0 + j < nc) ? wt[(int64_t)(c0 + j) * nbp + k] : LevelOps<T>::zero();
+    }
+    __syncthreads();
+    T acc[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = LevelOps<T>::zero();
+    for (int k = 0; k < nbp; ++k) {
+        const T vv = vs[k][rr];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] = acc[i] + vv * ws_[k][cq * 4 + i];
+    }
+    if (r0 + rr < dv)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = c0 + cq * 4 + i;
+            if (c < nc) a[(int64_t)c * ld + r0 + rr] = a[(int64_t)c * ld + r0 + rr] - acc[i];
+        }
+}
+
 
 // Compact reflectors left behind by the dataflow kernels (taus[j], v0s[j] = v_j[0]),
 // for forming Q afterwards.
@@ -579,58 +713,110 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
     const bool flow = !barrier_kernel;
     const int maxb = max_coop_blocks(flow ? (const void *)ffn : (const void *)kfn, THREADS, 0);
     if (maxb <= 0) { set_error("sk_qr_r: kernel cannot be co-resident"); return SK_ERR_ARG; }
-    const int64_t units = nq_max(d) * n;
-    int blocks = (int)std::min<int64_t>(std::min<int64_t>(maxb, sm_count()), (units + WARPS - 1) / WARPS + 1);
-    if (blocks < 2) blocks = std::min(2, maxb);
-    int di = (int)d, ni = (int)n;
-    int64_t ldw = d;
-    // shared-memory-resident columns whenever they fit (SK_QR_SMEM=0 forces the global one)
     static const char *qr_smem_env = getenv("SK_QR_SMEM");
     const bool try_smem = flow && !(qr_smem_env && strcmp(qr_smem_env, "0") == 0);
-    bool launched = false;
-    if (try_smem) {
-        auto sfn = householder_flow_kernel<T, true>;
-        const int gs = (int)std::min<int64_t>(sm_count(), n);
-        const int64_t nloc = (n + gs - 1) / gs;
-        int optin = 0, dev = 0;
-        cudaFuncAttributes fa{};
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        const bool fa_ok = cudaFuncGetAttributes(&fa, (const void *)sfn) == cudaSuccess;
-        // as many of each CTA's columns as fit (the later ones); SK_QR_SMEM=full: all or none
-        const int64_t room = (int64_t)optin - (int64_t)fa.sharedSizeBytes - 1024 -
-                             (int64_t)(nloc * nq_max(d) * sizeof(T));
-        const int64_t fit = room > 0 ? room / (int64_t)(d * sizeof(T)) : 0;
-        const bool whole_only = qr_smem_env && strcmp(qr_smem_env, "full") == 0;
-        // partly resident only when at least half of a CTA's columns fit: binary32 at
-        // 6144 x 2048 (9 of 14) 46.6 -> 42.3 ms; binary64 (4 of 14) measured slower
-        int qs = (int)std::max<int64_t>(0, nloc - fit);
-        if ((whole_only && qs > 0) || 2 * qs > nloc) qs = (int)nloc;
-        const size_t smem = (size_t)((nloc - qs) * d + nloc * nq_max(d)) * sizeof(T);
-        if (gs >= 2 && fa_ok && qs < nloc &&
-            smem + fa.sharedSizeBytes + 1024 <= (size_t)optin &&
-            cudaFuncSetAttribute((const void *)sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
-            max_coop_blocks((const void *)sfn, THREADS, smem) >= gs) {
-            SK_CUDA(cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st));
-            void *args[] = {&w, &ldw, &di, &ni, &alphas, &part, &taus, &v0s, &flags, &ctl, &qs};
-            SK_CUDA(cudaLaunchCooperativeKernel((const void *)sfn, dim3(gs), dim3(THREADS), args, smem, st));
-            SK_LAUNCH_CHECK("householder_flow_kernel (smem)");
-            launched = true;
+    // one dataflow / barrier factorisation of the d_v x n_v view at wv (column stride d)
+    auto launch_view = [&](T *wv, int dv_, int nv_, T *alv, T *tauv, T *v0v) -> int {
+        const int64_t units = nq_max(dv_) * nv_;
+        int blocks = (int)std::min<int64_t>(std::min<int64_t>(maxb, sm_count()), (units + WARPS - 1) / WARPS + 1);
+        if (blocks < 2) blocks = std::min(2, maxb);
+        int di = dv_, ni = nv_;
+        int64_t ldw = d;
+        // shared-memory-resident columns whenever they fit (SK_QR_SMEM=0 forces the global one)
+        if (try_smem) {
+            auto sfn = householder_flow_kernel<T, true>;
+            const int gs = (int)std::min<int64_t>(sm_count(), nv_);
+            const int64_t nloc = (nv_ + gs - 1) / gs;
+            int optin = 0, dev = 0;
+            cudaFuncAttributes fa{};
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            const bool fa_ok = cudaFuncGetAttributes(&fa, (const void *)sfn) == cudaSuccess;
+            // as many of each CTA's columns as fit (the later ones); SK_QR_SMEM=full: all or none
+            const int64_t room = (int64_t)optin - (int64_t)fa.sharedSizeBytes - 1024 -
+                                 (int64_t)(nloc * nq_max(dv_) * sizeof(T));
+            const int64_t fit = room > 0 ? room / (int64_t)(dv_ * sizeof(T)) : 0;
+            const bool whole_only = qr_smem_env && strcmp(qr_smem_env, "full") == 0;
+            // partly resident only when at least half of a CTA's columns fit: binary32 at
+            // 6144 x 2048 (9 of 14) 46.6 -> 42.3 ms; binary64 (4 of 14) measured slower
+            int qs = (int)std::max<int64_t>(0, nloc - fit);
+            if ((whole_only && qs > 0) || 2 * qs > nloc) qs = (int)nloc;
+            const size_t smem = (size_t)((nloc - qs) * dv_ + nloc * nq_max(dv_)) * sizeof(T);
+            if (gs >= 2 && fa_ok && qs < nloc && smem + fa.sharedSizeBytes + 1024 <= (size_t)optin &&
+                cudaFuncSetAttribute((const void *)sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+                    cudaSuccess &&
+                max_coop_blocks((const void *)sfn, THREADS, smem) >= gs) {
+                SK_CUDA(cudaMemsetAsync(flags, 0, (size_t)nv_ * sizeof(int), st));
+                void *args[] = {&wv, &ldw, &di, &ni, &alv, &part, &tauv, &v0v, &flags, &ctl, &qs};
+                SK_CUDA(cudaLaunchCooperativeKernel((const void *)sfn, dim3(gs), dim3(THREADS), args, smem, st));
+                SK_LAUNCH_CHECK("householder_flow_kernel (smem)");
+                return SK_OK;
+            }
+            cudaGetLastError();   // a refused attribute / occupancy query falls back below
         }
-        cudaGetLastError();   // a refused attribute / occupancy query falls back below
-    }
-    if (launched) {
-    } else if (flow && (n + blocks - 1) / blocks <= MAXCH) {
-        SK_CUDA(cudaMemsetAsync(flags, 0, (size_t)n * sizeof(int), st));
-        int qs0 = 0;
-        void *args[] = {&w, &ldw, &di, &ni, &alphas, &part, &taus, &v0s, &flags, &ctl, &qs0};
-        SK_CUDA(cudaLaunchCooperativeKernel((const void *)ffn, dim3(blocks), dim3(THREADS), args, 0, st));
-        SK_LAUNCH_CHECK("householder_flow_kernel");
-    } else {
+        if (flow && (nv_ + blocks - 1) / blocks <= MAXCH) {
+            SK_CUDA(cudaMemsetAsync(flags, 0, (size_t)nv_ * sizeof(int), st));
+            int qs0 = 0;
+            void *args[] = {&wv, &ldw, &di, &ni, &alv, &part, &tauv, &v0v, &flags, &ctl, &qs0};
+            SK_CUDA(cudaLaunchCooperativeKernel((const void *)ffn, dim3(blocks), dim3(THREADS), args, 0, st));
+            SK_LAUNCH_CHECK("householder_flow_kernel");
+            return SK_OK;
+        }
         if (refl) { set_error("sk_qr: Q needs the dataflow kernel (n too large)"); return SK_ERR_ARG; }
-        void *args[] = {&w, &ldw, &di, &ni, &alphas, &part, &ctl};
+        void *args[] = {&wv, &ldw, &di, &ni, &alv, &part, &ctl};
         SK_CUDA(cudaLaunchCooperativeKernel((const void *)kfn, dim3(blocks), dim3(THREADS), args, 0, st));
         SK_LAUNCH_CHECK("householder_kernel");
+        return SK_OK;
+    };
+    // binary32 / binary64 with more than one panel: blocked WY (SK_QR_BLOCKED=0: the
+    // column-at-a-time dataflow kernel over the whole matrix)
+    static const char *blk_env = getenv("SK_QR_BLOCKED");
+    // measured at 6144 x 2048 with the dataflow panel kernel: binary64 75.2 -> 66.3 ms,
+    // binary32 42.3 -> 46.8 ms (the partly shared-memory resident whole-matrix kernel
+    // wins there); SK_QR_BLOCKED=1 forces it for binary32 too
+    const bool want_blocked = std::is_same<T, double>::value ? !(blk_env && blk_env[0] == '0')
+                                                             : (blk_env && blk_env[0] == '1');
+    const bool blocked = !HALF && flow && n > NBQ && d <= BLOCKED_MAX_D && want_blocked;
+    if (!blocked) {
+        const int rc0 = launch_view(w, (int)d, (int)n, alphas, taus, v0s);
+        if (rc0 != SK_OK) return rc0;
+    } else {
+        unsigned char *q = reinterpret_cast<unsigned char *>(flags) + align_up((size_t)n * sizeof(int), 256);
+        T *vb = reinterpret_cast<T *>(q);
+        q += align_up((size_t)d * NBQ * sizeof(T), 256);
+        T *vtv = reinterpret_cast<T *>(q);
+        q += align_up((size_t)NBQ * NBQ * sizeof(T), 256);
+        T *tm = reinterpret_cast<T *>(q);
+        q += align_up((size_t)NBQ * NBQ * sizeof(T), 256);
+        T *gm = reinterpret_cast<T *>(q);
+        q += align_up((size_t)NBQ * n * sizeof(T), 256);
+        T *wm = reinterpret_cast<T *>(q);
+        for (int64_t j0 = 0; j0 < n; j0 += NBQ) {
+            const int nbp = (int)std::min<int64_t>(NBQ, n - j0), dv = (int)(d - j0);
+            T *wp = w + j0 * d + j0;
+            const int rc0 = launch_view(wp, dv, nbp, alphas + j0, taus + j0, v0s + j0);
+            if (rc0 != SK_OK) return rc0;
+            int fl[2];
+            SK_CUDA(cudaMemcpyAsync(fl, &ctl->fail_code, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+            SK_CUDA(cudaStreamSynchronize(st));
+            if (fl[0] != SK_OK) {
+                set_error("reflector %lld collapsed at working precision", (long long)(fl[1] + j0));
+                return fill_status(status, fl[0], (int)(fl[1] + j0), 0.0, 0.0);
+            }
+            const int nc = (int)(n - j0 - nbp);
+            if (nc <= 0) break;
+            T *at = wp + (int64_t)nbp * d;   // trailing columns, rows j0..
+            qrb_make_v<T><<<(unsigned)std::min<int64_t>(((int64_t)dv * nbp + 255) / 256, 4096), 256, 0, st>>>(
+                wp, d, dv, nbp, v0s + j0, vb);
+            qrb_gemm_tn<T><<<(unsigned)((nbp + 31) / 32), 256, 0, st>>>(vb, dv, vb, dv, dv, nbp, nbp, vtv, nbp);
+            qrb_larft<T><<<1, NBQ, 0, st>>>(vtv, taus + j0, nbp, tm);
+            qrb_gemm_tn<T><<<(unsigned)((nc + 31) / 32), 256, 0, st>>>(vb, dv, at, d, dv, nbp, nc, gm, nbp);
+            qrb_tmul<T><<<(unsigned)std::min<int64_t>(((int64_t)nbp * nc + 255) / 256, 4096), 256, 0, st>>>(
+                tm, gm, nbp, nc, wm);
+            qrb_update<T><<<dim3((unsigned)((dv + 31) / 32), (unsigned)((nc + 31) / 32)), 256, 0, st>>>(at, d, vb, dv,
+                                                                                                   nbp, wm, nc);
+            SK_LAUNCH_CHECK("blocked QR trailing update");
+        }
     }
     int fail[2];
     SK_CUDA(cudaMemcpyAsync(fail, &ctl->fail_code, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
