@@ -32,7 +32,9 @@
 // extract_r.  v.v differs from x.x only in element 0, so only chunk 0 is redone.
 // The Q factor is not formed (build_preconditioner only uses R,
 // src/solvers.py:196-197); see DESIGN.md for the reference's non-finite-Q check.
+#include <cstdio>
 #include <type_traits>
+#include <vector>
 
 #include "common.cuh"
 
@@ -537,12 +539,15 @@ inline int64_t nq_max(int64_t d) { return (d + CH - 1) / CH; }
 
 constexpr int NBQ = 64;          // panel width of the blocked (WY) binary32 / binary64 QR
 constexpr int64_t BLOCKED_MAX_D = 32768;   // sketch heights; taller (TSQR blocks) keep the dataflow kernel
+constexpr int QRB_SPLIT_MAX = 32;          // row slabs of the V^T [V | A_trail] products
 
 template <typename T>
 size_t blocked_ws_bytes(int64_t d, int64_t n) {
     if (std::is_same<T, __half>::value || d > BLOCKED_MAX_D || n <= NBQ) return 0;
-    return align_up((size_t)d * NBQ * sizeof(T), 256) + 2 * align_up((size_t)NBQ * NBQ * sizeof(T), 256) +
-           2 * align_up((size_t)NBQ * n * sizeof(T), 256);   // V, V^T V, T, G, W
+    const size_t one = align_up((size_t)d * NBQ * sizeof(T), 256) + 2 * align_up((size_t)NBQ * NBQ * sizeof(T), 256) +
+                       2 * align_up((size_t)NBQ * n * sizeof(T), 256) +   // V, V^T V, T, G, W
+                       align_up((size_t)QRB_SPLIT_MAX * NBQ * std::max<int64_t>(n, NBQ) * sizeof(T), 256);   // partials
+    return 2 * one;   // the lookahead pipeline keeps two sets (panel parity / stream)
 }
 
 template <typename T>
@@ -563,6 +568,192 @@ size_t ws_bytes(int64_t d, int64_t n) {
 // (src/precision.py:181-187), so R agrees to level roundoff, with the reference's
 // sign convention (the panel reflectors are the same Householder steps).
 
+// Panel factorisation on one thread-block cluster (QPC_CL CTAs, the panel's rows split
+// in contiguous slabs held in shared memory), ONE cluster barrier per column: each CTA
+// publishes, for column j, the partial sum of squares of x = P[j:, j] below the diagonal
+// and the partial dots x . P[j:, c] for every later column c (row j included), plus -- on
+// the CTA owning row j -- x0 and the row-j entries P[j, c]; after the barrier every CTA
+// sums the partials in rank order (distributed shared memory) and forms alpha, v0, tau and
+// v . P[:, c] = x . P[:, c] - alpha P[j, c] identically, then updates its slab.  The
+// partial records alternate between two buffers, so a CTA may write column j+1's while a
+// slower one still reads column j's.  Same Householder step and sign convention as
+// householder_reduce (src/dense.py:137-160): norm 0, v.v 0 and a non-finite tau raise
+// RankDeficient.  At the end the CTAs form V^T V of the panel (cluster-reduced) and rank
+// 0 builds T = (diag(1/tau) + striu(V^T V))^-1 (the compact-WY T of xLARFT).
+constexpr int QPC_THREADS = 512, QPC_WARPS = QPC_THREADS / 32;
+constexpr int QPC_CL = 8;
+template <typename T, int NBP>
+__global__ void __launch_bounds__(QPC_THREADS) qrb_panel_cluster(T *wp, int64_t ld, int dv, int nbp, int slab,
+                                                                  T *alphas, T *taus, T *v0s, Ctl<T> *ctl, int col0,
+                                                                  T *tm /* NBQ x NBQ, col-major */, T *sbuf) {
+    using O = LevelOps<T>;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char qpc_raw[];
+    T *P = reinterpret_cast<T *>(qpc_raw);                 // [NBP][slab]: this CTA's rows of the panel
+    // partial record per buffer: [0] sum x^2 below the diagonal, [1] x0 (owner), [2 + c] dot x.P_c,
+    // [2 + NBP + c] P[j, c] (owner)
+    __shared__ T rec[2][2 + 2 * NBP];
+    __shared__ T red[QPC_WARPS];
+    __shared__ T tcol[NBP];
+    __shared__ T vtv[NBP][NBP + 1];
+    __shared__ T tau_s[NBP];
+    const int rank = (int)cluster.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r_lo = rank * slab, r_hi = min(dv, r_lo + slab), nr = max(0, r_hi - r_lo);
+    for (int c = 0; c < nbp; ++c)
+        for (int i = tid; i < nr; i += QPC_THREADS) P[c * slab + i] = wp[(int64_t)c * ld + r_lo + i];
+    __syncthreads();
+    int done = nbp;
+    for (int j = 0; j < nbp; ++j) {
+        T *rb = rec[j & 1];
+        const bool own = j >= r_lo && j < r_hi;
+        const int i0 = max(0, j + 1 - r_lo);               // first slab row below the diagonal
+        // ---- partials of column j: sum of squares (rows > j), dots with later columns (rows >= j)
+        T sq = O::zero();
+        for (int i = i0 + tid; i < nr; i += QPC_THREADS) { const T x = P[j * slab + i]; sq = sq + x * x; }
+        for (int o = 16; o > 0; o >>= 1) sq = sq + __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) red[warp] = sq;
+        const T *pjc = P + j * slab;
+        for (int c = j + 1 + warp; c < nbp; c += QPC_WARPS) {
+            const T *pcc = P + c * slab;
+            T d0 = O::zero(), d1 = O::zero();
+            int i = i0 + lane;
+            for (; i + 32 < nr; i += 64) {
+                d0 = d0 + pjc[i] * pcc[i];
+                d1 = d1 + pjc[i + 32] * pcc[i + 32];
+            }
+            if (i < nr) d0 = d0 + pjc[i] * pcc[i];
+            T dsum = d0 + d1;
+            for (int o = 16; o > 0; o >>= 1) dsum = dsum + __shfl_xor_sync(0xffffffffu, dsum, o);
+            if (lane == 0) {
+                const T pj = own ? P[c * slab + (j - r_lo)] : O::zero();
+                const T xj = own ? P[j * slab + (j - r_lo)] : O::zero();
+                rb[2 + c] = dsum + xj * pj;
+                rb[2 + NBP + c] = pj;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            T t = O::zero();
+            for (int k = 0; k < QPC_WARPS; ++k) t = t + red[k];
+            rb[0] = t;
+            rb[1] = own ? P[j * slab + (j - r_lo)] : O::zero();
+        }
+        cluster.sync();
+        // ---- alpha, v0, tau and t_c (identical in every CTA: fixed rank order)
+        // all remote loads in flight first (a distributed-shared-memory read is a round trip
+        // through the cluster network), then the fixed-order sums
+        T rs_[QPC_CL], xs_[QPC_CL];
+#pragma unroll
+        for (int k = 0; k < QPC_CL; ++k) {
+            const T *ps = cluster.map_shared_rank(rb, k);
+            rs_[k] = ps[0];
+            xs_[k] = ps[1];
+        }
+        T rest = rs_[0], x0 = xs_[0];
+#pragma unroll
+        for (int k = 1; k < QPC_CL; ++k) {
+            rest = rest + rs_[k];
+            x0 = x0 + xs_[k];
+        }
+        const T nrm = O::sqrt(rest + x0 * x0);
+        const T alpha = (x0 >= O::zero()) ? -nrm : nrm;
+        const T v0 = x0 - alpha;
+        const T vv = rest + v0 * v0;
+        const T tau = T(2) / vv;
+        if ((nrm == O::zero()) || (vv == O::zero()) || !O::finite(tau)) {
+            if (rank == 0 && tid == 0 && ctl->fail_code == SK_OK) {
+                ctl->fail_code = SK_RANK_DEFICIENT;
+                ctl->fail_col = col0 + j;
+            }
+            done = j;
+            break;   // uniform over the cluster (same values everywhere)
+        }
+        for (int c = j + 1 + tid; c < nbp; c += QPC_THREADS) {
+            T dxs[QPC_CL], pjs[QPC_CL];
+#pragma unroll
+            for (int k = 0; k < QPC_CL; ++k) {
+                const T *ps = cluster.map_shared_rank(rb, k);
+                dxs[k] = ps[2 + c];
+                pjs[k] = ps[2 + NBP + c];
+            }
+            T dx = dxs[0], pj = pjs[0];
+#pragma unroll
+            for (int k = 1; k < QPC_CL; ++k) {
+                dx = dx + dxs[k];
+                pj = pj + pjs[k];
+            }
+            tcol[c] = tau * (dx - alpha * pj);               // tau v . P[:, c]
+        }
+        if (tid == 0) tau_s[j] = tau;
+        __syncthreads();
+        // ---- update the later columns of this slab: P[:, c] -= t_c v (v_j = v0 on row j)
+        for (int c = j + 1 + warp; c < nbp; c += QPC_WARPS) {
+            const T tc = tcol[c];
+            T *pcc = P + c * slab;
+            int i = i0 + lane;
+#pragma unroll 1
+            for (; i + 96 < nr; i += 128) {
+                const T a0 = pcc[i], a1 = pcc[i + 32], a2 = pcc[i + 64], a3 = pcc[i + 96];
+                const T x0_ = pjc[i], x1_ = pjc[i + 32], x2_ = pjc[i + 64], x3_ = pjc[i + 96];
+                pcc[i] = a0 - tc * x0_;
+                pcc[i + 32] = a1 - tc * x1_;
+                pcc[i + 64] = a2 - tc * x2_;
+                pcc[i + 96] = a3 - tc * x3_;
+            }
+            for (; i < nr; i += 32) pcc[i] = pcc[i] - tc * pjc[i];
+            if (lane == 0 && own) pcc[j - r_lo] = pcc[j - r_lo] - tc * v0;
+        }
+        if (tid == 0 && own) P[j * slab + (j - r_lo)] = v0;  // compact storage: v on and below the diagonal
+        if (rank == 0 && tid == 0) { alphas[j] = alpha; taus[j] = tau; v0s[j] = v0; }
+        __syncthreads();
+    }
+    // ---- V^T V of the panel (rows >= the reflector's diagonal; zeros above it), one warp per entry
+    if (done == nbp && tm) {
+        for (int e = warp; e < nbp * nbp; e += QPC_WARPS) {
+            const int a_ = e % nbp, b_ = e / nbp;
+            if (a_ > b_) continue;                           // upper triangle incl. diagonal
+            T sacc = O::zero();
+            const int ilo = max(0, b_ - r_lo);               // V[:, a] and V[:, b] both live from row b
+            for (int i = ilo + lane; i < nr; i += 32) sacc = sacc + P[a_ * slab + i] * P[b_ * slab + i];
+            for (int o = 16; o > 0; o >>= 1) sacc = sacc + __shfl_xor_sync(0xffffffffu, sacc, o);
+            if (lane == 0) vtv[a_][b_] = sacc;
+        }
+    }
+    __syncthreads();
+    for (int c = 0; c < nbp; ++c)
+        for (int i = tid; i < nr; i += QPC_THREADS) wp[(int64_t)c * ld + r_lo + i] = P[c * slab + i];
+    cluster.sync();   // every CTA's partials are ready and its slab is written back (P is free)
+    if (done == nbp && tm && rank == 0) {
+        // S = diag(1/tau) + striu(V^T V) summed over the CTAs, staged in the freed slab area
+        T *Ssm = P;                                          // [NBP][NBP + 1]
+        T *Tsm = P + NBP * (NBP + 1);                        // [NBP][NBP + 1]: column b of T in Tsm[.][b]
+        for (int e = tid; e < nbp * nbp; e += QPC_THREADS) {
+            const int a_ = e % nbp, b_ = e / nbp;
+            if (a_ >= b_) continue;
+            T vs_[QPC_CL];
+#pragma unroll
+            for (int k = 0; k < QPC_CL; ++k) vs_[k] = *cluster.map_shared_rank(&vtv[a_][b_], k);
+            T sacc = vs_[0];
+#pragma unroll
+            for (int k = 1; k < QPC_CL; ++k) sacc = sacc + vs_[k];
+            Ssm[a_ * (NBP + 1) + b_] = sacc;
+        }
+        __syncthreads();
+        if (tid < nbp) {   // column b of T = S^-1: t_b = tau_b, t_r = -tau_r sum_{r<k<=b} S_rk t_k
+            const int b_ = tid;
+            Tsm[b_ * (NBP + 1) + b_] = tau_s[b_];
+            for (int r = b_ - 1; r >= 0; --r) {
+                T sacc = O::zero();
+                for (int k = r + 1; k <= b_; ++k) sacc = sacc + Ssm[r * (NBP + 1) + k] * Tsm[k * (NBP + 1) + b_];
+                Tsm[r * (NBP + 1) + b_] = -tau_s[r] * sacc;
+            }
+            for (int r = 0; r <= b_; ++r) tm[(int64_t)b_ * NBQ + r] = Tsm[r * (NBP + 1) + b_];
+        }
+    }
+    cluster.sync();   // no CTA leaves while rank 0 may still read its shared memory
+}
+
 // V (dv x nbp, column-major, ld dv): zeros above the diagonal, v0 on it, the compact
 // reflector storage of the panel below it
 template <typename T>
@@ -576,24 +767,29 @@ __global__ void qrb_make_v(const T *wp, int64_t ld, int dv, int nbp, const T *v0
 
 // C (nbp x nc, ld nbp) = X^T Y over dv rows; X: dv x nbp (ld ldx), Y: dv x nc (ld ldy).
 // CTA: all nbp (<= 64) rows of C x 32 columns; thread (c = tid % 32, kq = tid / 32): 8 k.
+// Split over rows: gridDim.y slabs of rows, slab z writes its partial C to c + z * pstride;
+// qrb_reduce sums the partials in slab order (deterministic).
 template <typename T>
 __global__ void __launch_bounds__(256) qrb_gemm_tn(const T *x, int64_t ldx, const T *y, int64_t ldy, int dv, int nbp,
-                                                   int nc, T *c, int64_t ldc) {
+                                                   int nc, T *c, int64_t ldc, int64_t pstride) {
     __shared__ T xs[32][NBQ + 1];
     __shared__ T ys[32][33];
     const int tid = threadIdx.x, cc = tid & 31, kq = tid >> 5;
     const int c0 = blockIdx.x * 32;
+    const int rows_per = ((dv + gridDim.y - 1) / gridDim.y + 31) / 32 * 32;
+    const int rb = blockIdx.y * rows_per, re = min(dv, rb + rows_per);
+    c += (int64_t)blockIdx.y * pstride;
     T acc[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = LevelOps<T>::zero();
-    for (int r0 = 0; r0 < dv; r0 += 32) {
+    for (int r0 = rb; r0 < re; r0 += 32) {
         for (int e = tid; e < 32 * NBQ; e += 256) {
             const int rr = e & 31, k = e >> 5;
-            xs[rr][k] = (r0 + rr < dv && k < nbp) ? x[(int64_t)k * ldx + r0 + rr] : LevelOps<T>::zero();
+            xs[rr][k] = (r0 + rr < re && k < nbp) ? x[(int64_t)k * ldx + r0 + rr] : LevelOps<T>::zero();
         }
         for (int e = tid; e < 32 * 32; e += 256) {
             const int rr = e & 31, j = e >> 5;
-            ys[rr][j] = (r0 + rr < dv && c0 + j < nc) ? y[(int64_t)(c0 + j) * ldy + r0 + rr] : LevelOps<T>::zero();
+            ys[rr][j] = (r0 + rr < re && c0 + j < nc) ? y[(int64_t)(c0 + j) * ldy + r0 + rr] : LevelOps<T>::zero();
         }
         __syncthreads();
 #pragma unroll 8
@@ -608,6 +804,15 @@ __global__ void __launch_bounds__(256) qrb_gemm_tn(const T *x, int64_t ldx, cons
 #pragma unroll
         for (int i = 0; i < 8; ++i)
             if (kq * 8 + i < nbp) c[(int64_t)(c0 + cc) * ldc + kq * 8 + i] = acc[i];
+}
+
+template <typename T>
+__global__ void qrb_reduce(const T *part, int64_t pstride, int nsplit, int64_t count, T *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        T s = part[i];
+        for (int z = 1; z < nsplit; ++z) s = s + part[(int64_t)z * pstride + i];
+        out[i] = s;
+    }
 }
 
 // xLARFT (forward, columnwise): T upper nbp x nbp (column-major, ld NBQ) from V^T V and tau
@@ -771,11 +976,10 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
     // binary32 / binary64 with more than one panel: blocked WY (SK_QR_BLOCKED=0: the
     // column-at-a-time dataflow kernel over the whole matrix)
     static const char *blk_env = getenv("SK_QR_BLOCKED");
-    // measured at 6144 x 2048 with the dataflow panel kernel: binary64 75.2 -> 66.3 ms,
-    // binary32 42.3 -> 46.8 ms (the partly shared-memory resident whole-matrix kernel
-    // wins there); SK_QR_BLOCKED=1 forces it for binary32 too
-    const bool want_blocked = std::is_same<T, double>::value ? !(blk_env && blk_env[0] == '0')
-                                                             : (blk_env && blk_env[0] == '1');
+    // (with the dataflow kernel as the panel factorisation it measured binary64 75.2 ->
+    // 66.3 ms, binary32 42.3 -> 46.8 ms at 6144 x 2048; the cluster panel kernel is the
+    // default panel path, SK_QR_PANEL=flow the dataflow one)
+    const bool want_blocked = !(blk_env && blk_env[0] == '0');
     const bool blocked = !HALF && flow && n > NBQ && d <= BLOCKED_MAX_D && want_blocked;
     if (!blocked) {
         const int rc0 = launch_view(w, (int)d, (int)n, alphas, taus, v0s);
@@ -791,31 +995,207 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
         T *gm = reinterpret_cast<T *>(q);
         q += align_up((size_t)NBQ * n * sizeof(T), 256);
         T *wm = reinterpret_cast<T *>(q);
-        for (int64_t j0 = 0; j0 < n; j0 += NBQ) {
-            const int nbp = (int)std::min<int64_t>(NBQ, n - j0), dv = (int)(d - j0);
-            T *wp = w + j0 * d + j0;
-            const int rc0 = launch_view(wp, dv, nbp, alphas + j0, taus + j0, v0s + j0);
-            if (rc0 != SK_OK) return rc0;
-            int fl[2];
-            SK_CUDA(cudaMemcpyAsync(fl, &ctl->fail_code, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-            SK_CUDA(cudaStreamSynchronize(st));
-            if (fl[0] != SK_OK) {
-                set_error("reflector %lld collapsed at working precision", (long long)(fl[1] + j0));
-                return fill_status(status, fl[0], (int)(fl[1] + j0), 0.0, 0.0);
+        q += align_up((size_t)NBQ * n * sizeof(T), 256);
+        T *pm = reinterpret_cast<T *>(q);   // split partials
+        const int sms_ = sm_count();
+        // C (nbp x nc) = V^T Y over dv rows, split in row slabs so ~2 CTAs per SM work
+        auto gemm_tn = [&](const T *yv, int64_t ldy, int dv_, int nbp_, int nc_, T *cout) {
+            const int ncb = (nc_ + 31) / 32;
+            const int ns = std::max(1, std::min(QRB_SPLIT_MAX, (2 * sms_ + ncb - 1) / ncb));
+            const int64_t ps = (int64_t)nbp_ * nc_;
+            qrb_gemm_tn<T><<<dim3((unsigned)ncb, (unsigned)ns), 256, 0, st>>>(vb, dv_, yv, ldy, dv_, nbp_, nc_, pm,
+                                                                              nbp_, ps);
+            qrb_reduce<T><<<(unsigned)std::min<int64_t>((ps + 255) / 256, 2048), 256, 0, st>>>(pm, ps, ns, ps, cout);
+        };
+        // panel width: 64 (binary32) / 32 (binary64) columns so that the panel fits the
+        // shared memory of one 8-CTA cluster (slab x width x sizeof(T) <= 200 KB)
+        constexpr int NBW = std::is_same<T, double>::value ? 32 : 64;
+        static const char *pc_env = getenv("SK_QR_PANEL");   // "flow": dataflow-kernel panels
+        const bool cluster_ok = !(pc_env && pc_env[0] == 'f');
+        static const bool qprof = getenv("SK_QR_PROF") != nullptr;   // panel / trailing split to stderr
+        cudaEvent_t qe[3] = {nullptr, nullptr, nullptr};
+        float t_panel = 0.f, t_trail = 0.f;
+        if (qprof)
+            for (auto &e : qe) cudaEventCreate(&e);
+        // ---- lookahead pipeline (every panel on the cluster kernel): the main stream
+        //      factors panel p+1 (after applying H_p to its columns) while a side stream
+        //      applies H_p to the columns beyond it
+        static const char *la_env = getenv("SK_QR_LOOKAHEAD");
+        const int slab0 = (int)((d + QPC_CL - 1) / QPC_CL);
+        const bool lookahead = cluster_ok && !qprof && !(la_env && la_env[0] == '0') &&
+                               (size_t)slab0 * NBW * sizeof(T) <= 200 * 1024;
+        if (lookahead) {
+            // second buffer set right after the first (blocked_ws_bytes reserves both)
+            unsigned char *q2 = reinterpret_cast<unsigned char *>(pm) +
+                                align_up((size_t)QRB_SPLIT_MAX * NBQ * std::max<int64_t>(n, NBQ) * sizeof(T), 256);
+            T *vb2 = reinterpret_cast<T *>(q2);
+            q2 += align_up((size_t)d * NBQ * sizeof(T), 256);
+            q2 += align_up((size_t)NBQ * NBQ * sizeof(T), 256);     // (second V^T V staging: unused)
+            T *tm2 = reinterpret_cast<T *>(q2);
+            q2 += align_up((size_t)NBQ * NBQ * sizeof(T), 256);
+            T *gm2 = reinterpret_cast<T *>(q2);
+            q2 += align_up((size_t)NBQ * n * sizeof(T), 256);
+            T *wm2 = reinterpret_cast<T *>(q2);
+            q2 += align_up((size_t)NBQ * n * sizeof(T), 256);
+            T *pm2 = reinterpret_cast<T *>(q2);
+            T *vbs[2] = {vb, vb2}, *tms[2] = {tm, tm2};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            static cudaStream_t side[64] = {};
+            if (!side[dev]) SK_CUDA(cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking));
+            cudaStream_t us = side[dev];
+            const int np = (int)((n + NBW - 1) / NBW);
+            std::vector<cudaEvent_t> ev_t(np), ev_u(np);
+            for (int i = 0; i < np; ++i) {
+                SK_CUDA(cudaEventCreateWithFlags(&ev_t[i], cudaEventDisableTiming));
+                SK_CUDA(cudaEventCreateWithFlags(&ev_u[i], cudaEventDisableTiming));
             }
+            SK_CUDA(cudaEventRecord(ev_u[0], st));     // placeholder order point for the side stream
+            SK_CUDA(cudaStreamWaitEvent(us, ev_u[0], 0));
+            // apply H (V: dvh x nbh at vbuf, T at tmat) to the dvh x nc block at a (ld d) on stream s
+            auto apply = [&](cudaStream_t s, const T *vbuf, const T *tmat, int dvh, int nbh, T *a, int nc, T *g, T *w_,
+                             T *pp) {
+                const int ncb = (nc + 31) / 32;
+                const int ns = std::max(1, std::min(QRB_SPLIT_MAX, (2 * sms_ + ncb - 1) / ncb));
+                const int64_t ps = (int64_t)nbh * nc;
+                qrb_gemm_tn<T><<<dim3((unsigned)ncb, (unsigned)ns), 256, 0, s>>>(vbuf, dvh, a, d, dvh, nbh, nc, pp, nbh,
+                                                                                 ps);
+                qrb_reduce<T><<<(unsigned)std::min<int64_t>((ps + 255) / 256, 2048), 256, 0, s>>>(pp, ps, ns, ps, g);
+                qrb_tmul<T><<<(unsigned)std::min<int64_t>((ps + 255) / 256, 4096), 256, 0, s>>>(tmat, g, nbh, nc, w_);
+                qrb_update<T><<<dim3((unsigned)((dvh + 31) / 32), (unsigned)ncb), 256, 0, s>>>(a, d, vbuf, dvh, nbh, w_,
+                                                                                              nc);
+            };
+            for (int pi = 0; pi < np; ++pi) {
+                const int64_t j0 = (int64_t)pi * NBW;
+                const int nbp = (int)std::min<int64_t>(NBW, n - j0), dv = (int)(d - j0);
+                T *wp = w + j0 * d + j0;
+                if (pi >= 1) {
+                    // H_{p-1} to this panel's columns, after the side stream applied H_{p-2} to them
+                    if (pi >= 2) SK_CUDA(cudaStreamWaitEvent(st, ev_u[pi - 2], 0));
+                    const int64_t jp = j0 - NBW;
+                    apply(st, vbs[(pi - 1) & 1], tms[(pi - 1) & 1], (int)(d - jp), NBW, w + j0 * d + jp, nbp, gm, wm, pm);
+                }
+                const int slab = (dv + QPC_CL - 1) / QPC_CL;
+                const size_t psmem = std::max((size_t)slab * NBW, (size_t)2 * NBW * (NBW + 1)) * sizeof(T);
+                auto pfn = qrb_panel_cluster<T, NBW>;
+                SK_CUDA(cudaFuncSetAttribute((const void *)pfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(QPC_CL);
+                cfg.blockDim = dim3(QPC_THREADS);
+                cfg.dynamicSmemBytes = psmem;
+                cfg.stream = st;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = QPC_CL;
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                int64_t ldw = d;
+                int c0i = (int)j0;
+                const bool more = j0 + nbp < n;
+                T *tmo = more ? tms[pi & 1] : nullptr;
+                SK_CUDA(cudaLaunchKernelEx(&cfg, pfn, wp, ldw, dv, nbp, slab, alphas + j0, taus + j0, v0s + j0, ctl, c0i,
+                                           tmo, vtv));
+                SK_LAUNCH_CHECK("qrb_panel_cluster");
+                if (!more) break;
+                qrb_make_v<T><<<(unsigned)std::min<int64_t>(((int64_t)dv * nbp + 255) / 256, 4096), 256, 0, st>>>(
+                    wp, d, dv, nbp, v0s + j0, vbs[pi & 1]);
+                SK_CUDA(cudaEventRecord(ev_t[pi], st));
+                // side stream: H_p to the columns beyond the next panel
+                const int64_t cbeg = j0 + nbp + NBW;
+                if (cbeg < n) {
+                    SK_CUDA(cudaStreamWaitEvent(us, ev_t[pi], 0));
+                    apply(us, vbs[pi & 1], tms[pi & 1], dv, nbp, w + cbeg * d + j0, (int)(n - cbeg), gm2, wm2, pm2);
+                }
+                SK_CUDA(cudaEventRecord(ev_u[pi], us));
+            }
+            SK_LAUNCH_CHECK("blocked QR lookahead");
+            // join: the main stream waits for the side stream's last update
+            cudaEvent_t done_ev;
+            SK_CUDA(cudaEventCreateWithFlags(&done_ev, cudaEventDisableTiming));
+            SK_CUDA(cudaEventRecord(done_ev, us));
+            SK_CUDA(cudaStreamWaitEvent(st, done_ev, 0));
+            SK_CUDA(cudaEventDestroy(done_ev));
+            for (int i = 0; i < np; ++i) {
+                cudaEventDestroy(ev_t[i]);
+                cudaEventDestroy(ev_u[i]);
+            }
+        }
+        bool have_t = false;
+        for (int64_t j0 = 0; j0 < (lookahead ? 0 : n); j0 += NBW) {
+            if (qprof) cudaEventRecord(qe[0], st);
+            const int nbp = (int)std::min<int64_t>(NBW, n - j0), dv = (int)(d - j0);
+            T *wp = w + j0 * d + j0;
+            const int slab = (dv + QPC_CL - 1) / QPC_CL;
+            // the slab, and afterwards rank 0's S and T staging (2 x NBW x (NBW + 1))
+            const size_t psmem = std::max((size_t)slab * NBW, (size_t)2 * NBW * (NBW + 1)) * sizeof(T);
+            if (cluster_ok && psmem <= 200 * 1024) {
+                auto pfn = qrb_panel_cluster<T, NBW>;
+                SK_CUDA(cudaFuncSetAttribute((const void *)pfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(QPC_CL);
+                cfg.blockDim = dim3(QPC_THREADS);
+                cfg.dynamicSmemBytes = psmem;
+                cfg.stream = st;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = QPC_CL;
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                int64_t ldw = d;
+                int c0i = (int)j0;
+                T *tmo = (j0 + nbp < n) ? tm : nullptr;   // T of the compact WY form, when a trailing update follows
+                SK_CUDA(cudaLaunchKernelEx(&cfg, pfn, wp, ldw, dv, nbp, slab, alphas + j0, taus + j0, v0s + j0, ctl, c0i,
+                                           tmo, vtv));
+                have_t = true;
+                SK_LAUNCH_CHECK("qrb_panel_cluster");
+                // a collapse is recorded with its global column and checked once at the end
+                // (the later panels then work on garbage that is never returned)
+            } else {
+                have_t = false;
+                const int rc0 = launch_view(wp, dv, nbp, alphas + j0, taus + j0, v0s + j0);
+                if (rc0 != SK_OK) return rc0;
+                int fl[2];
+                SK_CUDA(cudaMemcpyAsync(fl, &ctl->fail_code, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+                SK_CUDA(cudaStreamSynchronize(st));
+                if (fl[0] != SK_OK) {
+                    set_error("reflector %lld collapsed at working precision", (long long)(fl[1] + j0));
+                    return fill_status(status, fl[0], (int)(fl[1] + j0), 0.0, 0.0);
+                }
+            }
+            if (qprof) cudaEventRecord(qe[1], st);
             const int nc = (int)(n - j0 - nbp);
             if (nc <= 0) break;
             T *at = wp + (int64_t)nbp * d;   // trailing columns, rows j0..
             qrb_make_v<T><<<(unsigned)std::min<int64_t>(((int64_t)dv * nbp + 255) / 256, 4096), 256, 0, st>>>(
                 wp, d, dv, nbp, v0s + j0, vb);
-            qrb_gemm_tn<T><<<(unsigned)((nbp + 31) / 32), 256, 0, st>>>(vb, dv, vb, dv, dv, nbp, nbp, vtv, nbp);
-            qrb_larft<T><<<1, NBQ, 0, st>>>(vtv, taus + j0, nbp, tm);
-            qrb_gemm_tn<T><<<(unsigned)((nc + 31) / 32), 256, 0, st>>>(vb, dv, at, d, dv, nbp, nc, gm, nbp);
+            if (!have_t) {   // the cluster kernel forms T itself
+                gemm_tn(vb, dv, dv, nbp, nbp, vtv);
+                qrb_larft<T><<<1, NBQ, 0, st>>>(vtv, taus + j0, nbp, tm);
+            }
+            gemm_tn(at, d, dv, nbp, nc, gm);
             qrb_tmul<T><<<(unsigned)std::min<int64_t>(((int64_t)nbp * nc + 255) / 256, 4096), 256, 0, st>>>(
                 tm, gm, nbp, nc, wm);
             qrb_update<T><<<dim3((unsigned)((dv + 31) / 32), (unsigned)((nc + 31) / 32)), 256, 0, st>>>(at, d, vb, dv,
                                                                                                    nbp, wm, nc);
             SK_LAUNCH_CHECK("blocked QR trailing update");
+            if (qprof) {
+                cudaEventRecord(qe[2], st);
+                cudaEventSynchronize(qe[2]);
+                float a_ = 0.f, b_ = 0.f;
+                cudaEventElapsedTime(&a_, qe[0], qe[1]);
+                cudaEventElapsedTime(&b_, qe[1], qe[2]);
+                t_panel += a_;
+                t_trail += b_;
+            }
+        }
+        if (qprof) {
+            fprintf(stderr, "blocked qr d=%lld n=%lld T=%d: panels %.2f ms, trailing %.2f ms\n", (long long)d, (long long)n,
+                    (int)sizeof(T), t_panel, t_trail);
+            for (auto &e : qe) cudaEventDestroy(e);
         }
     }
     int fail[2];
