@@ -1011,7 +1011,31 @@ int run(T *w, int64_t d, int64_t n, double scale, double *r, int64_t ldr, sk_sta
         // shared memory of one 8-CTA cluster (slab x width x sizeof(T) <= 200 KB)
         constexpr int NBW = std::is_same<T, double>::value ? 32 : 64;
         static const char *pc_env = getenv("SK_QR_PANEL");   // "flow": dataflow-kernel panels
-        const bool cluster_ok = !(pc_env && pc_env[0] == 'f');
+        // the cluster panel kernel needs 8 co-scheduled CTAs with ~200 KB of shared memory
+        // each (one GPC); where that cannot be scheduled the dataflow panels are used
+        bool cluster_ok = !(pc_env && pc_env[0] == 'f');
+        if (cluster_ok) {
+            auto pfn0 = qrb_panel_cluster<T, std::is_same<T, double>::value ? 32 : 64>;
+            const size_t sm0 = 200 * 1024;   // the largest panel the per-panel check admits
+            int nclusters = 0;
+            cudaLaunchConfig_t qc = {};
+            qc.gridDim = dim3(QPC_CL);
+            qc.blockDim = dim3(QPC_THREADS);
+            qc.dynamicSmemBytes = sm0;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = QPC_CL;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            qc.attrs = qa;
+            qc.numAttrs = 1;
+            if (cudaFuncSetAttribute((const void *)pfn0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm0) !=
+                    cudaSuccess ||
+                cudaOccupancyMaxActiveClusters(&nclusters, (const void *)pfn0, &qc) != cudaSuccess || nclusters < 1) {
+                cluster_ok = false;
+                cudaGetLastError();
+            }
+        }
         static const bool qprof = getenv("SK_QR_PROF") != nullptr;   // panel / trailing split to stderr
         cudaEvent_t qe[3] = {nullptr, nullptr, nullptr};
         float t_panel = 0.f, t_trail = 0.f;
