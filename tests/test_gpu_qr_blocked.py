@@ -20,9 +20,15 @@ def sq():
     return mod
 
 
-@pytest.fixture(autouse=True)
-def blocked_everywhere(monkeypatch):
-    monkeypatch.setenv("SK_QR_BLOCKED", "1")     # binary32 too (its default is the whole-matrix kernel)
+@pytest.fixture(autouse=True, params=["cluster+lookahead", "cluster", "flow-panels"])
+def blocked_everywhere(request, monkeypatch):
+    """every panel path: cluster panels with the side-stream lookahead (default), cluster
+    panels in order (SK_QR_LOOKAHEAD=0), dataflow-kernel panels (SK_QR_PANEL=flow)"""
+    monkeypatch.setenv("SK_QR_BLOCKED", "1")
+    if request.param == "cluster":
+        monkeypatch.setenv("SK_QR_LOOKAHEAD", "0")
+    elif request.param == "flow-panels":
+        monkeypatch.setenv("SK_QR_PANEL", "flow")
 
 
 @pytest.mark.parametrize("level", ["binary32", "binary64"])
