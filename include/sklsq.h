@@ -95,6 +95,40 @@ int sk_residual(const double *a, int64_t rows, int64_t cols, int64_t lda, const 
                 const double *b, double *r, double *out_host, void *ws, size_t ws_bytes,
                 sk_stream_t stream);
 
+/* Stream-ordered sk_residual: out_dev[0] = ||A x - b||^2, out_dev[1] = ||x||^2 (device
+ * doubles), no host synchronisation (the deferred-verdict / CUDA-graph solve path). */
+int sk_residual_async(const double *a, int64_t rows, int64_t cols, int64_t lda, const double *x,
+                      const double *b, double *r, double *out_dev, void *ws, size_t ws_bytes,
+                      sk_stream_t stream);
+
+/* ---- deferred numerical verdicts (CUDA-graph capture of a whole solve) ----
+ * sk_defer_verdicts(status_dev) installs a DEVICE sk_status record (caller-zeroed) on
+ * the calling host thread; NULL removes it.  While installed, the entry points that
+ * return a numerical verdict on a device-resident path (sk_qr_r, sk_trsm_right_upper_f64,
+ * sk_lu_solve_f64, sk_chol_solve_f64, sk_trsv_f64) do not synchronise: they enqueue a
+ * check that stores the verdict (code, index, value, aux as in sk_status) into the
+ * record and return SK_OK.  The first failure in stream order wins, so one read of the
+ * record after the solve raises what the eager calls would have raised first.  Kernels
+ * with data-dependent control flow (LU, Cholesky) run on the identity once a failure is
+ * recorded (their outputs are then meaningless; the record says so).  Entry points whose
+ * result is a host value (sk_cast_stats, sk_residual, sk_kappa0_*, sk_jacobi_sv_f64,
+ * sk_level_overflow, the INT8 Ozaki engines, the FFT sketch planner, ...) return
+ * SK_ERR_ARG while verdicts are deferred.  Replaces the host-side exception points of
+ * src/solvers.py:168-252 (raise sites kept in order). */
+int sk_defer_verdicts(sk_status *status_dev);
+/* *flag_dev != 0 -> record `code` (e.g. the sketch's overflow flag -> SK_OVERFLOW). */
+int sk_note_flag(const int *flag_dev, int code, sk_stream_t stream);
+/* *x_dev > 0 -> record `code` (e.g. sk_cast_stats_async's non-finite count -> SK_NON_FINITE). */
+int sk_note_positive(const double *x_dev, int code, sk_stream_t stream);
+/* first exactly-zero diagonal entry of the row-major n x n R -> `code` with its index
+ * (src/solvers.py:197-199's RankDeficient on the sketched factor). */
+int sk_note_zero_diagonal(const double *r, int64_t ldr, int64_t n, int code, sk_stream_t stream);
+/* if a failure is recorded: overwrite the rows x cols matrix (2/4/8-byte elements, ld
+ * elements, col_major 0/1) with the identity, so later data-dependent kernels see a
+ * well-conditioned operand. */
+int sk_guard_identity(int elem_bytes, void *a, int64_t rows, int64_t cols, int64_t ld, int col_major,
+                      sk_stream_t stream);
+
 /* ---- FP64 tensor-pipe (DMMA) products ------------------------------------ */
 /* G (n x n, row-major, ldg) = X^T Y with X (m x n, ldx), Y (m x n, ldy).
  * If Y == X the SYRK path runs (lower tiles + exact mirror; numpy's a.T @ a is

@@ -45,6 +45,12 @@ SIGNATURES = {
     "sk_cast_stats_async": (_i32, [_p, _i32, _i64, _i64, _i64, _p, _i64, _p, _p, _sz, _p]),
     "sk_level_overflow": (_i32, [_p, _i64, _i64, _i64, _i32, _pi, _p, _sz, _p]),
     "sk_residual": (_i32, [_p, _i64, _i64, _i64, _p, _p, _p, _pd, _p, _sz, _p]),
+    "sk_residual_async": (_i32, [_p, _i64, _i64, _i64, _p, _p, _p, _p, _p, _sz, _p]),
+    "sk_defer_verdicts": (_i32, [_p]),
+    "sk_note_flag": (_i32, [_p, _i32, _p]),
+    "sk_note_positive": (_i32, [_p, _i32, _p]),
+    "sk_note_zero_diagonal": (_i32, [_p, _i64, _i64, _i32, _p]),
+    "sk_guard_identity": (_i32, [_i32, _p, _i64, _i64, _i64, _i32, _p]),
     "sk_gram_workspace": (_sz, [_i64, _i64]),
     "sk_gram_f64": (_i32, [_p, _i64, _p, _i64, _i64, _i64, _p, _i64, _i32, _p, _sz, _p]),
     "sk_gram_ozaki_workspace": (_sz, [_i64, _i64, _i32]),

@@ -86,6 +86,7 @@ size_t sk_kappa0_workspace(int64_t m, int64_t n) {
 
 int sk_kappa0_f64(const double *a, int64_t lda, int64_t m, int64_t n, double *kappa0_host, int *overflowed_host,
                   void *ws, size_t ws_bytes, sk_stream_t stream) {
+    SK_NO_DEFER("sk_kappa0_f64");
     if (!ws || ws_bytes < sk_kappa0_workspace(m, n)) {
         set_error("sk_kappa0_f64: workspace too small");
         return SK_ERR_ARG;
@@ -107,11 +108,13 @@ int sk_sketch(int level, int transform, const double *a, int64_t lda, int64_t m_
 
 int sk_demote_check(const double *a, int64_t rows, int64_t cols, int64_t lda, int level, int *overflowed_host,
                     void *ws, size_t ws_bytes, sk_stream_t stream) {
+    SK_NO_DEFER("sk_demote_check");
     return sk_level_overflow(a, rows, cols, lda, level, overflowed_host, ws, ws_bytes, stream);
 }
 
 int sk_residual_norms(const double *a, int64_t rows, int64_t cols, int64_t lda, const double *x, const double *b,
                       double *r, double *out_host, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    SK_NO_DEFER("sk_residual_norms");
     return sk_residual(a, rows, cols, lda, x, b, r, out_host, ws, ws_bytes, stream);
 }
 

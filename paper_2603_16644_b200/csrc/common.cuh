@@ -50,6 +50,33 @@ struct DevStatus {
     double aux;
 };
 
+// ------------------------------------------------------ deferred verdicts --
+// sk_defer_verdicts (include/sklsq.h): while a device status record is installed on
+// the calling host thread, the entry points that would synchronise to read a
+// numerical verdict enqueue note_verdict instead and return SK_OK (CUDA-graph capture
+// of a whole solve).  The first failure in stream order wins.
+DevStatus *deferred_status();
+// if *code != 0 (or, with want_code > 0, if *code != 0 then want_code): record it, with
+// the optional index / value / aux read from the device
+int note_verdict(const int *code, int want_code, const int *index, const double *value, const double *aux,
+                 cudaStream_t st);
+// entry points whose result is a host value: refused while verdicts are deferred
+#define SK_NO_DEFER(name)                                                                      \
+    do {                                                                                       \
+        if (::sk::deferred_status()) {                                                         \
+            ::sk::set_error("%s returns a host value: not available under sk_defer_verdicts", name); \
+            return SK_ERR_ARG;                                                                 \
+        }                                                                                      \
+    } while (0)
+// first exactly-zero diagonal entry of the row-major n x n R -> `code` with its index
+int note_zero_diagonal(const double *r, int64_t ldr, int64_t n, int code, cudaStream_t st);
+// if status->code != 0: overwrite the rows x cols matrix (elements of `elem_bytes`
+// bytes, 2 = binary16, 4 = binary32, 8 = binary64; ld elements; col_major or row-major)
+// with the identity, so the data-dependent kernels after a recorded failure see a
+// well-conditioned operand instead of garbage (their results are never returned)
+int guard_identity(void *a, int elem_bytes, int64_t rows, int64_t cols, int64_t ld, bool col_major,
+                   cudaStream_t st);
+
 // ------------------------------------------------------------ DMMA (FP64) --
 // mma.sync m8n8k4 f64: A 8x4 (row), B 4x8 (col), C/D 8x8.  Lowers to DMMA.8x8x4
 // on sm_100a (tcgen05 has no f64 kind).  Fragment ownership, lane = 4*g + t:

@@ -50,6 +50,17 @@ __global__ void sym_stats(const double *a, int n, double *out) {
         atomicAdd(out + 2, nf);
     }
 }
+// deferred verdicts: the host gates of the LU / Cholesky solves on the device.
+// lu != nullptr: non-finite -> SK_NON_FINITE, pivot threshold n eps max|a| into the LU
+// control; else the Cholesky gates (non-finite, asymmetry > 10 eps max|s|)
+__global__ void nxn_gate(const double *stats, int n, void *lu_ctl, DevStatus *ds) {
+    const double mx = stats[0], dev = stats[1], nf = stats[2];
+    int code = 0;
+    if (nf > 0) code = SK_NON_FINITE;
+    else if (!lu_ctl && dev > 10.0 * 2.220446049250313e-16 * mx) code = SK_NOT_SYMMETRIC;
+    if (lu_ctl) reinterpret_cast<double *>(lu_ctl)[2] = (double)n * 2.220446049250313e-16 * mx;   // LuCtl::thresh
+    if (code && ds->code == 0) { ds->code = code; ds->index = -1; ds->value = dev; ds->aux = mx; }
+}
 __global__ void trace_kernel(const double *a, int n, double *out) {
     double s = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) s += a[(int64_t)i * n + i];
@@ -793,6 +804,79 @@ lu_smem_kernel(double *w, int n, double *gl, int *piv, int *flags, double *lout,
     }
 }
 
+// Small n (n x n doubles fit one CTA's shared memory): the whole LU in ONE CTA, every
+// step's element updates spread over all threads instead of one column per CTA.  The
+// arithmetic is lu_smem_kernel's op for op (first-maximum pivot, __ddiv_rn multipliers,
+// a - l * u rounded twice, whole-row swaps), so the factors are bitwise the same; what
+// goes away is the inter-CTA flag chain (config 1, n = 100: ~3.8 us per step).
+constexpr int LU_SMALL_MAX = 160;
+__global__ void __launch_bounds__(1024, 1)
+lu_small_kernel(double *w, int n, int *piv, int *perm, double *lout, LuCtl *ctl) {
+    extern __shared__ double W[];                 // column-major n x n
+    __shared__ double s_pv;
+    __shared__ int s_p, s_piv[LU_SMALL_MAX], s_perm[LU_SMALL_MAX];
+    const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31;
+    const double thresh = ctl->thresh;
+    for (int64_t e = tid; e < (int64_t)n * n; e += T) W[e] = w[e];
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+        double *ck = W + (int64_t)k * n;
+        if (tid < 32) {   // pivot: first maximum of |A[k:, k]|
+            double bv = -1.0;
+            int bi = INT32_MAX;
+            for (int i = k + lane; i < n; i += 32) better(bv, bi, fabs(ck[i]), i);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                better(bv, bi, ov, oi);
+            }
+            if (lane == 0) { s_pv = bv; s_p = bi; }
+        }
+        __syncthreads();
+        const double pv = s_pv;
+        const int p = s_p;
+        if (pv < thresh || pv == 0.0 || !(pv == pv)) {   // uniform
+            if (tid == 0) { ctl->fail_code = SK_NUMERICALLY_SINGULAR; ctl->fail_col = k; ctl->fail_value = pv; }
+            for (int i = tid; i < n; i += T) perm[i] = i;   // a valid permutation for deferred callers
+            return;
+        }
+        if (p != k && p < n)   // swap rows k and p in every column
+            for (int j = tid; j < n; j += T) {
+                double *cj = W + (int64_t)j * n;
+                const double t = cj[k];
+                cj[k] = cj[p];
+                cj[p] = t;
+            }
+        if (tid == 0) { piv[k] = p; s_piv[k] = p; }
+        __syncthreads();
+        const double akk = ck[k];
+        for (int i = k + 1 + tid; i < n; i += T) ck[i] = __ddiv_rn(ck[i], akk);
+        __syncthreads();
+        for (int j = k + 1 + (tid >> 5); j < n; j += T >> 5) {   // trailing block: a warp per column
+            double *cj = W + (int64_t)j * n;
+            const double u = cj[k];
+            for (int i = k + 1 + lane; i < n; i += 32) cj[i] = __dsub_rn(cj[i], __dmul_rn(ck[i], u));
+        }
+        __syncthreads();
+    }
+    for (int i = tid; i < n; i += T) s_perm[i] = i;
+    __syncthreads();
+    if (tid == 0)   // perm = the row swaps (k, piv[k]) applied in order to the identity
+        for (int k = 0; k < n; ++k) {
+            const int p = s_piv[k];
+            if (p != k) { const int t = s_perm[k]; s_perm[k] = s_perm[p]; s_perm[p] = t; }
+        }
+    __syncthreads();
+    for (int i = tid; i < n; i += T) perm[i] = s_perm[i];
+    for (int c = tid >> 5; c < n; c += T >> 5)
+        for (int i = tid & 31; i < n; i += 32) {
+            const double v = W[(int64_t)c * n + i];
+            w[(int64_t)c * n + i] = v;
+            lout[(int64_t)c * n + i] = i > c ? v : 0.0;
+        }
+}
+
 // perm = the row swaps (k, pivots[k]) applied in order to the identity (one thread)
 __global__ void perm_from_pivots(const int *pivots, int n, int *perm) {
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
@@ -1033,6 +1117,11 @@ static int chol_factor(const double *s, int n, Ws &ws, sk_status *status, cudaSt
     SK_CUDA(cudaMemsetAsync(ws.l, 0, (size_t)n * n * sizeof(double), st));
     symmetrize<<<(unsigned)std::min<int64_t>(((int64_t)n * n + 255) / 256, 4096), 256, 0, st>>>(s, n, ws.w);
     SK_LAUNCH_CHECK("symmetrize");
+    DevStatus *defer = deferred_status();
+    if (defer) {   // after an earlier recorded failure the factorisation runs on the identity
+        int rc = guard_identity(ws.w, 8, n, n, n, true, st);
+        if (rc) return rc;
+    }
     // blocked: one CTA per SM (3 grid barriers per 32-column panel)
     const int blocks = coop_blocks((const void *)chol_blocked_kernel, THREADS, 0,
                                    std::min<int64_t>(sm_count(), ((int64_t)n * n / 2 + 1023) / 1024 + 1));
@@ -1044,6 +1133,7 @@ static int chol_factor(const double *s, int n, Ws &ws, sk_status *status, cudaSt
     SK_LAUNCH_CHECK("chol_blocked_kernel");
     lower_to_l<<<(unsigned)std::min<int64_t>(((int64_t)n * n + 255) / 256, 4096), 256, 0, st>>>(ws.w, n, ws.l);
     SK_LAUNCH_CHECK("lower_to_l");
+    if (defer) return note_verdict(&ctl->fail_code, 0, &ctl->fail_col, &ctl->fail_value, nullptr, st);
     FactorCtl h;
     SK_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(h), cudaMemcpyDeviceToHost, st));
     SK_CUDA(cudaStreamSynchronize(st));
@@ -1077,13 +1167,18 @@ int sk_chol_solve_f64(const double *s, int64_t n, const double *rhs, double *x, 
     SK_CUDA(cudaMemsetAsync(ws.stats, 0, 4 * sizeof(double), st));
     sym_stats<<<(unsigned)std::min<int64_t>((n * n + 255) / 256, 1024), 256, 0, st>>>(s, (int)n, ws.stats);
     SK_LAUNCH_CHECK("sym_stats");
-    double h[4];
-    SK_CUDA(cudaMemcpyAsync(h, ws.stats, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
-    SK_CUDA(cudaStreamSynchronize(st));
-    if (h[2] > 0) { set_error("s contains non-finite entries"); return fill_status(status, SK_NON_FINITE, -1, 0, 0); }
-    if (h[1] > 10.0 * 2.220446049250313e-16 * h[0]) {
-        set_error("s is not symmetric within 10*eps relative tolerance");
-        return fill_status(status, SK_NOT_SYMMETRIC, -1, h[1], h[0]);
+    if (DevStatus *defer = deferred_status()) {
+        nxn_gate<<<1, 1, 0, st>>>(ws.stats, (int)n, nullptr, defer);
+        SK_LAUNCH_CHECK("nxn_gate");
+    } else {
+        double h[4];
+        SK_CUDA(cudaMemcpyAsync(h, ws.stats, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        SK_CUDA(cudaStreamSynchronize(st));
+        if (h[2] > 0) { set_error("s contains non-finite entries"); return fill_status(status, SK_NON_FINITE, -1, 0, 0); }
+        if (h[1] > 10.0 * 2.220446049250313e-16 * h[0]) {
+            set_error("s is not symmetric within 10*eps relative tolerance");
+            return fill_status(status, SK_NOT_SYMMETRIC, -1, h[1], h[0]);
+        }
     }
     int rc = chol_factor(s, (int)n, ws, status, st);
     if (rc != SK_OK) return rc;
@@ -1097,6 +1192,7 @@ int sk_chol_solve_f64(const double *s, int64_t n, const double *rhs, double *x, 
 }
 
 int sk_gram_check(const double *g, int64_t n, double *out_host, void *wsp, size_t ws_bytes, sk_stream_t stream) {
+    SK_NO_DEFER("sk_gram_check");
     if (!g || !out_host || n <= 0 || !wsp || ws_bytes < 64) {
         set_error("sk_gram_check: bad arguments");
         return SK_ERR_ARG;
@@ -1118,6 +1214,7 @@ int sk_gram_check(const double *g, int64_t n, double *out_host, void *wsp, size_
 
 int sk_chol_factor_f64(const double *s, int64_t n, double *r, sk_status *status, void *wsp, size_t ws_bytes,
                        sk_stream_t stream) {
+    SK_NO_DEFER("sk_chol_factor_f64");
     if (!s || !r || n <= 0 || n > 65536 || !wsp || ws_bytes < sk_nxn_workspace(n)) {
         set_error("sk_chol_factor_f64: bad arguments");
         return SK_ERR_ARG;
@@ -1144,17 +1241,28 @@ int sk_lu_solve_f64(const double *g, int64_t n, const double *rhs, double *x, sk
     SK_CUDA(cudaMemsetAsync(ws.stats, 0, 4 * sizeof(double), st));
     sym_stats<<<(unsigned)std::min<int64_t>((n * n + 255) / 256, 1024), 256, 0, st>>>(g, (int)n, ws.stats);
     SK_LAUNCH_CHECK("sym_stats");
-    double h[4];
-    SK_CUDA(cudaMemcpyAsync(h, ws.stats, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
-    SK_CUDA(cudaStreamSynchronize(st));
-    if (h[2] > 0) { set_error("a contains non-finite entries"); return fill_status(status, SK_NON_FINITE, -1, 0, 0); }
-    LuCtl c{};
-    c.thresh = (double)n * 2.220446049250313e-16 * h[0];   // n * eps * max|a|
     LuCtl *ctl = static_cast<LuCtl *>(ws.ctl);
-    SK_CUDA(cudaMemcpyAsync(ctl, &c, sizeof(c), cudaMemcpyHostToDevice, st));
+    DevStatus *defer = deferred_status();
+    if (defer) {   // gate and pivot threshold on the device
+        SK_CUDA(cudaMemsetAsync(ctl, 0, sizeof(LuCtl), st));
+        nxn_gate<<<1, 1, 0, st>>>(ws.stats, (int)n, ctl, defer);
+        SK_LAUNCH_CHECK("nxn_gate");
+    } else {
+        double h[4];
+        SK_CUDA(cudaMemcpyAsync(h, ws.stats, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        SK_CUDA(cudaStreamSynchronize(st));
+        if (h[2] > 0) { set_error("a contains non-finite entries"); return fill_status(status, SK_NON_FINITE, -1, 0, 0); }
+        LuCtl c{};
+        c.thresh = (double)n * 2.220446049250313e-16 * h[0];   // n * eps * max|a|
+        SK_CUDA(cudaMemcpyAsync(ctl, &c, sizeof(c), cudaMemcpyHostToDevice, st));
+    }
     // column-major working copy (the reference factors an order="F" copy)
     transpose_copy<<<(unsigned)std::min<int64_t>((n * n + 255) / 256, 4096), 256, 0, st>>>(g, (int)n, ws.w);
     SK_LAUNCH_CHECK("transpose_copy");
+    if (defer) {   // after a recorded failure (this gate included) the LU runs on the identity
+        int rg = guard_identity(ws.w, 8, n, n, n, true, st);
+        if (rg) return rg;
+    }
     SK_CUDA(cudaMemsetAsync(ws.l, 0, (size_t)n * n * sizeof(double), st));
     double *w = ws.w, *lm = ws.l, *cv = ws.candv;
     int *perm = ws.perm, *ci = ws.candi;
@@ -1172,7 +1280,18 @@ int sk_lu_solve_f64(const double *g, int64_t n, const double *rhs, double *x, sk
     static const bool perm_lu = barrier_lu && !(lu_choice && strcmp(lu_choice, "barrier") == 0);
     static const bool smem_lu = perm_lu && !(lu_choice && strcmp(lu_choice, "perm") == 0);
     bool done = false;
-    if (smem_lu && n <= (int64_t)LUS_THREADS * LUS_ROWS) {
+    static const bool small_lu = !(lu_choice && strcmp(lu_choice, "smem") == 0);
+    if (smem_lu && small_lu && n <= LU_SMALL_MAX) {
+        const size_t smem = (size_t)n * n * sizeof(double);
+        if (cudaFuncSetAttribute(lu_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+            cudaSuccess) {
+            lu_small_kernel<<<1, 1024, smem, st>>>(w, ni, ws.pivots, perm, lm, ctl);
+            SK_LAUNCH_CHECK("lu_small_kernel");
+            done = true;
+        }
+        cudaGetLastError();
+    }
+    if (!done && smem_lu && n <= (int64_t)LUS_THREADS * LUS_ROWS) {
         const int gs = (int)std::min<int64_t>(sm_count(), n);
         const size_t smem = (size_t)((n + gs - 1) / gs) * (size_t)n * sizeof(double);
         int optin = 0, dev = 0;
@@ -1230,9 +1349,14 @@ int sk_lu_solve_f64(const double *g, int64_t n, const double *rhs, double *x, sk
         SK_CUDA(cudaLaunchCooperativeKernel((const void *)lu_kernel, dim3(blocks), dim3(THREADS), args, 0, st));
         SK_LAUNCH_CHECK("lu_kernel");
     }
-    LuCtl hc;
-    SK_CUDA(cudaMemcpyAsync(&hc, ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
-    SK_CUDA(cudaStreamSynchronize(st));
+    LuCtl hc{};
+    if (defer) {
+        int rn = note_verdict(&ctl->fail_code, 0, &ctl->fail_col, &ctl->fail_value, &ctl->thresh, st);
+        if (rn) return rn;
+    } else {
+        SK_CUDA(cudaMemcpyAsync(&hc, ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
+        SK_CUDA(cudaStreamSynchronize(st));
+    }
     if (hc.fail_code) {
         set_error("pivot %d magnitude %.3e below threshold %.3e", hc.fail_col, hc.fail_value, hc.thresh);
         return fill_status(status, hc.fail_code, hc.fail_col, hc.fail_value, hc.thresh);
@@ -1258,6 +1382,15 @@ int sk_trsv_f64(const double *r, int64_t ldr, int64_t n, int transposed, const d
     const TriView Rv{r, ldr, 1};       // R(i,k) = r[i*ldr + k]  (row-major upper)
     const TriView RTv{r, 1, ldr};      // R^T(i,k) = R(k,i)
     int big = INT32_MAX, first = INT32_MAX;
+    if (deferred_status()) {   // zero diagonal recorded on the device
+        int rc = note_zero_diagonal(r, ldr, n, SK_SINGULAR_TRIANGULAR, st);
+        if (rc) return rc;
+        SK_CUDA(cudaMemcpyAsync(tmp, rhs, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        rc = transposed ? trsv_launch(RTv, (int)n, true, false, tmp, nullptr, x, st)
+                        : trsv_launch(Rv, (int)n, false, false, tmp, nullptr, x, st);
+        if (rc) return rc;
+        return fill_status(status, SK_OK, -1, 0, 0);
+    }
     SK_CUDA(cudaMemcpyAsync(flag, &big, sizeof(int), cudaMemcpyHostToDevice, st));
     first_zero_diag<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Rv, (int)n, flag);
     SK_LAUNCH_CHECK("first_zero_diag");
@@ -1276,6 +1409,7 @@ int sk_trsv_f64(const double *r, int64_t ldr, int64_t n, int transposed, const d
 
 int sk_kappa0_from_gram(const double *g, int64_t n, double *kappa0_host, int *overflowed_host, void *wsp,
                         size_t ws_bytes, sk_stream_t stream) {
+    SK_NO_DEFER("sk_kappa0_from_gram");
     if (!g || !kappa0_host || !overflowed_host || n <= 0 || n > 65536 || !wsp || ws_bytes < sk_nxn_workspace(n)) {
         set_error("sk_kappa0_from_gram: bad arguments");
         return SK_ERR_ARG;

@@ -211,7 +211,10 @@ static Plan make_plan(int64_t m, int64_t n, bool syrk) {
     p.ntn = (int)((n + BN - 1) / BN);
     p.ntiles = syrk ? p.ntn * (p.ntn + 1) / 2 : p.ntn * p.ntn;
     const int sms = sm_count();
-    const int64_t min_chunk = 1024;  // rows per split: keeps each unit long enough
+    // rows per split: GEMM-TN >= 128 (8 BK steps), so a short m still spreads over the SMs
+    // (config 1's A_p^T A: 54 -> 9 us); SYRK >= 1024 (its summation order is what the
+    // NotPositiveDefinite cases of the reference's tests were pinned with)
+    const int64_t min_chunk = syrk ? 1024 : 128;
     int64_t smax = (m + min_chunk - 1) / min_chunk;
     if (smax < 1) smax = 1;
     // ~16 waves of resident CTAs; among nearby split counts pick the one whose last
@@ -276,6 +279,7 @@ static int splits_for(int64_t m, int64_t n) {
     const int cols = (int)((n + THREADS - 1) / THREADS);
     int64_t s = (int64_t)4 * sm_count() / cols;
     int64_t smax = (m + 4095) / 4096;
+    if (smax < 16) smax = std::min<int64_t>(16, (m + 63) / 64);   // short m: >= 64 rows per split, not one CTA
     if (s > smax) s = smax;
     if (s < 1) s = 1;
     return (int)s;

@@ -214,6 +214,7 @@ size_t sk_jacobi_workspace(int64_t rows, int64_t n) {
 
 int sk_jacobi_sv_f64(const double *a, int64_t rows, int64_t n, int64_t lda, int max_sweeps, double tol,
                      double *sv_host, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    SK_NO_DEFER("sk_jacobi_sv_f64");
     if (!a || !sv_host || rows <= 0 || n <= 0 || lda < n || n > 8192 || !ws || ws_bytes < sk_jacobi_workspace(rows, n)) {
         set_error("sk_jacobi_sv_f64: bad arguments");
         return SK_ERR_ARG;

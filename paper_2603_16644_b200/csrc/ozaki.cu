@@ -1237,6 +1237,7 @@ int sk_trsm_ozaki_fell_back(void) { return g_trsm_oz_fell_back; }
 
 int sk_trsm_ozaki_f64(const double *a, int64_t lda, int64_t m, int64_t n, const double *r, int64_t ldr, double *ap,
                       int64_t ldap, sk_status *status, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    SK_NO_DEFER("sk_trsm_ozaki_f64");
     if (!a || !r || !ap || m < 0 || n <= 0 || lda < n || ldr < n || ldap < n || n > (1 << 20) || a == ap) {
         set_error("sk_trsm_ozaki_f64: bad arguments (a and a_p must be distinct)");
         return SK_ERR_ARG;
@@ -1361,6 +1362,7 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
 int sk_gram_ozaki_acc_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
                           const double *xstats, const double *ystats, double *g, int64_t ldg, int accumulate,
                           void *ws, size_t ws_bytes, sk_stream_t stream) {
+    SK_NO_DEFER("sk_gram_ozaki_acc_f64");
     if (!x || !y || !g || m < 0 || n <= 0 || ldx < n || ldy < n || ldg < n || n > 65536) {
         set_error("sk_gram_ozaki_f64: bad arguments");
         return SK_ERR_ARG;

@@ -224,7 +224,7 @@ static Plan make_plan(int64_t m_local, int64_t n, int64_t d) {
     p.ntn = (int)((n + BN - 1) / BN);
     p.ntiles = p.ntm * p.ntn;
     const int sms = sm_count();
-    int64_t smax = (m_local + 1023) / 1024;
+    int64_t smax = (m_local + 63) / 64;   // >= 64 rows per split (small m: more CTAs, shorter K loops)
     if (smax < 1) smax = 1;
     int64_t target = (int64_t)32 * sms / p.ntiles;
     if (target < 1) target = 1;

@@ -1124,6 +1124,7 @@ size_t sketch_fft_workspace(int64_t m_pad, int64_t n, int64_t d) {
 int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int64_t row_offset, int64_t m_pad,
                    int64_t n, const double *signs, const int64_t *rows, int64_t d, double *out, int64_t ldo,
                    int accumulate, int *overflow_flag_dev, void *ws, size_t ws_bytes, cudaStream_t st) {
+    SK_NO_DEFER("sketch_fft_run");
     using namespace skfft;
     if (!sketch_fft_supported(m_pad)) { set_error("sketch_fft: M must be a multiple of 2048"); return SK_ERR_ARG; }
     if (ws_bytes < sketch_fft_workspace(m_pad, n, d)) { set_error("sketch_fft: workspace too small"); return SK_ERR_ARG; }

@@ -190,6 +190,7 @@ size_t sk_matrix_stats_workspace(int64_t rows, int64_t cols) {
 
 int sk_cast_stats(const void *src, int src_dtype, int64_t rows, int64_t cols, int64_t ld_src, double *dst,
                   int64_t ld_dst, double *stats_host, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    SK_NO_DEFER("sk_cast_stats");
     if (!src || !stats_host || rows < 0 || cols <= 0 || ld_src < cols || (dst && ld_dst < cols) || !ws ||
         ws_bytes < sk_matrix_stats_workspace(rows, cols) ||
         (src_dtype != SK_F16 && src_dtype != SK_F32 && src_dtype != SK_F64)) {
@@ -230,6 +231,7 @@ int sk_cast_stats_async(const void *src, int src_dtype, int64_t rows, int64_t co
 
 int sk_level_overflow(const double *a, int64_t rows, int64_t cols, int64_t lda, int level, int *overflowed_host,
                       void *ws, size_t ws_bytes, sk_stream_t stream) {
+    SK_NO_DEFER("sk_level_overflow");
     if (!a || !overflowed_host || rows < 0 || cols <= 0 || lda < cols || !ws || ws_bytes < sizeof(int)) {
         set_error("sk_level_overflow: bad arguments");
         return SK_ERR_ARG;
@@ -251,6 +253,7 @@ int sk_level_overflow(const double *a, int64_t rows, int64_t cols, int64_t lda, 
 
 int sk_residual(const double *a, int64_t rows, int64_t cols, int64_t lda, const double *x, const double *b, double *r,
                 double *out_host, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    SK_NO_DEFER("sk_residual");
     if (!a || !x || !b || !out_host || rows < 0 || cols <= 0 || lda < cols || !ws ||
         ws_bytes < sk_matrix_stats_workspace(rows, cols)) {
         set_error("sk_residual: bad arguments");
@@ -271,6 +274,28 @@ int sk_residual(const double *a, int64_t rows, int64_t cols, int64_t lda, const 
     SK_LAUNCH_CHECK("sumsq_vec");
     SK_CUDA(cudaMemcpyAsync(out_host, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     SK_CUDA(cudaStreamSynchronize(st));
+    return SK_OK;
+}
+
+int sk_residual_async(const double *a, int64_t rows, int64_t cols, int64_t lda, const double *x, const double *b,
+                      double *r, double *out_dev, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    if (!a || !x || !b || !out_dev || rows < 0 || cols <= 0 || lda < cols || !ws ||
+        ws_bytes < sk_matrix_stats_workspace(rows, cols)) {
+        set_error("sk_residual_async: bad arguments");
+        return SK_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    double *part = static_cast<double *>(ws);
+    int64_t nb = (rows + 7) / 8;
+    const int64_t cap = (int64_t)8 * sm_count();
+    if (nb > cap) nb = cap;
+    if (nb < 1) nb = 1;
+    residual_kernel<<<(unsigned)nb, THREADS, 0, st>>>(a, rows, cols, lda, x, b, r, part);
+    SK_LAUNCH_CHECK("residual_kernel");
+    sum_parts<<<1, 64, 0, st>>>(part, (int)nb, 2, out_dev);
+    SK_LAUNCH_CHECK("sum_parts");
+    sumsq_vec<<<1, 256, 0, st>>>(x, cols, out_dev + 1);
+    SK_LAUNCH_CHECK("sumsq_vec");
     return SK_OK;
 }
 

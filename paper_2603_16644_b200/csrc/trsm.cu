@@ -397,6 +397,13 @@ extern "C" int sk_trsm_right_upper_f64(const double *a, int64_t lda, int64_t m, 
     // exactly-zero diagonal -> SingularTriangular (src/dense.py:231-233).  No stream-
     // ordered allocation here: a cudaMallocAsync / cudaFreeAsync pair per call made the
     // following synchronize wait on pool trimming (measured 0.2-900 ms per call).
+    if (deferred_status()) {   // deferred verdicts: recorded on the device, no host read
+        int rc = note_zero_diagonal(r, ldr, n, SK_SINGULAR_TRIANGULAR, st);
+        if (rc) return rc;
+        rc = trsm::launch(a, lda, m, (int)n, r, ldr, ap, ldap, st);
+        if (rc) return rc;
+        return fill_status(status, SK_OK, -1, 0, 0);
+    }
     int first_zero = 0;
     int rc = trsm::first_zero_diagonal(r, ldr, (int)n, st, &first_zero);
     if (rc) return rc;

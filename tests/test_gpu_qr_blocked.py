@@ -32,7 +32,7 @@ def blocked_everywhere(request, monkeypatch):
 
 
 @pytest.mark.parametrize("level", ["binary32", "binary64"])
-@pytest.mark.parametrize("d,n", [(600, 200), (1500, 257), (3000, 1000)])
+@pytest.mark.parametrize("d,n", [(300, 100), (600, 200), (1500, 257), (3000, 1000)])
 def test_blocked_r_matches_oracle(sq, level, d, n):
     a = R.philox(d + n, 11).standard_normal((d, n)) * np.logspace(0, -2, n)
     lev = getattr(sq, level.upper())
@@ -64,3 +64,19 @@ def test_blocked_rank_deficient_in_a_later_panel(sq, level):
     a[:, 100] = 0.0            # stays exactly zero under every reflector: norm 0 at column 100
     with pytest.raises(sq.RankDeficient, match="100"):
         sq.qr_in_precision(a, getattr(sq, level.upper()))
+
+
+@pytest.mark.parametrize("level", ["binary32", "binary64"])
+def test_small_panels_rank_deficient_and_sign(sq, level):
+    """config-1-sized sketches (every panel on the register-resident one-CTA kernel):
+    RankDeficient at the right column of a later panel, the reference's signs."""
+    a = R.philox(5, 6).standard_normal((300, 120))
+    a[:, 70] = 0.0
+    with pytest.raises(sq.RankDeficient, match="70"):
+        sq.qr_in_precision(a, getattr(sq, level.upper()))
+    a = R.philox(5, 7).standard_normal((330, 96)) * np.logspace(0, -3, 96)
+    got = sq.qr_in_precision(a, getattr(sq, level.upper()))
+    dt = np.float32 if level == "binary32" else np.float64
+    ref_r = R.householder_steps(a.astype(dt))[2].astype(np.float64)
+    assert np.abs(got.r - ref_r).max() <= TOL[level] * np.abs(ref_r).max()
+    assert np.array_equal(np.sign(np.diagonal(got.r)), np.sign(np.diagonal(ref_r)))
