@@ -810,39 +810,54 @@ lu_smem_kernel(double *w, int n, double *gl, int *piv, int *flags, double *lout,
 // a - l * u rounded twice, whole-row swaps), so the factors are bitwise the same; what
 // goes away is the inter-CTA flag chain (config 1, n = 100: ~3.8 us per step).
 constexpr int LU_SMALL_MAX = 160;
-__global__ void __launch_bounds__(1024, 1)
+__global__ void __launch_bounds__(512, 1)
 lu_small_kernel(double *w, int n, int *piv, int *perm, double *lout, LuCtl *ctl) {
     extern __shared__ double W[];                 // column-major n x n
-    __shared__ double s_pv;
+    __shared__ double s_pv, s_akk;
     __shared__ int s_p, s_piv[LU_SMALL_MAX], s_perm[LU_SMALL_MAX];
-    const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31;
+    const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
     const double thresh = ctl->thresh;
     for (int64_t e = tid; e < (int64_t)n * n; e += T) W[e] = w[e];
     __syncthreads();
-    for (int k = 0; k < n; ++k) {
-        double *ck = W + (int64_t)k * n;
-        if (tid < 32) {   // pivot: first maximum of |A[k:, k]|
-            double bv = -1.0;
-            int bi = INT32_MAX;
-            for (int i = k + lane; i < n; i += 32) better(bv, bi, fabs(ck[i]), i);
+    // pivot of column k: first maximum of |A[k:, k]| (one warp), with its signed value
+    auto pivot = [&](int k) {
+        const double *ck = W + (int64_t)k * n;
+        double bv = -1.0;
+        int bi = INT32_MAX;
+        for (int i = k + lane; i < n; i += 32) better(bv, bi, fabs(ck[i]), i);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                better(bv, bi, ov, oi);
-            }
-            if (lane == 0) { s_pv = bv; s_p = bi; }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            better(bv, bi, ov, oi);
         }
-        __syncthreads();
-        const double pv = s_pv;
+        if (lane == 0) { s_pv = bv; s_p = bi; s_akk = bi < n ? ck[bi] : 0.0; }
+    };
+    if (warp == 0) pivot(0);
+    __syncthreads();
+    // two barriers per step: (1) multipliers of column k (with its row swap folded in)
+    // and the row swap of every other column; (2) the trailing update, where warp 0 takes
+    // column k + 1 alone and then finds its pivot while the other warps update the rest
+    for (int k = 0; k < n; ++k) {
+        const double pv = s_pv, akk = s_akk;
         const int p = s_p;
         if (pv < thresh || pv == 0.0 || !(pv == pv)) {   // uniform
             if (tid == 0) { ctl->fail_code = SK_NUMERICALLY_SINGULAR; ctl->fail_col = k; ctl->fail_value = pv; }
             for (int i = tid; i < n; i += T) perm[i] = i;   // a valid permutation for deferred callers
             return;
         }
-        if (p != k && p < n)   // swap rows k and p in every column
+        double *ck = W + (int64_t)k * n;
+        for (int i = k + tid; i < n; i += T) {
+            if (i == k) {
+                if (p != k) ck[p] = __ddiv_rn(ck[k], akk);   // old row k lands in row p
+                ck[k] = akk;
+            } else if (i != p) {
+                ck[i] = __ddiv_rn(ck[i], akk);
+            }
+        }
+        if (p != k)
             for (int j = tid; j < n; j += T) {
+                if (j == k) continue;
                 double *cj = W + (int64_t)j * n;
                 const double t = cj[k];
                 cj[k] = cj[p];
@@ -850,13 +865,20 @@ lu_small_kernel(double *w, int n, int *piv, int *perm, double *lout, LuCtl *ctl)
             }
         if (tid == 0) { piv[k] = p; s_piv[k] = p; }
         __syncthreads();
-        const double akk = ck[k];
-        for (int i = k + 1 + tid; i < n; i += T) ck[i] = __ddiv_rn(ck[i], akk);
-        __syncthreads();
-        for (int j = k + 1 + (tid >> 5); j < n; j += T >> 5) {   // trailing block: a warp per column
-            double *cj = W + (int64_t)j * n;
-            const double u = cj[k];
-            for (int i = k + 1 + lane; i < n; i += 32) cj[i] = __dsub_rn(cj[i], __dmul_rn(ck[i], u));
+        if (warp == 0) {
+            if (k + 1 < n) {
+                double *cj = W + (int64_t)(k + 1) * n;
+                const double u = cj[k];
+                for (int i = k + 1 + lane; i < n; i += 32) cj[i] = __dsub_rn(cj[i], __dmul_rn(ck[i], u));
+                __syncwarp();
+                pivot(k + 1);
+            }
+        } else {
+            for (int j = k + 2 + (warp - 1); j < n; j += nw - 1) {   // a warp per column
+                double *cj = W + (int64_t)j * n;
+                const double u = cj[k];
+                for (int i = k + 1 + lane; i < n; i += 32) cj[i] = __dsub_rn(cj[i], __dmul_rn(ck[i], u));
+            }
         }
         __syncthreads();
     }
@@ -864,13 +886,13 @@ lu_small_kernel(double *w, int n, int *piv, int *perm, double *lout, LuCtl *ctl)
     __syncthreads();
     if (tid == 0)   // perm = the row swaps (k, piv[k]) applied in order to the identity
         for (int k = 0; k < n; ++k) {
-            const int p = s_piv[k];
-            if (p != k) { const int t = s_perm[k]; s_perm[k] = s_perm[p]; s_perm[p] = t; }
+            const int q = s_piv[k];
+            if (q != k) { const int t = s_perm[k]; s_perm[k] = s_perm[q]; s_perm[q] = t; }
         }
     __syncthreads();
     for (int i = tid; i < n; i += T) perm[i] = s_perm[i];
-    for (int c = tid >> 5; c < n; c += T >> 5)
-        for (int i = tid & 31; i < n; i += 32) {
+    for (int c = warp; c < n; c += nw)
+        for (int i = lane; i < n; i += 32) {
             const double v = W[(int64_t)c * n + i];
             w[(int64_t)c * n + i] = v;
             lout[(int64_t)c * n + i] = i > c ? v : 0.0;
@@ -1285,7 +1307,7 @@ int sk_lu_solve_f64(const double *g, int64_t n, const double *rhs, double *x, sk
         const size_t smem = (size_t)n * n * sizeof(double);
         if (cudaFuncSetAttribute(lu_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
             cudaSuccess) {
-            lu_small_kernel<<<1, 1024, smem, st>>>(w, ni, ws.pivots, perm, lm, ctl);
+            lu_small_kernel<<<1, 512, smem, st>>>(w, ni, ws.pivots, perm, lm, ctl);
             SK_LAUNCH_CHECK("lu_small_kernel");
             done = true;
         }
