@@ -784,11 +784,11 @@ constexpr int QPS_THREADS = 1024;
 // rows per lane: 16 (binary32, dv <= 512); 12 (binary64, dv <= 384: 64 registers per thread)
 template <typename T> constexpr int qps_rpl() { return sizeof(T) == 8 ? 12 : 16; }
 template <typename T> constexpr int panel_small_rows() { return 32 * qps_rpl<T>(); }
-template <typename T, int NBP>
+template <typename T, int NBP, int QPS_RPL>
 __global__ void __launch_bounds__(QPS_THREADS, 1) qrb_panel_small(T *wp, int64_t ld, int dv, int nbp, T *alphas,
                                                                  T *taus, T *v0s, Ctl<T> *ctl, int col0, T *tm) {
     using O = LevelOps<T>;
-    constexpr int QPS_RPL = qps_rpl<T>(), PANEL_SMALL_ROWS = panel_small_rows<T>();
+    constexpr int PANEL_SMALL_ROWS = panel_small_rows<T>();   // (QPS_RPL = ceil(dv / 32), even)
     constexpr int CPW = (NBP + 31) / 32;
     extern __shared__ __align__(16) unsigned char qps_raw[];
     T *vb = reinterpret_cast<T *>(qps_raw);             // [2][PANEL_SMALL_ROWS]: the current reflector
@@ -863,11 +863,10 @@ __global__ void __launch_bounds__(QPS_THREADS, 1) qrb_panel_small(T *wp, int64_t
                 for (int t = 0; t < QPS_RPL; ++t) dsum = dsum + v[lane + 32 * t] * x[q][t];
                 for (int o = 16; o > 0; o >>= 1) dsum = dsum + __shfl_xor_sync(0xffffffffu, dsum, o);
                 const T tc = tau * dsum;
+                // (v is zero above j and below dv, so the whole register column takes the
+                // update unpredicated: x - tc * 0 == x)
 #pragma unroll
-                for (int t = 0; t < QPS_RPL; ++t) {
-                    const int i = lane + 32 * t;
-                    if (i >= j && i < dv) x[q][t] = x[q][t] - tc * v[i];
-                }
+                for (int t = 0; t < QPS_RPL; ++t) x[q][t] = x[q][t] - tc * v[lane + 32 * t];
             }
         }
     }
@@ -947,7 +946,18 @@ int launch_panel(T *wp, int64_t ld, int dv, int nbp, T *alphas, T *taus, T *v0s,
                  T *vtv, cudaStream_t st) {
     if (dv <= panel_small_rows<T>()) {
         const size_t ssmem = (size_t)(2 * panel_small_rows<T>() + NBW * (dv | 1)) * sizeof(T);
-        auto sfn = qrb_panel_small<T, NBW>;
+        const int rpl = std::max(2, ((dv + 31) / 32 + 1) & ~1);   // register rows per lane, even
+        auto sfn = qrb_panel_small<T, NBW, 16>;
+        switch (rpl) {
+            case 2: sfn = qrb_panel_small<T, NBW, 2>; break;
+            case 4: sfn = qrb_panel_small<T, NBW, 4>; break;
+            case 6: sfn = qrb_panel_small<T, NBW, 6>; break;
+            case 8: sfn = qrb_panel_small<T, NBW, 8>; break;
+            case 10: sfn = qrb_panel_small<T, NBW, 10>; break;
+            case 12: sfn = qrb_panel_small<T, NBW, 12>; break;
+            case 14: sfn = qrb_panel_small<T, NBW, sizeof(T) == 8 ? 12 : 14>; break;
+            default: break;
+        }
         SK_CUDA(cudaFuncSetAttribute((const void *)sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
         sfn<<<1, QPS_THREADS, ssmem, st>>>(wp, ld, dv, nbp, alphas, taus, v0s, ctl, c0, tm);
         SK_LAUNCH_CHECK("qrb_panel_small");
