@@ -62,3 +62,39 @@ def test_product_path_fails_loudly_without_device(monkeypatch):
     import paper_2603_16644_b200 as sq
     with pytest.raises(_lib.LibraryUnavailable):
         sq.algorithm1_pipeline(np.eye(4, 2), np.ones(4))
+
+
+def test_deferred_verdict_entry_points_refuse_without_a_record():
+    """sk_note_* / sk_guard_identity need sk_defer_verdicts first: without a device
+    status record they fail loudly (SK_ERR_ARG) before touching any device memory."""
+    if not os.path.exists(LIB):
+        pytest.skip("libsklsq.so not built")
+    lib = ctypes.CDLL(LIB)
+    lib.sk_last_error.restype = ctypes.c_char_p
+    lib.sk_defer_verdicts(None)
+    assert lib.sk_note_flag(ctypes.c_void_p(1), ctypes.c_int(5), None) == -2
+    assert lib.sk_note_positive(ctypes.c_void_p(1), ctypes.c_int(9), None) == -2
+    assert lib.sk_note_zero_diagonal(ctypes.c_void_p(1), ctypes.c_int64(4), ctypes.c_int64(4), ctypes.c_int(1),
+                                     None) == -2
+    assert lib.sk_guard_identity(8, ctypes.c_void_p(1), ctypes.c_int64(4), ctypes.c_int64(4), ctypes.c_int64(4), 1,
+                                 None) == -2
+    assert b"sk_defer_verdicts" in lib.sk_last_error()
+
+
+def test_pipeline_plan_validates_before_touching_the_device():
+    """PipelinePlan checks its arguments like algorithm1_pipeline (ValueError) before it
+    needs a GPU; with no GPU the product path fails loudly (no CPU fallback)."""
+    import paper_2603_16644_b200 as sq
+    from paper_2603_16644_b200 import _lib
+    with pytest.raises(ValueError):
+        sq.PipelinePlan(100, 10, method="sne")
+    with pytest.raises(ValueError):
+        sq.PipelinePlan(100, 10, precision="quad")
+    with pytest.raises(ValueError):
+        sq.PipelinePlan(5, 10)
+    with pytest.raises(ValueError):
+        sq.PipelinePlan(100, 10, d_factor=0.5)
+    import torch
+    if not torch.cuda.is_available():
+        with pytest.raises(_lib.LibraryUnavailable):
+            sq.PipelinePlan(100, 10, method="hpne", precision="single")
