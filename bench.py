@@ -60,6 +60,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-e2e-pageable", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-config1", action="store_true", help="skip the config-1 latency report")
     p.add_argument("--cpu-rows", type=int, default=8192, help="row-slice height (full n) for the CPU legs")
     return p.parse_args()
 
@@ -663,6 +664,11 @@ def run_ours(args, rank, world):
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "ms", "cores": cpu_cores(), "kind": "port", "sample": f"failed: {ex!r}"}
     extra = {}
+    if world == 1 and not args.no_config1:
+        try:
+            extra["config1_latency"] = config1_latency()
+        except Exception as ex:  # noqa: BLE001 -- an extra report; never fails the bench line
+            extra["config1_latency"] = {"error": repr(ex)}
     if world == 1 and m == CONFIG3_M:
         extra["config4_t1_extrapolated_ms"] = {
             "value": 4 * ms, "basis": "linear-in-m extrapolation 4 x T(1 GPU, 4M x 2048): config 4 "
@@ -688,6 +694,35 @@ def run_ours(args, rank, world):
             "gpu_launches": int(launches),
             "gpu_launches_per_step": launches / args.steps, "clocks": clk}
     print(json.dumps(line), flush=True)
+
+
+def config1_latency(reps=50):
+    """Config 1 (1000 x 100, kappa 1e8, rho 1e-6; the reference's CPU-runnable case, HPNE
+    "single") per-solve latency from device arrays: the eager algorithm1_pipeline against
+    one PipelinePlan graph replay (deferred verdicts).  Host wall time per solve including
+    the result read (the solve is latency-bound); an extra report, not the headline."""
+    import torch
+    import paper_2603_16644_b200 as sq
+    from paper_2603_16644_b200.probgen import generate_problem_device
+    a, b, _ = generate_problem_device(1000, 100, 1e8, 1e-6, 11)
+    out = {"config": "1000 x 100, kappa 1e8, rho 1e-6, hpne, precision single, device arrays", "reps": reps}
+    plan = sq.PipelinePlan(1000, 100, method="hpne", precision="single", seed=1)
+
+    def eager():
+        return sq.algorithm1_pipeline(a, b, "hpne", "single", seed=1, diagnostics=False)
+
+    for name, fn in (("eager_ms", eager), ("graph_ms", lambda: plan.solve(a, b))):
+        for _ in range(5):
+            rep = fn()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(reps):
+            rep = fn()
+        torch.cuda.synchronize()
+        out[name] = (time.perf_counter() - t) / reps * 1e3
+        out[name.replace("_ms", "_x")] = rep.x_hat
+    out["x_bitwise_equal"] = bool((out.pop("eager_x") == out.pop("graph_x")).all())
+    return out
 
 
 def rep_kappa0(rep):
