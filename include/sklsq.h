@@ -14,7 +14,9 @@
  *    a function says otherwise.  No torch types appear in any signature.
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Work is
  *    stream-ordered.  Functions that return a numerical verdict (QR, Cholesky, LU,
- *    kappa0, finiteness) synchronise `stream` before returning it.
+ *    kappa0, finiteness) synchronise `stream` before returning it -- unless verdicts
+ *    are deferred to a device record (sk_defer_verdicts, below), which makes a whole
+ *    solve capturable as one CUDA graph.
  *  - `ws` / `ws_bytes`: caller-owned device workspace; query the size with the
  *    matching *_workspace() call.  No allocation happens on the hot path.
  *  - Return: SK_OK (0), a numerical failure code (>0, 1:1 with the reference
