@@ -114,7 +114,7 @@ int sk_residual_async(const double *a, int64_t rows, int64_t cols, int64_t lda, 
  * with data-dependent control flow (LU, Cholesky) run on the identity once a failure is
  * recorded (their outputs are then meaningless; the record says so).  Entry points whose
  * result is a host value (sk_cast_stats, sk_residual, sk_kappa0_*, sk_jacobi_sv_f64,
- * sk_level_overflow, the INT8 Ozaki engines, the FFT sketch planner, ...) return
+ * sk_level_overflow, the INT8 Ozaki engines, ...) return
  * SK_ERR_ARG while verdicts are deferred.  Replaces the host-side exception points of
  * src/solvers.py:168-252 (raise sites kept in order). */
 int sk_defer_verdicts(sk_status *status_dev);

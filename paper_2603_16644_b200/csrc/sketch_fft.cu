@@ -994,6 +994,57 @@ int64_t colblock(int64_t m_pad, int64_t n) {
 }  // namespace skfft
 
 namespace skfft {
+// Request lists of pass B, built on the device (no host round trip, so the sketch can
+// run with verdicts deferred / inside a CUDA graph): the d sampled rows and their
+// mirrors t = row, (M - row) mod M grouped by k2 = t mod N2, stably ordered by
+// (sample, mirror) inside each group, exactly the order of the host construction.
+// ptr[k2] .. ptr[k2 + 1] index the group; s / w / k1 = t / N2 per request.
+__global__ void __launch_bounds__(1024) plan_requests(const int64_t *rows, int64_t d, int64_t M, int *ptr, int *rs,
+                                                      int *rw, int64_t *rk1) {
+    __shared__ int cnt[N2 + 1];
+    const int tid = threadIdx.x;
+    for (int i = tid; i <= N2; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    for (int64_t q = tid; q < 2 * d; q += blockDim.x) {
+        const int64_t r = rows[q >> 1];
+        const int64_t t = (q & 1) ? (M - r) % M : r;
+        atomicAdd(&cnt[(int)(t % N2) + 1], 1);
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int i = 0; i < N2; ++i) cnt[i + 1] += cnt[i];
+    __syncthreads();
+    for (int i = tid; i <= N2; i += blockDim.x) ptr[i] = cnt[i];
+    __syncthreads();
+    if (tid >= 32) return;
+    // one warp places the requests in q order: lanes with the same group take
+    // consecutive slots (rank among the lower lanes of the group), the group's lowest
+    // lane advances its fill pointer
+    for (int64_t q0 = 0; q0 < 2 * d; q0 += 32) {
+        const int64_t q = q0 + tid;
+        const bool ok = q < 2 * d;
+        int key = -1;
+        int64_t t = 0;
+        if (ok) {
+            const int64_t r = rows[q >> 1];
+            t = (q & 1) ? (M - r) % M : r;
+            key = (int)(t % N2);
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const int rank = __popc(peers & ((1u << tid) - 1u));
+        const int base = ok ? cnt[key] : 0;
+        __syncwarp();
+        if (ok) {
+            const int at = base + rank;
+            rs[at] = (int)(q >> 1);
+            rw[at] = (int)(q & 1);
+            rk1[at] = t / N2;
+            if (rank == 0) cnt[key] = base + __popc(peers);
+        }
+        __syncwarp();
+    }
+}
+
 struct SketchFftCall {
     const double *a;
     int64_t lda, m_local, row_offset, M, M1, n, cb;
@@ -1124,7 +1175,6 @@ size_t sketch_fft_workspace(int64_t m_pad, int64_t n, int64_t d) {
 int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int64_t row_offset, int64_t m_pad,
                    int64_t n, const double *signs, const int64_t *rows, int64_t d, double *out, int64_t ldo,
                    int accumulate, int *overflow_flag_dev, void *ws, size_t ws_bytes, cudaStream_t st) {
-    SK_NO_DEFER("sketch_fft_run");
     using namespace skfft;
     if (!sketch_fft_supported(m_pad)) { set_error("sketch_fft: M must be a multiple of 2048"); return SK_ERR_ARG; }
     if (ws_bytes < sketch_fft_workspace(m_pad, n, d)) { set_error("sketch_fft: workspace too small"); return SK_ERR_ARG; }
@@ -1147,31 +1197,38 @@ int sketch_fft_run(int level, const double *a, int64_t lda, int64_t m_local, int
     unsigned char *tables = p;   // twiddle tables in the transform precision (filled below)
     p += align_up((size_t)(N2 + M1) * sizeof(double2), 256);
     uint16_t *sbits = reinterpret_cast<uint16_t *>(p);   // packed signs (filled below)
-    // ---- request lists grouped by k2 (host; d entries)
-    std::vector<int64_t> hrows((size_t)d);
-    SK_CUDA(cudaMemcpyAsync(hrows.data(), rows, (size_t)d * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SK_CUDA(cudaStreamSynchronize(st));
-    std::vector<int> cnt(N2 + 1, 0), hs(2 * d), hw(2 * d);
-    std::vector<int64_t> hk1(2 * d);
-    for (int64_t s = 0; s < d; ++s)
-        for (int w = 0; w < 2; ++w) {
-            const int64_t t = (w == 0) ? hrows[s] : (M - hrows[s]) % M;
-            cnt[(t % N2) + 1]++;
-        }
-    for (int i = 0; i < N2; ++i) cnt[i + 1] += cnt[i];
-    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
-    for (int64_t s = 0; s < d; ++s)
-        for (int w = 0; w < 2; ++w) {
-            const int64_t t = (w == 0) ? hrows[s] : (M - hrows[s]) % M;
-            const int at = fill[t % N2]++;
-            hs[at] = (int)s;
-            hw[at] = w;
-            hk1[at] = t / N2;
-        }
-    SK_CUDA(cudaMemcpyAsync(d_ptr, cnt.data(), (size_t)(N2 + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
-    SK_CUDA(cudaMemcpyAsync(d_s, hs.data(), (size_t)2 * d * sizeof(int), cudaMemcpyHostToDevice, st));
-    SK_CUDA(cudaMemcpyAsync(d_w, hw.data(), (size_t)2 * d * sizeof(int), cudaMemcpyHostToDevice, st));
-    SK_CUDA(cudaMemcpyAsync(d_k1, hk1.data(), (size_t)2 * d * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    // ---- request lists grouped by k2 (device; SK_FFT_HOST_PLAN=1: the host construction,
+    //      same arrays, kept for A/B checks; never with deferred verdicts)
+    const char *hp_env = getenv("SK_FFT_HOST_PLAN");
+    if (!(hp_env && hp_env[0] == '1') || deferred_status()) {
+        plan_requests<<<1, 1024, 0, st>>>(rows, d, M, d_ptr, d_s, d_w, d_k1);
+        SK_LAUNCH_CHECK("plan_requests");
+    } else {
+        std::vector<int64_t> hrows((size_t)d);
+        SK_CUDA(cudaMemcpyAsync(hrows.data(), rows, (size_t)d * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        SK_CUDA(cudaStreamSynchronize(st));
+        std::vector<int> cnt(N2 + 1, 0), hs(2 * d), hw(2 * d);
+        std::vector<int64_t> hk1(2 * d);
+        for (int64_t s = 0; s < d; ++s)
+            for (int w = 0; w < 2; ++w) {
+                const int64_t t = (w == 0) ? hrows[s] : (M - hrows[s]) % M;
+                cnt[(t % N2) + 1]++;
+            }
+        for (int i = 0; i < N2; ++i) cnt[i + 1] += cnt[i];
+        std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+        for (int64_t s = 0; s < d; ++s)
+            for (int w = 0; w < 2; ++w) {
+                const int64_t t = (w == 0) ? hrows[s] : (M - hrows[s]) % M;
+                const int at = fill[t % N2]++;
+                hs[at] = (int)s;
+                hw[at] = w;
+                hk1[at] = t / N2;
+            }
+        SK_CUDA(cudaMemcpyAsync(d_ptr, cnt.data(), (size_t)(N2 + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+        SK_CUDA(cudaMemcpyAsync(d_s, hs.data(), (size_t)2 * d * sizeof(int), cudaMemcpyHostToDevice, st));
+        SK_CUDA(cudaMemcpyAsync(d_w, hw.data(), (size_t)2 * d * sizeof(int), cudaMemcpyHostToDevice, st));
+        SK_CUDA(cudaMemcpyAsync(d_k1, hk1.data(), (size_t)2 * d * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    }
     const int vec = ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (lda % 2 == 0);
     SketchFftCall c{a, lda, m_local, row_offset, M, M1, n, cb, signs, sbits, rows, d, out, ldo, accumulate, overflow_flag_dev,
                     y, zbuf, d_ptr, d_s, d_w, d_k1, tables, level, vec};

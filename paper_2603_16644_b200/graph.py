@@ -21,10 +21,10 @@ a plan's results equal the eager call's bit for bit in every case.
 
 The plan owns every buffer (inputs, sketch operator, A_s, R_s, A_p, G, workspaces), so
 nothing it captured can be reallocated underneath the graph.  It covers the engines
-whose results do not need a host round trip: the DMMA / tcgen05 sketch, the FP64 DMMA
-TRSM and Gram.  Shapes for which the eager pipeline picks the FFT sketch or the INT8
-Ozaki engines (large, bandwidth-bound solves where a graph buys nothing) are refused
-at construction.  Not in the reference's API: an addition for serving many small solves.
+whose results do not need a host round trip: the FFT / DMMA / tcgen05 sketches, the FP64
+DMMA TRSM and Gram.  Shapes for which the eager pipeline picks the INT8 Ozaki engines
+(large, bandwidth-bound solves where a graph buys nothing; their operand guards decide
+a fallback on the host) are refused at construction.  Not in the reference's API: an addition for serving many small solves.
 """
 
 from __future__ import annotations
@@ -54,16 +54,12 @@ class _LevelGraph:
     """Buffers and the captured graph of one precision level."""
 
     def __init__(self, plan: "PipelinePlan", level: PrecisionLevel):
-        from .dense import _gram_engine, _new_ap, _trsm_engine
+        from .dense import _new_ap
         lib = _lib.lib()
         m, n, d = plan.m, plan.n, plan.d
         dev = plan.dev
         self.level = level
         self.op, self.dsk = _make_sketch_dev(m, d, plan.transform, plan.seed)
-        if plan.transform == DCT2 and self.op.m_pad >= 2048 and self.op.m_pad % 2048 == 0:
-            raise ValueError(f"PipelinePlan: m = {m} takes the FFT sketch (host-planned); use algorithm1_pipeline")
-        if _gram_engine(m, n, False, None) != "dmma" or _trsm_engine(m, n, False, None) != "dmma":
-            raise ValueError(f"PipelinePlan: {m} x {n} takes the INT8 Ozaki engines; use algorithm1_pipeline")
         self.total = torch.zeros((n, d), dtype=torch.float64, device=dev)
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self.a_s = torch.empty((n, d), dtype=level.torch_dtype, device=dev)
@@ -172,6 +168,9 @@ class PipelinePlan:
         self.d = int(math.ceil(d_factor * n))
         if self.d < n:
             raise ValueError(f"d_factor {d_factor} gives d={self.d} < n={n}")
+        from .dense import _gram_engine, _trsm_engine
+        if _gram_engine(m, n, False, None) != "dmma" or _trsm_engine(m, n, False, None) != "dmma":
+            raise ValueError(f"PipelinePlan: {m} x {n} takes the INT8 Ozaki engines; use algorithm1_pipeline")
         self.dev = device()
         self.a = torch.empty((m, n), dtype=torch.float64, device=self.dev)
         self.b = torch.empty(m, dtype=torch.float64, device=self.dev)

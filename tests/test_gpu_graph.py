@@ -99,11 +99,22 @@ def test_plan_failures_raise_like_eager():
     _same(plan.solve(p.a, p.b, p.x_star), _eager(p.a, p.b, "pne", "single", p.x_star))
 
 
-def test_plan_refuses_host_planned_engines():
+def test_plan_refuses_host_decided_engines_and_bad_methods():
     with pytest.raises(ValueError):
-        PipelinePlan(4096, 32, method="pne", precision="single")      # FFT sketch (m % 2048 == 0)
+        PipelinePlan(1 << 20, 2048, method="pne", precision="single")   # INT8 Ozaki Gram / TRSM
     with pytest.raises(ValueError):
         PipelinePlan(100, 10, method="sne")
+
+
+@pytest.mark.parametrize("prec", ["half", "single", "double"])
+def test_plan_with_the_fft_sketch_equals_eager(prec):
+    """m % 2048 == 0 takes the FFT sketch, whose pass-B request lists are planned on the
+    device: the whole solve still captures, bitwise the eager result."""
+    p = planted_problem(4096, 64, 1e3, 1e-6, 21)
+    plan = PipelinePlan(4096, 64, method="hpne", precision=prec, seed=2)
+    ref = _eager(p.a, p.b, "hpne", prec, p.x_star, seed=2)
+    for _ in range(2):
+        _same(plan.solve(p.a, p.b, p.x_star), ref)
 
 
 def test_deferred_verdicts_refuse_host_value_entry_points():

@@ -127,3 +127,16 @@ def test_fft_tall_m1_beyond_pass_b_table(env):
     dm, f2 = _sum(env, op, a, 64, "dmma")
     fft, dm = fft.cpu().numpy(), dm.cpu().numpy()
     assert np.abs(fft - dm).max() <= 1e-11 * np.abs(dm).max()
+
+
+@pytest.mark.parametrize("m,n,d,level", [(4096, 20, 60, 64), (65536, 130, 390, 32), (1 << 20, 64, 6144, 16)])
+def test_device_request_planning_equals_host(env, monkeypatch, m, n, d, level):
+    """pass-B request lists built on the device (plan_requests, no host round trip) give
+    the same sketch, bit for bit, as the host construction (SK_FFT_HOST_PLAN=1)."""
+    torch, sq, S = env
+    a = torch.from_numpy(R.philox(m + d, 5).standard_normal((m, n))).cuda()
+    op = sq.make_sketch(m, d, "dct2", seed=4)
+    dev, _ = _sum(env, op, a, level, "fft")
+    monkeypatch.setenv("SK_FFT_HOST_PLAN", "1")
+    host, _ = _sum(env, op, a, level, "fft")
+    assert torch.equal(dev, host)
