@@ -18,14 +18,16 @@ sys.path.insert(0, sys.argv[1])
 import paper_2603_16644_b200 as sq
 from oracle import restatement as R
 out = {}
-for n, kind in ((2048, "gauss"), (2048, "ties"), (1500, "gauss"), (64, "ties"), (2048, "singular")):
+for n, kind in ((2048, "gauss"), (2048, "ties"), (1500, "gauss"), (64, "ties"), (2048, "singular"),
+                (1, "gauss"), (2, "ties"), (31, "gauss"), (32, "ties"), (33, "gauss"), (100, "gauss"),
+                (160, "ties"), (161, "gauss"), (120, "singular")):
     g = R.philox(n, 11)
     if kind == "ties":
         a = g.integers(-2, 3, size=(n, n)).astype(np.float64)   # many equal pivot magnitudes
     else:
         a = g.standard_normal((n, n))
     if kind == "singular":
-        a[:, 700] = a[:, 3] * 2.0
+        a[:, min(700, n - 1)] = a[:, 3] * 2.0
     rhs = g.standard_normal(n)
     key = f"{n}_{kind}"
     try:
@@ -48,10 +50,15 @@ def _run(tmp_path, tag, env_extra):
 
 @pytest.mark.gpu
 def test_smem_lu_bitwise_equals_perm_lu(tmp_path):
-    smem = _run(tmp_path, "smem", {})
+    """default (one-CTA lu_small_kernel for n <= 160, lu_smem_kernel above) vs
+    SK_LU_KERNEL=smem (the dataflow kernel at every n <= 2048) vs SK_LU_KERNEL=perm."""
+    smem = _run(tmp_path, "default", {})
+    flow = _run(tmp_path, "smem", {"SK_LU_KERNEL": "smem"})
     perm = _run(tmp_path, "perm", {"SK_LU_KERNEL": "perm"})
-    assert sorted(smem) == sorted(perm)
+    assert sorted(smem) == sorted(perm) == sorted(flow)
     for k in smem:
         assert np.array_equal(smem[k], perm[k], equal_nan=True), k
+        assert np.array_equal(flow[k], perm[k], equal_nan=True), k
+    assert "120_singular_err" in smem
     assert "2048_singular_err" in smem                       # NumericallySingular, same column and value
     assert np.isfinite(smem["2048_gauss"]).all() and np.isfinite(smem["2048_ties"]).all()

@@ -32,7 +32,7 @@ def blocked_everywhere(request, monkeypatch):
 
 
 @pytest.mark.parametrize("level", ["binary32", "binary64"])
-@pytest.mark.parametrize("d,n", [(300, 100), (600, 200), (1500, 257), (3000, 1000)])
+@pytest.mark.parametrize("d,n", [(70, 65), (200, 129), (300, 100), (600, 200), (1500, 257), (3000, 1000)])
 def test_blocked_r_matches_oracle(sq, level, d, n):
     a = R.philox(d + n, 11).standard_normal((d, n)) * np.logspace(0, -2, n)
     lev = getattr(sq, level.upper())
