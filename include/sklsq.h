@@ -110,11 +110,14 @@ int sk_residual_async(const double *a, int64_t rows, int64_t cols, int64_t lda, 
  * sk_lu_solve_f64, sk_chol_solve_f64, sk_trsv_f64) do not synchronise: they enqueue a
  * check that stores the verdict (code, index, value, aux as in sk_status) into the
  * record and return SK_OK.  The first failure in stream order wins, so one read of the
- * record after the solve raises what the eager calls would have raised first.  Kernels
+ * record after the solve raises what the eager calls would have raised first.  The INT8
+ * Ozaki-II engines (sk_gram_ozaki_acc_f64 with accumulate = 0, sk_trsm_ozaki_f64) keep
+ * their operand guard on the device too (flag 256 bytes past their workspace, which must
+ * then be 256 bytes larger) and run the DMMA fallback gated on it.  Kernels
  * with data-dependent control flow (LU, Cholesky) run on the identity once a failure is
  * recorded (their outputs are then meaningless; the record says so).  Entry points whose
  * result is a host value (sk_cast_stats, sk_residual, sk_kappa0_*, sk_jacobi_sv_f64,
- * sk_level_overflow, the INT8 Ozaki engines, ...) return
+ * sk_level_overflow, ...) return
  * SK_ERR_ARG while verdicts are deferred.  Replaces the host-side exception points of
  * src/solvers.py:168-252 (raise sites kept in order). */
 int sk_defer_verdicts(sk_status *status_dev);

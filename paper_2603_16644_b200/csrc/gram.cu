@@ -98,7 +98,8 @@ __device__ __forceinline__ void load_stage(double *xs, double *ys, const double 
 template <bool VEC16, bool SYRK>
 __global__ void __launch_bounds__(THREADS, SK_GRAM_MINB)
 gram_tn_kernel(const double *__restrict__ x, int64_t ldx, const double *__restrict__ y, int64_t ldy,
-               int64_t m, int n, int ntn, int ntiles, int64_t kchunk, double *__restrict__ part) {
+               int64_t m, int n, int ntn, int ntiles, int64_t kchunk, double *__restrict__ part, const int *gate) {
+    if (gate && *gate == 0) return;   // gated fallback (deferred verdicts): run only when flagged
     extern __shared__ __align__(16) double smem[];
     double *xs_base = smem;
     double *ys_base = smem + STAGES * BK * PITCH;
@@ -186,7 +187,8 @@ gram_tn_kernel(const double *__restrict__ x, int64_t ldx, const double *__restri
 // halves so the result is exactly symmetric.
 template <bool SYRK>
 __global__ void gram_reduce_kernel(const double *__restrict__ part, int splits, int ntiles, int ntn,
-                                   int n, double *__restrict__ gout, int64_t ldg, int accumulate) {
+                                   int n, double *__restrict__ gout, int64_t ldg, int accumulate, const int *gate) {
+    if (gate && *gate == 0) return;
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= (int64_t)n * n) return;
     int i = (int)(idx / n), j = (int)(idx % n);
@@ -290,6 +292,13 @@ static int splits_for(int64_t m, int64_t n) {
 
 using namespace sk;
 
+namespace sk {
+namespace gram {
+int gram_f64_gated(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n, double *g,
+                   int64_t ldg, int accumulate, void *ws, size_t ws_bytes, sk_stream_t stream, const int *gate);
+}  // namespace gram
+}  // namespace sk
+
 extern "C" {
 
 size_t sk_gram_workspace(int64_t m, int64_t n) {
@@ -299,6 +308,17 @@ size_t sk_gram_workspace(int64_t m, int64_t n) {
 
 int sk_gram_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
                 double *g, int64_t ldg, int accumulate, void *ws, size_t ws_bytes, sk_stream_t stream) {
+    return sk::gram::gram_f64_gated(x, ldx, y, ldy, m, n, g, ldg, accumulate, ws, ws_bytes, stream, nullptr);
+}
+
+}  // extern "C"
+
+namespace sk {
+namespace gram {
+// sk_gram_f64 whose kernels run only when *gate != 0 (gate == nullptr: always): the
+// stream-ordered DMMA fallback of the INT8 Gram under deferred verdicts
+int gram_f64_gated(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n, double *g,
+                   int64_t ldg, int accumulate, void *ws, size_t ws_bytes, sk_stream_t stream, const int *gate) {
     if (!x || !y || !g || m < 0 || n <= 0 || ldx < n || ldy < n || ldg < n || n > (1 << 20)) {
         set_error("sk_gram_f64: bad arguments");
         return SK_ERR_ARG;
@@ -324,7 +344,7 @@ int sk_gram_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int6
         auto kfn = gram::gram_tn_kernel<V, S>;                                                     \
         SK_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram::SMEM)); \
         kfn<<<units, gram::THREADS, gram::SMEM, st>>>(x, ldx, y, ldy, m, (int)n, p.ntn, p.ntiles, \
-                                                      p.kchunk, part);                             \
+                                                      p.kchunk, part, gate);                       \
     } while (0)
         if (vec && syrk) SK_GRAM_LAUNCH(true, true);
         else if (vec) SK_GRAM_LAUNCH(true, false);
@@ -337,12 +357,18 @@ int sk_gram_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int6
     const int rb = 256;
     const unsigned rg = (unsigned)((total + rb - 1) / rb);
     if (syrk)
-        gram::gram_reduce_kernel<true><<<rg, rb, 0, st>>>(part, p.splits, p.ntiles, p.ntn, (int)n, g, ldg, accumulate);
+        gram::gram_reduce_kernel<true><<<rg, rb, 0, st>>>(part, p.splits, p.ntiles, p.ntn, (int)n, g, ldg, accumulate,
+                                                            gate);
     else
-        gram::gram_reduce_kernel<false><<<rg, rb, 0, st>>>(part, p.splits, p.ntiles, p.ntn, (int)n, g, ldg, accumulate);
+        gram::gram_reduce_kernel<false><<<rg, rb, 0, st>>>(part, p.splits, p.ntiles, p.ntn, (int)n, g, ldg, accumulate,
+                                                             gate);
     SK_LAUNCH_CHECK("gram_reduce_kernel");
     return SK_OK;
 }
+}  // namespace gram
+}  // namespace sk
+
+extern "C" {
 
 size_t sk_gemv_t_workspace(int64_t m, int64_t n) {
     return (size_t)gemvt::splits_for(m, n) * (size_t)n * sizeof(double);

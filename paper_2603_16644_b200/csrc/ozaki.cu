@@ -1087,9 +1087,14 @@ struct TrsmWs {
 
 }  // namespace oz
 
+namespace gram {
+int gram_f64_gated(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n, double *g,
+                   int64_t ldg, int accumulate, void *ws, size_t ws_bytes, sk_stream_t stream, const int *gate);
+}  // namespace gram
+
 namespace trsm {
 int launch(const double *a, int64_t lda, int64_t m, int n, const double *r, int64_t ldr, double *ap, int64_t ldap,
-           cudaStream_t st);
+           cudaStream_t st, const int *gate = nullptr);
 int first_zero_diagonal(const double *r, int64_t ldr, int n, cudaStream_t st, int *out);
 }  // namespace trsm
 
@@ -1237,7 +1242,6 @@ int sk_trsm_ozaki_fell_back(void) { return g_trsm_oz_fell_back; }
 
 int sk_trsm_ozaki_f64(const double *a, int64_t lda, int64_t m, int64_t n, const double *r, int64_t ldr, double *ap,
                       int64_t ldap, sk_status *status, void *ws, size_t ws_bytes, sk_stream_t stream) {
-    SK_NO_DEFER("sk_trsm_ozaki_f64");
     if (!a || !r || !ap || m < 0 || n <= 0 || lda < n || ldr < n || ldap < n || n > (1 << 20) || a == ap) {
         set_error("sk_trsm_ozaki_f64: bad arguments (a and a_p must be distinct)");
         return SK_ERR_ARG;
@@ -1247,12 +1251,26 @@ int sk_trsm_ozaki_f64(const double *a, int64_t lda, int64_t m, int64_t n, const 
         return SK_ERR_ARG;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    int first_zero = 0;
-    int rc = trsm::first_zero_diagonal(r, ldr, (int)n, st, &first_zero);
-    if (rc) return rc;
-    if (first_zero != INT32_MAX) {
-        set_error("zero diagonal entry at index %d", first_zero);
-        return fill_status(status, SK_SINGULAR_TRIANGULAR, first_zero, 0.0, 0.0);
+    // deferred verdicts: zero diagonal recorded on the device; the spiky / non-finite
+    // guard flag on the device past the workspace, the DMMA re-solve gated on it
+    const bool defer = deferred_status() != nullptr;
+    const size_t flag_off = sk_trsm_ozaki_workspace(m, n);
+    int rc = SK_OK;
+    if (defer) {
+        if (ws_bytes < flag_off + 256) {
+            set_error("sk_trsm_ozaki_f64: under deferred verdicts needs %zu workspace bytes", flag_off + 256);
+            return SK_ERR_ARG;
+        }
+        rc = note_zero_diagonal(r, ldr, n, SK_SINGULAR_TRIANGULAR, st);
+        if (rc) return rc;
+    } else {
+        int first_zero = 0;
+        rc = trsm::first_zero_diagonal(r, ldr, (int)n, st, &first_zero);
+        if (rc) return rc;
+        if (first_zero != INT32_MAX) {
+            set_error("zero diagonal entry at index %d", first_zero);
+            return fill_status(status, SK_SINGULAR_TRIANGULAR, first_zero, 0.0, 0.0);
+        }
     }
     g_trsm_oz_fell_back = 0;
     static const int64_t base = getenv("SK_TRSM_OZ_BASE") ? atoll(getenv("SK_TRSM_OZ_BASE")) : 1024;
@@ -1264,12 +1282,13 @@ int sk_trsm_ozaki_f64(const double *a, int64_t lda, int64_t m, int64_t n, const 
         if (rc) return rc;
         return fill_status(status, SK_OK, -1, 0, 0);
     }
-    int *flag = trsm_guard_slot();
+    int *flag = defer ? reinterpret_cast<int *>(static_cast<uint8_t *>(ws) + flag_off) : trsm_guard_slot();
     if (!flag) {
         set_error("sk_trsm_ozaki_f64: pinned guard slot unavailable");
         return SK_ERR_CUDA;
     }
-    *reinterpret_cast<volatile int *>(flag) = 0;   // the stream is idle (synchronized above)
+    if (defer) SK_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    else *reinterpret_cast<volatile int *>(flag) = 0;   // the stream is idle (synchronized above)
     oz::TrsmWs W;
     W.plan = oz::trsm_plan(m, n);
     uint8_t *w = static_cast<uint8_t *>(ws);
@@ -1294,6 +1313,11 @@ int sk_trsm_ozaki_f64(const double *a, int64_t lda, int64_t m, int64_t n, const 
     rc = oz::trsm_rec(a, lda, ap, ldap, m, n, r, ldr, W, st);
     if (rc) return rc;
     if (oz::TrsmProf *prof = oz::trsm_prof()) prof->report();
+    if (defer) {   // spiky rows of A_p / columns of R, or non-finite values: the DMMA solve, gated
+        rc = trsm::launch(a, lda, m, (int)n, r, ldr, ap, ldap, st, flag);
+        if (rc) return rc;
+        return fill_status(status, SK_OK, -1, 0, 0);
+    }
     SK_CUDA(cudaStreamSynchronize(st));
     if (*reinterpret_cast<volatile int *>(flag)) {
         // spiky rows of A_p / columns of R, or non-finite values: redo on the DMMA path
@@ -1362,7 +1386,6 @@ int sk_gram_ozaki_ex_f64(const double *x, int64_t ldx, const double *y, int64_t 
 int sk_gram_ozaki_acc_f64(const double *x, int64_t ldx, const double *y, int64_t ldy, int64_t m, int64_t n,
                           const double *xstats, const double *ystats, double *g, int64_t ldg, int accumulate,
                           void *ws, size_t ws_bytes, sk_stream_t stream) {
-    SK_NO_DEFER("sk_gram_ozaki_acc_f64");
     if (!x || !y || !g || m < 0 || n <= 0 || ldx < n || ldy < n || ldg < n || n > 65536) {
         set_error("sk_gram_ozaki_f64: bad arguments");
         return SK_ERR_ARG;
@@ -1402,15 +1425,25 @@ int sk_gram_ozaki_acc_f64(const double *x, int64_t ldx, const double *y, int64_t
         if (rc) return rc;
         sy = stats + 2 * n;
     }
-    int *flag = guard_slot();
+    // deferred verdicts: the guard flag lives on the device, past both engines' workspace,
+    // and the DMMA fallback runs gated on it after the INT8 product (which then computed
+    // garbage that the fallback overwrites); no host read
+    const bool defer = deferred_status() != nullptr;
+    const size_t flag_off = std::max(sk_gram_ozaki_workspace(m, n, syrk), sk_gram_workspace(m, n));
+    if (defer && (accumulate || ws_bytes < flag_off + 256)) {
+        set_error("sk_gram_ozaki_f64: under deferred verdicts needs accumulate = 0 and %zu workspace bytes",
+                  flag_off + 256);
+        return SK_ERR_ARG;
+    }
+    int *flag = defer ? reinterpret_cast<int *>(static_cast<uint8_t *>(ws) + flag_off) : guard_slot();
     if (!flag) {
         set_error("sk_gram_ozaki_f64: pinned guard slot unavailable");
         return SK_ERR_CUDA;
     }
     oz::guard_kernel<<<1, 1024, 0, st>>>(sx, sy, (int)n, m, flag);
     SK_LAUNCH_CHECK("oz guard");
-    SK_CUDA(cudaStreamSynchronize(st));
-    if (*reinterpret_cast<volatile int *>(flag)) {
+    if (!defer) SK_CUDA(cudaStreamSynchronize(st));
+    if (!defer && *reinterpret_cast<volatile int *>(flag)) {
         // spiky columns or non-finite input: the FP64 DMMA Gram (same workspace)
         g_oz_fell_back = 1;
         if (ws_bytes < sk_gram_workspace(m, n)) {
@@ -1528,6 +1561,8 @@ int sk_gram_ozaki_acc_f64(const double *x, int64_t ldx, const double *y, int64_t
                 syrk ? "syrk" : "gemm", (long long)m, tot, pre_ms, res_ms, gemm_ms, tot - pre_ms - res_ms - gemm_ms);
         for (int i = 0; i < npe; ++i) cudaEventDestroy(pe[i]);
     }
+    if (defer)   // spiky or non-finite columns: the FP64 DMMA Gram, gated on the device flag
+        return gram::gram_f64_gated(x, ldx, y, ldy, m, n, g, ldg, 0, ws, ws_bytes, stream, flag);
     return SK_OK;
 }
 

@@ -145,7 +145,8 @@ __device__ __forceinline__ void load_block(double *ts, double *rs, const double 
 
 __global__ void __launch_bounds__(THREADS, MINB)
 trsm_kernel(const double *a, int64_t lda, int64_t m, int n, const double *__restrict__ r, int64_t ldr, double *ap,
-            int64_t ldap, bool vec) {
+            int64_t ldap, bool vec, const int *gate) {
+    if (gate && *gate == 0) return;   // gated fallback (deferred verdicts): run only when flagged
     extern __shared__ __align__(16) double smem[];
     double *as_base = smem;
     double *bs_base = as_base + STAGES * BMR * APITCH;
@@ -354,14 +355,14 @@ int *zero_diag_slot() {
 
 // the kernel alone (no argument or diagonal checks); used by the blocked INT8 TRSM too
 int launch(const double *a, int64_t lda, int64_t m, int n, const double *r, int64_t ldr, double *ap, int64_t ldap,
-           cudaStream_t st) {
+           cudaStream_t st, const int *gate) {
     if (m == 0) return SK_OK;
     const bool vec = ((reinterpret_cast<uintptr_t>(ap) | reinterpret_cast<uintptr_t>(r) |
                        reinterpret_cast<uintptr_t>(a)) % 16 == 0) &&
                      (ldap % 2 == 0) && (ldr % 2 == 0) && (lda % 2 == 0);
     SK_CUDA(cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     const unsigned grid = (unsigned)((m + BMR - 1) / BMR);
-    trsm_kernel<<<grid, THREADS, SMEM, st>>>(a, lda, m, n, r, ldr, ap, ldap, vec);
+    trsm_kernel<<<grid, THREADS, SMEM, st>>>(a, lda, m, n, r, ldr, ap, ldap, vec, gate);
     SK_LAUNCH_CHECK("trsm_kernel");
     return SK_OK;
 }
@@ -400,7 +401,7 @@ extern "C" int sk_trsm_right_upper_f64(const double *a, int64_t lda, int64_t m, 
     if (deferred_status()) {   // deferred verdicts: recorded on the device, no host read
         int rc = note_zero_diagonal(r, ldr, n, SK_SINGULAR_TRIANGULAR, st);
         if (rc) return rc;
-        rc = trsm::launch(a, lda, m, (int)n, r, ldr, ap, ldap, st);
+        rc = trsm::launch(a, lda, m, (int)n, r, ldr, ap, ldap, st, nullptr);
         if (rc) return rc;
         return fill_status(status, SK_OK, -1, 0, 0);
     }
@@ -411,7 +412,7 @@ extern "C" int sk_trsm_right_upper_f64(const double *a, int64_t lda, int64_t m, 
         set_error("zero diagonal entry at index %d", first_zero);
         return fill_status(status, SK_SINGULAR_TRIANGULAR, first_zero, 0.0, 0.0);
     }
-    rc = trsm::launch(a, lda, m, (int)n, r, ldr, ap, ldap, st);
+    rc = trsm::launch(a, lda, m, (int)n, r, ldr, ap, ldap, st, nullptr);
     if (rc) return rc;
     return fill_status(status, SK_OK, -1, 0, 0);
 }

@@ -21,10 +21,11 @@ a plan's results equal the eager call's bit for bit in every case.
 
 The plan owns every buffer (inputs, sketch operator, A_s, R_s, A_p, G, workspaces), so
 nothing it captured can be reallocated underneath the graph.  It covers the engines
-whose results do not need a host round trip: the FFT / DMMA / tcgen05 sketches, the FP64
-DMMA TRSM and Gram.  Shapes for which the eager pipeline picks the INT8 Ozaki engines
-(large, bandwidth-bound solves where a graph buys nothing; their operand guards decide
-a fallback on the host) are refused at construction.  Not in the reference's API: an addition for serving many small solves.
+of every engine the eager pipeline picks: the FFT / DMMA / tcgen05 sketches, the FP64
+DMMA or INT8 Ozaki-II TRSM and Gram (whose operand guards, which choose the DMMA
+fallback, stay on the device: the fallback kernels run gated on the guard flag).  The
+solve's A_p is held in full (the eager pipeline's row-chunked TRSM -> Gram for A_p that
+does not fit beside A is not captured).  Not in the reference's API: an addition for serving many small solves.
 """
 
 from __future__ import annotations
@@ -54,7 +55,7 @@ class _LevelGraph:
     """Buffers and the captured graph of one precision level."""
 
     def __init__(self, plan: "PipelinePlan", level: PrecisionLevel):
-        from .dense import _new_ap
+        from .dense import _gram_engine, _new_ap, _trsm_engine
         lib = _lib.lib()
         m, n, d = plan.m, plan.n, plan.d
         dev = plan.dev
@@ -68,10 +69,22 @@ class _LevelGraph:
         self.g = torch.empty((n, n), dtype=torch.float64, device=dev)
         self.rhs = torch.empty(n, dtype=torch.float64, device=dev)
         self.y = torch.empty(n, dtype=torch.float64, device=dev)
+        # the engines the eager pipeline picks for this shape (INT8 Ozaki Gram with A_p^T b
+        # from the column scan, INT8 Ozaki TRSM; their fallbacks gated on device flags that
+        # sit 256 bytes past their workspaces under deferred verdicts)
+        self.gram_oz = _gram_engine(m, n, False, None) == "ozaki"
+        self.trsm_oz = _trsm_engine(m, n, False, None) == "ozaki"
+        self.st = torch.empty(3 * n, dtype=torch.float64, device=dev)   # column max, sum of squares, A_p^T b
         tc = _lib.TRANSFORM_CODE[plan.transform]
-        ws = max(lib.sk_matrix_stats_workspace(m, n), lib.sk_sketch_workspace_ex(level.code, tc, m, self.op.m_pad, n, d),
+        sizes = [lib.sk_matrix_stats_workspace(m, n), lib.sk_sketch_workspace_ex(level.code, tc, m, self.op.m_pad, n, d),
                  lib.sk_qr_workspace(level.code, d, n), lib.sk_gram_workspace(m, n), lib.sk_nxn_workspace(n),
-                 2 * 8 * n + 1024)
+                 2 * 8 * n + 1024, lib.sk_colstats_workspace(n)]
+        if self.gram_oz:
+            syrk = plan.method == "pne"
+            sizes.append(max(lib.sk_gram_ozaki_workspace(m, n, int(syrk)), lib.sk_gram_workspace(m, n)) + 256)
+        if self.trsm_oz:
+            sizes.append(lib.sk_trsm_ozaki_workspace(m, n) + 256)
+        ws = max(sizes)
         self.ws = torch.empty(int(ws) + 256, dtype=torch.uint8, device=dev)
         self.ws_side = torch.empty(int(lib.sk_gemv_t_workspace(m, n)) + 256, dtype=torch.uint8, device=dev)
         self.side = torch.cuda.Stream(device=dev)
@@ -116,23 +129,36 @@ class _LevelGraph:
             _c(lib.sk_note_zero_diagonal(self.r.data_ptr(), n, n, SK_RANK_DEFICIENT, st), "sk_note_zero_diagonal")
             # src/solvers.py:205-215: A_p = A R_s^-1
             ap, ldap = self.ap.data_ptr(), self.ap.stride(0)
-            _c(lib.sk_trsm_right_upper_f64(a, n, m, n, self.r.data_ptr(), n, ap, ldap, None, st), "sk_trsm")
-            # src/solvers.py:218-252: A_p^T b on a second stream under the Gram
-            cur = torch.cuda.current_stream()
-            self.side.wait_stream(cur)
-            with torch.cuda.stream(self.side):
-                _c(lib.sk_gemv_t_f64(ap, ldap, m, n, b, self.rhs.data_ptr(), 0, self.ws_side.data_ptr(),
-                                     self.ws_side.numel(), self.side.cuda_stream), "sk_gemv_t_f64")
+            if self.trsm_oz:
+                _c(lib.sk_trsm_ozaki_f64(a, n, m, n, self.r.data_ptr(), n, ap, ldap, None, ws, wn, st),
+                   "sk_trsm_ozaki_f64")
+            else:
+                _c(lib.sk_trsm_right_upper_f64(a, n, m, n, self.r.data_ptr(), n, ap, ldap, None, st), "sk_trsm")
             yp, ldy = (ap, ldap) if plan.method == "pne" else (a, n)
-            _c(lib.sk_gram_f64(ap, ldap, yp, ldy, m, n, self.g.data_ptr(), n, 0, ws, wn, st), "sk_gram_f64")
-            cur.wait_stream(self.side)
+            if self.gram_oz:
+                # src/solvers.py:218-252 on the INT8 engine: one column scan of A_p gives its
+                # scales and A_p^T b (solvers._gram_and_rhs), then the Ozaki-II product
+                stp = self.st.data_ptr()
+                _c(lib.sk_colstats_f64(ap, ldap, m, n, b, stp, ws, wn, st), "sk_colstats_f64")
+                _c(lib.sk_gram_ozaki_acc_f64(ap, ldap, yp, ldy, m, n, stp, stp if plan.method == "pne" else None,
+                                             self.g.data_ptr(), n, 0, ws, wn, st), "sk_gram_ozaki_acc_f64")
+                rhs = stp + 16 * n
+            else:
+                # A_p^T b on a second stream under the DMMA Gram
+                cur = torch.cuda.current_stream()
+                self.side.wait_stream(cur)
+                with torch.cuda.stream(self.side):
+                    _c(lib.sk_gemv_t_f64(ap, ldap, m, n, b, self.rhs.data_ptr(), 0, self.ws_side.data_ptr(),
+                                         self.ws_side.numel(), self.side.cuda_stream), "sk_gemv_t_f64")
+                _c(lib.sk_gram_f64(ap, ldap, yp, ldy, m, n, self.g.data_ptr(), n, 0, ws, wn, st), "sk_gram_f64")
+                cur.wait_stream(self.side)
+                rhs = self.rhs.data_ptr()
             if plan.method == "pne":
-                _c(lib.sk_chol_solve_f64(self.g.data_ptr(), n, self.rhs.data_ptr(), self.y.data_ptr(), None, ws, wn,
-                                         st), "sk_chol_solve_f64")
+                _c(lib.sk_chol_solve_f64(self.g.data_ptr(), n, rhs, self.y.data_ptr(), None, ws, wn, st),
+                   "sk_chol_solve_f64")
                 _c(lib.sk_trsv_f64(self.r.data_ptr(), n, n, 0, self.y.data_ptr(), x, None, ws, wn, st), "sk_trsv_f64")
             else:
-                _c(lib.sk_lu_solve_f64(self.g.data_ptr(), n, self.rhs.data_ptr(), x, None, ws, wn, st),
-                   "sk_lu_solve_f64")
+                _c(lib.sk_lu_solve_f64(self.g.data_ptr(), n, rhs, x, None, ws, wn, st), "sk_lu_solve_f64")
             # src/solvers.py:99-117: ||A x - b||^2 and ||x||^2
             _c(lib.sk_residual_async(a, m, n, n, x, b, None, res, ws, wn, st), "sk_residual_async")
         finally:
@@ -168,9 +194,6 @@ class PipelinePlan:
         self.d = int(math.ceil(d_factor * n))
         if self.d < n:
             raise ValueError(f"d_factor {d_factor} gives d={self.d} < n={n}")
-        from .dense import _gram_engine, _trsm_engine
-        if _gram_engine(m, n, False, None) != "dmma" or _trsm_engine(m, n, False, None) != "dmma":
-            raise ValueError(f"PipelinePlan: {m} x {n} takes the INT8 Ozaki engines; use algorithm1_pipeline")
         self.dev = device()
         self.a = torch.empty((m, n), dtype=torch.float64, device=self.dev)
         self.b = torch.empty(m, dtype=torch.float64, device=self.dev)

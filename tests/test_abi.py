@@ -94,8 +94,6 @@ def test_pipeline_plan_validates_before_touching_the_device():
         sq.PipelinePlan(5, 10)
     with pytest.raises(ValueError):
         sq.PipelinePlan(100, 10, d_factor=0.5)
-    with pytest.raises(ValueError):                   # the INT8 Ozaki engines decide fallbacks on the host
-        sq.PipelinePlan(1 << 20, 2048, method="pne", precision="single")
     import torch
     if not torch.cuda.is_available():
         with pytest.raises(_lib.LibraryUnavailable):

@@ -99,11 +99,39 @@ def test_plan_failures_raise_like_eager():
     _same(plan.solve(p.a, p.b, p.x_star), _eager(p.a, p.b, "pne", "single", p.x_star))
 
 
-def test_plan_refuses_host_decided_engines_and_bad_methods():
-    with pytest.raises(ValueError):
-        PipelinePlan(1 << 20, 2048, method="pne", precision="single")   # INT8 Ozaki Gram / TRSM
+def test_plan_refuses_bad_methods():
     with pytest.raises(ValueError):
         PipelinePlan(100, 10, method="sne")
+
+
+@pytest.mark.parametrize("m,n,method,prec", [(140000, 256, "hpne", "single"),   # INT8 Gram (GEMM-TN)
+                                             (140000, 256, "pne", "double"),    # INT8 Gram (SYRK)
+                                             (9000, 1100, "pne", "single"),     # + INT8 TRSM
+                                             (9000, 1100, "hpne", "auto")])
+def test_plan_with_the_int8_engines_equals_eager(m, n, method, prec):
+    """Shapes on the INT8 Ozaki-II Gram / TRSM: their guard flags stay on the device and
+    the DMMA fallbacks run gated on them, so the graph is bitwise the eager solve."""
+    p = planted_problem(m, n, 1e3, 1e-6, 31)
+    a, b = torch.from_numpy(p.a).cuda(), torch.from_numpy(p.b).cuda()
+    plan = PipelinePlan(m, n, method=method, precision=prec, seed=3)
+    ref = _eager(a, b, method, prec, p.x_star, seed=3)
+    for _ in range(2):
+        _same(plan.solve(a, b, p.x_star), ref)
+
+
+def test_plan_int8_gram_guard_fallback_equals_eager():
+    """A spiky column (one entry dominating its column norm) trips the INT8 Gram's guard:
+    eager falls back to the DMMA Gram on the host's read of the flag, the graph runs the
+    gated DMMA Gram on the device flag; the results are the same bits."""
+    from paper_2603_16644_b200 import dense as D
+    p = planted_problem(140000, 256, 1e3, 1e-6, 32)
+    a = p.a.copy()
+    a[77, 5] *= 1e6
+    a_d, b_d = torch.from_numpy(a).cuda(), torch.from_numpy(p.b).cuda()
+    plan = PipelinePlan(140000, 256, method="hpne", precision="double", seed=3)
+    ref = _eager(a_d, b_d, "hpne", "double", None, seed=3)
+    assert _lib.lib().sk_gram_ozaki_fell_back() == 1        # the eager Gram did fall back
+    _same(plan.solve(a_d, b_d), ref)
 
 
 @pytest.mark.parametrize("prec", ["half", "single", "double"])
