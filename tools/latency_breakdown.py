@@ -24,13 +24,20 @@ def main():
     ap.add_argument("--method", default="hpne")
     ap.add_argument("--precision", default="single")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--kappa", type=float, default=1e8)
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
 
     import paper_2603_16644_b200 as sq
     from oracle.problems import planted_problem
-    p = planted_problem(args.m, args.n, 1e8, 1e-6, 11)
+    if args.m * args.n <= 4_000_000:
+        p = planted_problem(args.m, args.n, args.kappa, 1e-6, 11)
+    else:                                     # large: the device generator, copied to the host
+        from paper_2603_16644_b200.probgen import generate_problem_device
+        from types import SimpleNamespace
+        a_d, b_d, x_d = generate_problem_device(args.m, args.n, args.kappa, 1e-6, 11)
+        p = SimpleNamespace(a=a_d.cpu().numpy(), b=b_d.cpu().numpy(), x_star=x_d.cpu().numpy())
     a, b = torch.from_numpy(p.a).cuda(), torch.from_numpy(p.b).cuda()
 
     def solve():
@@ -68,7 +75,7 @@ def main():
     pr.disable()
     s = io.StringIO()
     pstats.Stats(pr, stream=s).sort_stats("tottime").print_stats(25)
-    out = {"m": args.m, "n": args.n, "method": args.method, "precision": args.precision,
+    out = {"m": args.m, "n": args.n, "kappa": args.kappa, "method": args.method, "precision": args.precision,
            "wall_ms_per_solve": wall, "gpu_kernel_ms_per_solve": gpu_us / 1e3 / args.reps,
            "sync_calls_per_solve": syncs / args.reps, "blocking_memcpy_per_solve": memcpy / args.reps,
            "kernels": {k: {"per_solve": v[0] / args.reps, "us_per_solve": v[1] / args.reps}
