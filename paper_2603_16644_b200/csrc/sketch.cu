@@ -23,6 +23,9 @@ namespace sk {
 namespace sketch {
 
 constexpr int BM = 128, BN = 128, BK = 16, THREADS = 256, WM = 32, WN = 64;
+#ifndef SK_OMEGA_ANCHOR
+#define SK_OMEGA_ANCHOR 16   // k-steps between exact operator phases (1: exact every step)
+#endif
 constexpr int APITCH = BK + 4;   // Omega tile [i][k], 20 = 4 (mod 16)
 constexpr int BPITCH = BN + 4;   // A tile [k][c], 132 = 4 (mod 16)
 constexpr size_t SMEM = sizeof(double) * (2 * BM * APITCH + 2 * BK * BPITCH + 2 * BM * BK);
@@ -76,18 +79,36 @@ sketch_kernel(const double *__restrict__ a, int64_t lda, int64_t m_local, int64_
     }
     (void)rot;
     int over = 0;
+    // block base phase e^{i pi p / 2M}, p = rr (2 jg0 + 1) mod 4M: exact (sincospi of the
+    // exactly reduced integer phase) every SK_OMEGA_ANCHOR k-steps, advanced in between by
+    // the fixed rotation of one k-step (p += 2 BK rr): the per-step 64-bit modular products
+    // and FP64 sincospi dominated the kernel's instruction stream (ncu: DMMA 17% of the
+    // instructions at config-2 shape); the rotation adds <= SK_OMEGA_ANCHOR roundings
+    const uint64_t f1 = (uint64_t)rr % (uint64_t)fourM;
+    const uint64_t dstep = (f1 * (uint64_t)(2 * BK)) % (uint64_t)fourM;
+    double c_step = 1.0, s_step = 0.0;
+    if (TRANSFORM == SK_DCT2) sincospi((double)dstep / (2.0 * M), &s_step, &c_step);
+    double cb_cur = 1.0, sb_cur = 0.0;
+    int gen_count = 0;
 
     auto gen_omega = [&](double *dst, int64_t kb) {
         // columns kb + gh*8 + u (local rows of A), global jg = row_offset + local
         const int64_t jl0 = kb + gh * 8;
         if (TRANSFORM == SK_DCT2) {
-            const int64_t jg0 = row_offset + jl0;
-            // both factors < 4M < 2^32, so the product fits in 64 bits
-            const uint64_t f1 = (uint64_t)rr % (uint64_t)fourM;
-            const uint64_t f2 = (uint64_t)(2 * jg0 + 1) % (uint64_t)fourM;
-            const int64_t p = (int64_t)((f1 * f2) % (uint64_t)fourM);
             double sb, cb;
-            sincospi((double)p / (2.0 * M), &sb, &cb);
+            if (gen_count % SK_OMEGA_ANCHOR == 0) {
+                const int64_t jg0 = row_offset + jl0;
+                // both factors < 4M < 2^32, so the product fits in 64 bits
+                const uint64_t f2 = (uint64_t)(2 * jg0 + 1) % (uint64_t)fourM;
+                const int64_t p = (int64_t)((f1 * f2) % (uint64_t)fourM);
+                sincospi((double)p / (2.0 * M), &sb, &cb);
+            } else {
+                cb = cb_cur * c_step - sb_cur * s_step;
+                sb = sb_cur * c_step + cb_cur * s_step;
+            }
+            cb_cur = cb;
+            sb_cur = sb;
+            ++gen_count;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 double v = cr * (cb * rc[u] - sb * rs[u]);
