@@ -161,3 +161,27 @@ def test_deferred_verdicts_refuse_host_value_entry_points():
     finally:
         lib.sk_defer_verdicts(None)
     assert rc == -2 and b"sk_defer_verdicts" in lib.sk_last_error()
+
+
+def test_plans_on_two_host_threads():
+    """The deferred-verdict record is per host thread and each plan owns its buffers and
+    streams: two threads replaying their own plans concurrently get the eager results."""
+    import threading
+    probs = [planted_problem(800, 70, 1e4, 1e-6, s) for s in (41, 42)]
+    refs = [_eager(p.a, p.b, "hpne", "single", p.x_star, seed=7) for p in probs]
+    plans = [PipelinePlan(800, 70, method="hpne", precision="single", seed=7) for _ in probs]
+    errors = []
+
+    def work(i):
+        try:
+            for _ in range(20):
+                _same(plans[i].solve(probs[i].a, probs[i].b, probs[i].x_star), refs[i])
+        except Exception as ex:  # noqa: BLE001
+            errors.append(ex)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
