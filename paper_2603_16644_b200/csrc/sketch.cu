@@ -22,7 +22,7 @@
 namespace sk {
 namespace sketch {
 
-constexpr int BM = 128, BN = 128, BK = 16, THREADS = 256, WM = 32, WN = 64;
+constexpr int BM = 128, BN = 128, BK = 16, THREADS = 512, WM = 32, WN = 32;   // 16 warps of 32 x 32
 #ifndef SK_OMEGA_ANCHOR
 #define SK_OMEGA_ANCHOR 16   // k-steps between exact operator phases (1: exact every step)
 #endif
@@ -62,17 +62,18 @@ sketch_kernel(const double *__restrict__ a, int64_t lda, int64_t m_local, int64_
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const int wm = warp % (BM / WM), wn = warp / (BM / WM);
 
-    // Omega generator role: thread -> (row gi = tid/2, k half = tid%2 -> 8 columns)
-    const int gi = tid >> 1, gh = tid & 1;
+    // Omega generator role: thread -> (row gi = tid/4, k quarter = tid%4 -> 4 columns)
+    constexpr int GC = BM * BK / THREADS;   // generated columns per thread (4)
+    const int gi = tid / (BK / GC), gh = tid % (BK / GC);
     const bool grow_ok = (i0 + gi) < d;
     const int64_t rr = grow_ok ? rows[i0 + gi] : 0;
     const double M = (double)mpad;
     const int64_t fourM = 4 * mpad;
     const double cr = (rr == 0) ? sqrt(1.0 / M) : sqrt(2.0 / M);
-    double rc[8], rs[8];   // e^{i (gh*8 + u) pi r / M}, u = 0..7, relative to the block base
+    double rc[GC], rs[GC];   // e^{i (gh*GC + u) pi r / M}, u < GC, relative to the block base
     if (TRANSFORM == SK_DCT2) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < GC; ++u) {
             const int64_t q = (int64_t)(((uint64_t)rr * (uint64_t)(2 * u)) % (uint64_t)fourM);
             sincospi((double)q / (2.0 * M), &rs[u], &rc[u]);
         }
@@ -93,7 +94,7 @@ sketch_kernel(const double *__restrict__ a, int64_t lda, int64_t m_local, int64_
 
     auto gen_omega = [&](double *dst, int64_t kb) {
         // columns kb + gh*8 + u (local rows of A), global jg = row_offset + local
-        const int64_t jl0 = kb + gh * 8;
+        const int64_t jl0 = kb + gh * GC;
         if (TRANSFORM == SK_DCT2) {
             double sb, cb;
             if (gen_count % SK_OMEGA_ANCHOR == 0) {
@@ -110,29 +111,30 @@ sketch_kernel(const double *__restrict__ a, int64_t lda, int64_t m_local, int64_
             sb_cur = sb;
             ++gen_count;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < GC; ++u) {
                 double v = cr * (cb * rc[u] - sb * rs[u]);
                 if (!grow_ok || jl0 + u >= kend) v = 0.0;
-                dst[gi * APITCH + gh * 8 + u] = v;
+                dst[gi * APITCH + gh * GC + u] = v;
             }
         } else {
             const double inv = 1.0 / sqrt(M);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < GC; ++u) {
                 const int64_t jg = row_offset + jl0 + u;
                 double v = (__popcll((unsigned long long)(rr & jg)) & 1) ? -inv : inv;
                 if (!grow_ok || jl0 + u >= kend) v = 0.0;
-                dst[gi * APITCH + gh * 8 + u] = v;
+                dst[gi * APITCH + gh * GC + u] = v;
             }
         }
     };
-    // A tile loader role: thread -> (k row = tid/16, 8 columns = (tid%16)*8)
-    const int lk = tid >> 4, lc = (tid & 15) * 8;
-    double areg[8];
+    // A tile loader role: thread -> (k row, LC consecutive columns)
+    constexpr int LC = BK * BN / THREADS;   // 4
+    const int lk = tid / (BN / LC), lc = (tid % (BN / LC)) * LC;
+    double areg[LC];
     auto load_a = [&](int64_t kb) {
         const int64_t k = kb + lk;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < LC; ++u) {
             const int c = c0 + lc + u;
             areg[u] = (k < kend && c < n) ? a[k * lda + c] : 0.0;
         }
@@ -141,7 +143,7 @@ sketch_kernel(const double *__restrict__ a, int64_t lda, int64_t m_local, int64_
         const int64_t k = kb + lk;
         const double s = (k < kend) ? signs[row_offset + k] : 0.0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) dst[lk * BPITCH + lc + u] = s * demote<LEVEL>(areg[u], over);
+        for (int u = 0; u < LC; ++u) dst[lk * BPITCH + lc + u] = s * demote<LEVEL>(areg[u], over);
     };
 
     double acc[WM / 8][WN / 8][2];
